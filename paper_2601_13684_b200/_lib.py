@@ -1,0 +1,103 @@
+"""ctypes binding of the C ABI in include/hcb200.h (libhcb200.so).
+
+There is no fallback: if the library is missing or no CUDA device is
+present, every compute entry point raises.  PyTorch is used only for device
+memory and streams; all compute goes through the kernels behind this ABI.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "libhcb200.so"
+
+HC_OK, HC_EINVAL, HC_EINFEASIBLE, HC_ECUDA, HC_ENOMEM, HC_ESTATE = range(6)
+PAD_INDEX = 0xFFFFFFFF
+
+u32p = C.POINTER(C.c_uint32)
+
+
+class HCError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"hcb200 error {code}: {msg}")
+        self.code = code
+
+
+class TopkJob(C.Structure):
+    _fields_ = [
+        ("scores", C.c_void_p), ("idx", C.c_void_p), ("n", C.c_uint32), ("k", C.c_uint32),
+        ("out_idx", C.c_void_p), ("out_count", C.c_void_p), ("base_bitmap", C.c_void_p),
+        ("overlap_out", C.c_void_p),
+    ]
+
+
+class RecallHead(C.Structure):
+    _fields_ = [("idx", C.c_void_p), ("scores", C.c_void_p), ("dynamic", C.c_void_p)]
+
+
+_lib = None
+
+
+def _declare(lib):
+    vp, i32, u32 = C.c_void_p, C.c_int, C.c_uint32
+    sig = {
+        "hc_version": (C.c_char_p, []),
+        "hc_last_error": (C.c_char_p, []),
+        "hc_topk_batched": (i32, [vp, i32, u32, vp]),
+        "hc_select_topk": (i32, [vp, vp, u32, u32, vp, vp, vp]),
+        "hc_bitmap_from_indices": (i32, [vp, u32, vp, vp, u32, vp]),
+        "hc_trace_recall": (i32, [vp, i32, u32, C.c_uint64, u32, u32, u32, u32, vp, vp]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return sig
+
+
+EXPORTED = None
+
+
+def load():
+    """Load (never build) the shared library; raises if it is absent."""
+    global _lib, EXPORTED
+    if _lib is not None:
+        return _lib
+    path = Path(os.environ.get("HCB200_LIB", LIB_PATH))
+    if not path.exists():
+        raise ImportError(
+            f"{path} is missing: build it with `python -m paper_2601_13684_b200.build` "
+            "(there is no CPU fallback)")
+    lib = C.CDLL(str(path))
+    EXPORTED = sorted(_declare(lib))
+    _lib = lib
+    return lib
+
+
+def check(rc: int) -> None:
+    if rc != HC_OK:
+        msg = load().hc_last_error().decode(errors="replace")
+        raise HCError(rc, msg)
+
+
+def ptr(t) -> int:
+    """Device (or host) address of a torch tensor, or 0 for None."""
+    return 0 if t is None else int(t.data_ptr())
+
+
+def stream_handle(stream=None) -> int:
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def require_cuda():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise HCError(HC_ECUDA, "no CUDA device: the HeteroCache-B200 path has no CPU fallback")
+    load()

@@ -1,0 +1,53 @@
+// Trace-driven residency recall (CacheEngine._measure, engine.py:276-288).
+//
+// One thread per head walks its recorded row in record order and keeps two
+// float64 running sums, exactly as attention_recall (evaluation.py:41-59)
+// does in Python: IEEE double additions in the same order give the same
+// bits.  Membership follows CacheView.__contains__ (engine.py:98-107).
+
+#include "hc_common.cuh"
+
+namespace hc {
+namespace {
+
+__global__ void trace_recall_kernel(const hc_recall_head* __restrict__ heads, int n_heads,
+                                    uint32_t K, uint64_t stride, uint32_t L, uint32_t t,
+                                    uint32_t sinks, uint32_t recency, double* __restrict__ out) {
+  const int h = blockIdx.x * blockDim.x + threadIdx.x;
+  if (h >= n_heads) return;
+  hc_recall_head hd = heads[h];
+  hd.idx += stride * t;
+  hd.scores += stride * t;
+  // position >= L + t - recency  (signed: the floor may be negative)
+  const long long tail_floor = (long long)L + (long long)t - (long long)recency;
+  double total = 0.0, hit = 0.0;
+  for (uint32_t j = 0; j < K; ++j) {
+    const uint32_t p = __ldg(hd.idx + j);
+    if (p == HC_PAD_INDEX) continue;
+    const double s = (double)__ldg(hd.scores + j);
+    total = __dadd_rn(total, s);
+    bool in = (p >= L) || (hd.dynamic == nullptr) || (p < sinks) ||
+              ((long long)p >= tail_floor);
+    if (!in) in = (__ldg(hd.dynamic + (p >> 5)) >> (p & 31)) & 1u;
+    if (in) hit = __dadd_rn(hit, s);
+  }
+  out[h] = (total == 0.0) ? 1.0 : __ddiv_rn(hit, total);
+}
+
+}  // namespace
+}  // namespace hc
+
+extern "C" int hc_trace_recall(const hc_recall_head* heads_dev, int n_heads, uint32_t K,
+                               uint64_t step_stride, uint32_t prefill_len, uint32_t step,
+                               uint32_t sink_count,
+                               uint32_t recency_window, double* recall_out_dev, void* stream) {
+  HC_REQUIRE(n_heads >= 0 && (n_heads == 0 || (heads_dev && recall_out_dev)), HC_EINVAL,
+             "hc_trace_recall: bad arguments");
+  if (n_heads == 0) return HC_OK;
+  const int threads = 128;
+  hc::trace_recall_kernel<<<(n_heads + threads - 1) / threads, threads, 0,
+                            (cudaStream_t)stream>>>(heads_dev, n_heads, K, step_stride, prefill_len, step,
+                                                    sink_count, recency_window, recall_out_dev);
+  HC_CHECK_LAUNCH();
+  return HC_OK;
+}

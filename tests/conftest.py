@@ -28,3 +28,10 @@ def pytest_collection_modifyitems(config, items):
     for item in items:
         if "gpu" in item.keywords:
             item.add_marker(skip)
+
+
+def pytest_sessionstart(session):
+    # (Re)build the in-tree sm_100a library if any CUDA source is newer than it.
+    from paper_2601_13684_b200 import build
+
+    build.build()

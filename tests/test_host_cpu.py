@@ -1,0 +1,109 @@
+"""CPU-only checks of the host mirror and the C ABI library (no compute calls)."""
+
+import ctypes
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from golden_io import case_arrays, engine_cases, json_fixture, key
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def test_library_exports_every_header_symbol():
+    from paper_2601_13684_b200 import _lib
+
+    lib = _lib.load()
+    header = (ROOT / "include" / "hcb200.h").read_text()
+    declared = set(re.findall(r"^\s*(?:int|const char\*|void)\s+(hc_\w+)\s*\(", header, re.M))
+    assert declared, "no entry points parsed from include/hcb200.h"
+    for name in sorted(declared):
+        assert hasattr(lib, name), f"libhcb200.so does not export {name}"
+    assert set(_lib.EXPORTED) == declared, "ctypes declarations out of sync with the header"
+    assert lib.hc_version().startswith(b"hcb200")
+
+
+def test_library_rejects_bad_arguments_without_gpu():
+    from paper_2601_13684_b200 import _lib
+
+    lib = _lib.load()
+    assert lib.hc_topk_batched(None, 3, 0, None) == _lib.HC_EINVAL
+    assert b"bad jobs" in lib.hc_last_error()
+
+
+def test_budget_matches_reference_fixtures():
+    from paper_2601_13684_b200.budget import BudgetConfig, BudgetError, allocate
+    from paper_2601_13684_b200.profiling import taxonomy_from_roles
+    from paper_2601_13684_b200.budget import plan_budget
+
+    for c in json_fixture("budget_cases.json"):
+        cfg = c["config"]
+        exp = c["expected"]
+        bc = BudgetConfig(rho=cfg["rho"], epsilon=cfg["epsilon"], min_length=cfg["min_length"],
+                          rounding=cfg["rounding"])
+        stab = {key(h): s for h, s in c["stabilities"].items()}
+        if c.get("plan_budget"):
+            roles = {key(h): r for h, r in c["roles"].items()}
+            NL = 1 + max(l for l, _ in roles)
+            H = 1 + max(h for _, h in roles)
+            clusters = []
+            for l in range(NL):
+                sats = [(l, h) for h in range(H) if roles[(l, h)] == "satellite"]
+                clusters.append(((l, 0), sats))
+            tax = taxonomy_from_roles(roles, clusters, num_layers=NL, heads_per_layer=H,
+                                      s_stable=stab)
+            got = plan_budget(tax, bc, c["prefill_len"])
+        elif "error" in exp:
+            with pytest.raises(BudgetError):
+                allocate(stab, c["l_base"], bc, prefill_len=c["prefill_len"], num_full=0)
+            continue
+        else:
+            got = allocate(stab, c["l_base"], bc, prefill_len=c["prefill_len"],
+                           num_full=exp["num_full"])
+        assert got.l_base == exp["l_base"]
+        assert got.l_base_int == exp["l_base_int"]
+        assert {f"{l},{h}": n for (l, h), n in got.lengths.items()} == exp["lengths"]
+
+
+def test_trace_roundtrip_and_fingerprint():
+    from paper_2601_13684_b200.trace import (BadMagicError, TraceManifest,
+                                             TruncatedPayloadError, make_trace, read_trace,
+                                             trace_bytes, trace_fingerprint)
+
+    for case in engine_cases()[:6]:
+        idx, sc = case_arrays(case["name"])
+        m = TraceManifest(**case["manifest"])
+        tr = make_trace(m, idx, sc)
+        assert trace_fingerprint(tr) == case["expected"]["trace_sha256"]
+        blob = trace_bytes(tr)
+        back = read_trace(blob)
+        assert np.array_equal(back.indices, tr.indices) and np.array_equal(back.scores, tr.scores)
+        with pytest.raises(BadMagicError):
+            read_trace(b"NOTATRACE" + blob[9:])
+        with pytest.raises(TruncatedPayloadError):
+            read_trace(blob[:-3])
+
+
+def test_engine_config_validation_and_cache_view():
+    from paper_2601_13684_b200.engine import CacheView, EngineConfig, EngineError
+
+    for bad in (dict(tau_drift=2.0), dict(window=0), dict(transfer_bandwidth=0),
+                dict(update_delay_steps=-1), dict(variant="turbo")):
+        with pytest.raises(EngineError):
+            EngineConfig(**bad)
+    view = CacheView(prefill_len=100, step=5, base=frozenset({50}), sink_count=4, recency_window=8)
+    assert 50 in view and 0 in view and 3 in view and 4 not in view
+    assert 97 in view and 96 not in view and 104 in view
+    comp = CacheView(prefill_len=100, step=5, base=frozenset({0, 50}), sink_count=4,
+                     recency_window=8)
+    assert comp.size() == len({0, 50} | {0, 1, 2, 3} | {97, 98, 99}) + 5
+
+
+def test_completion_step_rule():
+    from paper_2601_13684_b200.engine import EngineConfig, completion_step
+
+    cfg = EngineConfig(update_delay_steps=3, transfer_bandwidth=500)
+    assert completion_step(24, 24576, cfg) == 50
+    assert completion_step(24, 1000, cfg) == 27
