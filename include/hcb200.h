@@ -110,6 +110,104 @@ int hc_trace_recall(const hc_recall_head* heads_dev, int n_heads, uint32_t K,
                     uint32_t sink_count, uint32_t recency_window, double* recall_out_dev,
                     void* stream);
 
+
+/* ---------------------------------------------------------------------------
+ * Tensor-mode engine: hierarchical KV store + per-step decode pipeline.
+ *
+ * Units are (batch b, layer l, kv head h), numbered u = (b*NL + l)*H + h.
+ * Roles per (layer, head) come from the taxonomy (profiling.py:38-40):
+ * volatile / pivot keep their full cache on the GPU; anchor / satellite keep
+ * a compressed cache of their planned length l_h (budget.py:144-208) plus
+ * sinks, recency tail and decode appends (CacheView, engine.py:98-115).
+ * Satellites' full prefill K/V live in a pinned host pool for retrieval.
+ * ------------------------------------------------------------------------- */
+typedef struct hc_engine hc_engine; /* opaque handle; one host thread per handle */
+
+enum hc_role { HC_ROLE_VOLATILE = 0, HC_ROLE_ANCHOR = 1, HC_ROLE_PIVOT = 2, HC_ROLE_SATELLITE = 3 };
+
+typedef struct hc_engine_desc {
+  int32_t batch;          /* sequences (the reference has one engine per sequence) */
+  int32_t num_layers;
+  int32_t kv_heads;       /* heads_per_layer of the trace manifest (trace.py:82-89) */
+  int32_t group;          /* query heads per KV head (GQA), 1..8                     */
+  int32_t head_dim;       /* 128                                                     */
+  int32_t prefill_len;    /* L                                                       */
+  int32_t max_decode;     /* capacity in decode steps                                */
+  int32_t sink_count;     /* EngineConfig.sink_count (engine.py:58)                  */
+  int32_t recency_window; /* EngineConfig.recency_window (engine.py:59), <= 32       */
+  int32_t l_base_int;     /* BudgetPlan.l_base_int (budget.py:206)                   */
+  int32_t chunk;          /* split-K rows per tile, multiple of 64 (0: 1024)         */
+  int32_t monitor;        /* drift monitoring on (variant != no_retrieval)           */
+  int32_t host_pool;      /* 1: satellite prefill K/V in pinned host memory          */
+} hc_engine_desc;
+
+/* CacheEngine.__init__ (engine.py:156-214): allocate and lay out the store.
+ * roles/lengths/cluster_pivot are [num_layers * kv_heads] host arrays;
+ * lengths[i] is the planned length of a compressed head (ignored for full
+ * heads); cluster_pivot[i] is the pivot head index of a satellite's cluster
+ * (same layer, profiling.py:237-239), -1 otherwise. */
+int hc_engine_create(const hc_engine_desc* desc, const int32_t* roles, const int32_t* lengths,
+                     const int32_t* cluster_pivot, hc_engine** out);
+int hc_engine_destroy(hc_engine* eng);
+/* device bytes, pinned host bytes, arena rows, number of pivot units */
+int hc_engine_info(const hc_engine* eng, int64_t* out4);
+
+/* prefill_init (engine.py:263-274) for one layer: k/v [B, H, L, 128] bf16 and
+ * q_last [B, H*G, 128] bf16 (the last prompt token's queries) on the device.
+ * Scores every head with the last token's GQA-mean attention (the step-0
+ * record, export.ts:125-127), selects top-l_h for compressed heads and
+ * top-l_base for pivots (K_base), gathers the selected rows into the
+ * compressed caches, copies full heads whole and satellites to the host pool. */
+int hc_engine_prefill_layer(hc_engine* eng, int32_t layer, const void* k_dev, const void* v_dev,
+                            const void* q_last_dev, void* stream);
+
+/* decode_step (engine.py:290-311) minus host bookkeeping: append the step's
+ * K/V (k_new/v_new [B, NL, H, 128]), run attention for every head of every
+ * layer (q/o [B, NL, H*G, 128]), form pivot score rows and their top-l_base
+ * sets with the |top & K_base| counts (Eq. 9). */
+int hc_engine_decode_step(hc_engine* eng, int32_t step, const void* q_dev, const void* k_new_dev,
+                          const void* v_new_dev, void* o_dev, void* stream);
+
+/* Copy the overlap counts of steps [first, last] (<= 64 steps back) into
+ * out [(last-first+1) x n_pivots] (pivot order = ascending unit), then sync. */
+int hc_engine_overlaps(hc_engine* eng, int32_t first, int32_t last, int32_t* out_host,
+                       void* stream);
+
+/* Fire a drift event for pivot unit `pivot_unit` at `step` (engine.py:322-357):
+ * select top-l_s of the pivot's current row for each satellite (sorted by
+ * head), restamp K_base with the current top set, and schedule the host ->
+ * HBM gather of the selected rows on the retrieval stream.  Writes one
+ * transfer id per satellite. */
+int hc_engine_fire(hc_engine* eng, int32_t pivot_unit, int32_t step, int32_t completion_step,
+                   int32_t* transfer_ids, void* stream);
+
+/* Landing of a due transfer (engine.py:293-299): the caller's stream waits
+ * for the gather, then the satellite serves the new set from this step on. */
+int hc_engine_land(hc_engine* eng, int32_t transfer_id, void* stream);
+
+/* Read back index sets (sorted ascending) and sync:
+ *   kind 0: fetched set of a transfer, 1: a compressed unit's current
+ *   dynamic set, 2: a pivot unit's current top-l_base set, 3: a compressed
+ *   unit's prefix-buffer positions. */
+int hc_engine_read_indices(hc_engine* eng, int32_t kind, int32_t id, uint32_t* out_host,
+                           int32_t capacity, int32_t* n_out, void* stream);
+
+/* Copy a pivot unit's probability row over [0, L + step) to dst (device). */
+int hc_engine_pivot_row(hc_engine* eng, int32_t pivot_unit, int32_t step, float* dst_dev,
+                        void* stream);
+
+/* Resident K/V rows summed over all units at `step` (the algorithmic bytes of
+ * the step are rows * 2 * head_dim * 2); syncs. */
+int hc_engine_resident_rows(hc_engine* eng, int32_t step, int64_t* rows_out, void* stream);
+
+/* Test hook: when set, prefill copies every layer's step-0 rows (the
+ * GQA-mean probability rows over [0, L) of all B*H units of the layer,
+ * unit order b*H + h) to dst [NL][B*H][L] fp32 (device). */
+int hc_engine_set_prefill_dump(hc_engine* eng, float* dst_dev);
+
+/* Number of attention tiles (CTAs) the step launches. */
+int hc_engine_active_tiles(const hc_engine* eng, int32_t step, int32_t* n_tiles);
+
 #ifdef __cplusplus
 }
 #endif

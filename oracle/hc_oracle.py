@@ -297,13 +297,15 @@ def _recall(L, t, base, sink_count, recency_window, idx_row, sc_row) -> float:
 def replay(indices, scores, *, prefill_len, bytes_per_kv_entry, roles, clusters,
            lengths, l_base_int, tau_drift=0.5, window=8, transfer_bandwidth=1 << 30,
            update_delay_steps=1, sink_count=4, recency_window=8,
-           variant="heterocache", eval_every_step=False, measure=True):
+           variant="heterocache", eval_every_step=False, measure=True, record_dynamic=False):
     """Straight-line restatement of CacheEngine.run (engine.py:372-416).
 
     indices/scores: (T+1, NL, H, K) trace arrays (dense rows are K = L+T with
     PAD suffixes).  clusters: list of (pivot, satellites).  Returns a dict with
     rows (list of dicts mirroring StepRow), events (dicts mirroring
-    RetrievalRecord) and final GPU sets.
+    RetrievalRecord) and final GPU sets.  measure=False skips the recall
+    diagnostic (NaN) for traces that only carry pivot rows after step 0;
+    record_dynamic=True also returns the dynamic sets in force at every step.
     """
     L = prefill_len
     T = indices.shape[0] - 1
@@ -340,21 +342,22 @@ def replay(indices, scores, *, prefill_len, bytes_per_kv_entry, roles, clusters,
     order = 0
 
     def measure_row(t):  # engine.py:276-288
-        if not measure:
-            return float("nan"), 0, 0
         recs, total_size = [], 0
         for hd in heads:
             base = None if hd in full else dynamic[hd]
             l, h = hd
-            recs.append(_recall(L, t, base, sink_count, recency_window,
-                                indices[t, l, h], scores[t, l, h]))
+            if measure:
+                recs.append(_recall(L, t, base, sink_count, recency_window,
+                                    indices[t, l, h], scores[t, l, h]))
             total_size += cache_view_size(L, t, base, sink_count, recency_window)
         charged = len(full) * L + sum(len(dynamic[hd]) for hd in comp)
-        return sum(recs) / len(recs), charged, total_size - charged
+        recall = sum(recs) / len(recs) if measure else float("nan")
+        return recall, charged, total_size - charged
 
     def in_flight(t):  # engine.py:140-143
         return sum(e["transfer_bytes"] for e in events if e["completion_step"] > t)
 
+    dyn_trace = [dict(dynamic)] if record_dynamic else None
     r, c, x = measure_row(0)
     rows = [dict(step=0, recall=r, gpu_entries=c, extra_entries=x, bytes_in_flight=0,
                  cumulative_bytes=0, retrieval_flag=0)]
@@ -363,6 +366,8 @@ def replay(indices, scores, *, prefill_len, bytes_per_kv_entry, roles, clusters,
         pending = [e for e in pending if e[0] > t]
         for _, _, s, ids in due:
             dynamic[s] = ids
+        if record_dynamic:
+            dyn_trace.append(dict(dynamic))
         r, c, x = measure_row(t)
         flag = 0
         if variant != "no_retrieval":
@@ -401,4 +406,4 @@ def replay(indices, scores, *, prefill_len, bytes_per_kv_entry, roles, clusters,
     final = {hd: frozenset(resident_positions(L, T, None if hd in full else dynamic[hd],
                                               sink_count, recency_window)) for hd in heads}
     return {"rows": rows, "events": events, "final_gpu": final, "dynamic": dynamic,
-            "k_base": k_base}
+            "k_base": k_base, "dynamic_trace": dyn_trace}

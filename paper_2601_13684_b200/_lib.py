@@ -34,6 +34,12 @@ class TopkJob(C.Structure):
     ]
 
 
+class EngineDesc(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in (
+        "batch", "num_layers", "kv_heads", "group", "head_dim", "prefill_len", "max_decode",
+        "sink_count", "recency_window", "l_base_int", "chunk", "monitor", "host_pool")]
+
+
 class RecallHead(C.Structure):
     _fields_ = [("idx", C.c_void_p), ("scores", C.c_void_p), ("dynamic", C.c_void_p)]
 
@@ -50,6 +56,19 @@ def _declare(lib):
         "hc_select_topk": (i32, [vp, vp, u32, u32, vp, vp, vp]),
         "hc_bitmap_from_indices": (i32, [vp, u32, vp, vp, u32, vp]),
         "hc_trace_recall": (i32, [vp, i32, u32, C.c_uint64, u32, u32, u32, u32, vp, vp]),
+        "hc_engine_create": (i32, [vp, vp, vp, vp, vp]),
+        "hc_engine_destroy": (i32, [vp]),
+        "hc_engine_info": (i32, [vp, vp]),
+        "hc_engine_prefill_layer": (i32, [vp, i32, vp, vp, vp, vp]),
+        "hc_engine_decode_step": (i32, [vp, i32, vp, vp, vp, vp, vp]),
+        "hc_engine_overlaps": (i32, [vp, i32, i32, vp, vp]),
+        "hc_engine_fire": (i32, [vp, i32, i32, i32, vp, vp]),
+        "hc_engine_land": (i32, [vp, i32, vp]),
+        "hc_engine_read_indices": (i32, [vp, i32, i32, vp, i32, vp, vp]),
+        "hc_engine_pivot_row": (i32, [vp, i32, i32, vp, vp]),
+        "hc_engine_resident_rows": (i32, [vp, i32, vp, vp]),
+        "hc_engine_set_prefill_dump": (i32, [vp, vp]),
+        "hc_engine_active_tiles": (i32, [vp, i32, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -46,7 +46,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not needs_build():
         return LIB
     tmp = LIB.with_suffix(".so.tmp")
-    cmd = [nvcc(), *ARCH, *FLAGS, "-o", str(tmp), *map(str, sources()), "-lcuda"]
+    cmd = [nvcc(), *ARCH, *FLAGS, "-o", str(tmp), *map(str, sources())]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = res.stdout + res.stderr
     (PKG / "build.log").write_text(log)

@@ -1,0 +1,413 @@
+// K4: fused ragged split-K flash-decoding over the hierarchical KV store.
+//
+// No reference implementation exists (the reference moves index sets only,
+// SPEC.md:103); semantics follow the exporter's attention
+// (pkg/exporter/src/model.ts:232-291): per query head softmax(q.K^T/sqrt(d))
+// over the head's resident rows, then P.V; GQA groups of G query heads share
+// one KV head.  Pivot heads also emit their scaled logits so the GQA-mean
+// probability row (model.ts:274-291) can be formed after the split-K merge.
+//
+// Decode attention is a stream over K/V (arithmetic intensity ~G flop/B, far
+// below the B200 ridge), so the kernel is built around HBM:
+//   * one CTA per tile of <= `chunk` rows of one unit; a producer warp
+//     streams 64-row K and V sub-tiles into a 3-stage shared-memory ring with
+//     TMA (cp.async.bulk.tensor, 128B swizzle) and mbarrier transaction
+//     counts; 2 CTAs per SM keep ~192 KB of loads in flight per SM;
+//   * four consumer warps each own 16 rows of every sub-tile: QK^T and PV on
+//     the tensor pipe with mma.sync m16n8k16 (bf16 in, fp32 accumulate; rows
+//     G..15 of the M=16 tile are zero), online softmax in exp2 domain with
+//     quad shuffles, conflict-free ldmatrix thanks to the swizzle;
+//   * warps merge through shared memory; each tile writes one (M, L, O)
+//     partial per query head; combine_kernel merges a unit's partials.
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "hc_common.cuh"
+#include "kv_layout.cuh"
+
+namespace hc {
+namespace {
+
+constexpr int kSub = 64;                      // rows per pipeline stage
+constexpr int kConsumerWarps = 4;
+constexpr int kThreadsAttn = (kConsumerWarps + 1) * 32;
+constexpr int kStages = 3;
+constexpr int kBoxBytes = kSub * 128;         // 64 rows x 64 bf16 (one swizzle span)
+constexpr int kStageBytes = 4 * kBoxBytes;    // K lo/hi halves + V lo/hi halves
+constexpr int kSmemAttn = kStages * kStageBytes + 1024 /*align*/ + 64 /*barriers*/;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int32_t c0,
+                                            int32_t c1, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                        uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1,
+                                          uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+// D += A(16x16, row) * B(16x8, col); rows 8..15 of A are zero here (a1=a3=0).
+__device__ __forceinline__ void mma_bf16(float (&d)[4], uint32_t a0, uint32_t a2, uint32_t b0,
+                                         uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+// Address of 16-byte chunk J (0..15, 8 bf16 each) of row r of a K or V
+// sub-tile stored as two 128B-swizzled 64-column boxes.
+__device__ __forceinline__ uint32_t swz(uint32_t base, int r, int J) {
+  return base + (J >> 3) * kBoxBytes + r * 128 + (((J & 7) ^ (r & 7)) << 4);
+}
+
+__global__ void __launch_bounds__(kThreadsAttn, 2)
+attn_tiles_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                  const AttnParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t sbase = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  uint8_t* sgen = smem_raw + (sbase - smem_u32(smem_raw));
+  const uint32_t bar_full = sbase + kStages * kStageBytes;  // kStages x 8 B
+  const uint32_t bar_empty = bar_full + kStages * 8;
+
+  const TileDesc tile = p.tiles[blockIdx.x];
+  const UnitDesc unit = p.units[tile.unit];
+  const TileRange rg = tile_range(unit, tile.seg_chunk, p.t, p.L, p.recency, p.chunk);
+  const int G = p.group;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* part = p.partial + size_t(tile.slot) * G * kPartStride;
+
+  if (rg.n <= 0) {  // nothing resident in this tile at this step
+    if (threadIdx.x < G) {
+      part[threadIdx.x * kPartStride + 0] = -INFINITY;
+      part[threadIdx.x * kPartStride + 1] = 0.f;
+    }
+    return;
+  }
+  const int n_sub = (rg.n + kSub - 1) / kSub;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(bar_full + 8 * s, 1);
+      mbar_init(bar_empty + 8 * s, kConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == kConsumerWarps) {
+    // ---------------- producer: TMA K/V sub-tiles into the ring ----------------
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmK)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmV)) : "memory");
+      for (int s = 0; s < n_sub; ++s) {
+        const int st = s % kStages;
+        const uint32_t ph = (s / kStages) & 1;
+        mbar_wait(bar_empty + 8 * st, ph ^ 1);
+        const uint32_t dst = sbase + st * kStageBytes;
+        const uint32_t fb = bar_full + 8 * st;
+        mbar_expect_tx(fb, kStageBytes);
+        const int32_t row = int32_t(rg.row + int64_t(s) * kSub);
+        tma_load_2d(dst + 0 * kBoxBytes, &tmK, 0, row, fb);
+        tma_load_2d(dst + 1 * kBoxBytes, &tmK, 64, row, fb);
+        tma_load_2d(dst + 2 * kBoxBytes, &tmV, 0, row, fb);
+        tma_load_2d(dst + 3 * kBoxBytes, &tmV, 64, row, fb);
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers ----------------
+  const int g = lane >> 2;   // query head row of the MMA tile
+  const int c = lane & 3;    // column pair
+  const bool row_ok = g < G;
+  // Q A-fragments for 8 k-steps (a0: d 16kk+2c.., a2: d 16kk+8+2c..)
+  uint32_t qa0[8], qa2[8];
+  {
+    const __nv_bfloat16* q = reinterpret_cast<const __nv_bfloat16*>(p.q) +
+                             (size_t(unit.q_row) + (row_ok ? g : 0)) * kHeadDim;
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      const uint32_t lo = *reinterpret_cast<const uint32_t*>(q + 16 * kk + 2 * c);
+      const uint32_t hi = *reinterpret_cast<const uint32_t*>(q + 16 * kk + 8 + 2 * c);
+      qa0[kk] = row_ok ? lo : 0u;
+      qa2[kk] = row_ok ? hi : 0u;
+    }
+  }
+  float o[16][4];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  float m_run = -INFINITY, l_run = 0.f;
+  const int tb = warp * 16;  // this warp's 16 rows of each sub-tile
+  float* lg = nullptr;
+  if (unit.pivot_slot >= 0 && rg.pos >= 0 && row_ok)
+    lg = p.logits + (size_t(unit.pivot_slot) * G + g) * p.logit_stride + rg.pos;
+
+  for (int s = 0; s < n_sub; ++s) {
+    const int st = s % kStages;
+    mbar_wait(bar_full + 8 * st, (s / kStages) & 1);
+    const uint32_t sK = sbase + st * kStageBytes;
+    const uint32_t sV = sK + 2 * kBoxBytes;
+
+    // S = Q K^T for rows tb..tb+15 (two n-tiles of 8 rows)
+    float sc[2][4];
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.f;
+      const int r = tb + nt * 8 + (lane & 7);
+#pragma unroll
+      for (int kp = 0; kp < 4; ++kp) {
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4(swz(sK, r, 4 * kp + (lane >> 3)), b0, b1, b2, b3);
+        mma_bf16(sc[nt], qa0[2 * kp], qa2[2 * kp], b0, b1);
+        mma_bf16(sc[nt], qa0[2 * kp + 1], qa2[2 * kp + 1], b2, b3);
+      }
+    }
+    // scale, mask, emit pivot logits
+    const int base_tok = s * kSub + tb;
+    float x[2][2];
+    float mloc = -INFINITY;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int tok = base_tok + nt * 8 + 2 * c + e;
+        const float v = sc[nt][e] * p.scale_log2;
+        x[nt][e] = tok < rg.n ? v : -INFINITY;
+        mloc = fmaxf(mloc, x[nt][e]);
+      }
+      if (lg) {
+        const int tok = base_tok + nt * 8 + 2 * c;
+        if (tok + 1 < rg.n) {
+          *reinterpret_cast<float2*>(lg + tok) = make_float2(x[nt][0], x[nt][1]);
+        } else if (tok < rg.n) {
+          lg[tok] = x[nt][0];
+        }
+      }
+    }
+    mloc = fmaxf(mloc, __shfl_xor_sync(0xffffffffu, mloc, 1));
+    mloc = fmaxf(mloc, __shfl_xor_sync(0xffffffffu, mloc, 2));
+    const float m_new = fmaxf(m_run, mloc);
+    const float mb = (m_new == -INFINITY) ? 0.f : m_new;
+    const float alpha = exp2f(m_run - mb);
+    float pr[2][2];
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) pr[nt][e] = exp2f(x[nt][e] - mb);
+    l_run = l_run * alpha + (pr[0][0] + pr[0][1]) + (pr[1][0] + pr[1][1]);
+    m_run = m_new;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      o[i][0] *= alpha;
+      o[i][1] *= alpha;
+    }
+    const uint32_t pa0 = pack_bf16(pr[0][0], pr[0][1]);
+    const uint32_t pa2 = pack_bf16(pr[1][0], pr[1][1]);
+    // O += P V over this warp's 16 rows; V fragments via transposed ldmatrix
+    {
+      const int r = tb + ((lane >> 3) & 1) * 8 + (lane & 7);
+#pragma unroll
+      for (int dp = 0; dp < 8; ++dp) {
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4_t(swz(sV, r, 2 * dp + (lane >> 4)), b0, b1, b2, b3);
+        mma_bf16(o[2 * dp], pa0, pa2, b0, b1);
+        mma_bf16(o[2 * dp + 1], pa0, pa2, b2, b3);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(bar_empty + 8 * st);
+  }
+
+  // ---------------- merge the four warps through (reused) shared memory ----------------
+  l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
+  l_run += __shfl_xor_sync(0xffffffffu, l_run, 2);
+  asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");  // ring no longer read
+  float* ws = reinterpret_cast<float*>(sgen);  // [warp][8 rows][132]
+  float* mine = ws + warp * 8 * kPartStride + g * kPartStride;
+  if (c == 0) {
+    mine[0] = m_run;
+    mine[1] = l_run;
+  }
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    *reinterpret_cast<float2*>(mine + 4 + i * 8 + 2 * c) = make_float2(o[i][0], o[i][1]);
+  }
+  asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
+  const int d = threadIdx.x;  // 0..127
+  for (int gg = 0; gg < G; ++gg) {
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < kConsumerWarps; ++w) M = fmaxf(M, ws[(w * 8 + gg) * kPartStride]);
+    const float mb = (M == -INFINITY) ? 0.f : M;
+    float Ls = 0.f, acc = 0.f;
+#pragma unroll
+    for (int w = 0; w < kConsumerWarps; ++w) {
+      const float* src = ws + (w * 8 + gg) * kPartStride;
+      const float f = exp2f(src[0] - mb);
+      Ls += src[1] * f;
+      acc += src[4 + d] * f;
+    }
+    float* dst = part + gg * kPartStride;
+    dst[4 + d] = acc;
+    if (d == 0) {
+      dst[0] = M;
+      dst[1] = Ls;
+    }
+  }
+}
+
+// Merge a unit's split-K partials; write O (bf16) and, for pivots, (M, L).
+__global__ void __launch_bounds__(128) combine_kernel(const AttnParams p) {
+  const UnitDesc u = p.units[blockIdx.x];
+  const int n = unit_slots(u, p.t, p.L, p.chunk);
+  const int d = threadIdx.x;
+  const int G = p.group;
+  for (int g = 0; g < G; ++g) {
+    float M = -INFINITY;
+    for (int i = 0; i < n; ++i)
+      M = fmaxf(M, p.partial[(size_t(u.slot0 + i) * G + g) * kPartStride]);
+    const float mb = (M == -INFINITY) ? 0.f : M;
+    float Ls = 0.f, acc = 0.f;
+    for (int i = 0; i < n; ++i) {
+      const float* src = p.partial + (size_t(u.slot0 + i) * G + g) * kPartStride;
+      const float li = src[1];
+      if (li == 0.f) continue;  // empty tile: O slot never written
+      const float f = exp2f(src[0] - mb);
+      Ls += li * f;
+      acc += src[4 + d] * f;
+    }
+    __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.out);
+    if (out) out[(size_t(u.q_row) + g) * kHeadDim + d] = __float2bfloat16_rn(acc / Ls);
+    if (u.pivot_slot >= 0 && d == 0) {
+      p.stats[(size_t(u.pivot_slot) * G + g) * 2 + 0] = M;
+      p.stats[(size_t(u.pivot_slot) * G + g) * 2 + 1] = Ls;
+    }
+  }
+}
+
+// GQA-mean probability row of every pivot over [0, L + t):
+//   row[pos] = (sum_j exp(s_j - M_j) * (1 / L_j)) / G   (model.ts:283-289 order)
+__global__ void score_rows_kernel(const AttnParams p, const int32_t* __restrict__ pivot_units,
+                                  int n_pivots) {
+  const int pv = blockIdx.y;
+  if (pv >= n_pivots) return;
+  const UnitDesc u = p.units[pivot_units[pv]];
+  const int slot = u.pivot_slot;
+  const int len = p.L + p.t;
+  const int G = p.group;
+  float Mj[8], inv[8];
+  for (int j = 0; j < G; ++j) {
+    Mj[j] = p.stats[(size_t(slot) * G + j) * 2 + 0];
+    inv[j] = 1.0f / p.stats[(size_t(slot) * G + j) * 2 + 1];
+  }
+  float* row = p.rows + size_t(slot) * p.row_stride;
+  const float* lg = p.logits + size_t(slot) * G * p.logit_stride;
+  for (int pos = blockIdx.x * blockDim.x + threadIdx.x; pos < len; pos += gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    for (int j = 0; j < G; ++j) acc += exp2f(lg[size_t(j) * p.logit_stride + pos] - Mj[j]) * inv[j];
+    row[pos] = acc / float(G);
+  }
+}
+
+}  // namespace
+
+// ---- host launchers (used by engine.cu and the raw test entry point) ----
+
+int make_kv_tensor_map(CUtensorMap* map, const void* base, int64_t rows) {
+  HC_REQUIRE(rows > 0 && rows < (int64_t(1) << 31), HC_EINVAL, "arena rows out of TMA range");
+  HC_REQUIRE((reinterpret_cast<uintptr_t>(base) & 15) == 0, HC_EINVAL, "arena not 16B aligned");
+  const cuuint64_t dims[2] = {cuuint64_t(kHeadDim), cuuint64_t(rows)};
+  const cuuint64_t strides[1] = {cuuint64_t(kHeadDim * 2)};
+  const cuuint32_t box[2] = {64u, cuuint32_t(kSub)};
+  const cuuint32_t estr[2] = {1u, 1u};
+  // resolve the driver entry point at run time: the library must load (and
+  // export its ABI) on hosts without libcuda, e.g. the CPU build container
+  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeFn encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    HC_CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    HC_REQUIRE(fn && q == cudaDriverEntryPointSuccess, HC_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    encode = reinterpret_cast<EncodeFn>(fn);
+  }
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                                      const_cast<void*>(base), dims, strides, box, estr,
+                                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  HC_REQUIRE(r == CUDA_SUCCESS, HC_ECUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
+  return HC_OK;
+}
+
+int launch_attention(const CUtensorMap& tmK, const CUtensorMap& tmV, const AttnParams& p,
+                     int n_tiles, const int32_t* pivot_units_dev, int n_pivots,
+                     cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    HC_CUDA_TRY(cudaFuncSetAttribute(attn_tiles_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemAttn));
+    configured = true;
+  }
+  HC_REQUIRE(p.group >= 1 && p.group <= 8, HC_EINVAL, "GQA group must be 1..8");
+  if (n_tiles > 0) {
+    attn_tiles_kernel<<<n_tiles, kThreadsAttn, kSmemAttn, st>>>(tmK, tmV, p);
+    HC_CHECK_LAUNCH();
+  }
+  if (p.n_units > 0) {
+    combine_kernel<<<p.n_units, 128, 0, st>>>(p);
+    HC_CHECK_LAUNCH();
+  }
+  if (n_pivots > 0 && p.rows) {
+    const int len = p.L + p.t;
+    dim3 grid((len + 1023) / 1024 < 64 ? (len + 1023) / 1024 : 64, n_pivots);
+    score_rows_kernel<<<grid, 1024, 0, st>>>(p, pivot_units_dev, n_pivots);
+    HC_CHECK_LAUNCH();
+  }
+  return HC_OK;
+}
+
+}  // namespace hc

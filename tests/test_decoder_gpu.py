@@ -1,0 +1,225 @@
+"""GPU parity of the tensor-mode decoder (K4 attention, K1/K2 monitor, K3 retrieval).
+
+Protocol:
+  * selection / trigger / byte / completion parity is bit-exact GIVEN THE SAME
+    fp32 score rows: the GPU's own step-0 rows (all heads) and per-step pivot
+    rows are dumped, turned into dense trace records, and replayed through
+    the pinned oracle engine (oracle/hc_oracle.replay, itself pinned to the
+    reference); every event, fetched index set, completion step, byte count
+    and StepRow integer must match, as must the dynamic sets in force;
+  * score rows are checked against the fp32 oracle within tolerance
+    (GPU exp2 vs CPU exp);
+  * attention outputs are checked against the fp32 oracle over exactly the
+    CacheView resident set of each head (engine.py:98-115) at that step.
+    Stated tolerance: |O_gpu - O_ref| <= 2e-2 + 2e-2 * |O_ref| (bf16 K/V/Q in,
+    bf16 P for the PV product, bf16 output).
+"""
+
+import numpy as np
+import pytest
+
+from oracle import hc_oracle as O
+from oracle.attention_oracle import gqa_mean_row, unit_attention
+
+pytestmark = pytest.mark.gpu
+
+O_ATOL = 2e-2
+O_RTOL = 2e-2
+ROW_ATOL = 2e-6
+ROW_RTOL = 2e-3
+
+
+def _build(variant="heterocache", delay=1, bandwidth=1 << 30, B=2, NL=2, L=700, T=40,
+           chunk=256, host_pool=True, window=8, eval_every_step=False, shift=13, seed=3):
+    import torch
+
+    from paper_2601_13684_b200.decoder import HeteroCacheDecoder
+    from paper_2601_13684_b200.engine import EngineConfig
+    from paper_2601_13684_b200.workload import ModelShape, SyntheticKV, plan_for, Workload
+
+    model = ModelShape("tiny-qwen", NL, 16, 4)
+    w = Workload("tiny", model, L, B, 0.10, T, 0, layers=NL)
+    tax, plan = plan_for(w)
+    cfg = EngineConfig(tau_drift=0.5, window=window, update_delay_steps=delay,
+                       transfer_bandwidth=bandwidth, variant=variant,
+                       eval_every_step=eval_every_step)
+    dec = HeteroCacheDecoder(tax, plan, cfg, batch=B, group=model.group, max_decode=T,
+                             chunk=chunk, host_pool=host_pool)
+    gen = SyntheticKV(model, batch=B, prefill_len=L, num_layers=NL, hot=plan.l_base_int,
+                      seed=seed)
+    dump = torch.zeros(NL, B * model.kv_heads, L, device="cuda")
+    dec.lib.hc_engine_set_prefill_dump(dec.handle, dump.data_ptr())
+    kv = []
+    for l in range(NL):
+        k, v, q = gen.layer_kv(l)
+        dec.prefill_layer(l, k, v, q)
+        kv.append((k, v, q))
+    torch.cuda.synchronize()
+    dec.finish_prefill()
+    return dict(dec=dec, gen=gen, kv=kv, dump=dump.cpu().numpy(), tax=tax, plan=plan, cfg=cfg,
+                model=model, B=B, NL=NL, L=L, T=T, shift=shift)
+
+
+def _run(ctx, check_steps=()):
+    import torch
+
+    dec, gen = ctx["dec"], ctx["gen"]
+    B, NL, L, T, H = ctx["B"], ctx["NL"], ctx["L"], ctx["T"], ctx["model"].kv_heads
+    G = ctx["model"].group
+    rows = {}  # (b, pivot, t) -> row
+    outs, news = {}, []
+    dyn_seen = {}
+    for t in range(1, T + 1):
+        q, kn, vn = gen.step_inputs(t, ctx["shift"])
+        o = torch.empty_like(q)
+        dec.decode_step(t, q, kn, vn, o)
+        news.append((q, kn, vn))
+        for b in range(B if dec.monitor else 0):
+            for p in dec.pivots:
+                buf = torch.empty(L + t, device="cuda")
+                dec.pivot_row(b, p, t, buf)
+                rows[(b, p, t)] = buf
+        if t in check_steps:
+            outs[t] = o.clone()
+            dyn_seen[t] = {(b, hd): dec.dynamic_set(b, hd) for b in range(B) for hd in dec.comp}
+    torch.cuda.synchronize()
+    rows = {k: v.cpu().numpy() for k, v in rows.items()}
+    return rows, outs, news, dyn_seen
+
+
+def _oracle_replay(ctx, rows, b):
+    dec, L, T, NL = ctx["dec"], ctx["L"], ctx["T"], ctx["NL"]
+    H = ctx["model"].kv_heads
+    K = L + T
+    idx = np.full((T + 1, NL, H, K), O.PAD_INDEX, dtype=np.uint32)
+    sc = np.zeros((T + 1, NL, H, K), dtype=np.float32)
+    for l in range(NL):
+        for h in range(H):
+            idx[0, l, h, :L] = np.arange(L)
+            sc[0, l, h, :L] = ctx["dump"][l, b * H + h]
+    for t in range(1, T + 1):
+        for p in dec.pivots:
+            idx[t, p[0], p[1], :L + t] = np.arange(L + t)
+            sc[t, p[0], p[1], :L + t] = rows[(b, p, t)]
+    roles = {hd: pr.role for hd, pr in ctx["tax"].heads.items()}
+    clusters = [(c.pivot, tuple(c.satellites)) for c in ctx["tax"].clusters]
+    cfg = ctx["cfg"]
+    return O.replay(idx, sc, prefill_len=L, bytes_per_kv_entry=512, roles=roles,
+                    clusters=clusters, lengths=dict(ctx["plan"].lengths),
+                    l_base_int=ctx["plan"].l_base_int, tau_drift=cfg.tau_drift,
+                    window=cfg.window, transfer_bandwidth=cfg.transfer_bandwidth,
+                    update_delay_steps=cfg.update_delay_steps, sink_count=cfg.sink_count,
+                    recency_window=cfg.recency_window, variant=cfg.variant,
+                    eval_every_step=cfg.eval_every_step, measure=False, record_dynamic=True)
+
+
+def _check_events(ctx, rows):
+    dec = ctx["dec"]
+    fired = 0
+    for b in range(ctx["B"]):
+        ref = _oracle_replay(ctx, rows, b)
+        got = [dict(trigger_step=e.trigger_step, pivot=e.pivot, completion_step=e.completion_step,
+                    transfer_bytes=e.transfer_bytes, fetches=e.fetches)
+               for e in dec.states[b].events]
+        assert got == ref["events"], f"sequence {b}: event log differs from the oracle"
+        fired += len(got)
+        st_rows = dec.states[b].rows
+        assert len(st_rows) == len(ref["rows"])
+        for g, e in zip(st_rows, ref["rows"]):
+            assert (g.step, g.gpu_entries, g.extra_entries, g.bytes_in_flight, g.cumulative_bytes,
+                    g.retrieval_flag) == (e["step"], e["gpu_entries"], e["extra_entries"],
+                                          e["bytes_in_flight"], e["cumulative_bytes"],
+                                          e["retrieval_flag"]), (b, g.step)
+        for hd in dec.comp:
+            assert set(dec.dynamic_set(b, hd).tolist()) == set(ref["dynamic"][hd]), (b, hd)
+    return fired
+
+
+def _unit_kv(ctx, news, b, l, h, t):
+    """Position-indexed K/V [L+t, D] of one unit (prefill + decode appends)."""
+    import torch
+
+    k, v, _ = ctx["kv"][l]
+    ks = [k[b, h].float().cpu()] + [news[s][1][b, l, h][None].float().cpu() for s in range(t)]
+    vs = [v[b, h].float().cpu()] + [news[s][2][b, l, h][None].float().cpu() for s in range(t)]
+    return torch.cat(ks), torch.cat(vs)
+
+
+def test_decoder_events_rows_and_outputs_match_oracle():
+    ctx = _build()
+    rows, outs, news, dyn_seen = _run(ctx, check_steps=(1, 7, 16, 26, 40))
+    fired = _check_events(ctx, rows)
+    assert fired >= 1, "planted topic shift must trigger a retrieval"
+    dec, L, H, G = ctx["dec"], ctx["L"], ctx["model"].kv_heads, ctx["model"].group
+    cfg = ctx["cfg"]
+    worst = 0.0
+    for b in range(ctx["B"]):
+        ref = _oracle_replay(ctx, rows, b)
+        for t, o in outs.items():
+            dyn_t = ref["dynamic_trace"][t]
+            for l in range(ctx["NL"]):
+                for h in range(H):
+                    hd = (l, h)
+                    base = None if hd in dec.full else dyn_t[hd]
+                    if base is not None:
+                        assert set(dyn_seen[t][(b, hd)].tolist()) == set(base), (t, b, hd)
+                    res = sorted(O.resident_positions(L, t, base, cfg.sink_count,
+                                                      cfg.recency_window))
+                    kk, vv = _unit_kv(ctx, news, b, l, h, t)
+                    q = news[t - 1][0][b, l, h * G:(h + 1) * G].float().cpu()
+                    o_ref, p = unit_attention(q, kk, vv, res)
+                    got = o[b, l, h * G:(h + 1) * G].float().cpu()
+                    err = (got - o_ref).abs()
+                    assert bool((err <= O_ATOL + O_RTOL * o_ref.abs()).all()), \
+                        (t, b, hd, float(err.max()))
+                    worst = max(worst, float(err.max()))
+                    if hd in dec.pivots:  # score row vs fp32 oracle
+                        row_ref = gqa_mean_row(p).numpy()
+                        row = rows[(b, hd, t)]
+                        assert np.allclose(row, row_ref, atol=ROW_ATOL, rtol=ROW_RTOL), (t, b, hd)
+    print(f"max |O - O_ref| = {worst:.3e}")
+
+
+def test_prefill_rows_match_oracle():
+    ctx = _build(T=4)
+    L, H, G = ctx["L"], ctx["model"].kv_heads, ctx["model"].group
+    for l in range(ctx["NL"]):
+        k, v, q = ctx["kv"][l]
+        for b in range(ctx["B"]):
+            for h in range(H):
+                _, p = unit_attention(q[b, h * G:(h + 1) * G].float().cpu(),
+                                      k[b, h].float().cpu(), v[b, h].float().cpu())
+                assert np.allclose(ctx["dump"][l, b * H + h], gqa_mean_row(p).numpy(),
+                                   atol=ROW_ATOL, rtol=ROW_RTOL)
+
+
+@pytest.mark.parametrize("kw", [
+    dict(delay=3), dict(bandwidth=20000, delay=2), dict(variant="no_allocation"),
+    dict(eval_every_step=True), dict(window=4, shift=9), dict(host_pool=False),
+])
+def test_decoder_variants_match_oracle(kw):
+    ctx = _build(**kw)
+    rows, _, _, _ = _run(ctx)
+    _check_events(ctx, rows)
+
+
+def test_no_retrieval_never_fires():
+    ctx = _build(variant="no_retrieval")
+    rows, outs, news, _ = _run(ctx, check_steps=(20,))
+    for st in ctx["dec"].states:
+        assert st.events == [] and all(r.retrieval_flag == 0 for r in st.rows)
+
+
+def test_resident_rows_match_cache_view_sizes():
+    ctx = _build(T=12)
+    dec = ctx["dec"]
+    rows, _, _, _ = _run(ctx)
+    got = dec.resident_rows(12)
+    want = 0
+    cfg = ctx["cfg"]
+    for b in range(ctx["B"]):
+        for hd in dec.taxonomy.heads:
+            base = None if hd in dec.full else dec.dynamic_set(b, hd).tolist()
+            want += len(O.resident_positions(ctx["L"], 12, base, cfg.sink_count,
+                                             cfg.recency_window))
+    assert got == want
