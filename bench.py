@@ -1,0 +1,409 @@
+#!/usr/bin/env python
+"""HeteroCache-B200 decode hot-path benchmark (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--workload cfg3]
+
+A "step" is one decode step of the workload's whole batch through the
+reference-facing API (HeteroCacheDecoder.decode_step, the tensor-mode
+CacheEngine.decode_step): append the token's K/V, fused ragged attention for
+every head of every layer over its resident set, pivot score rows, K1
+top-l_base + K2 overlap, and -- at window boundaries -- the drift test, fetch
+selection and host-pool retrieval on the side stream.
+
+N=1 default workload is cfg3 (Qwen2.5-7B-shaped, 128K context, batch 4, 5%
+compressed-head budget): the largest BASELINE.json config whose satellite
+host pool (15 GB pinned) and resident cache fit one B200 box comfortably.
+For N>1 (torchrun, one rank per GPU) every rank runs its own batch of the
+same workload (weak scaling, no data-path collective: sequences are
+independent); value = all ranks' steps / max-over-ranks time.
+
+--impl reference times the reference algorithm's CPU restatement (the
+oracle port: fp32 attention over the same resident sets + the reference
+selection / drift path) on the host cores, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "decode attn steps/sec & HBM GB/s @128K/224K ctx, 1/2/4/8 B200 vs host-CPU ref"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
+    ap.add_argument("--workload", default="cfg3")
+    ap.add_argument("--layers", type=int, default=0, help="override layer count (debug)")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--chunk", type=int, default=1024)
+    ap.add_argument("--link-mib-per-step", type=float, default=64.0,
+                    help="EngineConfig.transfer_bandwidth in MiB per decode step (host link model)")
+    return ap.parse_args()
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)", d
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)", {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.out = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=self.out, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.2)
+        self.proc.terminate()
+        self.proc.wait()
+        self.out.flush()
+        lines = [l.split(",") for l in Path(self.out.name).read_text().splitlines() if l.strip()]
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for f in lines:
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+                for n, v in zip(names, f[4:8]):
+                    if v.strip().lower() == "active":
+                        reasons.add(n)
+            except (ValueError, IndexError):
+                continue
+        sm.sort()
+        med = sm[len(sm) // 2] if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+
+def run_b200(args, rank, world):
+    import torch
+
+    from paper_2601_13684_b200 import _lib
+    from paper_2601_13684_b200.decoder import HeteroCacheDecoder
+    from paper_2601_13684_b200.engine import EngineConfig
+    from paper_2601_13684_b200.workload import CONFIGS, SyntheticKV, algorithmic_bytes, plan_for
+
+    w = CONFIGS[args.workload]
+    if args.layers:
+        from dataclasses import replace
+        w = replace(w, layers=args.layers)
+    m = w.model
+    tax, plan = plan_for(w)
+    K, W = args.steps, args.warmup
+    period = 100  # planted topic shift every `period` steps keeps retrieval in the timed region
+    cfg = EngineConfig(tau_drift=0.5, window=8, update_delay_steps=1,
+                       transfer_bandwidth=int(args.link_mib_per_step * (1 << 20)))
+    T = W + 2 * K + 8
+    lib = _lib.load()
+    dec = HeteroCacheDecoder(tax, plan, cfg, batch=w.batch, group=m.group, max_decode=T,
+                             chunk=args.chunk, host_pool=True, track_sets=False)
+    gen = SyntheticKV(m, batch=w.batch, prefill_len=w.prefill_len, num_layers=w.num_layers,
+                      hot=plan.l_base_int, seed=20261018 + 3 + rank)
+    t0 = time.time()
+    for l in range(w.num_layers):
+        k, v, q = gen.layer_kv(l)
+        dec.prefill_layer(l, k, v, q)
+        del k, v, q
+    torch.cuda.synchronize()
+    dec.finish_prefill()
+    prefill_s = time.time() - t0
+    # step inputs: 2 topics x 4 variants, cycled; topic flips every `period` steps
+    pool = {ph: [gen.step_inputs(100 + 10 * ph + i, 0 if ph else None) for i in range(4)]
+            for ph in (0, 1)}
+
+    def inputs(t):
+        return pool[(t // period) % 2][t % 4]
+
+    out = torch.empty_like(pool[0][0][0])
+    stream = torch.cuda.current_stream()
+    t = 0
+    for _ in range(W):
+        t += 1
+        q, kn, vn = inputs(t)
+        dec.decode_step(t, q, kn, vn, out, rows=False)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    # ---- timed: device-resident inputs ----
+    rows_first = dec.resident_rows(t + 1)
+    clocks = ClockSampler(torch.cuda.current_device())
+    clocks.start()
+    launches0 = lib.hc_launch_count()
+    dec.kernel_timing(True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    torch.cuda.nvtx.range_push("timed")
+    ev0.record(stream)
+    for _ in range(K):
+        t += 1
+        q, kn, vn = inputs(t)
+        dec.decode_step(t, q, kn, vn, out, rows=False)
+    ev1.record(stream)
+    torch.cuda.nvtx.range_pop()
+    torch.cuda.synchronize()
+    barrier()
+    ms = ev0.elapsed_time(ev1)
+    launches = lib.hc_launch_count() - launches0
+    phases = dec.kernel_timing(False)
+    attn_ms, attn_n = phases["attention"], phases["steps"]
+    clk = clocks.stop()
+    rows_last = dec.resident_rows(t)
+    events = sum(len(s.raw_events) for s in dec.states)
+
+    # ---- timed: end to end through the API with pinned host buffers ----
+    hq = [[x.cpu().pin_memory() for x in pool[ph][i]] for ph in (0, 1) for i in range(4)]
+    hout = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
+    dq, dkn, dvn = (torch.empty_like(x) for x in pool[0][0])
+    h2d = sum(x.numel() * x.element_size() for x in hq[0])
+    d2h = hout.numel() * hout.element_size()
+    barrier()
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for _ in range(K):
+        t += 1
+        src = hq[((t // period) % 2) * 4 + t % 4]
+        dq.copy_(src[0], non_blocking=True)
+        dkn.copy_(src[1], non_blocking=True)
+        dvn.copy_(src[2], non_blocking=True)
+        dec.decode_step(t, dq, dkn, dvn, out, rows=False)
+        hout.copy_(out, non_blocking=True)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms_e2e = ev0.elapsed_time(ev1)
+
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([ms, ms_e2e], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms, ms_e2e = tt.tolist()
+
+    rows_avg = (rows_first + rows_last) / 2.0
+    step_bytes = algorithmic_bytes(int(rows_avg), w.batch, w.num_layers, m.q_heads)
+    attn_bytes = rows_avg * 2 * m.head_dim * 2 + w.batch * w.num_layers * m.q_heads * m.head_dim * 2 * 2
+    attn_avg_ms = attn_ms / max(1, attn_n)
+    peak, peak_src, _ = peaks()
+    achieved = attn_bytes / (attn_avg_ms * 1e-3) / 1e9
+    traffic = None
+    tf = ROOT / "profiles" / f"traffic_{args.workload}.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get("dram_bytes_per_launch")
+    res = {
+        "metric": METRIC,
+        "value": world * K / (ms * 1e-3),
+        "unit": "steps/s",
+        "n_gpus": world,
+        "steps": K,
+        "warmup": W,
+        "ms_per_step": ms / K,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic: seeded bf16 K/V/Q with planted per-cluster hot sets and topic shifts",
+        "config": {
+            "workload": f"{args.workload}: {w.name} ({m.name}-shaped, {w.num_layers} layers, "
+                        f"{m.q_heads}q/{m.kv_heads}kv, d={m.head_dim})",
+            "prefill_len": w.prefill_len, "batch_per_gpu": w.batch, "layers": w.num_layers,
+            "compression": w.compression, "rho": plan.rho, "l_base_int": plan.l_base_int,
+            "roles_per_layer": list(m.layer_roles()),
+            "decode_window": cfg.window, "tau_drift": cfg.tau_drift,
+            "topic_shift_every_steps": period, "split_k_chunk": args.chunk,
+            "transfer_bandwidth_bytes_per_step": cfg.transfer_bandwidth,
+            "l2": f"inputs larger than L2: {step_bytes / 1e9:.2f} GB of resident K/V read per step",
+            "parallelism": f"replicas x{world} (weak: each GPU decodes its own batch)",
+        },
+        "hbm_gbs_step": step_bytes / (ms / K * 1e-3) / 1e9,
+        "algorithmic_bytes_per_step": int(step_bytes),
+        "e2e": {"value": world * K / (ms_e2e * 1e-3), "unit": "steps/s",
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "kernel": "attn_tiles_kernel (K4)",
+                     "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "peak_source": peak_src,
+                     "traffic": traffic,
+                     "bytes_per_launch": int(attn_bytes), "avg_launch_ms": attn_avg_ms,
+                     "launches_timed": attn_n},
+        "clocks": clk,
+        "phase_ms_per_step": {k: v / max(1, attn_n) for k, v in phases.items() if k != "steps"},
+        "retrieval_events_timed_run": events,
+        "prefill_seconds": prefill_s,
+        "device_bytes": dec.device_bytes, "pinned_host_bytes": dec.host_bytes,
+    }
+    dec.close()
+    return res, w
+
+
+# ---------------------------------------------------------------------------
+# CPU arm (oracle port): same resident sets, fp32 attention + reference selection
+# ---------------------------------------------------------------------------
+
+
+def cpu_step_timer(w, plan, tax, sample_layers=1, sample_batch=1, seconds=12.0, max_steps=None,
+                   warmup=1):
+    """Time the CPU restatement of one decode step on a bounded sample of the
+    workload; returns (seconds per full-workload step, cores, sample text, steps)."""
+    import numpy as np
+    import torch
+
+    from oracle import hc_oracle as O
+    from oracle.attention_oracle import gqa_mean_row, unit_attention
+
+    cores = os.cpu_count() or 1
+    torch.set_num_threads(cores)
+    m = w.model
+    L, H, G, D = w.prefill_len, m.kv_heads, m.group, m.head_dim
+    g = torch.Generator().manual_seed(7)
+    roles = m.layer_roles()
+    units = []
+    for _ in range(sample_layers * sample_batch):
+        k = torch.randn(H, L + 4096, D, generator=g)
+        v = torch.randn(H, L + 4096, D, generator=g)
+        ql = torch.randn(H * G, D, generator=g)
+        res, kbase = {}, {}
+        for h, r in enumerate(roles):
+            if r in ("anchor", "satellite"):
+                _, p = unit_attention(ql[h * G:(h + 1) * G], k[h, :L], v[h, :L])
+                dyn = O.top_k_dense(gqa_mean_row(p).numpy(), plan.lengths[(0, h)])
+                res[h] = np.union1d(dyn, np.arange(min(4, L)))
+            elif r == "pivot":
+                _, p = unit_attention(ql[h * G:(h + 1) * G], k[h, :L], v[h, :L])
+                kbase[h] = O.top_k_dense(gqa_mean_row(p).numpy(), plan.l_base_int)
+        units.append((k, v, res, kbase))
+
+    def one_step(t):
+        for k, v, res, kbase in units:
+            q = torch.randn(H * G, D, generator=g)
+            for h, r in enumerate(roles):
+                qh = q[h * G:(h + 1) * G]
+                if h in res:
+                    pos = np.concatenate([res[h], np.arange(L, L + t)])
+                    unit_attention(qh, k[h], v[h], torch.from_numpy(pos.astype(np.int64)))
+                else:
+                    _, p = unit_attention(qh, k[h, :L + t], v[h, :L + t])
+                    if r == "pivot":
+                        top = O.top_k_dense(gqa_mean_row(p).numpy(), plan.l_base_int)
+                        np.intersect1d(top, kbase[h], assume_unique=True).size
+
+    for t in range(1, warmup + 1):
+        one_step(t)
+    n, t = 0, warmup
+    start = time.perf_counter()
+    while True:
+        t += 1
+        one_step(t)
+        n += 1
+        el = time.perf_counter() - start
+        if (max_steps is not None and n >= max_steps) or (max_steps is None and el >= seconds):
+            break
+    per_sample = el / n
+    scale = (w.num_layers / sample_layers) * (w.batch / sample_batch)
+    sample = (f"{sample_layers} of {w.num_layers} layers x {sample_batch} of {w.batch} sequences, "
+              f"{n} timed steps; per-step time scaled by {scale:g}")
+    return per_sample * scale, cores, sample, n
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        from paper_2601_13684_b200.workload import CONFIGS, plan_for
+
+        w = CONFIGS[args.workload]
+        tax, plan = plan_for(w)
+        per_step, cores, sample, n = cpu_step_timer(
+            w, plan, tax, max_steps=max(1, args.steps), warmup=max(0, min(args.warmup, 3)))
+        v = 1.0 / per_step
+        res = {
+            "impl": "reference", "metric": METRIC, "value": v, "unit": "steps/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": per_step * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
+            "config": {"workload": f"{args.workload}: {w.name}", "prefill_len": w.prefill_len,
+                       "batch": w.batch, "layers": w.num_layers},
+            "cpu_baseline": {"value": v, "unit": "steps/s", "cores": cores, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": v, "unit": "steps/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(res))
+        return 0
+
+    import torch
+
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    res, w = run_b200(args, rank, world)
+    if rank == 0:
+        if world == 1 and not args.no_cpu_baseline:
+            from paper_2601_13684_b200.workload import plan_for
+
+            tax, plan = plan_for(w)
+            per_step, cores, sample, _ = cpu_step_timer(w, plan, tax, seconds=args.cpu_seconds)
+            res["cpu_baseline"] = {"value": 1.0 / per_step, "unit": "steps/s", "cores": cores,
+                                   "kind": "port", "sample": sample}
+        else:
+            res["cpu_baseline"] = None
+        print(json.dumps(res))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -42,6 +42,8 @@ enum hc_status {
 
 const char* hc_version(void);
 const char* hc_last_error(void);
+/* Kernels launched by this library since load (bench evidence). */
+unsigned long long hc_launch_count(void);
 
 /* ---------------------------------------------------------------------------
  * K1 -- deterministic top-k selection.
@@ -181,9 +183,21 @@ int hc_engine_overlaps(hc_engine* eng, int32_t first, int32_t last, int32_t* out
 int hc_engine_fire(hc_engine* eng, int32_t pivot_unit, int32_t step, int32_t completion_step,
                    int32_t* transfer_ids, void* stream);
 
+/* The same for every pivot that fires at `step` (one K1 launch, one
+ * restamp, one batched gather), in the given order (the reference's sorted
+ * pivot order, engine.py:313).  transfer_ids receives one id per satellite
+ * (pivot order, then satellite head order); if fetched_host (pinned) is not
+ * NULL the fetched positions are copied there asynchronously, concatenated
+ * in the same order (valid after the caller's stream has synchronised). */
+int hc_engine_fire_batch(hc_engine* eng, int32_t n, const int32_t* pivot_units, int32_t step,
+                         const int32_t* completion_steps, int32_t* transfer_ids,
+                         uint32_t* fetched_host, void* stream);
+
 /* Landing of a due transfer (engine.py:293-299): the caller's stream waits
  * for the gather, then the satellite serves the new set from this step on. */
 int hc_engine_land(hc_engine* eng, int32_t transfer_id, void* stream);
+/* Land several due transfers in (completion, order) order with one launch. */
+int hc_engine_land_batch(hc_engine* eng, int32_t n, const int32_t* transfer_ids, void* stream);
 
 /* Read back index sets (sorted ascending) and sync:
  *   kind 0: fetched set of a transfer, 1: a compressed unit's current
@@ -204,6 +218,13 @@ int hc_engine_resident_rows(hc_engine* eng, int32_t step, int64_t* rows_out, voi
  * GQA-mean probability rows over [0, L) of all B*H units of the layer,
  * unit order b*H + h) to dst [NL][B*H][L] fp32 (device). */
 int hc_engine_set_prefill_dump(hc_engine* eng, float* dst_dev);
+
+/* Per-step phase timeline for the roofline, from CUDA events on the
+ * launching stream.  Reports (syncs) the summed milliseconds since the last
+ * call of phase_ms[7] = {append, K4 attention, combine, pivot score rows,
+ * K1/K2 monitor, overlap copy, whole step} and the number of steps, then
+ * resets and enables (enable != 0) or disables recording. */
+int hc_engine_timing(hc_engine* eng, int32_t enable, double* phase_ms, int32_t* steps);
 
 /* Number of attention tiles (CTAs) the step launches. */
 int hc_engine_active_tiles(const hc_engine* eng, int32_t step, int32_t* n_tiles);

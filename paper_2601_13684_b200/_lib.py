@@ -52,6 +52,7 @@ def _declare(lib):
     sig = {
         "hc_version": (C.c_char_p, []),
         "hc_last_error": (C.c_char_p, []),
+        "hc_launch_count": (C.c_ulonglong, []),
         "hc_topk_batched": (i32, [vp, i32, u32, vp]),
         "hc_select_topk": (i32, [vp, vp, u32, u32, vp, vp, vp]),
         "hc_bitmap_from_indices": (i32, [vp, u32, vp, vp, u32, vp]),
@@ -64,11 +65,14 @@ def _declare(lib):
         "hc_engine_overlaps": (i32, [vp, i32, i32, vp, vp]),
         "hc_engine_fire": (i32, [vp, i32, i32, i32, vp, vp]),
         "hc_engine_land": (i32, [vp, i32, vp]),
+        "hc_engine_fire_batch": (i32, [vp, i32, vp, i32, vp, vp, vp, vp]),
+        "hc_engine_land_batch": (i32, [vp, i32, vp, vp]),
         "hc_engine_read_indices": (i32, [vp, i32, i32, vp, i32, vp, vp]),
         "hc_engine_pivot_row": (i32, [vp, i32, i32, vp, vp]),
         "hc_engine_resident_rows": (i32, [vp, i32, vp, vp]),
         "hc_engine_set_prefill_dump": (i32, [vp, vp]),
         "hc_engine_active_tiles": (i32, [vp, i32, vp]),
+        "hc_engine_timing": (i32, [vp, i32, vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

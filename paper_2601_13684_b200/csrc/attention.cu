@@ -296,56 +296,104 @@ attn_tiles_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant
   }
 }
 
-// Merge a unit's split-K partials; write O (bf16) and, for pivots, (M, L).
+// Merge a unit's split-K partials for one query head (block = (unit, g));
+// write O (bf16) and, for pivots, (M, L).  Slots are reduced in parallel:
+// block max of M_i, per-slot weights 2^(M_i - M) in shared memory, then each
+// thread d accumulates sum_i w_i O_i[d] with coalesced 512 B slot reads.
 __global__ void __launch_bounds__(128) combine_kernel(const AttnParams p) {
+  constexpr int kMaxSlots = 1024;
+  __shared__ float w[kMaxSlots];
+  __shared__ float red[4];
   const UnitDesc u = p.units[blockIdx.x];
-  const int n = unit_slots(u, p.t, p.L, p.chunk);
-  const int d = threadIdx.x;
+  const int g = blockIdx.y;
   const int G = p.group;
-  for (int g = 0; g < G; ++g) {
-    float M = -INFINITY;
-    for (int i = 0; i < n; ++i)
-      M = fmaxf(M, p.partial[(size_t(u.slot0 + i) * G + g) * kPartStride]);
-    const float mb = (M == -INFINITY) ? 0.f : M;
-    float Ls = 0.f, acc = 0.f;
-    for (int i = 0; i < n; ++i) {
-      const float* src = p.partial + (size_t(u.slot0 + i) * G + g) * kPartStride;
+  const int n = unit_slots(u, p.t, p.L, p.chunk);
+  const int d = threadIdx.x, lane = d & 31, wid = d >> 5;
+  const float* base = p.partial + (size_t(u.slot0) * G + g) * kPartStride;
+  const size_t sstride = size_t(G) * kPartStride;
+  float m = -INFINITY;
+  for (int i = d; i < n; i += 128) m = fmaxf(m, base[i * sstride]);
+  for (int off = 16; off; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+  if (lane == 0) red[wid] = m;
+  __syncthreads();
+  const float M = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
+  const float mb = (M == -INFINITY) ? 0.f : M;
+  __syncthreads();
+  float Ls = 0.f, acc = 0.f;
+  for (int c0 = 0; c0 < n; c0 += kMaxSlots) {
+    const int cn = min(kMaxSlots, n - c0);
+    for (int i = d; i < cn; i += 128) {
+      const float* src = base + (c0 + i) * sstride;
       const float li = src[1];
-      if (li == 0.f) continue;  // empty tile: O slot never written
-      const float f = exp2f(src[0] - mb);
+      const float f = li == 0.f ? 0.f : exp2f(src[0] - mb);  // empty tile: O never written
+      w[i] = f;
       Ls += li * f;
-      acc += src[4 + d] * f;
     }
-    __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.out);
-    if (out) out[(size_t(u.q_row) + g) * kHeadDim + d] = __float2bfloat16_rn(acc / Ls);
-    if (u.pivot_slot >= 0 && d == 0) {
-      p.stats[(size_t(u.pivot_slot) * G + g) * 2 + 0] = M;
-      p.stats[(size_t(u.pivot_slot) * G + g) * 2 + 1] = Ls;
+    __syncthreads();
+    int i = 0;
+    for (; i + 4 <= cn; i += 4) {
+      const float* src = base + (c0 + i) * sstride + 4 + d;
+      const float o0 = w[i] != 0.f ? src[0] : 0.f;
+      const float o1 = w[i + 1] != 0.f ? src[sstride] : 0.f;
+      const float o2 = w[i + 2] != 0.f ? src[2 * sstride] : 0.f;
+      const float o3 = w[i + 3] != 0.f ? src[3 * sstride] : 0.f;
+      acc += w[i] * o0 + w[i + 1] * o1 + w[i + 2] * o2 + w[i + 3] * o3;
     }
+    for (; i < cn; ++i) {
+      const float o = w[i] != 0.f ? base[(c0 + i) * sstride + 4 + d] : 0.f;
+      acc += w[i] * o;
+    }
+    __syncthreads();
+  }
+  for (int off = 16; off; off >>= 1) Ls += __shfl_xor_sync(0xffffffffu, Ls, off);
+  if (lane == 0) red[wid] = Ls;
+  __syncthreads();
+  Ls = (red[0] + red[1]) + (red[2] + red[3]);
+  __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.out);
+  if (out) out[(size_t(u.q_row) + g) * kHeadDim + d] = __float2bfloat16_rn(acc / Ls);
+  if (u.pivot_slot >= 0 && d == 0) {
+    p.stats[(size_t(u.pivot_slot) * G + g) * 2 + 0] = M;
+    p.stats[(size_t(u.pivot_slot) * G + g) * 2 + 1] = Ls;
   }
 }
 
 // GQA-mean probability row of every pivot over [0, L + t):
 //   row[pos] = (sum_j exp(s_j - M_j) * (1 / L_j)) / G   (model.ts:283-289 order)
-__global__ void score_rows_kernel(const AttnParams p, const int32_t* __restrict__ pivot_units,
-                                  int n_pivots) {
-  const int pv = blockIdx.y;
-  if (pv >= n_pivots) return;
-  const UnitDesc u = p.units[pivot_units[pv]];
+// 4 consecutive positions per thread (16 B loads of every head's logits).
+template <int G>
+__global__ void __launch_bounds__(256) score_rows_kernel(const AttnParams p,
+                                                         const int32_t* __restrict__ pivot_units) {
+  const UnitDesc u = p.units[pivot_units[blockIdx.y]];
   const int slot = u.pivot_slot;
   const int len = p.L + p.t;
-  const int G = p.group;
-  float Mj[8], inv[8];
+  float Mj[G], inv[G];
+#pragma unroll
   for (int j = 0; j < G; ++j) {
     Mj[j] = p.stats[(size_t(slot) * G + j) * 2 + 0];
     inv[j] = 1.0f / p.stats[(size_t(slot) * G + j) * 2 + 1];
   }
   float* row = p.rows + size_t(slot) * p.row_stride;
   const float* lg = p.logits + size_t(slot) * G * p.logit_stride;
-  for (int pos = blockIdx.x * blockDim.x + threadIdx.x; pos < len; pos += gridDim.x * blockDim.x) {
-    float acc = 0.f;
-    for (int j = 0; j < G; ++j) acc += exp2f(lg[size_t(j) * p.logit_stride + pos] - Mj[j]) * inv[j];
-    row[pos] = acc / float(G);
+  const int pos = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (pos >= len) return;
+  float4 x[G];
+#pragma unroll
+  for (int j = 0; j < G; ++j) x[j] = *reinterpret_cast<const float4*>(lg + size_t(j) * p.logit_stride + pos);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int j = 0; j < G; ++j) {
+    acc.x += exp2f(x[j].x - Mj[j]) * inv[j];
+    acc.y += exp2f(x[j].y - Mj[j]) * inv[j];
+    acc.z += exp2f(x[j].z - Mj[j]) * inv[j];
+    acc.w += exp2f(x[j].w - Mj[j]) * inv[j];
+  }
+  const float rg = float(G);
+  acc = make_float4(acc.x / rg, acc.y / rg, acc.z / rg, acc.w / rg);
+  if (pos + 3 < len) {
+    *reinterpret_cast<float4*>(row + pos) = acc;
+  } else {
+    const float a[4] = {acc.x, acc.y, acc.z, acc.w};
+    for (int e = 0; pos + e < len; ++e) row[pos + e] = a[e];
   }
 }
 
@@ -385,7 +433,8 @@ int make_kv_tensor_map(CUtensorMap* map, const void* base, int64_t rows) {
 
 int launch_attention(const CUtensorMap& tmK, const CUtensorMap& tmV, const AttnParams& p,
                      int n_tiles, const int32_t* pivot_units_dev, int n_pivots,
-                     cudaStream_t st) {
+                     cudaStream_t st, const cudaEvent_t* ev) {
+  // ev (optional): events recorded before K4, after K4, after combine, after score rows
   static bool configured = false;
   if (!configured) {
     HC_CUDA_TRY(cudaFuncSetAttribute(attn_tiles_kernel,
@@ -393,20 +442,30 @@ int launch_attention(const CUtensorMap& tmK, const CUtensorMap& tmV, const AttnP
     configured = true;
   }
   HC_REQUIRE(p.group >= 1 && p.group <= 8, HC_EINVAL, "GQA group must be 1..8");
+  if (ev) HC_CUDA_TRY(cudaEventRecord(ev[0], st));
   if (n_tiles > 0) {
     attn_tiles_kernel<<<n_tiles, kThreadsAttn, kSmemAttn, st>>>(tmK, tmV, p);
     HC_CHECK_LAUNCH();
   }
+  if (ev) HC_CUDA_TRY(cudaEventRecord(ev[1], st));
   if (p.n_units > 0) {
-    combine_kernel<<<p.n_units, 128, 0, st>>>(p);
+    combine_kernel<<<dim3(p.n_units, p.group), 128, 0, st>>>(p);
     HC_CHECK_LAUNCH();
   }
+  if (ev) HC_CUDA_TRY(cudaEventRecord(ev[2], st));
   if (n_pivots > 0 && p.rows) {
+    HC_REQUIRE(p.logit_stride % 4 == 0 && p.row_stride % 4 == 0, HC_EINVAL,
+               "score-row strides must be multiples of 4");
     const int len = p.L + p.t;
-    dim3 grid((len + 1023) / 1024 < 64 ? (len + 1023) / 1024 : 64, n_pivots);
-    score_rows_kernel<<<grid, 1024, 0, st>>>(p, pivot_units_dev, n_pivots);
+    dim3 grid((len + 1023) / 1024, n_pivots);
+    switch (p.group) {
+#define HC_ROWS(GG) case GG: score_rows_kernel<GG><<<grid, 256, 0, st>>>(p, pivot_units_dev); break;
+      HC_ROWS(1) HC_ROWS(2) HC_ROWS(3) HC_ROWS(4) HC_ROWS(5) HC_ROWS(6) HC_ROWS(7) HC_ROWS(8)
+#undef HC_ROWS
+    }
     HC_CHECK_LAUNCH();
   }
+  if (ev) HC_CUDA_TRY(cudaEventRecord(ev[3], st));
   return HC_OK;
 }
 

@@ -15,8 +15,10 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstring>
 #include <deque>
 #include <new>
+#include <tuple>
 #include <vector>
 
 #include "hc_common.cuh"
@@ -26,7 +28,8 @@ namespace hc {
 
 int make_kv_tensor_map(CUtensorMap* map, const void* base, int64_t rows);
 int launch_attention(const CUtensorMap& tmK, const CUtensorMap& tmV, const AttnParams& p,
-                     int n_tiles, const int32_t* pivot_units_dev, int n_pivots, cudaStream_t st);
+                     int n_tiles, const int32_t* pivot_units_dev, int n_pivots, cudaStream_t st,
+                     const cudaEvent_t* ev = nullptr);
 int launch_topk(const hc_topk_job* jobs_dev, int n_jobs, uint32_t n_add, cudaStream_t st);
 
 namespace {
@@ -49,94 +52,6 @@ __global__ void append_kernel(const UnitDesc* __restrict__ units, int n_units, i
   else V[row * 16 + lane - 16] = v_new[size_t(u) * 16 + lane - 16];
 }
 
-// Prefix position list of a compressed unit, valid from step t_c:
-//   [tail-only positions asc][sinks U (sel & [S, L)) asc]
-// `sel` is a K1 dense selection (ascending).  meta = {n_prefix, tail_mask,
-// #selected positions >= L (those are served by the append segment)}.
-__global__ void build_positions_kernel(const uint32_t* __restrict__ sel,
-                                       const uint32_t* __restrict__ sel_count, int L, int S,
-                                       int R, int t_c, uint32_t* __restrict__ pos_out,
-                                       int32_t* __restrict__ meta) {
-  __shared__ int s_lo, s_hi, s_ntail;
-  __shared__ uint32_t s_mask;
-  const int k = int(*sel_count);
-  const int sinks = S < L ? S : L;
-  if (threadIdx.x == 0) {
-    int a = 0, b = k;
-    while (a < b) { const int m = (a + b) >> 1; if (int(sel[m]) < sinks) a = m + 1; else b = m; }
-    const int lo = a;
-    b = k;
-    while (a < b) { const int m = (a + b) >> 1; if (int(sel[m]) < L) a = m + 1; else b = m; }
-    const int hi = a;
-    int nt = 0;
-    uint32_t mask = 0;
-    int first = L + t_c - R;
-    if (first < sinks) first = sinks;
-    for (int p = first; p < L; ++p) {
-      int x = lo, y = hi;
-      while (x < y) { const int m = (x + y) >> 1; if (int(sel[m]) < p) x = m + 1; else y = m; }
-      if (!(x < hi && int(sel[x]) == p)) {
-        pos_out[nt++] = uint32_t(p);
-        mask |= 1u << (p - (L - R));
-      }
-    }
-    s_lo = lo;
-    s_hi = hi;
-    s_ntail = nt;
-    s_mask = mask;
-  }
-  __syncthreads();
-  const int nt = s_ntail, lo = s_lo, hi = s_hi;
-  for (int i = threadIdx.x; i < sinks; i += blockDim.x) pos_out[nt + i] = uint32_t(i);
-  for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) pos_out[nt + sinks + (i - lo)] = sel[i];
-  if (threadIdx.x == 0) {
-    meta[0] = nt + sinks + (hi - lo);
-    meta[1] = int32_t(s_mask);
-    meta[2] = k - hi;
-  }
-}
-
-// Copy rows pos[j] of a [positions x 128] K/V source (device memory or
-// mapped pinned host memory: zero-copy over the host link) into arena rows
-// dst_row + j.  One warp moves one 512 B row pair per iteration, 4 in flight.
-__global__ void gather_rows_kernel(const uint4* __restrict__ srcK, const uint4* __restrict__ srcV,
-                                   const uint32_t* __restrict__ pos,
-                                   const int32_t* __restrict__ meta, int64_t dst_row,
-                                   uint4* __restrict__ K, uint4* __restrict__ V) {
-  const int n = meta[0];
-  const int lane = threadIdx.x & 31;
-  const int warps = gridDim.x * (blockDim.x >> 5);
-  constexpr int kUnroll = 4;
-  for (int j0 = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * kUnroll; j0 < n;
-       j0 += warps * kUnroll) {
-    uint4 v[kUnroll];
-#pragma unroll
-    for (int q = 0; q < kUnroll; ++q) {
-      const int j = j0 + q;
-      if (j < n) {
-        const size_t p = pos[j];
-        v[q] = lane < 16 ? srcK[p * 16 + lane] : srcV[p * 16 + lane - 16];
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < kUnroll; ++q) {
-      const int j = j0 + q;
-      if (j < n) {
-        const int64_t r = dst_row + j;
-        if (lane < 16) K[r * 16 + lane] = v[q];
-        else V[r * 16 + lane - 16] = v[q];
-      }
-    }
-  }
-}
-
-__global__ void set_prefix_kernel(UnitDesc* units, int u, int64_t row0, const int32_t* meta) {
-  units[u].row0 = row0;
-  units[u].n_prefix = meta[0];
-  units[u].tail_mask = uint32_t(meta[1]);
-  units[u].pad_ = meta[2];
-}
-
 __global__ void iota_kernel(int32_t* p, int n) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) p[i] = i;
 }
@@ -152,8 +67,8 @@ struct Transfer {
   int32_t* meta = nullptr;  // [3]
   bool gathered = false;
   bool landed = false;
-  cudaEvent_t selected = nullptr;  // on the caller's stream after selection
-  cudaEvent_t done = nullptr;      // on the retrieval stream after the gather
+  cudaEvent_t selected = nullptr;  // caller's stream, after selection (shared per batch)
+  cudaEvent_t done = nullptr;      // retrieval stream, after the gather (shared per batch)
 };
 
 #define HC_TRY(x)                    \
@@ -218,7 +133,19 @@ struct EngineImpl {
   __nv_bfloat16* pool = nullptr;          // [n_sat][2][L][128]
   bool pool_host = true;
   std::vector<Transfer> xfers;
+  std::vector<cudaEvent_t> events;  // owned events (retrieval / landing ordering)
+  // pinned staging ring for small host->device descriptor uploads: keeps every
+  // cudaMemcpyAsync truly asynchronous (pageable sources may sync the stream)
+  char* stage = nullptr;
+  size_t stage_cap = 0, stage_head = 0;
+  std::deque<std::tuple<size_t, size_t, cudaEvent_t>> stage_busy;  // (lo, hi, copy done)
   cudaStream_t retr = nullptr;
+  // per-step phase timeline (bench roofline): 7 events per step on the
+  // launching stream: start | append | K4 | combine | score rows | K1 | end
+  static constexpr int kPhaseEvents = 7;
+  bool timing = false;
+  std::vector<cudaEvent_t> tev;
+  size_t tev_used = 0;  // steps recorded
   // prefill scratch
   float* prefill_dump = nullptr;
   char* pf = nullptr;
@@ -239,9 +166,10 @@ namespace {
 
 int engine_destroy(EngineImpl& e) {
   cudaDeviceSynchronize();
+  for (auto& pr : e.stage_busy) cudaEventDestroy(std::get<2>(pr));
+  if (e.stage) cudaFreeHost(e.stage);
+  for (auto ev : e.events) cudaEventDestroy(ev);
   for (auto& x : e.xfers) {
-    if (x.selected) cudaEventDestroy(x.selected);
-    if (x.done) cudaEventDestroy(x.done);
     if (x.sel) cudaFree(x.sel);
     if (x.cnt) cudaFree(x.cnt);
     if (x.pos) cudaFree(x.pos);
@@ -263,6 +191,7 @@ int engine_destroy(EngineImpl& e) {
     else cudaFree(e.pool);
   }
   if (e.retr) cudaStreamDestroy(e.retr);
+  for (auto x : e.tev) cudaEventDestroy(x);
   return HC_OK;
 }
 
@@ -311,7 +240,7 @@ int engine_create(EngineImpl& e, const hc_engine_desc& c, const int32_t* roles,
   e.pre_pos.assign(e.n_units, nullptr);
   e.pre_meta.assign(e.n_units, nullptr);
   e.fifo.assign(e.n_units, {});
-  e.row_len = int64_t(e.L) + e.T;
+  e.row_len = (int64_t(e.L) + e.T + 3) / 4 * 4;  // 16-B aligned logit / score-row stride
   e.words = int((e.row_len + 31) / 32);
 
   // ---- arena rows and the static tile table ----
@@ -443,6 +372,8 @@ int engine_create(EngineImpl& e, const hc_engine_desc& c, const int32_t* roles,
       HC_TRY(dalloc((void**)&e.pool, bytes, &e.dev_bytes));
     }
   }
+  e.stage_cap = size_t(8) << 20;
+  HC_CUDA_TRY(cudaHostAlloc((void**)&e.stage, e.stage_cap, cudaHostAllocDefault));
   int lo_prio = 0, hi_prio = 0;
   HC_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
   HC_CUDA_TRY(cudaStreamCreateWithPriority(&e.retr, cudaStreamNonBlocking, hi_prio));
@@ -475,18 +406,232 @@ int active_tiles(const EngineImpl& e, int t) {
   return int(std::upper_bound(e.t_act.begin(), e.t_act.end(), uint32_t(t)) - e.t_act.begin());
 }
 
-// Position list + gather of a compressed unit's prefix buffer `buf_row`.
-int build_prefix(EngineImpl& e, int u, const uint32_t* sel, const uint32_t* cnt, int t_c,
-                 uint32_t* pos, int32_t* meta, const __nv_bfloat16* srcK,
-                 const __nv_bfloat16* srcV, int64_t buf_row, cudaStream_t st) {
-  build_positions_kernel<<<1, 256, 0, st>>>(sel, cnt, e.L, e.S, e.R, t_c, pos, meta);
+int engine_decode_step(EngineImpl& e, int t, const void* q, const void* kn, const void* vn,
+                       void* o, cudaStream_t st) {
+  HC_REQUIRE(t >= 1 && t <= e.T, HC_EINVAL, "step %d outside 1..%d", t, e.T);
+  cudaEvent_t* ev = nullptr;
+  if (e.timing) {
+    const size_t need = (e.tev_used + 1) * EngineImpl::kPhaseEvents;
+    while (e.tev.size() < need) {
+      cudaEvent_t x;
+      HC_CUDA_TRY(cudaEventCreate(&x));
+      e.tev.push_back(x);
+    }
+    ev = e.tev.data() + e.tev_used * EngineImpl::kPhaseEvents;
+    ++e.tev_used;
+    HC_CUDA_TRY(cudaEventRecord(ev[0], st));
+  }
+  append_kernel<<<(e.n_units + 7) / 8, 256, 0, st>>>(
+      e.d_units, e.n_units, e.L, t, reinterpret_cast<const uint4*>(kn),
+      reinterpret_cast<const uint4*>(vn), reinterpret_cast<uint4*>(e.K),
+      reinterpret_cast<uint4*>(e.V));
   HC_CHECK_LAUNCH();
-  const int blocks = std::max(1, std::min(64, (e.cap[u] + 31) / 32));
-  gather_rows_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const uint4*>(srcK),
-                                             reinterpret_cast<const uint4*>(srcV), pos, meta,
-                                             buf_row, reinterpret_cast<uint4*>(e.K),
-                                             reinterpret_cast<uint4*>(e.V));
+  AttnParams p = decode_params(e, t, q, o);
+  HC_TRY(launch_attention(e.tmK, e.tmV, p, active_tiles(e, t), e.d_piv_units, e.n_piv, st,
+                          ev ? ev + 1 : nullptr));
+  if (e.n_piv) {
+    HC_TRY(launch_topk(e.d_piv_jobs, e.n_piv, uint32_t(t), st));
+    if (ev) HC_CUDA_TRY(cudaEventRecord(ev[5], st));
+    HC_CUDA_TRY(cudaMemcpyAsync(e.ovl_ring + size_t(t % kRing) * e.n_piv, e.ovl_cur,
+                                size_t(e.n_piv) * 4, cudaMemcpyDeviceToDevice, st));
+  } else if (ev) {
+    HC_CUDA_TRY(cudaEventRecord(ev[5], st));
+  }
+  if (ev) HC_CUDA_TRY(cudaEventRecord(ev[6], st));
+  return HC_OK;
+}
+
+// Stream-ordered upload of a small host array: copy into the pinned staging
+// ring, cudaMallocAsync a device buffer on `st` and copy asynchronously.  The
+// caller frees *dev with cudaFreeAsync on the same stream.
+int upload(EngineImpl& e, const void* src, size_t bytes, cudaStream_t st, void** dev) {
+  const size_t need = (bytes + 255) & ~size_t(255);
+  HC_REQUIRE(need <= e.stage_cap, HC_EINVAL, "descriptor upload of %zu B too large", bytes);
+  if (e.stage_head + need > e.stage_cap) e.stage_head = 0;  // wrap
+  const size_t lo = e.stage_head, hi = lo + need;
+  // a region may be rewritten only after the copy that read it has executed
+  for (auto it = e.stage_busy.begin(); it != e.stage_busy.end();) {
+    const bool overlap = std::get<0>(*it) < hi && lo < std::get<1>(*it);
+    if (overlap || e.stage_busy.size() > 256) {
+      HC_CUDA_TRY(cudaEventSynchronize(std::get<2>(*it)));
+      HC_CUDA_TRY(cudaEventDestroy(std::get<2>(*it)));
+      it = e.stage_busy.erase(it);
+    } else {
+      ++it;
+    }
+  }
+  std::memcpy(e.stage + lo, src, bytes);
+  HC_CUDA_TRY(cudaMallocAsync(dev, need, st));
+  HC_CUDA_TRY(cudaMemcpyAsync(*dev, e.stage + lo, bytes, cudaMemcpyHostToDevice, st));
+  cudaEvent_t ev;
+  HC_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  HC_CUDA_TRY(cudaEventRecord(ev, st));
+  e.stage_busy.emplace_back(lo, hi, ev);
+  e.stage_head = hi;
+  return HC_OK;
+}
+
+// Batched retrieval plumbing: one launch builds the prefix position lists of
+// many transfers, one launch gathers all their rows from the host pool.
+struct XferDev {
+  const uint32_t* sel;
+  const uint32_t* cnt;
+  uint32_t* pos;
+  int32_t* meta;
+  const uint4* srcK;
+  const uint4* srcV;
+  int64_t dst_row;
+  int32_t t_c;
+  int32_t pad_;
+};
+
+__global__ void build_positions_batch_kernel(const XferDev* __restrict__ xs, int L, int S, int R) {
+  const XferDev x = xs[blockIdx.x];
+  __shared__ int s_lo, s_hi, s_ntail;
+  __shared__ uint32_t s_mask;
+  const uint32_t* sel = x.sel;
+  const int k = int(*x.cnt);
+  const int sinks = S < L ? S : L;
+  if (threadIdx.x == 0) {
+    int a = 0, b = k;
+    while (a < b) { const int m = (a + b) >> 1; if (int(sel[m]) < sinks) a = m + 1; else b = m; }
+    const int lo = a;
+    b = k;
+    while (a < b) { const int m = (a + b) >> 1; if (int(sel[m]) < L) a = m + 1; else b = m; }
+    const int hi = a;
+    int nt = 0;
+    uint32_t mask = 0;
+    int first = L + x.t_c - R;
+    if (first < sinks) first = sinks;
+    for (int p = first; p < L; ++p) {
+      int u = lo, v = hi;
+      while (u < v) { const int m = (u + v) >> 1; if (int(sel[m]) < p) u = m + 1; else v = m; }
+      if (!(u < hi && int(sel[u]) == p)) {
+        x.pos[nt++] = uint32_t(p);
+        mask |= 1u << (p - (L - R));
+      }
+    }
+    s_lo = lo;
+    s_hi = hi;
+    s_ntail = nt;
+    s_mask = mask;
+  }
+  __syncthreads();
+  const int nt = s_ntail, lo = s_lo, hi = s_hi;
+  for (int i = threadIdx.x; i < sinks; i += blockDim.x) x.pos[nt + i] = uint32_t(i);
+  for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) x.pos[nt + sinks + (i - lo)] = sel[i];
+  if (threadIdx.x == 0) {
+    x.meta[0] = nt + sinks + (hi - lo);
+    x.meta[1] = int32_t(s_mask);
+    x.meta[2] = k - hi;
+  }
+}
+
+__global__ void gather_rows_batch_kernel(const XferDev* __restrict__ xs, uint4* __restrict__ K,
+                                         uint4* __restrict__ V) {
+  const XferDev x = xs[blockIdx.y];
+  const int n = x.meta[0];
+  const int lane = threadIdx.x & 31;
+  const int warps = gridDim.x * (blockDim.x >> 5);
+  constexpr int kUnroll = 4;
+  for (int j0 = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * kUnroll; j0 < n;
+       j0 += warps * kUnroll) {
+    uint4 v[kUnroll];
+#pragma unroll
+    for (int q = 0; q < kUnroll; ++q) {
+      const int j = j0 + q;
+      if (j < n) {
+        const size_t p = x.pos[j];
+        v[q] = lane < 16 ? x.srcK[p * 16 + lane] : x.srcV[p * 16 + lane - 16];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kUnroll; ++q) {
+      const int j = j0 + q;
+      if (j < n) {
+        const int64_t r = x.dst_row + j;
+        if (lane < 16) K[r * 16 + lane] = v[q];
+        else V[r * 16 + lane - 16] = v[q];
+      }
+    }
+  }
+}
+
+struct LandDev {
+  int32_t unit;
+  int32_t pad_;
+  int64_t row0;
+  const int32_t* meta;
+};
+
+__global__ void set_prefix_batch_kernel(UnitDesc* units, const LandDev* __restrict__ ls, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const LandDev l = ls[i];
+  units[l.unit].row0 = l.row0;
+  units[l.unit].n_prefix = l.meta[0];
+  units[l.unit].tail_mask = uint32_t(l.meta[1]);
+  units[l.unit].pad_ = l.meta[2];
+}
+
+// K_base <- current top set for several pivots (one block per bitmap).
+__global__ void restamp_batch_kernel(uint32_t* kbase, const uint32_t* top_idx,
+                                     const uint32_t* top_cnt, const int32_t* slots, int words,
+                                     int lbase) {
+  const int s = slots[blockIdx.x];
+  uint32_t* bm = kbase + size_t(s) * words;
+  for (int w = threadIdx.x; w < words; w += blockDim.x) bm[w] = 0u;
+  __syncthreads();
+  const int c = min(int(top_cnt[s]), lbase);
+  const uint32_t* idx = top_idx + size_t(s) * lbase;
+  for (int i = threadIdx.x; i < c; i += blockDim.x) {
+    const uint32_t p = idx[i];
+    if (int(p >> 5) < words) atomicOr(bm + (p >> 5), 1u << (p & 31));
+  }
+}
+
+int new_event(EngineImpl& e, cudaEvent_t* out) {
+  cudaEvent_t ev;
+  HC_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  e.events.push_back(ev);
+  *out = ev;
+  return HC_OK;
+}
+
+// Issue the gathers of transfers `ids` (their units' staging buffers are free)
+// on the retrieval stream, after `after` (an event on the caller's stream).
+int issue_gathers(EngineImpl& e, const std::vector<int>& ids, cudaEvent_t after) {
+  if (ids.empty()) return HC_OK;
+  std::vector<XferDev> xd(ids.size());
+  int max_cap = 1;
+  for (size_t i = 0; i < ids.size(); ++i) {
+    Transfer& x = e.xfers[ids[i]];
+    const int u = x.unit;
+    x.buf = 1 - e.active[u];
+    const int ss = e.sat_slot[u];
+    const __nv_bfloat16* sk = e.pool + size_t(ss) * 2 * e.L * kHeadDim;
+    xd[i] = XferDev{x.sel, x.cnt, x.pos, x.meta, reinterpret_cast<const uint4*>(sk),
+                    reinterpret_cast<const uint4*>(sk + size_t(e.L) * kHeadDim),
+                    x.buf ? e.buf_row1[u] : e.buf_row0[u], x.completion, 0};
+    max_cap = std::max(max_cap, e.cap[u]);
+  }
+  HC_CUDA_TRY(cudaStreamWaitEvent(e.retr, after, 0));
+  XferDev* d = nullptr;
+  HC_TRY(upload(e, xd.data(), xd.size() * sizeof(XferDev), e.retr, (void**)&d));
+  build_positions_batch_kernel<<<int(xd.size()), 256, 0, e.retr>>>(d, e.L, e.S, e.R);
   HC_CHECK_LAUNCH();
+  const int per = std::max(1, std::min(16, (max_cap + 127) / 128));
+  gather_rows_batch_kernel<<<dim3(per, int(xd.size())), 256, 0, e.retr>>>(
+      d, reinterpret_cast<uint4*>(e.K), reinterpret_cast<uint4*>(e.V));
+  HC_CHECK_LAUNCH();
+  HC_CUDA_TRY(cudaFreeAsync(d, e.retr));
+  cudaEvent_t done;
+  HC_TRY(new_event(e, &done));
+  HC_CUDA_TRY(cudaEventRecord(done, e.retr));
+  for (int id : ids) {
+    e.xfers[id].done = done;
+    e.xfers[id].gathered = true;
+  }
   return HC_OK;
 }
 
@@ -495,15 +640,16 @@ int engine_prefill_layer(EngineImpl& e, int layer, const __nv_bfloat16* k,
   HC_REQUIRE(layer >= 0 && layer < e.NL, HC_EINVAL, "layer out of range");
   const int nu = e.B * e.H;  // units of this layer, i = b*H + h
   const int nch = (e.L + e.CH - 1) / e.CH;
+  const int64_t Lp = (int64_t(e.L) + 3) / 4 * 4;  // 16-B aligned row stride
   // scratch layout
   size_t off = 0;
   auto carve = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~size_t(255); return o; };
   const size_t o_units = carve(size_t(nu) * sizeof(UnitDesc));
   const size_t o_tiles = carve(size_t(nu) * nch * sizeof(TileDesc));
   const size_t o_part = carve(size_t(nu) * nch * e.G * kPartStride * 4);
-  const size_t o_logit = carve(size_t(nu) * e.G * e.L * 4);
+  const size_t o_logit = carve(size_t(nu) * e.G * Lp * 4);
   const size_t o_stats = carve(size_t(nu) * e.G * 2 * 4);
-  const size_t o_rows = carve(size_t(nu) * e.L * 4);
+  const size_t o_rows = carve(size_t(nu) * Lp * 4);
   const size_t o_iota = carve(size_t(nu) * 4);
   const size_t o_jobs = carve(size_t(nu) * sizeof(hc_topk_job));
   if (off > e.pf_bytes) {
@@ -552,8 +698,8 @@ int engine_prefill_layer(EngineImpl& e, int layer, const __nv_bfloat16* k,
   p.logits = reinterpret_cast<float*>(pf + o_logit);
   p.stats = reinterpret_cast<float*>(pf + o_stats);
   p.rows = reinterpret_cast<float*>(pf + o_rows);
-  p.logit_stride = e.L;
-  p.row_stride = e.L;
+  p.logit_stride = Lp;
+  p.row_stride = Lp;
   p.group = e.G;
   p.L = e.L;
   p.t = 0;
@@ -564,8 +710,9 @@ int engine_prefill_layer(EngineImpl& e, int layer, const __nv_bfloat16* k,
   HC_TRY(launch_attention(mk, mv, p, int(td.size()),
                           reinterpret_cast<int32_t*>(pf + o_iota), nu, st));
   if (e.prefill_dump)  // test hook: step-0 rows [NL][B*H][L]
-    HC_CUDA_TRY(cudaMemcpyAsync(e.prefill_dump + size_t(layer) * nu * e.L, p.rows,
-                                size_t(nu) * e.L * 4, cudaMemcpyDeviceToDevice, st));
+    HC_CUDA_TRY(cudaMemcpy2DAsync(e.prefill_dump + size_t(layer) * nu * e.L, size_t(e.L) * 4,
+                                  p.rows, size_t(Lp) * 4, size_t(e.L) * 4, nu,
+                                  cudaMemcpyDeviceToDevice, st));
 
   // K1: compressed heads select l_h (prefill_init, engine.py:265-268), pivots
   // select l_base for K_base (engine.py:269-271).
@@ -576,7 +723,7 @@ int engine_prefill_layer(EngineImpl& e, int layer, const __nv_bfloat16* k,
     const int u = (b * e.NL + layer) * e.H + h;
     const int r = e.role[layer * e.H + h];
     hc_topk_job j{};
-    j.scores = p.rows + size_t(i) * e.L;
+    j.scores = p.rows + size_t(i) * Lp;
     j.n = uint32_t(e.L);
     if (r == HC_ROLE_ANCHOR || r == HC_ROLE_SATELLITE) {
       j.k = uint32_t(e.length[layer * e.H + h]);
@@ -600,16 +747,21 @@ int engine_prefill_layer(EngineImpl& e, int layer, const __nv_bfloat16* k,
     HC_TRY(launch_topk(dj, int(jobs.size()), 0, st));
   }
   // K_base bitmaps for pivots
-  for (int u : job_unit) {
-    const int s = e.piv_slot[u];
-    if (s < 0) continue;
-    HC_REQUIRE(hc_bitmap_from_indices(e.kbase + size_t(s) * e.words, uint32_t(e.words),
-                                      e.top_idx + size_t(s) * e.lbase, e.top_cnt + s,
-                                      uint32_t(e.lbase), st) == HC_OK,
-               HC_ECUDA, "K_base bitmap failed");
+  std::vector<int32_t> pslots;
+  for (int u : job_unit)
+    if (e.piv_slot[u] >= 0) pslots.push_back(e.piv_slot[u]);
+  if (!pslots.empty()) {
+    int32_t* ds = nullptr;
+    HC_TRY(upload(e, pslots.data(), pslots.size() * 4, st, (void**)&ds));
+    restamp_batch_kernel<<<int(pslots.size()), 1024, 0, st>>>(e.kbase, e.top_idx, e.top_cnt, ds,
+                                                              e.words, e.lbase);
+    HC_CHECK_LAUNCH();
+    HC_CUDA_TRY(cudaFreeAsync(ds, st));
   }
-  // caches: full heads whole, compressed heads gathered, satellites to the host pool
+  // caches: full heads whole, compressed heads gathered (batched), satellites to the host pool
   const size_t rowb = size_t(kHeadDim) * 2;
+  std::vector<XferDev> xd;
+  std::vector<LandDev> lds;
   for (int i = 0; i < nu; ++i) {
     const int b = i / e.H, h = i % e.H;
     const int u = (b * e.NL + layer) * e.H + h;
@@ -623,10 +775,11 @@ int engine_prefill_layer(EngineImpl& e, int layer, const __nv_bfloat16* k,
                                   cudaMemcpyDeviceToDevice, st));
       continue;
     }
-    HC_TRY(build_prefix(e, u, e.dyn_sel[u], e.dyn_cnt[u], 1, e.pre_pos[u], e.pre_meta[u], sk, sv,
-                        e.buf_row0[u], st));
-    set_prefix_kernel<<<1, 1, 0, st>>>(e.d_units, u, e.buf_row0[u], e.pre_meta[u]);
-    HC_CHECK_LAUNCH();
+    // decode starts at step 1: the recency tail then covers [L+1-R, L)
+    xd.push_back(XferDev{e.dyn_sel[u], e.dyn_cnt[u], e.pre_pos[u], e.pre_meta[u],
+                         reinterpret_cast<const uint4*>(sk), reinterpret_cast<const uint4*>(sv),
+                         e.buf_row0[u], 1, 0});
+    lds.push_back(LandDev{u, 0, e.buf_row0[u], e.pre_meta[u]});
     e.active[u] = 0;
     const int ss = e.sat_slot[u];
     if (ss >= 0) {
@@ -637,137 +790,164 @@ int engine_prefill_layer(EngineImpl& e, int layer, const __nv_bfloat16* k,
       HC_CUDA_TRY(cudaMemcpyAsync(dv, sv, rowb * e.L, kind, st));
     }
   }
-  // prefill descriptors/jobs were uploaded from host vectors on `st`: make the
-  // uploads complete before those vectors go out of scope.
-  HC_CUDA_TRY(cudaStreamSynchronize(st));
-  return HC_OK;
-}
-
-int engine_decode_step(EngineImpl& e, int t, const void* q, const void* kn, const void* vn,
-                       void* o, cudaStream_t st) {
-  HC_REQUIRE(t >= 1 && t <= e.T, HC_EINVAL, "step %d outside 1..%d", t, e.T);
-  append_kernel<<<(e.n_units + 7) / 8, 256, 0, st>>>(
-      e.d_units, e.n_units, e.L, t, reinterpret_cast<const uint4*>(kn),
-      reinterpret_cast<const uint4*>(vn), reinterpret_cast<uint4*>(e.K),
-      reinterpret_cast<uint4*>(e.V));
-  HC_CHECK_LAUNCH();
-  AttnParams p = decode_params(e, t, q, o);
-  HC_TRY(launch_attention(e.tmK, e.tmV, p, active_tiles(e, t), e.d_piv_units, e.n_piv, st));
-  if (e.n_piv) {
-    HC_TRY(launch_topk(e.d_piv_jobs, e.n_piv, uint32_t(t), st));
-    HC_CUDA_TRY(cudaMemcpyAsync(e.ovl_ring + size_t(t % kRing) * e.n_piv, e.ovl_cur,
-                                size_t(e.n_piv) * 4, cudaMemcpyDeviceToDevice, st));
+  if (!xd.empty()) {
+    XferDev* dx = nullptr;
+    LandDev* dl = nullptr;
+    int max_cap = 1;
+    for (const auto& l : lds) max_cap = std::max(max_cap, e.cap[l.unit]);
+    HC_TRY(upload(e, xd.data(), xd.size() * sizeof(XferDev), st, (void**)&dx));
+    HC_TRY(upload(e, lds.data(), lds.size() * sizeof(LandDev), st, (void**)&dl));
+    build_positions_batch_kernel<<<int(xd.size()), 256, 0, st>>>(dx, e.L, e.S, e.R);
+    HC_CHECK_LAUNCH();
+    const int per = std::max(1, std::min(64, (max_cap + 127) / 128));
+    gather_rows_batch_kernel<<<dim3(per, int(xd.size())), 256, 0, st>>>(
+        dx, reinterpret_cast<uint4*>(e.K), reinterpret_cast<uint4*>(e.V));
+    HC_CHECK_LAUNCH();
+    set_prefix_batch_kernel<<<int((lds.size() + 127) / 128), 128, 0, st>>>(e.d_units, dl,
+                                                                           int(lds.size()));
+    HC_CHECK_LAUNCH();
+    HC_CUDA_TRY(cudaFreeAsync(dx, st));
+    HC_CUDA_TRY(cudaFreeAsync(dl, st));
   }
+  // (host vectors above were staged by cudaMemcpyAsync from pageable memory)
   return HC_OK;
 }
 
-int issue_gather(EngineImpl& e, int id) {
-  Transfer& x = e.xfers[id];
-  const int u = x.unit;
-  x.buf = 1 - e.active[u];
-  const int64_t dst = x.buf ? e.buf_row1[u] : e.buf_row0[u];
-  const int ss = e.sat_slot[u];
-  const __nv_bfloat16* sk = e.pool + size_t(ss) * 2 * e.L * kHeadDim;
-  const __nv_bfloat16* sv = sk + size_t(e.L) * kHeadDim;
-  HC_CUDA_TRY(cudaStreamWaitEvent(e.retr, x.selected, 0));
-  HC_TRY(build_prefix(e, u, x.sel, x.cnt, x.completion, x.pos, x.meta, sk, sv, dst, e.retr));
-  HC_CUDA_TRY(cudaEventRecord(x.done, e.retr));
-  x.gathered = true;
-  return HC_OK;
-}
-
-int engine_fire(EngineImpl& e, int pu, int t, int completion, int32_t* ids, cudaStream_t st) {
-  HC_REQUIRE(pu >= 0 && pu < e.n_units && e.piv_slot[pu] >= 0, HC_EINVAL, "unit %d is not a monitored pivot", pu);
-  const int s = e.piv_slot[pu];
-  const int LH = e.NL * e.H;
-  const int b = pu / LH, i = e.lh(pu), l = i / e.H, ph = i % e.H;
+int engine_fire_batch(EngineImpl& e, int n, const int32_t* pus, int t, const int32_t* completion,
+                      int32_t* ids, uint32_t* fetched_host, cudaStream_t st) {
   std::vector<hc_topk_job> jobs;
   std::vector<int> new_ids;
-  for (int h = 0; h < e.H; ++h) {
-    const int j = l * e.H + h;
-    if (e.role[j] != HC_ROLE_SATELLITE || e.cpivot[j] != ph) continue;
-    const int u = (b * e.NL + l) * e.H + h;
-    Transfer x;
-    x.unit = u;
-    x.k = e.length[j];
-    x.completion = completion;
-    HC_CUDA_TRY(cudaMallocAsync((void**)&x.sel, size_t(std::max(1, x.k)) * 4, st));
-    HC_CUDA_TRY(cudaMallocAsync((void**)&x.cnt, 4, st));
-    HC_CUDA_TRY(cudaMallocAsync((void**)&x.pos, size_t(std::max(1, e.cap[u])) * 4, st));
-    HC_CUDA_TRY(cudaMallocAsync((void**)&x.meta, 16, st));
-    HC_CUDA_TRY(cudaEventCreateWithFlags(&x.selected, cudaEventDisableTiming));
-    HC_CUDA_TRY(cudaEventCreateWithFlags(&x.done, cudaEventDisableTiming));
-    hc_topk_job jb{};
-    jb.scores = e.rowbuf + size_t(s) * e.row_len;
-    jb.n = uint32_t(e.L + t);
-    jb.k = uint32_t(x.k);
-    jb.out_idx = x.sel;
-    jb.out_count = x.cnt;
-    jobs.push_back(jb);
-    new_ids.push_back(int(e.xfers.size()));
-    e.xfers.push_back(x);
+  std::vector<int32_t> slots;
+  const int LH = e.NL * e.H;
+  for (int f = 0; f < n; ++f) {
+    const int pu = pus[f];
+    HC_REQUIRE(pu >= 0 && pu < e.n_units && e.piv_slot[pu] >= 0, HC_EINVAL,
+               "unit %d is not a monitored pivot", pu);
+    const int s = e.piv_slot[pu];
+    slots.push_back(s);
+    const int b = pu / LH, i = e.lh(pu), l = i / e.H, ph = i % e.H;
+    for (int h = 0; h < e.H; ++h) {
+      const int j = l * e.H + h;
+      if (e.role[j] != HC_ROLE_SATELLITE || e.cpivot[j] != ph) continue;
+      const int u = (b * e.NL + l) * e.H + h;
+      Transfer x;
+      x.unit = u;
+      x.k = std::min(e.length[j], e.L + t);
+      x.completion = completion[f];
+      HC_CUDA_TRY(cudaMallocAsync((void**)&x.sel, size_t(std::max(1, x.k)) * 4, st));
+      HC_CUDA_TRY(cudaMallocAsync((void**)&x.cnt, 4, st));
+      HC_CUDA_TRY(cudaMallocAsync((void**)&x.pos, size_t(std::max(1, e.cap[u])) * 4, st));
+      HC_CUDA_TRY(cudaMallocAsync((void**)&x.meta, 16, st));
+      hc_topk_job jb{};
+      jb.scores = e.rowbuf + size_t(s) * e.row_len;
+      jb.n = uint32_t(e.L + t);
+      jb.k = uint32_t(x.k);
+      jb.out_idx = x.sel;
+      jb.out_count = x.cnt;
+      jobs.push_back(jb);
+      new_ids.push_back(int(e.xfers.size()));
+      e.xfers.push_back(x);
+    }
   }
   if (!jobs.empty()) {
+    // pageable -> device copies are staged before cudaMemcpyAsync returns
     hc_topk_job* dj = nullptr;
-    HC_CUDA_TRY(cudaMallocAsync((void**)&dj, jobs.size() * sizeof(hc_topk_job), st));
-    HC_CUDA_TRY(cudaMemcpyAsync(dj, jobs.data(), jobs.size() * sizeof(hc_topk_job),
-                                cudaMemcpyHostToDevice, st));
+    HC_TRY(upload(e, jobs.data(), jobs.size() * sizeof(hc_topk_job), st, (void**)&dj));
     HC_TRY(launch_topk(dj, int(jobs.size()), 0, st));
     HC_CUDA_TRY(cudaFreeAsync(dj, st));
-    HC_CUDA_TRY(cudaStreamSynchronize(st));  // host job vector is about to go away
   }
-  // K_base <- current top set (engine.py:357)
-  HC_REQUIRE(hc_bitmap_from_indices(e.kbase + size_t(s) * e.words, uint32_t(e.words),
-                                    e.top_idx + size_t(s) * e.lbase, e.top_cnt + s,
-                                    uint32_t(e.lbase), st) == HC_OK,
-             HC_ECUDA, "K_base restamp failed");
-  for (size_t n = 0; n < new_ids.size(); ++n) {
-    Transfer& x = e.xfers[new_ids[n]];
-    HC_CUDA_TRY(cudaEventRecord(x.selected, st));
-    e.fifo[x.unit].push_back(new_ids[n]);
-    if (e.fifo[x.unit].size() == 1) HC_TRY(issue_gather(e, new_ids[n]));
-    ids[n] = new_ids[n];
+  if (n > 0) {  // K_base <- current top set (engine.py:357)
+    int32_t* ds = nullptr;
+    HC_TRY(upload(e, slots.data(), slots.size() * 4, st, (void**)&ds));
+    restamp_batch_kernel<<<n, 1024, 0, st>>>(e.kbase, e.top_idx, e.top_cnt, ds, e.words, e.lbase);
+    HC_CHECK_LAUNCH();
+    HC_CUDA_TRY(cudaFreeAsync(ds, st));
   }
-  return HC_OK;
+  size_t off = 0;
+  for (size_t q = 0; q < new_ids.size(); ++q) {
+    const Transfer& x = e.xfers[new_ids[q]];
+    if (fetched_host) {
+      HC_CUDA_TRY(cudaMemcpyAsync(fetched_host + off, x.sel, size_t(x.k) * 4,
+                                  cudaMemcpyDeviceToHost, st));
+    }
+    off += size_t(x.k);
+    ids[q] = new_ids[q];
+  }
+  cudaEvent_t selected;
+  HC_TRY(new_event(e, &selected));
+  HC_CUDA_TRY(cudaEventRecord(selected, st));
+  std::vector<int> now;
+  for (int id : new_ids) {
+    Transfer& x = e.xfers[id];
+    x.selected = selected;
+    e.fifo[x.unit].push_back(id);
+    if (e.fifo[x.unit].size() == 1) now.push_back(id);
+  }
+  return issue_gathers(e, now, selected);
 }
 
-int engine_land(EngineImpl& e, int id, cudaStream_t st) {
-  HC_REQUIRE(id >= 0 && id < int(e.xfers.size()), HC_EINVAL, "bad transfer id");
-  Transfer& x = e.xfers[id];
-  HC_REQUIRE(!x.landed, HC_ESTATE, "transfer %d already landed", id);
-  const int u = x.unit;
-  HC_REQUIRE(!e.fifo[u].empty() && e.fifo[u].front() == id, HC_ESTATE,
-             "transfer %d lands out of order", id);
-  if (!x.gathered) HC_TRY(issue_gather(e, id));
-  HC_CUDA_TRY(cudaStreamWaitEvent(st, x.done, 0));
-  const int64_t row0 = x.buf ? e.buf_row1[u] : e.buf_row0[u];
-  set_prefix_kernel<<<1, 1, 0, st>>>(e.d_units, u, row0, x.meta);
-  HC_CHECK_LAUNCH();
-  e.active[u] = x.buf;
-  // the transfer's buffers become the unit's dynamic-set / prefix records
-  if (e.dyn_owner[u] >= 0) {
-    Transfer& old = e.xfers[e.dyn_owner[u]];
-    HC_CUDA_TRY(cudaFreeAsync(old.sel, st));
-    HC_CUDA_TRY(cudaFreeAsync(old.cnt, st));
-    HC_CUDA_TRY(cudaFreeAsync(old.pos, st));
-    HC_CUDA_TRY(cudaFreeAsync(old.meta, st));
-    old.sel = nullptr;
-    old.cnt = nullptr;
-    old.pos = nullptr;
-    old.meta = nullptr;
+int engine_land_batch(EngineImpl& e, int n, const int32_t* ids, cudaStream_t st) {
+  std::vector<LandDev> lds;
+  std::vector<int> landed_units;
+  cudaEvent_t last_wait = nullptr;
+  auto flush = [&]() -> int {
+    if (lds.empty()) return HC_OK;
+    LandDev* d = nullptr;
+    HC_TRY(upload(e, lds.data(), lds.size() * sizeof(LandDev), st, (void**)&d));
+    set_prefix_batch_kernel<<<int((lds.size() + 127) / 128), 128, 0, st>>>(e.d_units, d,
+                                                                           int(lds.size()));
+    HC_CHECK_LAUNCH();
+    HC_CUDA_TRY(cudaFreeAsync(d, st));
+    lds.clear();
+    return HC_OK;
+  };
+  for (int q = 0; q < n; ++q) {
+    const int id = ids[q];
+    HC_REQUIRE(id >= 0 && id < int(e.xfers.size()), HC_EINVAL, "bad transfer id %d", id);
+    Transfer& x = e.xfers[id];
+    HC_REQUIRE(!x.landed, HC_ESTATE, "transfer %d already landed", id);
+    const int u = x.unit;
+    HC_REQUIRE(!e.fifo[u].empty() && e.fifo[u].front() == id, HC_ESTATE,
+               "transfer %d lands out of order", id);
+    if (!x.gathered) {
+      // its unit's staging buffer was busy with an earlier transfer that
+      // landed just before: apply pending descriptor updates, then gather
+      HC_TRY(flush());
+      cudaEvent_t ev;
+      HC_TRY(new_event(e, &ev));
+      HC_CUDA_TRY(cudaEventRecord(ev, st));
+      HC_TRY(issue_gathers(e, {id}, ev));
+    }
+    if (x.done != last_wait) {
+      HC_CUDA_TRY(cudaStreamWaitEvent(st, x.done, 0));
+      last_wait = x.done;
+    }
+    lds.push_back(LandDev{u, 0, x.buf ? e.buf_row1[u] : e.buf_row0[u], x.meta});
+    e.active[u] = x.buf;
+    if (e.dyn_owner[u] >= 0) {  // superseded records
+      Transfer& old = e.xfers[e.dyn_owner[u]];
+      for (void* ptr : {(void*)old.sel, (void*)old.cnt, (void*)old.pos, (void*)old.meta})
+        HC_CUDA_TRY(cudaFreeAsync(ptr, st));
+      old.sel = nullptr, old.cnt = nullptr, old.pos = nullptr, old.meta = nullptr;
+    }
+    e.dyn_owner[u] = id;
+    x.landed = true;
+    e.fifo[u].pop_front();
+    landed_units.push_back(u);
   }
-  e.dyn_owner[u] = id;
-  x.landed = true;
-  e.fifo[u].pop_front();
-  if (!e.fifo[u].empty()) {
-    // the next queued gather may only overwrite the old buffer once this
-    // stream no longer reads it: order it after the landing point
+  HC_TRY(flush());
+  // queued gathers may now overwrite the freed buffers: order them after this point
+  std::vector<int> next;
+  for (int u : landed_units)
+    if (!e.fifo[u].empty() && !e.xfers[e.fifo[u].front()].gathered) {
+      const int id = e.fifo[u].front();
+      if (std::find(next.begin(), next.end(), id) == next.end()) next.push_back(id);
+    }
+  if (!next.empty()) {
     cudaEvent_t ev;
-    HC_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    HC_TRY(new_event(e, &ev));
     HC_CUDA_TRY(cudaEventRecord(ev, st));
-    HC_CUDA_TRY(cudaStreamWaitEvent(e.retr, ev, 0));
-    HC_CUDA_TRY(cudaEventDestroy(ev));
-    HC_TRY(issue_gather(e, e.fifo[u].front()));
+    HC_TRY(issue_gathers(e, next, ev));
   }
   return HC_OK;
 }
@@ -853,13 +1033,28 @@ extern "C" int hc_engine_overlaps(hc_engine* eng, int32_t first, int32_t last, i
 extern "C" int hc_engine_fire(hc_engine* eng, int32_t pivot_unit, int32_t step,
                               int32_t completion_step, int32_t* transfer_ids, void* stream) {
   HC_REQUIRE(eng && transfer_ids, HC_EINVAL, "null argument");
-  return hc::engine_fire(eng->e, pivot_unit, step, completion_step, transfer_ids,
-                         (cudaStream_t)stream);
+  return hc::engine_fire_batch(eng->e, 1, &pivot_unit, step, &completion_step, transfer_ids,
+                               nullptr, (cudaStream_t)stream);
+}
+
+extern "C" int hc_engine_fire_batch(hc_engine* eng, int32_t n, const int32_t* pivot_units,
+                                    int32_t step, const int32_t* completion_steps,
+                                    int32_t* transfer_ids, uint32_t* fetched_host, void* stream) {
+  HC_REQUIRE(eng && (n == 0 || (pivot_units && completion_steps && transfer_ids)), HC_EINVAL,
+             "null argument");
+  return hc::engine_fire_batch(eng->e, n, pivot_units, step, completion_steps, transfer_ids,
+                               fetched_host, (cudaStream_t)stream);
 }
 
 extern "C" int hc_engine_land(hc_engine* eng, int32_t transfer_id, void* stream) {
   HC_REQUIRE(eng, HC_EINVAL, "null argument");
-  return hc::engine_land(eng->e, transfer_id, (cudaStream_t)stream);
+  return hc::engine_land_batch(eng->e, 1, &transfer_id, (cudaStream_t)stream);
+}
+
+extern "C" int hc_engine_land_batch(hc_engine* eng, int32_t n, const int32_t* transfer_ids,
+                                    void* stream) {
+  HC_REQUIRE(eng && (n == 0 || transfer_ids), HC_EINVAL, "null argument");
+  return hc::engine_land_batch(eng->e, n, transfer_ids, (cudaStream_t)stream);
 }
 
 extern "C" int hc_engine_read_indices(hc_engine* eng, int32_t kind, int32_t id, uint32_t* out,
@@ -941,5 +1136,31 @@ extern "C" int hc_engine_active_tiles(const hc_engine* eng, int32_t step, int32_
 extern "C" int hc_engine_set_prefill_dump(hc_engine* eng, float* dst_dev) {
   HC_REQUIRE(eng, HC_EINVAL, "null argument");
   eng->e.prefill_dump = dst_dev;
+  return HC_OK;
+}
+
+extern "C" int hc_engine_timing(hc_engine* eng, int32_t enable, double* phase_ms,
+                                int32_t* steps) {
+  HC_REQUIRE(eng, HC_EINVAL, "null argument");
+  auto& e = eng->e;
+  constexpr int P = hc::EngineImpl::kPhaseEvents;
+  if (phase_ms && steps) {
+    for (int k = 0; k < P; ++k) phase_ms[k] = 0;
+    for (size_t i = 0; i < e.tev_used; ++i) {
+      const cudaEvent_t* ev = e.tev.data() + i * P;
+      HC_CUDA_TRY(cudaEventSynchronize(ev[P - 1]));
+      for (int k = 1; k < P; ++k) {
+        float ms = 0;
+        HC_CUDA_TRY(cudaEventElapsedTime(&ms, ev[k - 1], ev[k]));
+        phase_ms[k - 1] += ms;
+      }
+      float tot = 0;
+      HC_CUDA_TRY(cudaEventElapsedTime(&tot, ev[0], ev[P - 1]));
+      phase_ms[P - 1] += tot;
+    }
+    *steps = int32_t(e.tev_used);
+  }
+  e.tev_used = 0;
+  e.timing = enable != 0;
   return HC_OK;
 }

@@ -26,8 +26,13 @@ void set_error(const char* fmt, ...);
     }                                                                          \
   } while (0)
 
+// Every kernel launch is followed by HC_CHECK_LAUNCH(), which also counts it
+// (hc_launch_count(): the bench reports how many of our kernels ran).
+void count_launch();
+
 #define HC_CHECK_LAUNCH()                                                      \
   do {                                                                         \
+    ::hc::count_launch();                                                      \
     cudaError_t _e = cudaGetLastError();                                       \
     if (_e != cudaSuccess) {                                                   \
       ::hc::set_error("%s:%d launch -> %s", __FILE__, __LINE__,                \

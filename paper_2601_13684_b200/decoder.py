@@ -38,21 +38,49 @@ ROLE_CODE = {"volatile": 0, "anchor": 1, "pivot": 2, "satellite": 3}
 
 
 @dataclass
+class _Event:
+    """A fired retrieval; fetched sets arrive asynchronously (pinned D2H)."""
+
+    trigger_step: int
+    pivot: tuple
+    completion_step: int
+    transfer_bytes: int
+    sats: tuple
+    ks: list
+    tids: list = field(default_factory=list)
+    offsets: list = field(default_factory=list)
+    fetched: list = None
+
+    def record(self) -> RetrievalRecord:
+        if self.fetched is None:
+            raise EngineError("fetched sets not yet available: call decoder.sync() first")
+        return RetrievalRecord(
+            trigger_step=self.trigger_step, pivot=self.pivot,
+            completion_step=self.completion_step, transfer_bytes=self.transfer_bytes,
+            fetches=tuple((s, tuple(int(x) for x in f)) for s, f in zip(self.sats, self.fetched)))
+
+
+@dataclass
 class SequenceState:
     """Per-sequence mirror of CacheState (engine.py:126-143)."""
 
     step: int = 0
-    buffers: dict = field(default_factory=dict)       # pivot -> overlap values
-    pending: list = field(default_factory=list)       # (completion, order, satellite, tid)
-    events: list = field(default_factory=list)        # RetrievalRecord
+    buffers: dict = field(default_factory=dict)       # pivot -> overlap values (sliding mode)
+    pending: list = field(default_factory=list)       # (completion, order, sat, tid, k, event)
+    raw_events: list = field(default_factory=list)    # _Event, trigger order
     cumulative_bytes: int = 0
     order: int = 0
     dyn_count: dict = field(default_factory=dict)     # compressed head -> |dynamic|
     dyn_sets: dict = field(default_factory=dict)      # compressed head -> sorted positions
     rows: list = field(default_factory=list)
 
+    @property
+    def events(self) -> list:
+        """RetrievalRecords (reporting.py:58-91), materialised on demand."""
+        return [e.record() for e in self.raw_events]
+
     def bytes_in_flight(self, step: int) -> int:
-        return sum(e.transfer_bytes for e in self.events if e.completion_step > step)
+        return sum(e.transfer_bytes for e in self.raw_events if e.completion_step > step)
 
 
 class HeteroCacheDecoder:
@@ -106,6 +134,11 @@ class HeteroCacheDecoder:
         self.pivot_units.sort()
         self.pivot_slot = {u: i for i, u in enumerate(self.pivot_units)}
         self.states = [SequenceState() for _ in range(self.B)]
+        self._cols = [[self.pivot_slot[self.unit(b, p)] for p in self.pivots] if self.monitor
+                      else [] for b in range(self.B)]
+        self._pinned = None
+        self._uncollected = []
+        self._fire_events = []
         self._prefilled = set()
 
     # ---- helpers -------------------------------------------------------------
@@ -206,17 +239,24 @@ class HeteroCacheDecoder:
         """q/out: [B, NL, H*G, D] bf16; k_new/v_new: [B, NL, H, D] bf16 (device)."""
         cfg = self.config
         sh = _lib.stream_handle(stream)
-        # 1. land due transfers, per sequence in (completion, order) order
-        for b, st in enumerate(self.states):
-            due = sorted((x for x in st.pending if x[0] <= t), key=lambda x: (x[0], x[1]))
-            if due:
-                st.pending = [x for x in st.pending if x[0] > t]
-                for _, _, s, tid, fetched in due:
-                    _lib.check(self.lib.hc_engine_land(self.handle, tid, sh))
-                    st.dyn_count[s] = len(fetched)
+        # 1. land due transfers (engine.py:293-299): per sequence in (completion,
+        #    order) order, all sequences in one batched call
+        land = []
+        for st in self.states:
+            if st.pending and st.pending[0][0] <= t:  # pending is kept sorted
+                k = 0
+                while k < len(st.pending) and st.pending[k][0] <= t:
+                    _, _, s, tid, n, ev = st.pending[k]
+                    land.append(tid)
+                    st.dyn_count[s] = n
                     if self.track_sets:
-                        st.dyn_sets[s] = fetched
+                        st.dyn_sets[s] = ev.fetched[ev.tids.index(tid)]
+                    k += 1
+                del st.pending[:k]
             st.step = t
+        if land:
+            ids = np.asarray(land, dtype=np.int32)
+            _lib.check(self.lib.hc_engine_land_batch(self.handle, len(ids), ids.ctypes.data, sh))
         # 2-4. append, attention, pivot rows, top-l_base + overlap counts
         _lib.check(self.lib.hc_engine_decode_step(self.handle, t, _lib.ptr(q), _lib.ptr(k_new),
                                                   _lib.ptr(v_new), _lib.ptr(out), sh))
@@ -225,54 +265,108 @@ class HeteroCacheDecoder:
             boundary = cfg.eval_every_step or (t % cfg.window == 0)
             if boundary:
                 first = t if cfg.eval_every_step else max(1, t - cfg.window + 1)
-                self._decide(t, first, flags, stream)
+                self._decide(t, first, flags, sh)
         if rows:
             for b, st in enumerate(self.states):
                 st.rows.append(self._row(st, t, flags[b]))
         return flags
 
-    def _decide(self, t: int, first: int, flags: list, stream) -> None:
-        """Window test and firing (engine.py:305-360) for every sequence."""
+    def _decide(self, t: int, first: int, flags: list, sh) -> None:
+        """Window median test and firing (engine.py:305-360), vectorised over pivots.
+
+        Boundary mode: the buffers hold exactly this window's values (they are
+        cleared at every boundary), so medians are one np.median over axis 0
+        (same partition + mean-of-middle-pair arithmetic as the reference's
+        per-list np.median).  Sliding mode keeps per-pivot lists.
+        """
         cfg = self.config
         n = t - first + 1
         counts = np.empty((n, len(self.pivot_units)), dtype=np.int32)
-        _lib.check(self.lib.hc_engine_overlaps(self.handle, first, t, counts.ctypes.data,
-                                               _lib.stream_handle(stream)))
+        _lib.check(self.lib.hc_engine_overlaps(self.handle, first, t, counts.ctypes.data, sh))
+        self._collect_fetched()  # the sync above completed every earlier fetch copy
+        vals = counts / self.l_base_int  # float64, == int / int in Python
+        fire_units, fire_done = [], []
         for b, st in enumerate(self.states):
-            for p in self.pivots:
-                col = self.pivot_slot[self.unit(b, p)]
-                st.buffers[p].extend(int(c) / self.l_base_int for c in counts[:, col])
-            for p in self.pivots:
-                if cfg.eval_every_step:
-                    ready = len(st.buffers[p]) >= cfg.window
-                else:
-                    ready = t % cfg.window == 0
-                if not ready:
+            cols = self._cols[b]
+            if cfg.eval_every_step:
+                fired_mask = []
+                for j, p in enumerate(self.pivots):
+                    buf = st.buffers[p]
+                    buf.extend(vals[:, cols[j]].tolist())
+                    fired = len(buf) >= cfg.window and \
+                        bool(np.median(buf[-cfg.window:]) < cfg.tau_drift)
+                    if fired:
+                        st.buffers[p] = []
+                    fired_mask.append(fired)
+            else:
+                fired_mask = (np.median(vals[:, cols], axis=0) < cfg.tau_drift).tolist()
+            for j, p in enumerate(self.pivots):
+                if not fired_mask[j]:
                     continue
-                fired = bool(np.median(st.buffers[p][-cfg.window:]) < cfg.tau_drift)
-                if fired:
-                    flags[b] = 1
-                    self._fire(b, st, p, t, stream)
-                if fired or not cfg.eval_every_step:
-                    st.buffers[p] = []
+                flags[b] = 1
+                sats = self.satellites_of[p]
+                ks = [min(self.effective_length(s), self.L + t) for s in sats]
+                nbytes = sum(ks) * self.bytes_per_entry
+                st.cumulative_bytes += nbytes
+                done = completion_step(t, st.cumulative_bytes, cfg)
+                ev = _Event(trigger_step=t, pivot=p, completion_step=done, transfer_bytes=nbytes,
+                            sats=sats, ks=ks)
+                st.raw_events.append(ev)
+                fire_units.append(self.unit(b, p))
+                fire_done.append(done)
+                self._fire_events.append((st, ev))
+        if fire_units:
+            self._fire_batch(t, fire_units, fire_done, sh)
 
-    def _fire(self, b: int, st: SequenceState, p, t: int, stream) -> None:
-        sats = self.satellites_of[p]
-        ks = [min(self.effective_length(s), self.L + t) for s in sats]
-        nbytes = sum(ks) * self.bytes_per_entry
-        st.cumulative_bytes += nbytes
-        done = completion_step(t, st.cumulative_bytes, self.config)
-        ids = np.zeros(len(sats), dtype=np.int32)
-        _lib.check(self.lib.hc_engine_fire(self.handle, self.unit(b, p), t, done, ids.ctypes.data,
-                                           _lib.stream_handle(stream)))
-        fetches = []
-        for s, k, tid in zip(sats, ks, ids.tolist()):
-            got = self.read_indices(0, tid, k, stream)
-            fetches.append((s, tuple(int(x) for x in got)))
-            st.pending.append((done, st.order, s, tid, got))
-            st.order += 1
-        st.events.append(RetrievalRecord(trigger_step=t, pivot=p, completion_step=done,
-                                         transfer_bytes=nbytes, fetches=tuple(fetches)))
+    def _fire_batch(self, t: int, units, done, sh) -> None:
+        import torch
+
+        evs = self._fire_events
+        self._fire_events = []
+        total = sum(sum(ev.ks) for _, ev in evs)
+        if self._pinned is None or self._pinned.numel() < total:
+            self._pinned = torch.empty(max(total, 1 << 20), dtype=torch.int32, pin_memory=True)
+        n_ids = sum(len(ev.sats) for _, ev in evs)
+        ids = np.zeros(n_ids, dtype=np.int32)
+        u = np.asarray(units, dtype=np.int32)
+        d = np.asarray(done, dtype=np.int32)
+        _lib.check(self.lib.hc_engine_fire_batch(self.handle, len(u), u.ctypes.data, t,
+                                                 d.ctypes.data, ids.ctypes.data,
+                                                 self._pinned.data_ptr(), sh))
+        q = 0
+        off = 0
+        for st, ev in evs:
+            ev.tids = ids[q:q + len(ev.sats)].tolist()
+            ev.offsets = []
+            for k in ev.ks:
+                ev.offsets.append((off, k))
+                off += k
+            q += len(ev.sats)
+            for s, k, tid in zip(ev.sats, ev.ks, ev.tids):
+                st.pending.append((ev.completion_step, st.order, s, tid, k, ev))
+                st.order += 1
+            self._uncollected.append(ev)
+        # completion steps are nondecreasing in firing order, but keep the
+        # (completion, order) landing order explicit (engine.py:293-296)
+        for st in self.states:
+            st.pending.sort(key=lambda x: (x[0], x[1]))
+        if self.track_sets:
+            self.sync()
+
+    def _collect_fetched(self) -> None:
+        """Copy fetched index sets out of the pinned staging buffer (after a sync)."""
+        if not self._uncollected:
+            return
+        buf = self._pinned.numpy().view(np.uint32)
+        for ev in self._uncollected:
+            ev.fetched = [np.sort(buf[o:o + k]) for o, k in ev.offsets]
+        self._uncollected = []
+
+    def sync(self, stream=None) -> None:
+        import torch
+
+        torch.cuda.current_stream().synchronize() if stream is None else stream.synchronize()
+        self._collect_fetched()
 
     # ---- measurement helpers ------------------------------------------------------
 
@@ -281,6 +375,17 @@ class HeteroCacheDecoder:
         _lib.check(self.lib.hc_engine_resident_rows(self.handle, t, C.byref(out),
                                                     _lib.stream_handle(stream)))
         return out.value
+
+    PHASES = ("append", "attention", "combine", "score_rows", "monitor", "ovl_copy", "step")
+
+    def kernel_timing(self, enable: bool = True) -> dict:
+        """Summed device milliseconds per decode-step phase since the last call."""
+        ms = (C.c_double * 7)()
+        n = C.c_int32()
+        _lib.check(self.lib.hc_engine_timing(self.handle, int(enable), ms, C.byref(n)))
+        out = dict(zip(self.PHASES, list(ms)))
+        out["steps"] = n.value
+        return out
 
     def active_tiles(self, t: int) -> int:
         n = C.c_int32()
@@ -292,6 +397,7 @@ class HeteroCacheDecoder:
                                                 _lib.stream_handle(stream)))
 
     def report(self, b: int, decode_steps: int, trace_sha256: str = "") -> SimulationReport:
+        self.sync()
         st = self.states[b]
         return SimulationReport(policy=self.config.variant, trace_sha256=trace_sha256,
                                 num_layers=self.NL, heads_per_layer=self.H, prefill_len=self.L,

@@ -17,7 +17,8 @@ def test_library_exports_every_header_symbol():
 
     lib = _lib.load()
     header = (ROOT / "include" / "hcb200.h").read_text()
-    declared = set(re.findall(r"^\s*(?:int|const char\*|void)\s+(hc_\w+)\s*\(", header, re.M))
+    declared = set(re.findall(r"^\s*(?:int|const char\*|void|unsigned long long)\s+(hc_\w+)\s*\(",
+                              header, re.M))
     assert declared, "no entry points parsed from include/hcb200.h"
     for name in sorted(declared):
         assert hasattr(lib, name), f"libhcb200.so does not export {name}"
