@@ -88,6 +88,15 @@ int hc_select_topk(const float* scores_dev, const uint32_t* idx_dev, uint32_t n,
 int hc_bitmap_from_indices(uint32_t* bitmap_dev, uint32_t n_words, const uint32_t* idx_dev,
                            const uint32_t* count_dev, uint32_t max_count, void* stream);
 
+/* Drift-monitor form of K1+K2 for dense rows (pivot_overlap, engine.py:242-245):
+ * for each of n_rows rows (row r at rows_dev + r*row_stride, n scores) and
+ * bitmap r (kbase_dev + r*words), write the composite-key threshold of the
+ * top-k set (selected <=> (score_key << 32 | ~pos) >= thr) and the overlap
+ * |top_k & base|.  Synchronises the stream (test entry point). */
+int hc_monitor_rows(const float* rows_dev, int64_t row_stride, int32_t n_rows, uint32_t n,
+                    uint32_t k, const uint32_t* kbase_dev, int32_t words, uint64_t* thr_dev,
+                    uint32_t* ovl_dev, void* stream);
+
 /* ---------------------------------------------------------------------------
  * Trace-driven residency diagnostics (CacheView + attention_recall).
  *

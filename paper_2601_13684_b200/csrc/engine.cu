@@ -31,6 +31,12 @@ int launch_attention(const CUtensorMap& tmK, const CUtensorMap& tmV, const AttnP
                      int n_tiles, const int32_t* pivot_units_dev, int n_pivots, cudaStream_t st,
                      const cudaEvent_t* ev = nullptr);
 int launch_topk(const hc_topk_job* jobs_dev, int n_jobs, uint32_t n_add, cudaStream_t st);
+int launch_monitor(const float* rows, int64_t row_stride, const int32_t* slots, int n_rows,
+                   uint32_t n, uint32_t k, const uint32_t* kbase, int words, uint64_t* thr,
+                   uint32_t* ovl, cudaStream_t st);
+int launch_restamp_threshold(const float* rows, int64_t row_stride, const int32_t* slots,
+                             int n_rows, uint32_t n, const uint64_t* thr, uint32_t* kbase,
+                             int words, cudaStream_t st);
 
 namespace {
 
@@ -116,6 +122,9 @@ struct EngineImpl {
   float *logits = nullptr, *stats = nullptr, *rowbuf = nullptr;
   uint32_t *top_idx = nullptr, *top_cnt = nullptr, *kbase = nullptr;
   uint32_t *ovl_cur = nullptr, *ovl_ring = nullptr;
+  uint64_t* thr = nullptr;          // per pivot slot: composite-key threshold of its top set
+  int32_t* d_piv_slots = nullptr;   // iota over pivot slots
+  int last_t = 0;                   // last decode step run
   hc_topk_job* d_piv_jobs = nullptr;
   // compressed units
   std::vector<int32_t> cap;               // prefix capacity per unit (0 for full)
@@ -183,6 +192,7 @@ int engine_destroy(EngineImpl& e) {
   }
   void* ptrs[] = {e.d_units, e.K, e.V, e.d_tiles, e.partial, e.d_piv_units, e.logits, e.stats,
                   e.rowbuf, e.top_idx, e.top_cnt, e.kbase, e.ovl_cur, e.ovl_ring, e.d_piv_jobs,
+                  e.thr, e.d_piv_slots,
                   e.pf};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -334,6 +344,13 @@ int engine_create(EngineImpl& e, const hc_engine_desc& c, const int32_t* roles,
   HC_TRY(dalloc((void**)&e.kbase, size_t(np) * e.words * 4, &e.dev_bytes));
   HC_TRY(dalloc((void**)&e.ovl_cur, size_t(np) * 4, &e.dev_bytes));
   HC_TRY(dalloc((void**)&e.ovl_ring, size_t(np) * kRing * 4, &e.dev_bytes));
+  HC_TRY(dalloc((void**)&e.thr, size_t(np) * 8, &e.dev_bytes));
+  {
+    std::vector<int32_t> iota(np);
+    for (int i = 0; i < np; ++i) iota[i] = i;
+    HC_TRY(dalloc((void**)&e.d_piv_slots, size_t(np) * 4, &e.dev_bytes));
+    HC_CUDA_TRY(cudaMemcpy(e.d_piv_slots, iota.data(), size_t(np) * 4, cudaMemcpyHostToDevice));
+  }
   std::vector<hc_topk_job> jobs(np);
   for (int s = 0; s < e.n_piv; ++s) {
     hc_topk_job& j = jobs[s];
@@ -429,8 +446,11 @@ int engine_decode_step(EngineImpl& e, int t, const void* q, const void* kn, cons
   AttnParams p = decode_params(e, t, q, o);
   HC_TRY(launch_attention(e.tmK, e.tmV, p, active_tiles(e, t), e.d_piv_units, e.n_piv, st,
                           ev ? ev + 1 : nullptr));
+  e.last_t = t;
   if (e.n_piv) {
-    HC_TRY(launch_topk(e.d_piv_jobs, e.n_piv, uint32_t(t), st));
+    // K1+K2: top-l_base threshold and |top & K_base| per pivot (engine.py:305-311)
+    HC_TRY(launch_monitor(e.rowbuf, e.row_len, e.d_piv_slots, e.n_piv, uint32_t(e.L + t),
+                          uint32_t(e.lbase), e.kbase, e.words, e.thr, e.ovl_cur, st));
     if (ev) HC_CUDA_TRY(cudaEventRecord(ev[5], st));
     HC_CUDA_TRY(cudaMemcpyAsync(e.ovl_ring + size_t(t % kRing) * e.n_piv, e.ovl_cur,
                                 size_t(e.n_piv) * 4, cudaMemcpyDeviceToDevice, st));
@@ -856,11 +876,11 @@ int engine_fire_batch(EngineImpl& e, int n, const int32_t* pus, int t, const int
     HC_TRY(launch_topk(dj, int(jobs.size()), 0, st));
     HC_CUDA_TRY(cudaFreeAsync(dj, st));
   }
-  if (n > 0) {  // K_base <- current top set (engine.py:357)
+  if (n > 0) {  // K_base <- current top set (engine.py:357), from the monitor threshold
     int32_t* ds = nullptr;
     HC_TRY(upload(e, slots.data(), slots.size() * 4, st, (void**)&ds));
-    restamp_batch_kernel<<<n, 1024, 0, st>>>(e.kbase, e.top_idx, e.top_cnt, ds, e.words, e.lbase);
-    HC_CHECK_LAUNCH();
+    HC_TRY(launch_restamp_threshold(e.rowbuf, e.row_len, ds, n, uint32_t(e.L + t), e.thr,
+                                    e.kbase, e.words, st));
     HC_CUDA_TRY(cudaFreeAsync(ds, st));
   }
   size_t off = 0;
@@ -1081,8 +1101,21 @@ extern "C" int hc_engine_read_indices(hc_engine* eng, int32_t kind, int32_t id, 
     }
   } else if (kind == 2) {
     HC_REQUIRE(id >= 0 && id < e.n_units && e.piv_slot[id] >= 0, HC_EINVAL, "not a pivot");
-    list = e.top_idx + size_t(e.piv_slot[id]) * e.lbase;
-    cnt = e.top_cnt + e.piv_slot[id];
+    const int s = e.piv_slot[id];
+    list = e.top_idx + size_t(s) * e.lbase;
+    cnt = e.top_cnt + s;
+    if (e.last_t > 0) {  // the monitor keeps only a threshold: materialise the set
+      hc_topk_job jb{};
+      jb.scores = e.rowbuf + size_t(s) * e.row_len;
+      jb.n = uint32_t(e.L + e.last_t);
+      jb.k = uint32_t(e.lbase);
+      jb.out_idx = e.top_idx + size_t(s) * e.lbase;
+      jb.out_count = e.top_cnt + s;
+      hc_topk_job* dj = nullptr;
+      HC_TRY(hc::upload(e, &jb, sizeof(jb), st, (void**)&dj));
+      HC_TRY(hc::launch_topk(dj, 1, 0, st));
+      HC_CUDA_TRY(cudaFreeAsync(dj, st));
+    }
   } else {
     HC_REQUIRE(false, HC_EINVAL, "bad kind %d", kind);
   }

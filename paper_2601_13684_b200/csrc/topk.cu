@@ -12,6 +12,9 @@
 // pivot / satellite / compressed head of a step.  All integer work -- no
 // fast-math, no FTZ dependence (subnormal scores from 0.9^i compare exactly).
 
+#include <algorithm>
+#include <vector>
+
 #include "hc_common.cuh"
 
 namespace hc {
@@ -262,4 +265,280 @@ extern "C" int hc_bitmap_from_indices(uint32_t* bitmap_dev, uint32_t n_words,
                                                                        max_count);
   HC_CHECK_LAUNCH();
   return HC_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Drift-monitor top-k (K1 + K2 fused), dense pivot rows.
+//
+// The monitor needs, per pivot and step, only the size of the overlap
+// |top_{l_base}(row) & K_base| (engine.py:305-311) -- not the index list --
+// plus the selection threshold so that K_base can be restamped if the pivot
+// fires (engine.py:357).  One CTA per row, two streaming passes:
+//   1. 13-bit histogram of the score keys (smem, 8192 bins) -> bucket b1
+//      holding the k-th largest composite key;
+//   2. count K_base bits of every key above b1, collect the keys inside b1
+//      as (score, ~index) composites into shared memory;
+// then an 8-bit radix select over the candidates only (score low bits and
+// the index tie-break) yields the exact composite threshold T (selected <=>
+// key >= T, the same set as metrics.py:26-45), and the candidates >= T add
+// their K_base bits.  If the bucket overflows shared memory the select falls
+// back to streaming radix passes over the row restricted to b1.
+// ---------------------------------------------------------------------------
+namespace hc {
+namespace {
+
+constexpr int kMonThreads = 1024;
+constexpr int kMonBins = 8192;      // 13-bit first digit: key32 >> 19
+constexpr int kMonCand = 16384;     // shared-memory candidate capacity
+constexpr int kMonSmem = kMonBins * 4 + kMonCand * 8 + 64 * 4;
+
+__device__ __forceinline__ uint64_t ckey(uint32_t k32, uint32_t pos) {
+  return (uint64_t(k32) << 32) | uint64_t(~pos);
+}
+
+// Block-wide: find the bin (scanning from the top of `hist[nb]`) that holds
+// the rem-th largest entry.  Returns via sh[0] = bin, sh[1] = rank in bin,
+// sh[2] = bin count.  Every thread owns nb / blockDim.x consecutive bins.
+template <int NB>
+__device__ void block_find_bucket(const uint32_t* hist, uint32_t rem, uint32_t* sh,
+                                  uint32_t* warp_tot) {
+  constexpr int per = NB / kMonThreads;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint32_t local = 0;
+#pragma unroll
+  for (int j = 0; j < per; ++j) local += hist[NB - 1 - (tid * per + j)];
+  uint32_t incl = local;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += v;
+  }
+  if (lane == 31) warp_tot[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t v = warp_tot[lane];
+    uint32_t wi = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, wi, off);
+      if (lane >= off) wi += u;
+    }
+    warp_tot[lane] = wi - v;
+  }
+  __syncthreads();
+  const uint32_t excl = warp_tot[warp] + incl - local;
+  if (excl < rem && rem <= excl + local) {
+    uint32_t above = excl;
+    for (int j = 0; j < per; ++j) {
+      const int bin = NB - 1 - (tid * per + j);
+      const uint32_t c = hist[bin];
+      if (above < rem && rem <= above + c) {
+        sh[0] = uint32_t(bin);
+        sh[1] = rem - above;
+        sh[2] = c;
+        break;
+      }
+      above += c;
+    }
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kMonThreads, 1)
+monitor_kernel(const float* __restrict__ rows, int64_t row_stride, const int32_t* __restrict__ slots,
+               uint32_t n, uint32_t k, const uint32_t* __restrict__ kbase, int words,
+               uint64_t* __restrict__ thr_out, uint32_t* __restrict__ ovl_out) {
+  extern __shared__ __align__(16) uint8_t mon_smem[];
+  uint32_t* hist = reinterpret_cast<uint32_t*>(mon_smem);
+  uint64_t* cand = reinterpret_cast<uint64_t*>(mon_smem + kMonBins * 4);
+  uint32_t* misc = reinterpret_cast<uint32_t*>(mon_smem + kMonBins * 4 + kMonCand * 8);
+  uint32_t* sh = misc;            // [0..3] results
+  uint32_t* warp_tot = misc + 8;  // [32]
+  const int s = slots[blockIdx.x];
+  const float* __restrict__ row = rows + size_t(s) * row_stride;
+  const uint32_t* __restrict__ bm = kbase + size_t(s) * words;
+  const int tid = threadIdx.x, lane = tid & 31;
+
+  if (k >= n) {  // everything is selected
+    uint32_t c = 0;
+    for (uint32_t i = tid; i < n; i += kMonThreads) c += (__ldg(bm + (i >> 5)) >> (i & 31)) & 1u;
+    for (int off = 16; off; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
+    if (tid == 0) sh[3] = 0;
+    __syncthreads();
+    if (lane == 0) atomicAdd(&sh[3], c);
+    __syncthreads();
+    if (tid == 0) { thr_out[s] = 0; ovl_out[s] = sh[3]; }
+    return;
+  }
+  for (int j = tid; j < kMonBins; j += kMonThreads) hist[j] = 0;
+  if (tid == 0) sh[3] = 0;  // candidate count
+  __syncthreads();
+  const uint32_t n4 = n >> 2;
+  const float4* __restrict__ row4 = reinterpret_cast<const float4*>(row);
+  for (uint32_t i = tid; i < n4; i += kMonThreads) {
+    const float4 v = __ldg(row4 + i);
+    atomicAdd(&hist[score_key(v.x) >> 19], 1u);
+    atomicAdd(&hist[score_key(v.y) >> 19], 1u);
+    atomicAdd(&hist[score_key(v.z) >> 19], 1u);
+    atomicAdd(&hist[score_key(v.w) >> 19], 1u);
+  }
+  for (uint32_t i = n4 * 4 + tid; i < n; i += kMonThreads) atomicAdd(&hist[score_key(__ldg(row + i)) >> 19], 1u);
+  __syncthreads();
+  block_find_bucket<kMonBins>(hist, k, sh, warp_tot);
+  const uint32_t b1 = sh[0];
+  uint32_t rem = sh[1];
+  const bool whole = (sh[2] == rem);
+  __syncthreads();
+
+  // pass 2: K_base bits above b1, candidates inside b1
+  uint32_t ovl = 0;
+  auto visit = [&](uint32_t pos, float x) {
+    const uint32_t k32 = score_key(x);
+    const uint32_t d = k32 >> 19;
+    const uint32_t bit = (__ldg(bm + (pos >> 5)) >> (pos & 31)) & 1u;
+    if (d > b1 || (whole && d == b1)) ovl += bit;
+    else if (!whole && d == b1) {
+      const uint32_t at = atomicAdd(&sh[3], 1u);
+      if (at < uint32_t(kMonCand)) cand[at] = ckey(k32, pos);
+    }
+  };
+  for (uint32_t i = tid; i < n4; i += kMonThreads) {
+    const float4 v = __ldg(row4 + i);
+    visit(4 * i, v.x);
+    visit(4 * i + 1, v.y);
+    visit(4 * i + 2, v.z);
+    visit(4 * i + 3, v.w);
+  }
+  for (uint32_t i = n4 * 4 + tid; i < n; i += kMonThreads) visit(i, __ldg(row + i));
+  __syncthreads();
+
+  uint64_t T = uint64_t(b1) << 51;  // lowest composite key of bucket b1
+  if (!whole) {
+    const uint32_t m = sh[3];
+    const bool in_smem = m <= uint32_t(kMonCand);
+    uint64_t prefix = uint64_t(b1) << 51, mask = uint64_t(0x1fff) << 51;
+    // 8-bit radix over bits 50..0 of the composite key among the candidates
+    for (int shift = 43; ; shift -= 8) {
+      const int sh_eff = shift < 0 ? 0 : shift;
+      const uint64_t dmask = shift < 0 ? ((uint64_t(1) << (shift + 8)) - 1) : uint64_t(255);
+      for (int j = tid; j < kMonThreads; j += kMonThreads) hist[j] = 0;  // 1024-bin scan below
+      __syncthreads();
+      if (in_smem) {
+        for (uint32_t i = tid; i < m; i += kMonThreads) {
+          const uint64_t key = cand[i];
+          if ((key & mask) == prefix) atomicAdd(&hist[uint32_t((key >> sh_eff) & dmask)], 1u);
+        }
+      } else {
+        for (uint32_t i = tid; i < n; i += kMonThreads) {
+          const uint64_t key = ckey(score_key(__ldg(row + i)), i);
+          if ((key & mask) == prefix) atomicAdd(&hist[uint32_t((key >> sh_eff) & dmask)], 1u);
+        }
+      }
+      __syncthreads();
+      block_find_bucket<kMonThreads>(hist, rem, sh, warp_tot);  // 1024 >= 256 bins (zeros above)
+      const uint32_t b = sh[0];
+      rem = sh[1];
+      const bool done = (sh[2] == rem) || shift <= 0;
+      prefix |= uint64_t(b) << sh_eff;
+      mask |= dmask << sh_eff;
+      __syncthreads();
+      if (done) break;
+    }
+    T = prefix;  // selected <=> key >= prefix (bucket fully taken, or keys unique)
+    // candidates at or above T add their K_base bits
+    if (in_smem) {
+      for (uint32_t i = tid; i < m; i += kMonThreads) {
+        const uint64_t key = cand[i];
+        if (key >= T) {
+          const uint32_t pos = ~uint32_t(key);
+          ovl += (__ldg(bm + (pos >> 5)) >> (pos & 31)) & 1u;
+        }
+      }
+    } else {
+      for (uint32_t i = tid; i < n; i += kMonThreads) {
+        const uint64_t key = ckey(score_key(__ldg(row + i)), i);
+        if ((key >> 51) == b1 && key >= T) ovl += (__ldg(bm + (i >> 5)) >> (i & 31)) & 1u;
+      }
+    }
+  }
+  for (int off = 16; off; off >>= 1) ovl += __shfl_xor_sync(0xffffffffu, ovl, off);
+  if (tid == 0) sh[3] = 0;
+  __syncthreads();
+  if (lane == 0) atomicAdd(&sh[3], ovl);
+  __syncthreads();
+  if (tid == 0) {
+    thr_out[s] = T;
+    ovl_out[s] = sh[3];
+  }
+}
+
+// K_base <- {p : key(p) >= T} over [0, n) for the listed pivot slots
+// (engine.py:357), one warp per 32-position word via ballot.
+__global__ void restamp_threshold_kernel(const float* __restrict__ rows, int64_t row_stride,
+                                         const int32_t* __restrict__ slots, uint32_t n,
+                                         const uint64_t* __restrict__ thr, uint32_t* kbase,
+                                         int words) {
+  const int s = slots[blockIdx.y];
+  const float* row = rows + size_t(s) * row_stride;
+  const uint64_t T = thr[s];
+  uint32_t* bm = kbase + size_t(s) * words;
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  for (int w = blockIdx.x * wpb + (threadIdx.x >> 5); w < words; w += gridDim.x * wpb) {
+    const uint32_t pos = uint32_t(w) * 32 + lane;
+    const bool sel = pos < n && ckey(score_key(__ldg(row + pos)), pos) >= T;
+    const uint32_t word = __ballot_sync(0xffffffffu, sel);
+    if (lane == 0) bm[w] = word;
+  }
+}
+
+}  // namespace
+
+int launch_monitor(const float* rows, int64_t row_stride, const int32_t* slots, int n_rows,
+                   uint32_t n, uint32_t k, const uint32_t* kbase, int words, uint64_t* thr,
+                   uint32_t* ovl, cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    HC_CUDA_TRY(cudaFuncSetAttribute(monitor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kMonSmem));
+    configured = true;
+  }
+  if (n_rows <= 0) return HC_OK;
+  monitor_kernel<<<n_rows, kMonThreads, kMonSmem, st>>>(rows, row_stride, slots, n, k, kbase,
+                                                        words, thr, ovl);
+  HC_CHECK_LAUNCH();
+  return HC_OK;
+}
+
+int launch_restamp_threshold(const float* rows, int64_t row_stride, const int32_t* slots,
+                             int n_rows, uint32_t n, const uint64_t* thr, uint32_t* kbase,
+                             int words, cudaStream_t st) {
+  if (n_rows <= 0) return HC_OK;
+  const int blocks = std::min(64, (words + 7) / 8);
+  restamp_threshold_kernel<<<dim3(std::max(1, blocks), n_rows), 256, 0, st>>>(
+      rows, row_stride, slots, n, thr, kbase, words);
+  HC_CHECK_LAUNCH();
+  return HC_OK;
+}
+
+}  // namespace hc
+
+extern "C" int hc_monitor_rows(const float* rows_dev, int64_t row_stride, int32_t n_rows,
+                               uint32_t n, uint32_t k, const uint32_t* kbase_dev, int32_t words,
+                               uint64_t* thr_dev, uint32_t* ovl_dev, void* stream) {
+  HC_REQUIRE(rows_dev && kbase_dev && thr_dev && ovl_dev && n_rows >= 0, HC_EINVAL,
+             "hc_monitor_rows: bad arguments");
+  HC_REQUIRE(row_stride % 4 == 0 && int64_t(words) * 32 >= int64_t(n), HC_EINVAL,
+             "hc_monitor_rows: row stride must be a multiple of 4, bitmap must cover n");
+  cudaStream_t st = (cudaStream_t)stream;
+  int32_t* slots = nullptr;
+  HC_CUDA_TRY(cudaMallocAsync((void**)&slots, size_t(std::max(1, n_rows)) * 4, st));
+  std::vector<int32_t> iota(std::max(1, n_rows));
+  for (int i = 0; i < n_rows; ++i) iota[i] = i;
+  HC_CUDA_TRY(cudaMemcpyAsync(slots, iota.data(), iota.size() * 4, cudaMemcpyHostToDevice, st));
+  int rc = hc::launch_monitor(rows_dev, row_stride, slots, n_rows, n, k, kbase_dev, words,
+                              thr_dev, ovl_dev, st);
+  HC_CUDA_TRY(cudaFreeAsync(slots, st));
+  HC_CUDA_TRY(cudaStreamSynchronize(st));
+  return rc;
 }

@@ -125,3 +125,20 @@ def top_k_indices(scores, k: int, pool_kernel: int = 0) -> frozenset:
         sel, cnt = topk_rows(idx[None, :], sc[None, :], k)
         return frozenset(int(x) for x in sel[0, :cnt[0]])
     return top_k_indices(np.asarray(seq, dtype=np.float64), k)
+
+
+def monitor_rows(rows, k: int, base_bitmaps):
+    """Drift-monitor K1+K2 over dense rows: (thresholds [R] uint64, overlaps [R])."""
+    torch = _torch()
+    _lib.require_cuda()
+    R, n = rows.shape
+    stride = (n + 3) // 4 * 4
+    dev = torch.zeros((R, stride), dtype=torch.float32, device="cuda")
+    dev[:, :n] = torch.as_tensor(np.asarray(rows, dtype=np.float32))
+    words = base_bitmaps.shape[1]
+    bm = torch.as_tensor(np.ascontiguousarray(base_bitmaps, dtype=np.uint32).view(np.int32)).cuda()
+    thr = torch.zeros(R, dtype=torch.int64, device="cuda")
+    ovl = torch.zeros(R, dtype=torch.int32, device="cuda")
+    _lib.check(_lib.load().hc_monitor_rows(_lib.ptr(dev), stride, R, n, k, _lib.ptr(bm), words,
+                                           _lib.ptr(thr), _lib.ptr(ovl), _lib.stream_handle()))
+    return thr.cpu().numpy().view(np.uint64), ovl.cpu().numpy()

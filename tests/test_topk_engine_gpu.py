@@ -174,3 +174,38 @@ def test_profiling_matches_reference_taxonomy():
         for h, v in exp["s_stable"].items():
             assert tax.heads[key(h)].s_stable == v
             assert tax.heads[key(h)].s_sim == exp["s_sim"][h]
+
+
+@pytest.mark.parametrize("n,k", [(740, 70), (4097, 410), (131072 + 5, 6554), (237568, 22938),
+                                 (50000, 49999), (3000, 3000)])
+def test_monitor_threshold_and_overlap_bit_exact(n, k):
+    """Fused monitor K1+K2 (smem candidates and the streaming fallback for
+    tie-heavy rows whose threshold bucket overflows) vs the oracle."""
+    from paper_2601_13684_b200.ops import monitor_rows
+
+    rng = np.random.default_rng(n + k)
+    rows = _tie_heavy_rows(rng, 6, n)
+    rows[4] = rng.dirichlet(np.full(n, 0.05)).astype(np.float32)  # softmax-like, heavy tail
+    words = (n + 31) // 32
+    bms = np.zeros((6, words), dtype=np.uint32)
+    bases = []
+    for r in range(6):
+        b = rng.choice(n, size=max(1, n // 9), replace=False)
+        bases.append(set(b.tolist()))
+        np.bitwise_or.at(bms[r], b >> 5, np.uint32(1) << (b & 31).astype(np.uint32))
+    thr, ovl = monitor_rows(rows, k, bms)
+    for r in range(6):
+        top = O.top_k_dense(rows[r], k)
+        assert int(ovl[r]) == len(set(top.tolist()) & bases[r]), r
+        # the threshold reproduces exactly the selected set
+        keys = _composite_keys(rows[r])
+        assert np.array_equal(np.nonzero(keys >= thr[r])[0].astype(np.uint32), top), r
+
+
+def _composite_keys(row):
+    u = row.astype(np.float32).view(np.uint32).copy()
+    u[u == 0x80000000] = 0
+    neg = (u & 0x80000000) != 0
+    k32 = np.where(neg, ~u, u | np.uint32(0x80000000)).astype(np.uint64)
+    pos = np.arange(row.size, dtype=np.uint64)
+    return (k32 << np.uint64(32)) | (np.uint64(0xFFFFFFFF) - pos)
