@@ -220,10 +220,8 @@ def run_b200(args, rank, world):
     ms_e2e = ev0.elapsed_time(ev1)
 
     if world > 1:
-        import torch.distributed as dist
-        tt = torch.tensor([ms, ms_e2e], device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms, ms_e2e = tt.tolist()
+        from paper_2601_13684_b200.parallel import max_over_ranks
+        ms, ms_e2e = max_over_ranks([ms, ms_e2e], device="cuda")
 
     rows_avg = (rows_first + rows_last) / 2.0
     step_bytes = algorithmic_bytes(int(rows_avg), w.batch, w.num_layers, m.q_heads)
