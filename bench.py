@@ -132,7 +132,11 @@ def run_b200(args, rank, world):
     m = w.model
     tax, plan = plan_for(w)
     K, W = args.steps, args.warmup
-    period = 100  # planted topic shift every `period` steps keeps retrieval in the timed region
+    # one planted topic shift mid-run per timed loop (cfg4: every
+    # ~1.5 windows) -- every pivot of every layer and sequence drifts at that step
+    shifts = [W + K // 2, W + K + K // 2]
+    if w.shift_every:
+        shifts = list(range(W + w.shift_every, W + 2 * K + 1, w.shift_every))
     cfg = EngineConfig(tau_drift=0.5, window=8, update_delay_steps=1,
                        transfer_bandwidth=int(args.link_mib_per_step * (1 << 20)))
     T = W + 2 * K + 8
@@ -154,7 +158,7 @@ def run_b200(args, rank, world):
             for ph in (0, 1)}
 
     def inputs(t):
-        return pool[(t // period) % 2][t % 4]
+        return pool[sum(t >= x for x in shifts) % 2][t % 4]
 
     out = torch.empty_like(pool[0][0][0])
     stream = torch.cuda.current_stream()
@@ -173,9 +177,10 @@ def run_b200(args, rank, world):
     # ---- timed: device-resident inputs ----
     rows_first = dec.resident_rows(t + 1)
     clocks = ClockSampler(torch.cuda.current_device())
-    clocks.start()
+    if not os.environ.get("HC_BENCH_NO_CLOCKS"):
+        clocks.start()
     launches0 = lib.hc_launch_count()
-    dec.kernel_timing(True)
+    dec.kernel_timing(not os.environ.get("HC_BENCH_NO_TIMING"))
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     torch.cuda.synchronize()
@@ -192,6 +197,7 @@ def run_b200(args, rank, world):
     ms = ev0.elapsed_time(ev1)
     launches = lib.hc_launch_count() - launches0
     phases = dec.kernel_timing(False)
+    retr = dec.retrieval_stats()
     attn_ms, attn_n = phases["attention"], phases["steps"]
     clk = clocks.stop()
     rows_last = dec.resident_rows(t)
@@ -208,7 +214,7 @@ def run_b200(args, rank, world):
     ev0.record(stream)
     for _ in range(K):
         t += 1
-        src = hq[((t // period) % 2) * 4 + t % 4]
+        src = hq[(sum(t >= x for x in shifts) % 2) * 4 + t % 4]
         dq.copy_(src[0], non_blocking=True)
         dkn.copy_(src[1], non_blocking=True)
         dvn.copy_(src[2], non_blocking=True)
@@ -228,7 +234,7 @@ def run_b200(args, rank, world):
     attn_bytes = rows_avg * 2 * m.head_dim * 2 + w.batch * w.num_layers * m.q_heads * m.head_dim * 2 * 2
     attn_avg_ms = attn_ms / max(1, attn_n)
     peak, peak_src, _ = peaks()
-    achieved = attn_bytes / (attn_avg_ms * 1e-3) / 1e9
+    achieved = attn_bytes / (attn_avg_ms * 1e-3) / 1e9 if attn_avg_ms > 0 else 0.0
     traffic = None
     tf = ROOT / "profiles" / f"traffic_{args.workload}.json"
     if tf.exists():
@@ -253,7 +259,7 @@ def run_b200(args, rank, world):
             "compression": w.compression, "rho": plan.rho, "l_base_int": plan.l_base_int,
             "roles_per_layer": list(m.layer_roles()),
             "decode_window": cfg.window, "tau_drift": cfg.tau_drift,
-            "topic_shift_every_steps": period, "split_k_chunk": args.chunk,
+            "topic_shifts_at_steps": shifts, "split_k_chunk": args.chunk,
             "transfer_bandwidth_bytes_per_step": cfg.transfer_bandwidth,
             "l2": f"inputs larger than L2: {step_bytes / 1e9:.2f} GB of resident K/V read per step",
             "parallelism": f"replicas x{world} (weak: each GPU decodes its own batch)",
@@ -272,6 +278,9 @@ def run_b200(args, rank, world):
         "clocks": clk,
         "phase_ms_per_step": {k: v / max(1, attn_n) for k, v in phases.items() if k != "steps"},
         "retrieval_events_timed_run": events,
+        "retrieval": {"host_link_gbs": retr["host_link_gbs"], "bytes": retr["bytes"],
+                      "gather_ms": retr["gather_ms"], "landing_stall_ms_total": retr["landing_stall_ms"],
+                      "batches": retr["batches"]},
         "prefill_seconds": prefill_s,
         "device_bytes": dec.device_bytes, "pinned_host_bytes": dec.host_bytes,
     }

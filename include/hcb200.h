@@ -230,10 +230,20 @@ int hc_engine_set_prefill_dump(hc_engine* eng, float* dst_dev);
 
 /* Per-step phase timeline for the roofline, from CUDA events on the
  * launching stream.  Reports (syncs) the summed milliseconds since the last
- * call of phase_ms[7] = {append, K4 attention, combine, pivot score rows,
- * K1/K2 monitor, overlap copy, whole step} and the number of steps, then
+ * call of phase_ms[8] = {append, K4 attention, combine, pivot score rows,
+ * K1/K2 monitor, overlap copy, whole step, gaps between steps} and the
+ * number of steps, then
  * resets and enables (enable != 0) or disables recording. */
 int hc_engine_timing(hc_engine* eng, int32_t enable, double* phase_ms, int32_t* steps);
+
+/* Retrieval statistics since the last call (timing must be enabled):
+ * out4 = {bytes gathered over the host link (upper bound), gather-kernel
+ * milliseconds on the retrieval stream, milliseconds the caller's stream
+ * stalled waiting for due gathers at landings, gather batches}.  Syncs. */
+int hc_engine_retrieval_stats(hc_engine* eng, double* out4);
+
+/* Per-step idle gaps (ms) of the recorded timeline (does not reset). */
+int hc_engine_gaps(hc_engine* eng, float* out, int32_t cap, int32_t* n);
 
 /* Number of attention tiles (CTAs) the step launches. */
 int hc_engine_active_tiles(const hc_engine* eng, int32_t step, int32_t* n_tiles);

@@ -74,6 +74,8 @@ def _declare(lib):
         "hc_engine_set_prefill_dump": (i32, [vp, vp]),
         "hc_engine_active_tiles": (i32, [vp, i32, vp]),
         "hc_engine_timing": (i32, [vp, i32, vp, vp]),
+        "hc_engine_retrieval_stats": (i32, [vp, vp]),
+        "hc_engine_gaps": (i32, [vp, vp, i32, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

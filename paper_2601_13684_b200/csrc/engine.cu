@@ -122,6 +122,7 @@ struct EngineImpl {
   float *logits = nullptr, *stats = nullptr, *rowbuf = nullptr;
   uint32_t *top_idx = nullptr, *top_cnt = nullptr, *kbase = nullptr;
   uint32_t *ovl_cur = nullptr, *ovl_ring = nullptr;
+  uint32_t* ovl_host = nullptr;     // pinned readback of the overlap window
   uint64_t* thr = nullptr;          // per pivot slot: composite-key threshold of its top set
   int32_t* d_piv_slots = nullptr;   // iota over pivot slots
   int last_t = 0;                   // last decode step run
@@ -155,6 +156,9 @@ struct EngineImpl {
   bool timing = false;
   std::vector<cudaEvent_t> tev;
   size_t tev_used = 0;  // steps recorded
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> gather_ev;  // retrieval-stream gathers
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> land_ev;    // caller-stream landing waits
+  int64_t gather_rows_issued = 0;
   // prefill scratch
   float* prefill_dump = nullptr;
   char* pf = nullptr;
@@ -177,6 +181,7 @@ int engine_destroy(EngineImpl& e) {
   cudaDeviceSynchronize();
   for (auto& pr : e.stage_busy) cudaEventDestroy(std::get<2>(pr));
   if (e.stage) cudaFreeHost(e.stage);
+  if (e.ovl_host) cudaFreeHost(e.ovl_host);
   for (auto ev : e.events) cudaEventDestroy(ev);
   for (auto& x : e.xfers) {
     if (x.sel) cudaFree(x.sel);
@@ -389,6 +394,16 @@ int engine_create(EngineImpl& e, const hc_engine_desc& c, const int32_t* roles,
       HC_TRY(dalloc((void**)&e.pool, bytes, &e.dev_bytes));
     }
   }
+  {  // keep stream-ordered allocations (fire / land descriptors) cached in the pool
+    int dev = 0;
+    cudaMemPool_t pool;
+    HC_CUDA_TRY(cudaGetDevice(&dev));
+    HC_CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t keep = ~uint64_t(0);
+    HC_CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  }
+  HC_CUDA_TRY(cudaHostAlloc((void**)&e.ovl_host, size_t(kRing) * std::max(1, e.n_piv) * 4,
+                            cudaHostAllocDefault));
   e.stage_cap = size_t(8) << 20;
   HC_CUDA_TRY(cudaHostAlloc((void**)&e.stage, e.stage_cap, cudaHostAllocDefault));
   int lo_prio = 0, hi_prio = 0;
@@ -610,9 +625,9 @@ __global__ void restamp_batch_kernel(uint32_t* kbase, const uint32_t* top_idx,
   }
 }
 
-int new_event(EngineImpl& e, cudaEvent_t* out) {
+int new_event(EngineImpl& e, cudaEvent_t* out, bool timed = false) {
   cudaEvent_t ev;
-  HC_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  HC_CUDA_TRY(cudaEventCreateWithFlags(&ev, timed ? cudaEventDefault : cudaEventDisableTiming));
   e.events.push_back(ev);
   *out = ev;
   return HC_OK;
@@ -620,37 +635,62 @@ int new_event(EngineImpl& e, cudaEvent_t* out) {
 
 // Issue the gathers of transfers `ids` (their units' staging buffers are free)
 // on the retrieval stream, after `after` (an event on the caller's stream).
-int issue_gathers(EngineImpl& e, const std::vector<int>& ids, cudaEvent_t after) {
-  if (ids.empty()) return HC_OK;
-  std::vector<XferDev> xd(ids.size());
-  int max_cap = 1;
-  for (size_t i = 0; i < ids.size(); ++i) {
-    Transfer& x = e.xfers[ids[i]];
-    const int u = x.unit;
-    x.buf = 1 - e.active[u];
-    const int ss = e.sat_slot[u];
-    const __nv_bfloat16* sk = e.pool + size_t(ss) * 2 * e.L * kHeadDim;
-    xd[i] = XferDev{x.sel, x.cnt, x.pos, x.meta, reinterpret_cast<const uint4*>(sk),
-                    reinterpret_cast<const uint4*>(sk + size_t(e.L) * kHeadDim),
-                    x.buf ? e.buf_row1[u] : e.buf_row0[u], x.completion, 0};
-    max_cap = std::max(max_cap, e.cap[u]);
-  }
+int issue_gathers(EngineImpl& e, const std::vector<int>& ids_in, cudaEvent_t after) {
+  if (ids_in.empty()) return HC_OK;
+  // one batch per completion step (ascending): a landing then waits only for
+  // the gathers that are due, not for the whole burst of a drift event
+  std::vector<int> ids(ids_in);
+  std::stable_sort(ids.begin(), ids.end(), [&](int a, int b) {
+    return e.xfers[a].completion < e.xfers[b].completion;
+  });
   HC_CUDA_TRY(cudaStreamWaitEvent(e.retr, after, 0));
-  XferDev* d = nullptr;
-  HC_TRY(upload(e, xd.data(), xd.size() * sizeof(XferDev), e.retr, (void**)&d));
-  build_positions_batch_kernel<<<int(xd.size()), 256, 0, e.retr>>>(d, e.L, e.S, e.R);
-  HC_CHECK_LAUNCH();
-  const int per = std::max(1, std::min(16, (max_cap + 127) / 128));
-  gather_rows_batch_kernel<<<dim3(per, int(xd.size())), 256, 0, e.retr>>>(
-      d, reinterpret_cast<uint4*>(e.K), reinterpret_cast<uint4*>(e.V));
-  HC_CHECK_LAUNCH();
-  HC_CUDA_TRY(cudaFreeAsync(d, e.retr));
-  cudaEvent_t done;
-  HC_TRY(new_event(e, &done));
-  HC_CUDA_TRY(cudaEventRecord(done, e.retr));
-  for (int id : ids) {
-    e.xfers[id].done = done;
-    e.xfers[id].gathered = true;
+  size_t lo = 0;
+  while (lo < ids.size()) {
+    size_t hi = lo + 1;
+    while (hi < ids.size() && e.xfers[ids[hi]].completion == e.xfers[ids[lo]].completion) ++hi;
+    std::vector<XferDev> xd;
+    int max_cap = 1;
+    int64_t rows = 0;
+    for (size_t i = lo; i < hi; ++i) {
+      Transfer& x = e.xfers[ids[i]];
+      const int u = x.unit;
+      x.buf = 1 - e.active[u];
+      const int ss = e.sat_slot[u];
+      const __nv_bfloat16* sk = e.pool + size_t(ss) * 2 * e.L * kHeadDim;
+      xd.push_back(XferDev{x.sel, x.cnt, x.pos, x.meta, reinterpret_cast<const uint4*>(sk),
+                           reinterpret_cast<const uint4*>(sk + size_t(e.L) * kHeadDim),
+                           x.buf ? e.buf_row1[u] : e.buf_row0[u], x.completion, 0});
+      max_cap = std::max(max_cap, e.cap[u]);
+      rows += x.k + std::min(e.S, e.L) + e.R;  // upper bound of the rows moved
+    }
+    XferDev* d = nullptr;
+    HC_TRY(upload(e, xd.data(), xd.size() * sizeof(XferDev), e.retr, (void**)&d));
+    build_positions_batch_kernel<<<int(xd.size()), 256, 0, e.retr>>>(d, e.L, e.S, e.R);
+    HC_CHECK_LAUNCH();
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    if (e.timing) {
+      HC_TRY(new_event(e, &t0, true));
+      HC_TRY(new_event(e, &t1, true));
+      HC_CUDA_TRY(cudaEventRecord(t0, e.retr));
+    }
+    const int per = std::max(1, std::min(16, (max_cap + 127) / 128));
+    gather_rows_batch_kernel<<<dim3(per, int(xd.size())), 256, 0, e.retr>>>(
+        d, reinterpret_cast<uint4*>(e.K), reinterpret_cast<uint4*>(e.V));
+    HC_CHECK_LAUNCH();
+    if (e.timing) {
+      HC_CUDA_TRY(cudaEventRecord(t1, e.retr));
+      e.gather_ev.emplace_back(t0, t1);
+    }
+    e.gather_rows_issued += rows;
+    HC_CUDA_TRY(cudaFreeAsync(d, e.retr));
+    cudaEvent_t done;
+    HC_TRY(new_event(e, &done));
+    HC_CUDA_TRY(cudaEventRecord(done, e.retr));
+    for (size_t i = lo; i < hi; ++i) {
+      e.xfers[ids[i]].done = done;
+      e.xfers[ids[i]].gathered = true;
+    }
+    lo = hi;
   }
   return HC_OK;
 }
@@ -939,7 +979,17 @@ int engine_land_batch(EngineImpl& e, int n, const int32_t* ids, cudaStream_t st)
       HC_TRY(issue_gathers(e, {id}, ev));
     }
     if (x.done != last_wait) {
+      cudaEvent_t w0 = nullptr, w1 = nullptr;
+      if (e.timing) {
+        HC_TRY(new_event(e, &w0, true));
+        HC_TRY(new_event(e, &w1, true));
+        HC_CUDA_TRY(cudaEventRecord(w0, st));
+      }
       HC_CUDA_TRY(cudaStreamWaitEvent(st, x.done, 0));
+      if (e.timing) {
+        HC_CUDA_TRY(cudaEventRecord(w1, st));
+        e.land_ev.emplace_back(w0, w1);
+      }
       last_wait = x.done;
     }
     lds.push_back(LandDev{u, 0, x.buf ? e.buf_row1[u] : e.buf_row0[u], x.meta});
@@ -1042,11 +1092,21 @@ extern "C" int hc_engine_overlaps(hc_engine* eng, int32_t first, int32_t last, i
   auto& e = eng->e;
   HC_REQUIRE(last >= first && last - first < hc::kRing, HC_EINVAL, "overlap window too long");
   cudaStream_t st = (cudaStream_t)stream;
-  for (int t = first; t <= last; ++t)
-    HC_CUDA_TRY(cudaMemcpyAsync(out + size_t(t - first) * e.n_piv,
-                                e.ovl_ring + size_t(t % hc::kRing) * e.n_piv,
-                                size_t(e.n_piv) * 4, cudaMemcpyDeviceToHost, st));
+  if (!e.ovl_host)
+    HC_CUDA_TRY(cudaHostAlloc((void**)&e.ovl_host, size_t(hc::kRing) * std::max(1, e.n_piv) * 4,
+                              cudaHostAllocDefault));
+  // the window is at most two contiguous runs of the ring: one or two async copies, one sync
+  const int n = last - first + 1;
+  const int r0 = first % hc::kRing;
+  const int run1 = std::min(n, hc::kRing - r0);
+  const size_t row = size_t(e.n_piv) * 4;
+  HC_CUDA_TRY(cudaMemcpyAsync(e.ovl_host, e.ovl_ring + size_t(r0) * e.n_piv, row * run1,
+                              cudaMemcpyDeviceToHost, st));
+  if (run1 < n)
+    HC_CUDA_TRY(cudaMemcpyAsync(e.ovl_host + size_t(run1) * e.n_piv, e.ovl_ring,
+                                row * (n - run1), cudaMemcpyDeviceToHost, st));
   HC_CUDA_TRY(cudaStreamSynchronize(st));
+  std::memcpy(out, e.ovl_host, row * n);
   return HC_OK;
 }
 
@@ -1178,7 +1238,7 @@ extern "C" int hc_engine_timing(hc_engine* eng, int32_t enable, double* phase_ms
   auto& e = eng->e;
   constexpr int P = hc::EngineImpl::kPhaseEvents;
   if (phase_ms && steps) {
-    for (int k = 0; k < P; ++k) phase_ms[k] = 0;
+    for (int k = 0; k <= P; ++k) phase_ms[k] = 0;
     for (size_t i = 0; i < e.tev_used; ++i) {
       const cudaEvent_t* ev = e.tev.data() + i * P;
       HC_CUDA_TRY(cudaEventSynchronize(ev[P - 1]));
@@ -1190,10 +1250,57 @@ extern "C" int hc_engine_timing(hc_engine* eng, int32_t enable, double* phase_ms
       float tot = 0;
       HC_CUDA_TRY(cudaEventElapsedTime(&tot, ev[0], ev[P - 1]));
       phase_ms[P - 1] += tot;
+      if (i > 0) {  // idle (or landing-stall) gap between consecutive steps
+        float gap = 0;
+        HC_CUDA_TRY(cudaEventElapsedTime(&gap, ev[-1], ev[0]));
+        phase_ms[P] += gap;
+      }
     }
     *steps = int32_t(e.tev_used);
   }
   e.tev_used = 0;
   e.timing = enable != 0;
+  return HC_OK;
+}
+
+extern "C" int hc_engine_retrieval_stats(hc_engine* eng, double* out4) {
+  HC_REQUIRE(eng && out4, HC_EINVAL, "null argument");
+  auto& e = eng->e;
+  double g = 0, w = 0;
+  for (auto& pr : e.gather_ev) {
+    HC_CUDA_TRY(cudaEventSynchronize(pr.second));
+    float ms = 0;
+    HC_CUDA_TRY(cudaEventElapsedTime(&ms, pr.first, pr.second));
+    g += ms;
+  }
+  for (auto& pr : e.land_ev) {
+    HC_CUDA_TRY(cudaEventSynchronize(pr.second));
+    float ms = 0;
+    HC_CUDA_TRY(cudaEventElapsedTime(&ms, pr.first, pr.second));
+    w += ms;
+  }
+  out4[0] = double(e.gather_rows_issued) * 2 * hc::kHeadDim * 2;  // bytes (upper bound)
+  out4[1] = g;                                                     // gather kernel ms
+  out4[2] = w;                                                     // landing stall ms
+  out4[3] = double(e.gather_ev.size());
+  e.gather_ev.clear();
+  e.land_ev.clear();
+  e.gather_rows_issued = 0;
+  return HC_OK;
+}
+
+extern "C" int hc_engine_gaps(hc_engine* eng, float* out, int32_t cap, int32_t* n) {
+  HC_REQUIRE(eng && out && n, HC_EINVAL, "null argument");
+  auto& e = eng->e;
+  constexpr int P = hc::EngineImpl::kPhaseEvents;
+  int m = 0;
+  for (size_t i = 1; i < e.tev_used && m < cap; ++i) {
+    const cudaEvent_t* ev = e.tev.data() + i * P;
+    HC_CUDA_TRY(cudaEventSynchronize(ev[P - 1]));
+    float gap = 0;
+    HC_CUDA_TRY(cudaEventElapsedTime(&gap, ev[-1], ev[0]));
+    out[m++] = gap;
+  }
+  *n = m;
   return HC_OK;
 }

@@ -137,7 +137,9 @@ class HeteroCacheDecoder:
         self._cols = [[self.pivot_slot[self.unit(b, p)] for p in self.pivots] if self.monitor
                       else [] for b in range(self.B)]
         self._pinned = None
+        self._pin_head = 0
         self._uncollected = []
+        np.median(np.zeros((2, 2)), axis=0)  # first call imports numpy.ma (~30 ms): not mid-run
         self._fire_events = []
         self._prefilled = set()
 
@@ -211,6 +213,14 @@ class HeteroCacheDecoder:
                 for p in self.pivots:
                     st.buffers[p] = []
             st.rows.append(self._row(st, 0, 0))
+        if self.monitor:  # pinned landing zone for fetched sets: every satellite firing at once
+            import torch
+
+            cap = sum(self.effective_length(s) for p in self.pivots
+                      for s in self.satellites_of[p]) * self.B
+            self._pinned = torch.empty(max(4 * cap, 1 << 16), dtype=torch.int32,
+                                       pin_memory=True)  # four full drift bursts
+            self._pin_head = 0
 
     # ---- decode -------------------------------------------------------------------
 
@@ -283,7 +293,6 @@ class HeteroCacheDecoder:
         n = t - first + 1
         counts = np.empty((n, len(self.pivot_units)), dtype=np.int32)
         _lib.check(self.lib.hc_engine_overlaps(self.handle, first, t, counts.ctypes.data, sh))
-        self._collect_fetched()  # the sync above completed every earlier fetch copy
         vals = counts / self.l_base_int  # float64, == int / int in Python
         fire_units, fire_done = [], []
         for b, st in enumerate(self.states):
@@ -319,22 +328,20 @@ class HeteroCacheDecoder:
             self._fire_batch(t, fire_units, fire_done, sh)
 
     def _fire_batch(self, t: int, units, done, sh) -> None:
-        import torch
-
         evs = self._fire_events
         self._fire_events = []
         total = sum(sum(ev.ks) for _, ev in evs)
-        if self._pinned is None or self._pinned.numel() < total:
-            self._pinned = torch.empty(max(total, 1 << 20), dtype=torch.int32, pin_memory=True)
+        self._reserve_pinned(total)
+        base = self._pin_head
         n_ids = sum(len(ev.sats) for _, ev in evs)
         ids = np.zeros(n_ids, dtype=np.int32)
         u = np.asarray(units, dtype=np.int32)
         d = np.asarray(done, dtype=np.int32)
         _lib.check(self.lib.hc_engine_fire_batch(self.handle, len(u), u.ctypes.data, t,
                                                  d.ctypes.data, ids.ctypes.data,
-                                                 self._pinned.data_ptr(), sh))
+                                                 self._pinned.data_ptr() + 4 * base, sh))
         q = 0
-        off = 0
+        off = base
         for st, ev in evs:
             ev.tids = ids[q:q + len(ev.sats)].tolist()
             ev.offsets = []
@@ -346,6 +353,7 @@ class HeteroCacheDecoder:
                 st.pending.append((ev.completion_step, st.order, s, tid, k, ev))
                 st.order += 1
             self._uncollected.append(ev)
+        self._pin_head = off
         # completion steps are nondecreasing in firing order, but keep the
         # (completion, order) landing order explicit (engine.py:293-296)
         for st in self.states:
@@ -353,13 +361,26 @@ class HeteroCacheDecoder:
         if self.track_sets:
             self.sync()
 
+    def _reserve_pinned(self, total: int) -> None:
+        """Fetched sets land in a pinned ring; collect lazily, only before reuse."""
+        import torch
+
+        if self._pinned is None or self._pinned.numel() < total:
+            self.sync()
+            self._pinned = torch.empty(max(total, 1 << 16), dtype=torch.int32, pin_memory=True)
+            self._pin_head = 0
+        if self._pin_head + total > self._pinned.numel():
+            self.sync()  # copy out what the ring still holds before overwriting it
+            self._pin_head = 0
+
     def _collect_fetched(self) -> None:
         """Copy fetched index sets out of the pinned staging buffer (after a sync)."""
         if not self._uncollected:
             return
-        buf = self._pinned.numpy().view(np.uint32)
-        for ev in self._uncollected:
-            ev.fetched = [np.sort(buf[o:o + k]) for o, k in ev.offsets]
+        end = max(o + k for ev in self._uncollected for o, k in ev.offsets)
+        store = self._pinned.numpy().view(np.uint32)[:end].copy()  # one bulk copy
+        for ev in self._uncollected:  # K1 dense output is already ascending
+            ev.fetched = [store[o:o + k] for o, k in ev.offsets]
         self._uncollected = []
 
     def sync(self, stream=None) -> None:
@@ -376,16 +397,25 @@ class HeteroCacheDecoder:
                                                     _lib.stream_handle(stream)))
         return out.value
 
-    PHASES = ("append", "attention", "combine", "score_rows", "monitor", "ovl_copy", "step")
+    PHASES = ("append", "attention", "combine", "score_rows", "monitor", "ovl_copy", "step",
+              "inter_step_gap")
 
     def kernel_timing(self, enable: bool = True) -> dict:
         """Summed device milliseconds per decode-step phase since the last call."""
-        ms = (C.c_double * 7)()
+        ms = (C.c_double * 8)()
         n = C.c_int32()
         _lib.check(self.lib.hc_engine_timing(self.handle, int(enable), ms, C.byref(n)))
         out = dict(zip(self.PHASES, list(ms)))
         out["steps"] = n.value
         return out
+
+    def retrieval_stats(self) -> dict:
+        """Host-link retrieval since the last call (needs kernel_timing enabled)."""
+        out = (C.c_double * 4)()
+        _lib.check(self.lib.hc_engine_retrieval_stats(self.handle, out))
+        b, g, w, n = list(out)
+        return {"bytes": b, "gather_ms": g, "landing_stall_ms": w, "batches": int(n),
+                "host_link_gbs": (b / (g * 1e-3) / 1e9) if g > 0 else None}
 
     def active_tiles(self, t: int) -> int:
         n = C.c_int32()
