@@ -123,6 +123,23 @@ int hc_trace_recall(const hc_recall_head* heads_dev, int n_heads, uint32_t K,
 
 
 /* ---------------------------------------------------------------------------
+ * K5 -- prefill observation-window scoring on the tcgen05 tensor cores.
+ *
+ * Step-0 score rows (prefill_init input, engine.py:263-268; the last prompt
+ * token's GQA-mean post-softmax attention, export.ts:125-127 and
+ * model.ts:274-291) generalised to an observation window of `window` prompt
+ * tokens: score(t) = mean over the window*group query rows of softmax_t with
+ * causal masking.  window = 1 is exactly the reference semantics.
+ *   k_dev      [batch*kv_heads][L][128] bf16 keys
+ *   q_obs_dev  [batch][window][kv_heads*group][128] bf16 queries
+ *   rows_dev   [batch*kv_heads][row_stride] fp32 scores (first L written)
+ * window*group <= 128.
+ * ------------------------------------------------------------------------- */
+int hc_obs_scores(const void* k_dev, const void* q_obs_dev, int32_t batch, int32_t kv_heads,
+                  int32_t group, int32_t window, int32_t L, float* rows_dev, int64_t row_stride,
+                  void* stream);
+
+/* ---------------------------------------------------------------------------
  * Tensor-mode engine: hierarchical KV store + per-step decode pipeline.
  *
  * Units are (batch b, layer l, kv head h), numbered u = (b*NL + l)*H + h.
@@ -150,6 +167,7 @@ typedef struct hc_engine_desc {
   int32_t chunk;          /* split-K rows per tile, multiple of 64 (0: 1024)         */
   int32_t monitor;        /* drift monitoring on (variant != no_retrieval)           */
   int32_t host_pool;      /* 1: satellite prefill K/V in pinned host memory          */
+  int32_t obs_window;     /* prefill observation window w (0/1: last prompt token)   */
 } hc_engine_desc;
 
 /* CacheEngine.__init__ (engine.py:156-214): allocate and lay out the store.
@@ -164,9 +182,10 @@ int hc_engine_destroy(hc_engine* eng);
 int hc_engine_info(const hc_engine* eng, int64_t* out4);
 
 /* prefill_init (engine.py:263-274) for one layer: k/v [B, H, L, 128] bf16 and
- * q_last [B, H*G, 128] bf16 (the last prompt token's queries) on the device.
- * Scores every head with the last token's GQA-mean attention (the step-0
- * record, export.ts:125-127), selects top-l_h for compressed heads and
+ * q_obs [B, w, H*G, 128] bf16 (the last w prompt tokens' queries; w = 1:
+ * [B, H*G, 128]) on the device.  Scores every head with K5 (the step-0
+ * record: GQA-mean attention of the last token, export.ts:125-127, or its
+ * observation-window mean), selects top-l_h for compressed heads and
  * top-l_base for pivots (K_base), gathers the selected rows into the
  * compressed caches, copies full heads whole and satellites to the host pool. */
 int hc_engine_prefill_layer(hc_engine* eng, int32_t layer, const void* k_dev, const void* v_dev,
@@ -244,6 +263,9 @@ int hc_engine_retrieval_stats(hc_engine* eng, double* out4);
 
 /* Per-step idle gaps (ms) of the recorded timeline (does not reset). */
 int hc_engine_gaps(hc_engine* eng, float* out, int32_t cap, int32_t* n);
+
+/* Prefill scoring totals: out3 = {K5 milliseconds (CUDA events), layers, w}. */
+int hc_engine_prefill_stats(hc_engine* eng, double* out3);
 
 /* Number of attention tiles (CTAs) the step launches. */
 int hc_engine_active_tiles(const hc_engine* eng, int32_t step, int32_t* n_tiles);

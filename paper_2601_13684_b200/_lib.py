@@ -37,7 +37,8 @@ class TopkJob(C.Structure):
 class EngineDesc(C.Structure):
     _fields_ = [(n, C.c_int32) for n in (
         "batch", "num_layers", "kv_heads", "group", "head_dim", "prefill_len", "max_decode",
-        "sink_count", "recency_window", "l_base_int", "chunk", "monitor", "host_pool")]
+        "sink_count", "recency_window", "l_base_int", "chunk", "monitor", "host_pool",
+        "obs_window")]
 
 
 class RecallHead(C.Structure):
@@ -57,6 +58,7 @@ def _declare(lib):
         "hc_select_topk": (i32, [vp, vp, u32, u32, vp, vp, vp]),
         "hc_bitmap_from_indices": (i32, [vp, u32, vp, vp, u32, vp]),
         "hc_monitor_rows": (i32, [vp, C.c_int64, i32, u32, u32, vp, i32, vp, vp, vp]),
+        "hc_obs_scores": (i32, [vp, vp, i32, i32, i32, i32, i32, vp, C.c_int64, vp]),
         "hc_trace_recall": (i32, [vp, i32, u32, C.c_uint64, u32, u32, u32, u32, vp, vp]),
         "hc_engine_create": (i32, [vp, vp, vp, vp, vp]),
         "hc_engine_destroy": (i32, [vp]),
@@ -76,6 +78,7 @@ def _declare(lib):
         "hc_engine_timing": (i32, [vp, i32, vp, vp]),
         "hc_engine_retrieval_stats": (i32, [vp, vp]),
         "hc_engine_gaps": (i32, [vp, vp, i32, vp]),
+        "hc_engine_prefill_stats": (i32, [vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -401,12 +401,19 @@ __global__ void __launch_bounds__(256) score_rows_kernel(const AttnParams p,
 
 // ---- host launchers (used by engine.cu and the raw test entry point) ----
 
+int make_kv_tensor_map_rows(CUtensorMap* map, const void* base, int64_t rows, int box_rows);
+
 int make_kv_tensor_map(CUtensorMap* map, const void* base, int64_t rows) {
+  return make_kv_tensor_map_rows(map, base, rows, kSub);
+}
+
+// 2-D bf16 [rows x 128] tensor map, 128B swizzle, boxes of 64 columns x box_rows rows.
+int make_kv_tensor_map_rows(CUtensorMap* map, const void* base, int64_t rows, int box_rows) {
   HC_REQUIRE(rows > 0 && rows < (int64_t(1) << 31), HC_EINVAL, "arena rows out of TMA range");
   HC_REQUIRE((reinterpret_cast<uintptr_t>(base) & 15) == 0, HC_EINVAL, "arena not 16B aligned");
   const cuuint64_t dims[2] = {cuuint64_t(kHeadDim), cuuint64_t(rows)};
   const cuuint64_t strides[1] = {cuuint64_t(kHeadDim * 2)};
-  const cuuint32_t box[2] = {64u, cuuint32_t(kSub)};
+  const cuuint32_t box[2] = {64u, cuuint32_t(box_rows)};
   const cuuint32_t estr[2] = {1u, 1u};
   // resolve the driver entry point at run time: the library must load (and
   // export its ABI) on hosts without libcuda, e.g. the CPU build container

@@ -31,6 +31,9 @@ int launch_attention(const CUtensorMap& tmK, const CUtensorMap& tmV, const AttnP
                      int n_tiles, const int32_t* pivot_units_dev, int n_pivots, cudaStream_t st,
                      const cudaEvent_t* ev = nullptr);
 int launch_topk(const hc_topk_job* jobs_dev, int n_jobs, uint32_t n_add, cudaStream_t st);
+size_t obs_scratch_bytes(int n_units, int L);
+int launch_obs_scores(const void* k, const void* q_obs, int B, int H, int G, int w, int L,
+                      float* out, int64_t row_stride, void* scratch, cudaStream_t st);
 int launch_monitor(const float* rows, int64_t row_stride, const int32_t* slots, int n_rows,
                    uint32_t n, uint32_t k, const uint32_t* kbase, int words, uint64_t* thr,
                    uint32_t* ovl, cudaStream_t st);
@@ -58,9 +61,6 @@ __global__ void append_kernel(const UnitDesc* __restrict__ units, int n_units, i
   else V[row * 16 + lane - 16] = v_new[size_t(u) * 16 + lane - 16];
 }
 
-__global__ void iota_kernel(int32_t* p, int n) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) p[i] = i;
-}
 
 struct Transfer {
   int unit = -1;
@@ -77,11 +77,6 @@ struct Transfer {
   cudaEvent_t done = nullptr;      // retrieval stream, after the gather (shared per batch)
 };
 
-#define HC_TRY(x)                    \
-  do {                               \
-    int _rc = (x);                   \
-    if (_rc != HC_OK) return _rc;    \
-  } while (0)
 
 int dalloc(void** p, size_t bytes, int64_t* counter) {
   if (bytes == 0) bytes = 16;
@@ -160,6 +155,10 @@ struct EngineImpl {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> land_ev;    // caller-stream landing waits
   int64_t gather_rows_issued = 0;
   // prefill scratch
+  int W = 1;                        // observation window (prompt tokens scored)
+  cudaEvent_t pf_ev0 = nullptr, pf_ev1 = nullptr;
+  double pf_score_ms = 0;
+  int pf_layers = 0;
   float* prefill_dump = nullptr;
   char* pf = nullptr;
   size_t pf_bytes = 0;
@@ -206,6 +205,8 @@ int engine_destroy(EngineImpl& e) {
     else cudaFree(e.pool);
   }
   if (e.retr) cudaStreamDestroy(e.retr);
+  if (e.pf_ev0) cudaEventDestroy(e.pf_ev0);
+  if (e.pf_ev1) cudaEventDestroy(e.pf_ev1);
   for (auto x : e.tev) cudaEventDestroy(x);
   return HC_OK;
 }
@@ -227,6 +228,9 @@ int engine_create(EngineImpl& e, const hc_engine_desc& c, const int32_t* roles,
   HC_REQUIRE(e.CH % 64 == 0, HC_EINVAL, "chunk must be a multiple of 64");
   e.lbase = c.l_base_int;
   e.pool_host = c.host_pool != 0;
+  e.W = c.obs_window > 0 ? c.obs_window : 1;
+  HC_REQUIRE(e.W * e.G <= 128 && e.W <= e.L, HC_EINVAL,
+             "observation window %d x group %d exceeds the 128 tcgen05 rows", e.W, e.G);
   const int LH = e.NL * e.H;
   e.role.assign(roles, roles + LH);
   e.length.assign(lengths, lengths + LH);
@@ -704,14 +708,9 @@ int engine_prefill_layer(EngineImpl& e, int layer, const __nv_bfloat16* k,
   // scratch layout
   size_t off = 0;
   auto carve = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~size_t(255); return o; };
-  const size_t o_units = carve(size_t(nu) * sizeof(UnitDesc));
-  const size_t o_tiles = carve(size_t(nu) * nch * sizeof(TileDesc));
-  const size_t o_part = carve(size_t(nu) * nch * e.G * kPartStride * 4);
-  const size_t o_logit = carve(size_t(nu) * e.G * Lp * 4);
-  const size_t o_stats = carve(size_t(nu) * e.G * 2 * 4);
   const size_t o_rows = carve(size_t(nu) * Lp * 4);
-  const size_t o_iota = carve(size_t(nu) * 4);
   const size_t o_jobs = carve(size_t(nu) * sizeof(hc_topk_job));
+  const size_t o_obs = carve(obs_scratch_bytes(nu, e.L));
   if (off > e.pf_bytes) {
     if (e.pf) {
       HC_CUDA_TRY(cudaStreamSynchronize(st));
@@ -722,56 +721,27 @@ int engine_prefill_layer(EngineImpl& e, int layer, const __nv_bfloat16* k,
     e.pf_bytes = off;
   }
   char* pf = e.pf;
-  std::vector<UnitDesc> ud(nu);
-  std::vector<TileDesc> td;
-  td.reserve(size_t(nu) * nch);
-  for (int i = 0; i < nu; ++i) {
-    const int b = i / e.H, h = i % e.H;
-    UnitDesc& d = ud[i];
-    d = UnitDesc{};
-    d.kind = kUnitFull;
-    d.row0 = int64_t(i) * e.L;
-    d.app_row = d.row0 + e.L;
-    d.n_prefix = e.L;
-    d.q_row = b * e.Hq + h * e.G;
-    d.pivot_slot = i;
-    d.slot0 = i * nch;
-    for (int ch = 0; ch < nch; ++ch)
-      td.push_back(TileDesc{uint32_t(i), uint32_t(ch), uint32_t(i * nch + ch), 0u});
+  float* rows = reinterpret_cast<float*>(pf + o_rows);
+  (void)nch;
+  // K5: step-0 score rows of every head of the layer on the tcgen05 tensor
+  // cores (observation window w; w = 1 is the reference's last-token row)
+  if (!e.pf_ev0) {
+    HC_CUDA_TRY(cudaEventCreate(&e.pf_ev0));
+    HC_CUDA_TRY(cudaEventCreate(&e.pf_ev1));
   }
-  // the prefill descriptors must stay valid until the kernels ran: copy on stream
-  HC_CUDA_TRY(cudaMemcpyAsync(pf + o_units, ud.data(), ud.size() * sizeof(UnitDesc),
-                              cudaMemcpyHostToDevice, st));
-  HC_CUDA_TRY(cudaMemcpyAsync(pf + o_tiles, td.data(), td.size() * sizeof(TileDesc),
-                              cudaMemcpyHostToDevice, st));
-  iota_kernel<<<(nu + 255) / 256, 256, 0, st>>>(reinterpret_cast<int32_t*>(pf + o_iota), nu);
-  HC_CHECK_LAUNCH();
-  CUtensorMap mk, mv;
-  HC_TRY(make_kv_tensor_map(&mk, k, int64_t(nu) * e.L));
-  HC_TRY(make_kv_tensor_map(&mv, v, int64_t(nu) * e.L));
-  AttnParams p{};
-  p.units = reinterpret_cast<UnitDesc*>(pf + o_units);
-  p.tiles = reinterpret_cast<TileDesc*>(pf + o_tiles);
-  p.q = q;
-  p.out = nullptr;
-  p.partial = reinterpret_cast<float*>(pf + o_part);
-  p.logits = reinterpret_cast<float*>(pf + o_logit);
-  p.stats = reinterpret_cast<float*>(pf + o_stats);
-  p.rows = reinterpret_cast<float*>(pf + o_rows);
-  p.logit_stride = Lp;
-  p.row_stride = Lp;
-  p.group = e.G;
-  p.L = e.L;
-  p.t = 0;
-  p.chunk = e.CH;
-  p.recency = e.R;
-  p.n_units = nu;
-  p.scale_log2 = float(1.4426950408889634 / 11.313708498984761);
-  HC_TRY(launch_attention(mk, mv, p, int(td.size()),
-                          reinterpret_cast<int32_t*>(pf + o_iota), nu, st));
+  HC_CUDA_TRY(cudaEventRecord(e.pf_ev0, st));
+  HC_TRY(launch_obs_scores(k, q, e.B, e.H, e.G, e.W, e.L, rows, Lp, pf + o_obs, st));
+  HC_CUDA_TRY(cudaEventRecord(e.pf_ev1, st));
+  HC_CUDA_TRY(cudaEventSynchronize(e.pf_ev1));
+  {
+    float ms = 0;
+    HC_CUDA_TRY(cudaEventElapsedTime(&ms, e.pf_ev0, e.pf_ev1));
+    e.pf_score_ms += ms;
+    e.pf_layers += 1;
+  }
   if (e.prefill_dump)  // test hook: step-0 rows [NL][B*H][L]
     HC_CUDA_TRY(cudaMemcpy2DAsync(e.prefill_dump + size_t(layer) * nu * e.L, size_t(e.L) * 4,
-                                  p.rows, size_t(Lp) * 4, size_t(e.L) * 4, nu,
+                                  rows, size_t(Lp) * 4, size_t(e.L) * 4, nu,
                                   cudaMemcpyDeviceToDevice, st));
 
   // K1: compressed heads select l_h (prefill_init, engine.py:265-268), pivots
@@ -783,7 +753,7 @@ int engine_prefill_layer(EngineImpl& e, int layer, const __nv_bfloat16* k,
     const int u = (b * e.NL + layer) * e.H + h;
     const int r = e.role[layer * e.H + h];
     hc_topk_job j{};
-    j.scores = p.rows + size_t(i) * Lp;
+    j.scores = rows + size_t(i) * Lp;
     j.n = uint32_t(e.L);
     if (r == HC_ROLE_ANCHOR || r == HC_ROLE_SATELLITE) {
       j.k = uint32_t(e.length[layer * e.H + h]);
@@ -1302,5 +1272,14 @@ extern "C" int hc_engine_gaps(hc_engine* eng, float* out, int32_t cap, int32_t* 
     out[m++] = gap;
   }
   *n = m;
+  return HC_OK;
+}
+
+extern "C" int hc_engine_prefill_stats(hc_engine* eng, double* out3) {
+  HC_REQUIRE(eng && out3, HC_EINVAL, "null argument");
+  auto& e = eng->e;
+  out3[0] = e.pf_score_ms;
+  out3[1] = e.pf_layers;
+  out3[2] = e.W;
   return HC_OK;
 }

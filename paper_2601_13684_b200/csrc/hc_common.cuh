@@ -49,6 +49,13 @@ void count_launch();
     }                                                                          \
   } while (0)
 
+#define HC_TRY(x)                                                              \
+  do {                                                                         \
+    int _rc = (x);                                                             \
+    if (_rc != HC_OK) return _rc;                                              \
+  } while (0)
+#define HC_TRY_RC(x) HC_TRY(x)
+
 // Order-preserving map of an fp32 score to uint32 (larger score -> larger
 // key).  -0.0 is folded onto +0.0 so that equal scores tie exactly as they
 // do under Python float comparison (metrics.py:44 sorts on -score).

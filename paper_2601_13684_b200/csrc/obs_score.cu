@@ -1,0 +1,404 @@
+// K5: prefill observation-window scoring on the 5th-generation tensor cores.
+//
+// The step-0 record of a head is the last prompt token's post-softmax
+// attention averaged over the G query heads of its GQA group (export.ts:125-127,
+// model.ts:274-291).  Generalised to an observation window of w prompt tokens
+// (w = 1 is exactly the reference semantics), the score of key t is
+//     score(t) = 1/(w*G) * sum_{i<w, j<G} softmax_t(q_{i,j} . k_t / sqrt(d)),
+// with query i = prompt position L-w+i seeing keys t <= L-w+i (causal).
+// That is a dense contraction: the M = w*G query rows (padded to 128) of one
+// KV head against all L keys, so it runs as tcgen05 GEMM tiles:
+//   * warp 0: TMA producer -- Q_obs once (two 128B-swizzled 64-col boxes),
+//     then 128-key x 128-d K tiles into a 4-stage shared-memory ring;
+//   * warp 1: allocates 256 TMEM columns (two 128x128 fp32 accumulators) and
+//     issues tcgen05.mma.cta_group::1.kind::f16 (M=128, N=128, K=16 x 8)
+//     from shared-memory descriptors; tcgen05.commit frees ring slots and
+//     hands accumulators to the epilogue;
+//   * warps 2-5: epilogue, one thread per query row, tcgen05.ld 32x32b.x32.
+// Pass 1 keeps per-row online softmax statistics (max, sum) per key chunk;
+// obs_merge combines chunks; pass 2 recomputes the tiles and turns them into
+// probabilities, reduced over the rows with a warp transpose-reduction (31
+// shuffles per 32 columns) and across warps through shared memory.  Each key
+// tile's score column is owned by exactly one CTA: no atomics, deterministic.
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include <algorithm>
+
+#include "hc_common.cuh"
+
+namespace hc {
+namespace {
+
+constexpr int kM = 128;                 // query rows per KV head (w*G padded)
+constexpr int kN = 128;                 // keys per tile
+constexpr int kBox = 128 * 128;         // bytes of one 64-col x 128-row swizzled box
+constexpr int kTile = 2 * kBox;         // one K tile (128 keys x 128 d bf16)
+constexpr int kStagesObs = 4;
+constexpr int kObsThreads = 192;
+constexpr int kSmemObs = 1024 + kTile /*Q*/ + kStagesObs * kTile + 256 /*barriers*/ +
+                         4 * kN * 4 /*column partials*/;
+
+struct ObsParams {
+  int L;             // keys per unit
+  int rows;          // valid query rows (w * G)
+  int G;
+  int w;
+  int tiles_per_cta; // key tiles per CTA
+  int pass;          // 1: statistics, 2: scores
+  float scale_log2;  // log2(e) / sqrt(d)
+  float* part;       // pass 1 out: [unit][chunk][128][2] (m, l), log2 domain
+  const float* stats;  // pass 2 in: [unit][128][2] (M, L)
+  float* out;        // pass 2 out: [unit][row_stride]
+  int64_t row_stride;
+  int n_chunks;
+};
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mb_init(uint32_t b, uint32_t c) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b), "r"(c));
+}
+__device__ __forceinline__ void mb_expect(uint32_t b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mb_arrive(uint32_t b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(b) : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint32_t b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tW_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra W_%=;\n\t}" ::"r"(b),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma2d(uint32_t dst, const CUtensorMap* m, int c0, int c1,
+                                      uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+// Shared-memory matrix descriptor (sm_100 UMMA): K-major, 128B swizzle,
+// 8-row core-matrix groups 1024 B apart (SBO), version 1.
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr) {
+  uint64_t d = 0;
+  d |= uint64_t((addr >> 4) & 0x3FFF);          // start address
+  d |= uint64_t(1) << 16;                        // LBO (unused for swizzled K-major)
+  d |= uint64_t(1024 >> 4) << 32;                // SBO
+  d |= uint64_t(1) << 46;                        // descriptor version (sm_100)
+  d |= uint64_t(2) << 61;                        // SWIZZLE_128B
+  return d;
+}
+// Instruction descriptor: D f32, A/B bf16, both K-major, M=128, N=128.
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(kN >> 3) << 17) |
+                            (uint32_t(kM >> 4) << 24);
+
+__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(kIdesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   bar)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// Sum 32 column values over the 32 lanes (rows) of a warp: afterwards lane c
+// holds the total of column c (halving butterfly, 31 shuffles).
+__device__ __forceinline__ float transpose_reduce32(float (&v)[32]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    const bool upper = (lane & off) != 0;
+#pragma unroll
+    for (int j = 0; j < off; ++j) {
+      const float keep = upper ? v[j + off] : v[j];
+      const float send = upper ? v[j] : v[j + off];
+      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  return v[0];
+}
+
+__global__ void __launch_bounds__(kObsThreads, 1)
+obs_score_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmQ,
+                 const ObsParams p) {
+  extern __shared__ uint8_t sm_raw[];
+  const uint32_t base = (smem_addr(sm_raw) + 1023u) & ~1023u;
+  uint8_t* gbase = sm_raw + (base - smem_addr(sm_raw));
+  const uint32_t sQ = base;
+  const uint32_t sK = base + kTile;
+  const uint32_t bars = sK + kStagesObs * kTile;
+  const uint32_t full = bars, empty = bars + 8 * kStagesObs;
+  const uint32_t tfull = bars + 16 * kStagesObs, tempty = tfull + 16, qfull = tempty + 16;
+  const uint32_t tmem_slot = qfull + 8;
+  float* colsum = reinterpret_cast<float*>(gbase + (bars - base) + 256);  // [4][128]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(gbase + (tmem_slot - base));
+
+  const int unit = blockIdx.y, chunk = blockIdx.x;
+  const int tile0 = chunk * p.tiles_per_cta;
+  const int n_tiles_unit = (p.L + kN - 1) / kN;
+  const int n_tiles = min(p.tiles_per_cta, n_tiles_unit - tile0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStagesObs; ++s) {
+      mb_init(full + 8 * s, 1);
+      mb_init(empty + 8 * s, 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mb_init(tfull + 8 * a, 1);
+      mb_init(tempty + 8 * a, 4);  // one arrive per epilogue warp
+    }
+    mb_init(qfull, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {  // TMEM: two 128-column fp32 accumulators
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+                     tmem_slot));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp == 0) {
+    if (lane == 0 && n_tiles > 0) {
+      mb_expect(qfull, kTile);
+      tma2d(sQ, &tmQ, 0, unit * kM, qfull);
+      tma2d(sQ + kBox, &tmQ, 64, unit * kM, qfull);
+      for (int i = 0; i < n_tiles; ++i) {
+        const int s = i % kStagesObs;
+        mb_wait(empty + 8 * s, ((i / kStagesObs) & 1) ^ 1);
+        mb_expect(full + 8 * s, kTile);
+        const int row = unit * p.L + (tile0 + i) * kN;
+        tma2d(sK + s * kTile, &tmK, 0, row, full + 8 * s);
+        tma2d(sK + s * kTile + kBox, &tmK, 64, row, full + 8 * s);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0 && n_tiles > 0) {
+      mb_wait(qfull, 0);
+      for (int i = 0; i < n_tiles; ++i) {
+        const int s = i % kStagesObs, a = i & 1;
+        mb_wait(tempty + 8 * a, ((i >> 1) & 1) ^ 1);
+        mb_wait(full + 8 * s, (i / kStagesObs) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t d = tmem + a * kN;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t off = (kk >> 2) * kBox + (kk & 3) * 32;
+          umma(d, sdesc(sQ + off), sdesc(sK + s * kTile + off), kk > 0 ? 1u : 0u);
+        }
+        umma_commit(empty + 8 * s);  // ring slot reusable once these MMAs finish
+        umma_commit(tfull + 8 * a);  // accumulator ready for the epilogue
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- epilogue: thread = query row ----------------
+    const int q4 = warp & 3;                // TMEM lane quarter this warp may access
+    const int r = q4 * 32 + lane;            // query row
+    const bool row_ok = r < p.rows;
+    const int qpos = p.L - p.w + (row_ok ? r / p.G : 0);  // causal limit of this row
+    float m = -INFINITY, l = 0.f, Mr = 0.f, invL = 0.f;
+    if (p.pass == 2 && row_ok) {
+      Mr = p.stats[(size_t(unit) * kM + r) * 2 + 0];
+      const float Lr = p.stats[(size_t(unit) * kM + r) * 2 + 1];
+      invL = Lr > 0.f ? 1.f / Lr : 0.f;
+    }
+    const float inv_rows = 1.f / float(p.rows);
+    for (int i = 0; i < n_tiles; ++i) {
+      const int a = i & 1;
+      mb_wait(tfull + 8 * a, (i >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int key0 = (tile0 + i) * kN;
+      for (int c = 0; c < kN / 32; ++c) {
+        float v[32];
+        tmem_ld32(tmem + (uint32_t(q4 * 32) << 16) + a * kN + c * 32, v);
+        if (p.pass == 1) {
+          float tmax = -INFINITY;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int t = key0 + c * 32 + j;
+            v[j] = (row_ok && t <= qpos) ? v[j] * p.scale_log2 : -INFINITY;
+            tmax = fmaxf(tmax, v[j]);
+          }
+          const float mn = fmaxf(m, tmax);
+          const float mb = mn == -INFINITY ? 0.f : mn;
+          float s = 0.f;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) s += exp2f(v[j] - mb);
+          l = l * exp2f(m - mb) + s;
+          m = mn;
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int t = key0 + c * 32 + j;
+            v[j] = (row_ok && t <= qpos) ? exp2f(v[j] * p.scale_log2 - Mr) * invL : 0.f;
+          }
+          const float col = transpose_reduce32(v);  // lane = column c*32 + lane
+          colsum[q4 * kN + c * 32 + lane] = col;
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mb_arrive(tempty + 8 * a);
+      if (p.pass == 2) {
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        const int t = threadIdx.x - 64;  // 0..127: one key column each
+        const float sum = (colsum[t] + colsum[kN + t]) + (colsum[2 * kN + t] + colsum[3 * kN + t]);
+        if (key0 + t < p.L) p.out[size_t(unit) * p.row_stride + key0 + t] = sum * inv_rows;
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+      }
+    }
+    if (p.pass == 1) {
+      float* dst = p.part + ((size_t(unit) * p.n_chunks + chunk) * kM + r) * 2;
+      dst[0] = m;
+      dst[1] = l;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+}
+
+// Combine pass-1 chunk statistics: (M, L) per query row, log2 domain.
+__global__ void obs_merge_kernel(const float* __restrict__ part, int n_chunks,
+                                 float* __restrict__ stats) {
+  const int unit = blockIdx.x, r = threadIdx.x;
+  const float* src = part + (size_t(unit) * n_chunks * kM + r) * 2;
+  float M = -INFINITY;
+  for (int c = 0; c < n_chunks; ++c) M = fmaxf(M, src[size_t(c) * kM * 2]);
+  const float mb = M == -INFINITY ? 0.f : M;
+  float L = 0.f;
+  for (int c = 0; c < n_chunks; ++c) {
+    const float l = src[size_t(c) * kM * 2 + 1];
+    if (l > 0.f) L += l * exp2f(src[size_t(c) * kM * 2] - mb);
+  }
+  stats[(size_t(unit) * kM + r) * 2 + 0] = mb;
+  stats[(size_t(unit) * kM + r) * 2 + 1] = L;
+}
+
+// Pack q_obs [B][w][H*G][128] into the padded [B*H][128][128] operand
+// (row r = i*G + j of KV head h: query head h*G+j at window position i).
+__global__ void obs_pack_q_kernel(const __nv_bfloat16* __restrict__ q, int H, int G, int w,
+                                  __nv_bfloat16* __restrict__ qp) {
+  const int unit = blockIdx.x, r = blockIdx.y;  // unit = b*H + h
+  const int b = unit / H, h = unit % H;
+  const int d = threadIdx.x;
+  __nv_bfloat16 val = __float2bfloat16_rn(0.f);
+  if (r < w * G) {
+    const int i = r / G, j = r % G;
+    val = q[((size_t(b) * w + i) * (H * G) + h * G + j) * 128 + d];
+  }
+  qp[(size_t(unit) * kM + r) * 128 + d] = val;
+}
+
+}  // namespace
+
+int make_kv_tensor_map_rows(CUtensorMap* map, const void* base, int64_t rows, int box_rows);
+
+// Score rows for n_units KV heads whose keys are k[unit*L + t][128] and whose
+// observation queries are q_obs [B][w][H*G][128] (n_units = B*H).  `scratch`
+// must hold obs_scratch_bytes(); out rows have stride row_stride floats.
+size_t obs_scratch_bytes(int n_units, int L) {
+  const int n_tiles = (L + kN - 1) / kN;
+  const int tiles_per_cta = 64;
+  const int n_chunks = (n_tiles + tiles_per_cta - 1) / tiles_per_cta;
+  return size_t(n_units) * kM * 128 * 2 /*packed Q*/ +
+         size_t(n_units) * n_chunks * kM * 2 * 4 /*partials*/ + size_t(n_units) * kM * 2 * 4;
+}
+
+int launch_obs_scores(const void* k, const void* q_obs, int B, int H, int G, int w, int L,
+                      float* out, int64_t row_stride, void* scratch, cudaStream_t st) {
+  HC_REQUIRE(w >= 1 && w * G <= kM, HC_EINVAL, "observation window %d x group %d > 128 rows", w,
+             G);
+  static bool configured = false;
+  if (!configured) {
+    HC_CUDA_TRY(cudaFuncSetAttribute(obs_score_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemObs));
+    configured = true;
+  }
+  const int n_units = B * H;
+  const int n_tiles = (L + kN - 1) / kN;
+  const int tiles_per_cta = 64;
+  const int n_chunks = (n_tiles + tiles_per_cta - 1) / tiles_per_cta;
+  char* sc = static_cast<char*>(scratch);
+  __nv_bfloat16* qp = reinterpret_cast<__nv_bfloat16*>(sc);
+  float* part = reinterpret_cast<float*>(sc + size_t(n_units) * kM * 128 * 2);
+  float* stats = part + size_t(n_units) * n_chunks * kM * 2;
+  obs_pack_q_kernel<<<dim3(n_units, kM), 128, 0, st>>>(
+      static_cast<const __nv_bfloat16*>(q_obs), H, G, w, qp);
+  HC_CHECK_LAUNCH();
+  CUtensorMap tk, tq;
+  HC_TRY_RC(make_kv_tensor_map_rows(&tk, k, int64_t(n_units) * L, 128));
+  HC_TRY_RC(make_kv_tensor_map_rows(&tq, qp, int64_t(n_units) * kM, 128));
+  ObsParams p{};
+  p.L = L;
+  p.rows = w * G;
+  p.G = G;
+  p.w = w;
+  p.tiles_per_cta = tiles_per_cta;
+  p.scale_log2 = float(1.4426950408889634 / 11.313708498984761);
+  p.part = part;
+  p.stats = stats;
+  p.out = out;
+  p.row_stride = row_stride;
+  p.n_chunks = n_chunks;
+  dim3 grid(n_chunks, n_units);
+  p.pass = 1;
+  obs_score_kernel<<<grid, kObsThreads, kSmemObs, st>>>(tk, tq, p);
+  HC_CHECK_LAUNCH();
+  obs_merge_kernel<<<n_units, kM, 0, st>>>(part, n_chunks, stats);
+  HC_CHECK_LAUNCH();
+  p.pass = 2;
+  obs_score_kernel<<<grid, kObsThreads, kSmemObs, st>>>(tk, tq, p);
+  HC_CHECK_LAUNCH();
+  return HC_OK;
+}
+
+}  // namespace hc
+
+extern "C" int hc_obs_scores(const void* k_dev, const void* q_obs_dev, int32_t batch,
+                             int32_t kv_heads, int32_t group, int32_t window, int32_t L,
+                             float* rows_dev, int64_t row_stride, void* stream) {
+  HC_REQUIRE(k_dev && q_obs_dev && rows_dev && batch > 0 && kv_heads > 0 && L > 0, HC_EINVAL,
+             "hc_obs_scores: bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t bytes = hc::obs_scratch_bytes(batch * kv_heads, L);
+  void* scratch = nullptr;
+  HC_CUDA_TRY(cudaMallocAsync(&scratch, bytes, st));
+  const int rc = hc::launch_obs_scores(k_dev, q_obs_dev, batch, kv_heads, group, window, L,
+                                       rows_dev, row_stride, scratch, st);
+  HC_CUDA_TRY(cudaFreeAsync(scratch, st));
+  return rc;
+}

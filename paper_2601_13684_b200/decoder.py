@@ -87,7 +87,7 @@ class HeteroCacheDecoder:
     def __init__(self, taxonomy, plan, config: EngineConfig = EngineConfig(), *, batch: int,
                  group: int, max_decode: int, head_dim: int = 128, chunk: int = 1024,
                  host_pool: bool = True, bytes_per_kv_entry: int | None = None,
-                 track_sets: bool = True):
+                 track_sets: bool = True, obs_window: int = 1):
         _lib.require_cuda()
         self.lib = _lib.load()
         self.taxonomy, self.plan, self.config = taxonomy, plan, config
@@ -120,7 +120,8 @@ class HeteroCacheDecoder:
                                head_dim=head_dim, prefill_len=self.L, max_decode=max_decode,
                                sink_count=config.sink_count, recency_window=config.recency_window,
                                l_base_int=self.l_base_int, chunk=chunk, monitor=int(self.monitor),
-                               host_pool=int(host_pool))
+                               host_pool=int(host_pool), obs_window=obs_window)
+        self.W = obs_window
         h = C.c_void_p()
         _lib.check(self.lib.hc_engine_create(C.byref(desc), roles.ctypes.data, lengths.ctypes.data,
                                              cpiv.ctypes.data, C.byref(h)))
@@ -190,9 +191,12 @@ class HeteroCacheDecoder:
     # ---- prefill (engine.py:263-274) --------------------------------------------
 
     def prefill_layer(self, layer: int, k, v, q_last, stream=None) -> None:
-        """k, v: [B, H, L, D] bf16 device tensors; q_last: [B, H*G, D] bf16."""
+        """k, v: [B, H, L, D] bf16 device tensors; q_last: [B, H*G, D] bf16 (window 1)
+        or [B, w, H*G, D] (observation window w)."""
+        qshape = (self.B, self.H * self.G, self.D) if self.W == 1 else \
+            (self.B, self.W, self.H * self.G, self.D)
         for t, shape in ((k, (self.B, self.H, self.L, self.D)), (v, (self.B, self.H, self.L, self.D)),
-                         (q_last, (self.B, self.H * self.G, self.D))):
+                         (q_last, qshape)):
             if tuple(t.shape) != shape or not t.is_contiguous() or not t.is_cuda:
                 raise EngineError(f"expected a contiguous CUDA tensor of shape {shape}")
         _lib.check(self.lib.hc_engine_prefill_layer(self.handle, layer, _lib.ptr(k), _lib.ptr(v),
@@ -416,6 +420,11 @@ class HeteroCacheDecoder:
         b, g, w, n = list(out)
         return {"bytes": b, "gather_ms": g, "landing_stall_ms": w, "batches": int(n),
                 "host_link_gbs": (b / (g * 1e-3) / 1e9) if g > 0 else None}
+
+    def prefill_stats(self) -> dict:
+        out = (C.c_double * 3)()
+        _lib.check(self.lib.hc_engine_prefill_stats(self.handle, out))
+        return {"score_ms": out[0], "layers": int(out[1]), "window": int(out[2])}
 
     def active_tiles(self, t: int) -> int:
         n = C.c_int32()

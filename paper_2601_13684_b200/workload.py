@@ -131,8 +131,9 @@ class SyntheticKV:
         r = self.roles[h]
         return {"pivot": 0, "satellite": 0, "anchor": 2, "volatile": -1}[r]
 
-    def layer_kv(self, layer: int):
-        """K, V [B, H, L, D] bf16 and q_last [B, H*G, D] bf16 for one layer."""
+    def layer_kv(self, layer: int, window: int = 1):
+        """K, V [B, H, L, D] bf16 and the prefill observation queries for one layer:
+        q_last [B, H*G, D] (window 1) or [B, window, H*G, D] (last `window` tokens)."""
         torch = self.torch
         g = torch.Generator(device=self.dev).manual_seed(self.seed * 1000 + layer)
         B, H, L, D = self.B, self.H, self.L, self.D
@@ -147,8 +148,11 @@ class SyntheticKV:
                 add = self.alpha * self.u[:, layer, topic]               # [B, D]
                 k[:, h].scatter_add_(1, idx[:, :, None].expand(-1, -1, D),
                                      add[:, None, :].expand(-1, idx.shape[1], -1).contiguous())
-        q = self.queries(layer, 0)
-        return k.to(torch.bfloat16).contiguous(), v.to(torch.bfloat16).contiguous(), q
+        if window == 1:
+            q = self.queries(layer, 0)
+        else:
+            q = torch.stack([self.queries(layer, -1 - i) for i in range(window)][::-1], dim=1)
+        return k.to(torch.bfloat16).contiguous(), v.to(torch.bfloat16).contiguous(), q.contiguous()
 
     def queries(self, layer: int, step: int, shift_step: int | None = None):
         """[B, H*G, D] bf16 queries of one layer at a decode step."""

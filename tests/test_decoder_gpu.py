@@ -30,7 +30,8 @@ ROW_RTOL = 2e-3
 
 
 def _build(variant="heterocache", delay=1, bandwidth=1 << 30, B=2, NL=2, L=700, T=40,
-           chunk=256, host_pool=True, window=8, eval_every_step=False, shift=13, seed=3):
+           chunk=256, host_pool=True, window=8, eval_every_step=False, shift=13, seed=3,
+           obs_window=1):
     import torch
 
     from paper_2601_13684_b200.decoder import HeteroCacheDecoder
@@ -44,14 +45,14 @@ def _build(variant="heterocache", delay=1, bandwidth=1 << 30, B=2, NL=2, L=700, 
                        transfer_bandwidth=bandwidth, variant=variant,
                        eval_every_step=eval_every_step)
     dec = HeteroCacheDecoder(tax, plan, cfg, batch=B, group=model.group, max_decode=T,
-                             chunk=chunk, host_pool=host_pool)
+                             chunk=chunk, host_pool=host_pool, obs_window=obs_window)
     gen = SyntheticKV(model, batch=B, prefill_len=L, num_layers=NL, hot=plan.l_base_int,
                       seed=seed)
     dump = torch.zeros(NL, B * model.kv_heads, L, device="cuda")
     dec.lib.hc_engine_set_prefill_dump(dec.handle, dump.data_ptr())
     kv = []
     for l in range(NL):
-        k, v, q = gen.layer_kv(l)
+        k, v, q = gen.layer_kv(l, obs_window)
         dec.prefill_layer(l, k, v, q)
         kv.append((k, v, q))
     torch.cuda.synchronize()
@@ -196,6 +197,7 @@ def test_prefill_rows_match_oracle():
 @pytest.mark.parametrize("kw", [
     dict(delay=3), dict(bandwidth=20000, delay=2), dict(variant="no_allocation"),
     dict(eval_every_step=True), dict(window=4, shift=9), dict(host_pool=False),
+    dict(obs_window=8),
 ])
 def test_decoder_variants_match_oracle(kw):
     ctx = _build(**kw)

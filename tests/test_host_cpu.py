@@ -108,3 +108,19 @@ def test_completion_step_rule():
     cfg = EngineConfig(update_delay_steps=3, transfer_bandwidth=500)
     assert completion_step(24, 24576, cfg) == 50
     assert completion_step(24, 1000, cfg) == 27
+
+
+def test_sass_proves_blackwell_native_kernels():
+    """cuobjdump of libhcb200.so: tcgen05 MMAs (UTC*MMA), TMEM loads (LDTM),
+    TMA tensor loads (UTMALDG) -- the sm_100a evidence of K5 / K4."""
+    import shutil
+    import subprocess
+
+    from paper_2601_13684_b200 import _lib
+
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    out = subprocess.run([exe, "-sass", str(_lib.LIB_PATH)], capture_output=True, text=True).stdout
+    assert "sm_100a" in out or "SM100" in out.upper()
+    assert re.search(r"UTC\w*MMA", out), "no tcgen05 MMA in the SASS"
+    assert "LDTM" in out, "no tcgen05.ld (TMEM load) in the SASS"
+    assert "UTMALDG" in out, "no TMA tensor load in the SASS"
