@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--chunk", type=int, default=1024)
+    ap.add_argument("--obs-window", type=int, default=0,
+                    help="prefill observation window (0: min(32, 128 // G))")
     ap.add_argument("--link-mib-per-step", type=float, default=64.0,
                     help="EngineConfig.transfer_bandwidth in MiB per decode step (host link model)")
     return ap.parse_args()
@@ -141,18 +143,25 @@ def run_b200(args, rank, world):
                        transfer_bandwidth=int(args.link_mib_per_step * (1 << 20)))
     T = W + 2 * K + 8
     lib = _lib.load()
+    obs = args.obs_window or max(1, min(32, 128 // m.group))  # w_obs = 32 (Llama)
     dec = HeteroCacheDecoder(tax, plan, cfg, batch=w.batch, group=m.group, max_decode=T,
-                             chunk=args.chunk, host_pool=True, track_sets=False)
+                             chunk=args.chunk, host_pool=True, track_sets=False, obs_window=obs)
     gen = SyntheticKV(m, batch=w.batch, prefill_len=w.prefill_len, num_layers=w.num_layers,
                       hot=plan.l_base_int, seed=20261018 + 3 + rank)
     t0 = time.time()
     for l in range(w.num_layers):
-        k, v, q = gen.layer_kv(l)
+        k, v, q = gen.layer_kv(l, obs)
         dec.prefill_layer(l, k, v, q)
         del k, v, q
     torch.cuda.synchronize()
     dec.finish_prefill()
     prefill_s = time.time() - t0
+    pst = dec.prefill_stats()
+    # K5 per layer: K read twice (two passes), 2*M*N*K flops per 128x128x128 tile and pass
+    units_l = w.batch * m.kv_heads
+    score_bytes = 2 * units_l * w.prefill_len * m.head_dim * 2
+    score_flops = 2 * 2 * units_l * ((w.prefill_len + 127) // 128 * 128) * 128 * m.head_dim
+    score_ms = pst["score_ms"] / max(1, pst["layers"])
     # step inputs: 2 topics x 4 variants, cycled; topic flips every `period` steps
     pool = {ph: [gen.step_inputs(100 + 10 * ph + i, 0 if ph else None) for i in range(4)]
             for ph in (0, 1)}
@@ -277,6 +286,13 @@ def run_b200(args, rank, world):
                      "launches_timed": attn_n},
         "clocks": clk,
         "phase_ms_per_step": {k: v / max(1, attn_n) for k, v in phases.items() if k != "steps"},
+        "prefill_scoring": {
+            "kernel": "obs_score_kernel (K5, tcgen05.mma kind::f16 M=128 N=128, TMEM accumulators)",
+            "obs_window": obs, "rows_valid": obs * m.group, "ms_per_layer": score_ms,
+            "hbm_gbs": score_bytes / (score_ms * 1e-3) / 1e9 if score_ms else None,
+            "tflops_issued": score_flops / (score_ms * 1e-3) / 1e12 if score_ms else None,
+            "tensor_peak_tflops": peaks()[2].get("bf16_tflops"),
+        },
         "retrieval_events_timed_run": events,
         "retrieval": {"host_link_gbs": retr["host_link_gbs"], "bytes": retr["bytes"],
                       "gather_ms": retr["gather_ms"], "landing_stall_ms_total": retr["landing_stall_ms"],
