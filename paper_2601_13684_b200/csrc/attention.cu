@@ -297,61 +297,50 @@ attn_tiles_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant
 }
 
 // Merge a unit's split-K partials for one query head (block = (unit, g));
-// write O (bf16) and, for pivots, (M, L).  Slots are reduced in parallel:
-// block max of M_i, per-slot weights 2^(M_i - M) in shared memory, then each
-// thread d accumulates sum_i w_i O_i[d] with coalesced 512 B slot reads.
+// write O (bf16) and, for pivots, (M, L).  Block max of the slot maxima,
+// then warp w folds slots w, w+4, ... with lane l owning output dims
+// 4l..4l+3 (512 B coalesced per slot, 4 slots in flight per warp), and the
+// four warp partials meet in shared memory.
 __global__ void __launch_bounds__(128) combine_kernel(const AttnParams p) {
-  constexpr int kMaxSlots = 1024;
-  __shared__ float w[kMaxSlots];
   __shared__ float red[4];
+  __shared__ float rls[4];
+  __shared__ __align__(16) float racc[4][128];
   const UnitDesc u = p.units[blockIdx.x];
   const int g = blockIdx.y;
   const int G = p.group;
   const int n = unit_slots(u, p.t, p.L, p.chunk);
-  const int d = threadIdx.x, lane = d & 31, wid = d >> 5;
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   const float* base = p.partial + (size_t(u.slot0) * G + g) * kPartStride;
   const size_t sstride = size_t(G) * kPartStride;
   float m = -INFINITY;
-  for (int i = d; i < n; i += 128) m = fmaxf(m, base[i * sstride]);
+  for (int i = tid; i < n; i += 128) m = fmaxf(m, base[i * sstride]);
   for (int off = 16; off; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
-  if (lane == 0) red[wid] = m;
+  if (lane == 0) red[w] = m;
   __syncthreads();
   const float M = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
   const float mb = (M == -INFINITY) ? 0.f : M;
-  __syncthreads();
-  float Ls = 0.f, acc = 0.f;
-  for (int c0 = 0; c0 < n; c0 += kMaxSlots) {
-    const int cn = min(kMaxSlots, n - c0);
-    for (int i = d; i < cn; i += 128) {
-      const float* src = base + (c0 + i) * sstride;
-      const float li = src[1];
-      const float f = li == 0.f ? 0.f : exp2f(src[0] - mb);  // empty tile: O never written
-      w[i] = f;
-      Ls += li * f;
-    }
-    __syncthreads();
-    int i = 0;
-    for (; i + 4 <= cn; i += 4) {
-      const float* src = base + (c0 + i) * sstride + 4 + d;
-      const float o0 = w[i] != 0.f ? src[0] : 0.f;
-      const float o1 = w[i + 1] != 0.f ? src[sstride] : 0.f;
-      const float o2 = w[i + 2] != 0.f ? src[2 * sstride] : 0.f;
-      const float o3 = w[i + 3] != 0.f ? src[3 * sstride] : 0.f;
-      acc += w[i] * o0 + w[i + 1] * o1 + w[i + 2] * o2 + w[i + 3] * o3;
-    }
-    for (; i < cn; ++i) {
-      const float o = w[i] != 0.f ? base[(c0 + i) * sstride + 4 + d] : 0.f;
-      acc += w[i] * o;
-    }
-    __syncthreads();
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  float ls = 0.f;
+#pragma unroll 4
+  for (int i = w; i < n; i += 4) {
+    const float* src = base + i * sstride;
+    const float li = src[1];
+    const float f = li == 0.f ? 0.f : exp2f(src[0] - mb);  // empty tile: O never written
+    const float4 o = reinterpret_cast<const float4*>(src + 4)[lane];
+    acc.x += f == 0.f ? 0.f : f * o.x;
+    acc.y += f == 0.f ? 0.f : f * o.y;
+    acc.z += f == 0.f ? 0.f : f * o.z;
+    acc.w += f == 0.f ? 0.f : f * o.w;
+    ls += f * li;
   }
-  for (int off = 16; off; off >>= 1) Ls += __shfl_xor_sync(0xffffffffu, Ls, off);
-  if (lane == 0) red[wid] = Ls;
+  reinterpret_cast<float4*>(racc[w])[lane] = acc;
+  if (lane == 0) rls[w] = ls;
   __syncthreads();
-  Ls = (red[0] + red[1]) + (red[2] + red[3]);
+  const float Ls = (rls[0] + rls[1]) + (rls[2] + rls[3]);
+  const float a = (racc[0][tid] + racc[1][tid]) + (racc[2][tid] + racc[3][tid]);
   __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.out);
-  if (out) out[(size_t(u.q_row) + g) * kHeadDim + d] = __float2bfloat16_rn(acc / Ls);
-  if (u.pivot_slot >= 0 && d == 0) {
+  if (out) out[(size_t(u.q_row) + g) * kHeadDim + tid] = __float2bfloat16_rn(a / Ls);
+  if (u.pivot_slot >= 0 && tid == 0) {
     p.stats[(size_t(u.pivot_slot) * G + g) * 2 + 0] = M;
     p.stats[(size_t(u.pivot_slot) * G + g) * 2 + 1] = Ls;
   }
