@@ -140,6 +140,22 @@ int hc_obs_scores(const void* k_dev, const void* q_obs_dev, int32_t batch, int32
                   void* stream);
 
 /* ---------------------------------------------------------------------------
+ * K6 -- head-similarity profiling counts on the tcgen05 tensor cores.
+ *
+ * Every overlap coefficient of the taxonomy (metrics.py:74-106:
+ * stability vs the prefill set, same-step peer agreement; profiling.py:286-367)
+ * is |A & B| / min(|A|, |B|) over top-k index sets.  For each batch (one
+ * trace x layer) this computes the full Gram matrix of the 0/1 indicator
+ * matrix of its `sets` index sets (sel_dev [n_batches][sets][k_stride]
+ * positions < n_positions, counts_dev [n_batches][sets] set sizes):
+ *   gram_dev[batch][i][j] = |S_i & S_j|   (fp32, exact below 2^24),
+ * with row pitch rows_pad = ceil(sets / 128) * 128.
+ * ------------------------------------------------------------------------- */
+int hc_gram_from_sets(const uint32_t* sel_dev, const uint32_t* counts_dev, int32_t n_batches,
+                      int32_t sets, int32_t k_stride, int32_t n_positions, float* gram_dev,
+                      void* stream);
+
+/* ---------------------------------------------------------------------------
  * Tensor-mode engine: hierarchical KV store + per-step decode pipeline.
  *
  * Units are (batch b, layer l, kv head h), numbered u = (b*NL + l)*H + h.

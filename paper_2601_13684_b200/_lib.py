@@ -59,6 +59,7 @@ def _declare(lib):
         "hc_bitmap_from_indices": (i32, [vp, u32, vp, vp, u32, vp]),
         "hc_monitor_rows": (i32, [vp, C.c_int64, i32, u32, u32, vp, i32, vp, vp, vp]),
         "hc_obs_scores": (i32, [vp, vp, i32, i32, i32, i32, i32, vp, C.c_int64, vp]),
+        "hc_gram_from_sets": (i32, [vp, vp, i32, i32, i32, i32, vp, vp]),
         "hc_trace_recall": (i32, [vp, i32, u32, C.c_uint64, u32, u32, u32, u32, vp, vp]),
         "hc_engine_create": (i32, [vp, vp, vp, vp, vp]),
         "hc_engine_destroy": (i32, [vp]),

@@ -391,6 +391,8 @@ __global__ void __launch_bounds__(256) score_rows_kernel(const AttnParams p,
 // ---- host launchers (used by engine.cu and the raw test entry point) ----
 
 int make_kv_tensor_map_rows(CUtensorMap* map, const void* base, int64_t rows, int box_rows);
+int make_bf16_tensor_map(CUtensorMap* map, const void* base, int64_t rows, int64_t cols,
+                         int box_cols, int box_rows);
 
 int make_kv_tensor_map(CUtensorMap* map, const void* base, int64_t rows) {
   return make_kv_tensor_map_rows(map, base, rows, kSub);
@@ -398,12 +400,17 @@ int make_kv_tensor_map(CUtensorMap* map, const void* base, int64_t rows) {
 
 // 2-D bf16 [rows x 128] tensor map, 128B swizzle, boxes of 64 columns x box_rows rows.
 int make_kv_tensor_map_rows(CUtensorMap* map, const void* base, int64_t rows, int box_rows) {
-  HC_REQUIRE(rows > 0 && rows < (int64_t(1) << 31), HC_EINVAL, "arena rows out of TMA range");
-  HC_REQUIRE((reinterpret_cast<uintptr_t>(base) & 15) == 0, HC_EINVAL, "arena not 16B aligned");
-  const cuuint64_t dims[2] = {cuuint64_t(kHeadDim), cuuint64_t(rows)};
-  const cuuint64_t strides[1] = {cuuint64_t(kHeadDim * 2)};
-  const cuuint32_t box[2] = {64u, cuuint32_t(box_rows)};
-  const cuuint32_t estr[2] = {1u, 1u};
+  return make_bf16_tensor_map(map, base, rows, kHeadDim, 64, box_rows);
+}
+
+// Generic 2-D bf16 [rows x cols] row-major tensor map with 128B swizzle
+// (box_cols * 2 must be <= 128 B), out-of-bounds boxes zero-filled.
+int make_bf16_tensor_map(CUtensorMap* map, const void* base, int64_t rows, int64_t cols,
+                         int box_cols, int box_rows) {
+  HC_REQUIRE(rows > 0 && rows < (int64_t(1) << 31), HC_EINVAL, "tensor rows out of TMA range");
+  HC_REQUIRE((reinterpret_cast<uintptr_t>(base) & 15) == 0 && (cols * 2) % 16 == 0, HC_EINVAL,
+             "tensor base / row pitch not 16-B aligned");
+  HC_REQUIRE(box_cols * 2 <= 128 && box_rows <= 256, HC_EINVAL, "bad TMA box");
   // resolve the driver entry point at run time: the library must load (and
   // export its ABI) on hosts without libcuda, e.g. the CPU build container
   using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -418,11 +425,14 @@ int make_kv_tensor_map_rows(CUtensorMap* map, const void* base, int64_t rows, in
     HC_REQUIRE(fn && q == cudaDriverEntryPointSuccess, HC_ECUDA, "cuTensorMapEncodeTiled unavailable");
     encode = reinterpret_cast<EncodeFn>(fn);
   }
-  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
-                                      const_cast<void*>(base), dims, strides, box, estr,
-                                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  const cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
+  const cuuint64_t strides[1] = {cuuint64_t(cols * 2)};
+  const cuuint32_t box[2] = {cuuint32_t(box_cols), cuuint32_t(box_rows)};
+  const cuuint32_t estr[2] = {1u, 1u};
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                      strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   HC_REQUIRE(r == CUDA_SUCCESS, HC_ECUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
   return HC_OK;
 }

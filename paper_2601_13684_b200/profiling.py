@@ -9,8 +9,10 @@ greedy star clustering (most unassigned neighbours, ties to the lowest
 
 Device work: every (trace, step, layer, head) top-k set is selected by the
 K1 kernel in one batched launch (the reference's per-row Python sort,
-metrics.py:113-129); set intersections for the overlap coefficients are
-counted on the host from the selected index arrays.
+metrics.py:113-129), and every intersection size the overlap coefficients
+need is an entry of a per-layer Gram matrix of the sets' 0/1 indicator
+matrix, computed by K6 on the tcgen05 tensor cores (exact integer counts in
+fp32).  Medians, the agreement graph and the clustering stay on the host.
 """
 
 from __future__ import annotations
@@ -196,17 +198,44 @@ def _overlap(a: set, b: set) -> float:
     return len(a & b) / min(len(a), len(b))
 
 
-def step_sets(trace, k: int):
-    """Per-(layer, head) list of per-step top-k sets, selected on the GPU (K1)."""
+def step_set_gram(trace, k: int):
+    """Per-layer intersection counts of all per-step top-k sets, on the GPU.
+
+    K1 selects every (step, layer, head) top-k set in one batched launch
+    (metrics.py:113-129); K6 forms the Gram matrix of the 0/1 indicator
+    matrix of each layer's (step, head) sets on the tcgen05 tensor cores.
+    Returns (gram [NL, S, S] int64 with S = (T+1)*H, set index t*H + h;
+    sizes [T+1, NL, H]).
+    """
+    import torch
+
+    from . import _lib
     from .ops import topk_rows
 
     idx = trace.indices
     T1, NL, H, K = idx.shape
     sel, cnt = topk_rows(idx.reshape(-1, K), trace.scores.reshape(-1, K), k)
-    sel = sel.reshape(T1, NL, H, -1)
-    cnt = cnt.reshape(T1, NL, H)
-    return {(l, h): [set(sel[s, l, h, :cnt[s, l, h]].tolist()) for s in range(T1)]
-            for l in range(NL) for h in range(H)}
+    kk = sel.shape[1]
+    sel = sel.reshape(T1, NL, H, kk).transpose(1, 0, 2, 3).reshape(NL, T1 * H, kk)
+    cnt4 = cnt.reshape(T1, NL, H)
+    sets = T1 * H
+    rows_pad = (sets + 127) // 128 * 128
+    d_sel = torch.from_numpy(np.ascontiguousarray(sel).view(np.int32)).cuda()
+    d_cnt = torch.from_numpy(np.ascontiguousarray(cnt4.transpose(1, 0, 2).reshape(NL, sets))
+                             .view(np.int32)).cuda()
+    gram = torch.zeros((NL, rows_pad, rows_pad), dtype=torch.float32, device="cuda")
+    n_pos = trace.manifest.prefill_len + trace.manifest.decode_steps
+    _lib.check(_lib.load().hc_gram_from_sets(_lib.ptr(d_sel), _lib.ptr(d_cnt), NL, sets, kk,
+                                             n_pos, _lib.ptr(gram), _lib.stream_handle()))
+    g = gram.cpu().numpy()[:, :sets, :sets].astype(np.int64)
+    return g, cnt4.astype(np.int64)
+
+
+def _ovl(inter: int, a: int, b: int) -> float:
+    """metrics.py:74-79 from counts: |A & B| / min(|A|, |B|)."""
+    if a == 0 or b == 0:
+        raise ValueError("overlap coefficient is undefined for empty index sets")
+    return int(inter) / min(int(a), int(b))
 
 
 def _geometry(traces):
@@ -226,16 +255,21 @@ def _profile_and_pairs(traces, config: ProfileConfig):
     pair = {}
     for tr in traces:
         m = tr.manifest
-        sets = step_sets(tr, config.effective_topk(m.prefill_len))
+        gram, size = step_set_gram(tr, config.effective_topk(m.prefill_len))
         T = m.decode_steps
         if T < 1:
             raise ValueError("stability requires at least one decode step")
-        for (l, h), own in sets.items():
-            acc[(l, h)][0] += float(np.median([_overlap(s, own[0]) for s in own[1:]]))
-            peers = [sets[(l, p)] for p in range(H) if p != h]
-            if peers:
-                acc[(l, h)][1] += float(np.median(
-                    [max(_overlap(own[t], p[t]) for p in peers) for t in range(1, T + 1)]))
+
+        def ov(l, t1, h1, t2, h2):
+            return _ovl(gram[l, t1 * H + h1, t2 * H + h2], size[t1, l, h1], size[t2, l, h2])
+
+        for l in range(NL):
+            for h in range(H):
+                acc[(l, h)][0] += float(np.median([ov(l, t, h, 0, h) for t in range(1, T + 1)]))
+                if H > 1:
+                    acc[(l, h)][1] += float(np.median(
+                        [max(ov(l, t, h, t, p) for p in range(H) if p != h)
+                         for t in range(1, T + 1)]))
         if config.adjacency_step is not None:
             if not 1 <= config.adjacency_step <= T:
                 raise TaxonomyError(f"adjacency step {config.adjacency_step} outside 1..{T}")
@@ -245,8 +279,7 @@ def _profile_and_pairs(traces, config: ProfileConfig):
         for l in range(NL):
             for h1 in range(H):
                 for h2 in range(h1 + 1, H):
-                    v = float(np.median([_overlap(sets[(l, h1)][t], sets[(l, h2)][t])
-                                         for t in steps]))
+                    v = float(np.median([ov(l, t, h1, t, h2) for t in steps]))
                     pair[(l, h1, h2)] = pair.get((l, h1, h2), 0.0) + v
     n = len(traces)
     scores = {hd: HeadScores(s_stable=a[0] / n, s_sim=a[1] / n) for hd, a in acc.items()}

@@ -209,3 +209,32 @@ def _composite_keys(row):
     k32 = np.where(neg, ~u, u | np.uint32(0x80000000)).astype(np.uint64)
     pos = np.arange(row.size, dtype=np.uint64)
     return (k32 << np.uint64(32)) | (np.uint64(0xFFFFFFFF) - pos)
+
+
+def test_gram_counts_exact():
+    """K6 tcgen05 Gram of indicator sets == exact set intersections."""
+    import torch
+
+    from paper_2601_13684_b200 import _lib
+
+    rng = np.random.default_rng(3)
+    B, S, k, n = 3, 150, 400, 5000
+    sel = np.zeros((B, S, k), dtype=np.uint32)
+    cnt = rng.integers(1, k + 1, size=(B, S)).astype(np.uint32)
+    sets = []
+    for b in range(B):
+        for s in range(S):
+            ids = rng.choice(n, size=int(cnt[b, s]), replace=False)
+            sel[b, s, :cnt[b, s]] = ids
+            sets.append(set(ids.tolist()))
+    rows_pad = 256
+    gram = torch.zeros((B, rows_pad, rows_pad), device="cuda")
+    d_sel = torch.from_numpy(sel.view(np.int32)).cuda()
+    d_cnt = torch.from_numpy(cnt.view(np.int32)).cuda()
+    _lib.check(_lib.load().hc_gram_from_sets(d_sel.data_ptr(), d_cnt.data_ptr(), B, S, k, n,
+                                             gram.data_ptr(), _lib.stream_handle()))
+    g = gram.cpu().numpy()
+    for b in range(B):
+        for i in range(0, S, 7):
+            for j in range(0, S, 5):
+                assert g[b, i, j] == len(sets[b * S + i] & sets[b * S + j]), (b, i, j)
