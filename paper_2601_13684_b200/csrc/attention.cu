@@ -22,6 +22,7 @@
 
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include "hc_common.cuh"
 #include "kv_layout.cuh"
@@ -178,9 +179,16 @@ attn_tiles_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant
   for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
   float m_run = -INFINITY, l_run = 0.f;
   const int tb = warp * 16;  // this warp's 16 rows of each sub-tile
-  float* lg = nullptr;
-  if (unit.pivot_slot >= 0 && rg.pos >= 0 && row_ok)
-    lg = p.logits + (size_t(unit.pivot_slot) * G + g) * p.logit_stride + rg.pos;
+  // pivot score-row material: fp16 e = 2^(x - m) per token (m = this warp's
+  // running max after the 16-token group, one fp32 per group), finalised by
+  // score_rows_kernel once the global (M, L) are known
+  __half* lg = nullptr;
+  float* mr = nullptr;
+  if (unit.pivot_slot >= 0 && rg.pos >= 0 && row_ok) {
+    const size_t hg = size_t(unit.pivot_slot) * G + g;
+    lg = reinterpret_cast<__half*>(p.logits) + hg * p.logit_stride + rg.pos;
+    mr = p.mref + hg * (p.logit_stride / 16) + rg.pos / 16;
+  }
 
   for (int s = 0; s < n_sub; ++s) {
     const int st = s % kStages;
@@ -215,14 +223,6 @@ attn_tiles_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant
         x[nt][e] = tok < rg.n ? v : -INFINITY;
         mloc = fmaxf(mloc, x[nt][e]);
       }
-      if (lg) {
-        const int tok = base_tok + nt * 8 + 2 * c;
-        if (tok + 1 < rg.n) {
-          *reinterpret_cast<float2*>(lg + tok) = make_float2(x[nt][0], x[nt][1]);
-        } else if (tok < rg.n) {
-          lg[tok] = x[nt][0];
-        }
-      }
     }
     mloc = fmaxf(mloc, __shfl_xor_sync(0xffffffffu, mloc, 1));
     mloc = fmaxf(mloc, __shfl_xor_sync(0xffffffffu, mloc, 2));
@@ -234,6 +234,18 @@ attn_tiles_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant
     for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
       for (int e = 0; e < 2; ++e) pr[nt][e] = exp2f(x[nt][e] - mb);
+    if (lg) {
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const int tok = base_tok + nt * 8 + 2 * c;
+        if (tok + 1 < rg.n) {
+          *reinterpret_cast<__half2*>(lg + tok) = __floats2half2_rn(pr[nt][0], pr[nt][1]);
+        } else if (tok < rg.n) {
+          lg[tok] = __float2half_rn(pr[nt][0]);
+        }
+      }
+      if (c == 0 && base_tok < rg.n) mr[base_tok / 16] = mb;
+    }
     l_run = l_run * alpha + (pr[0][0] + pr[0][1]) + (pr[1][0] + pr[1][1]);
     m_run = m_new;
 #pragma unroll
@@ -347,37 +359,36 @@ __global__ void __launch_bounds__(128) combine_kernel(const AttnParams p) {
 }
 
 // GQA-mean probability row of every pivot over [0, L + t):
-//   row[pos] = (sum_j exp(s_j - M_j) * (1 / L_j)) / G   (model.ts:283-289 order)
-// 4 consecutive positions per thread (16 B loads of every head's logits).
+//   row[pos] = (sum_j e_j(pos) * 2^(m_j(pos/16) - M_j) * (1 / L_j)) / G
+// i.e. (sum_j exp(s_j - max_j) / sum_j) / G in head order (model.ts:283-289).
+// 4 consecutive positions per thread (8 B of fp16 per head).
 template <int G>
 __global__ void __launch_bounds__(256) score_rows_kernel(const AttnParams p,
                                                          const int32_t* __restrict__ pivot_units) {
   const UnitDesc u = p.units[pivot_units[blockIdx.y]];
   const int slot = u.pivot_slot;
   const int len = p.L + p.t;
-  float Mj[G], inv[G];
-#pragma unroll
-  for (int j = 0; j < G; ++j) {
-    Mj[j] = p.stats[(size_t(slot) * G + j) * 2 + 0];
-    inv[j] = 1.0f / p.stats[(size_t(slot) * G + j) * 2 + 1];
-  }
-  float* row = p.rows + size_t(slot) * p.row_stride;
-  const float* lg = p.logits + size_t(slot) * G * p.logit_stride;
   const int pos = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (pos >= len) return;
-  float4 x[G];
-#pragma unroll
-  for (int j = 0; j < G; ++j) x[j] = *reinterpret_cast<const float4*>(lg + size_t(j) * p.logit_stride + pos);
+  const __half* lg = reinterpret_cast<const __half*>(p.logits) + size_t(slot) * G * p.logit_stride;
+  const float* mr = p.mref + size_t(slot) * G * (p.logit_stride / 16);
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
   for (int j = 0; j < G; ++j) {
-    acc.x += exp2f(x[j].x - Mj[j]) * inv[j];
-    acc.y += exp2f(x[j].y - Mj[j]) * inv[j];
-    acc.z += exp2f(x[j].z - Mj[j]) * inv[j];
-    acc.w += exp2f(x[j].w - Mj[j]) * inv[j];
+    const float Mj = p.stats[(size_t(slot) * G + j) * 2 + 0];
+    const float inv = 1.0f / p.stats[(size_t(slot) * G + j) * 2 + 1];
+    const float cj = exp2f(mr[size_t(j) * (p.logit_stride / 16) + pos / 16] - Mj) * inv;
+    const uint2 raw = *reinterpret_cast<const uint2*>(lg + size_t(j) * p.logit_stride + pos);
+    const float2 e01 = __half22float2(*reinterpret_cast<const __half2*>(&raw.x));
+    const float2 e23 = __half22float2(*reinterpret_cast<const __half2*>(&raw.y));
+    acc.x += e01.x * cj;
+    acc.y += e01.y * cj;
+    acc.z += e23.x * cj;
+    acc.w += e23.y * cj;
   }
   const float rg = float(G);
   acc = make_float4(acc.x / rg, acc.y / rg, acc.z / rg, acc.w / rg);
+  float* row = p.rows + size_t(slot) * p.row_stride;
   if (pos + 3 < len) {
     *reinterpret_cast<float4*>(row + pos) = acc;
   } else {
@@ -460,8 +471,8 @@ int launch_attention(const CUtensorMap& tmK, const CUtensorMap& tmV, const AttnP
   }
   if (ev) HC_CUDA_TRY(cudaEventRecord(ev[2], st));
   if (n_pivots > 0 && p.rows) {
-    HC_REQUIRE(p.logit_stride % 4 == 0 && p.row_stride % 4 == 0, HC_EINVAL,
-               "score-row strides must be multiples of 4");
+    HC_REQUIRE(p.logit_stride % 16 == 0 && p.row_stride % 4 == 0, HC_EINVAL,
+               "score-row strides must be multiples of 16 / 4");
     const int len = p.L + p.t;
     dim3 grid((len + 1023) / 1024, n_pivots);
     switch (p.group) {

@@ -114,7 +114,8 @@ struct EngineImpl {
   int n_piv = 0;
   int64_t row_len = 0;
   int words = 0;
-  float *logits = nullptr, *stats = nullptr, *rowbuf = nullptr;
+  void* logits = nullptr;  // fp16 per-token pivot material
+  float *mref = nullptr, *stats = nullptr, *rowbuf = nullptr;
   uint32_t *top_idx = nullptr, *top_cnt = nullptr, *kbase = nullptr;
   uint32_t *ovl_cur = nullptr, *ovl_ring = nullptr;
   uint32_t* ovl_host = nullptr;     // pinned readback of the overlap window
@@ -194,7 +195,8 @@ int engine_destroy(EngineImpl& e) {
     if (e.pre_pos[u]) cudaFree(e.pre_pos[u]);
     if (e.pre_meta[u]) cudaFree(e.pre_meta[u]);
   }
-  void* ptrs[] = {e.d_units, e.K, e.V, e.d_tiles, e.partial, e.d_piv_units, e.logits, e.stats,
+  void* ptrs[] = {e.d_units, e.K, e.V, e.d_tiles, e.partial, e.d_piv_units, e.logits, e.mref,
+                  e.stats,
                   e.rowbuf, e.top_idx, e.top_cnt, e.kbase, e.ovl_cur, e.ovl_ring, e.d_piv_jobs,
                   e.thr, e.d_piv_slots,
                   e.pf};
@@ -259,7 +261,7 @@ int engine_create(EngineImpl& e, const hc_engine_desc& c, const int32_t* roles,
   e.pre_pos.assign(e.n_units, nullptr);
   e.pre_meta.assign(e.n_units, nullptr);
   e.fifo.assign(e.n_units, {});
-  e.row_len = (int64_t(e.L) + e.T + 3) / 4 * 4;  // 16-B aligned logit / score-row stride
+  e.row_len = (int64_t(e.L) + e.T + 15) / 16 * 16;  // aligned logit / score-row stride
   e.words = int((e.row_len + 31) / 32);
 
   // ---- arena rows and the static tile table ----
@@ -345,7 +347,8 @@ int engine_create(EngineImpl& e, const hc_engine_desc& c, const int32_t* roles,
   if (e.n_piv)
     HC_CUDA_TRY(cudaMemcpy(e.d_piv_units, e.piv_units.data(), size_t(e.n_piv) * 4,
                            cudaMemcpyHostToDevice));
-  HC_TRY(dalloc((void**)&e.logits, size_t(np) * e.G * e.row_len * 4, &e.dev_bytes));
+  HC_TRY(dalloc((void**)&e.logits, size_t(np) * e.G * e.row_len * 2, &e.dev_bytes));
+  HC_TRY(dalloc((void**)&e.mref, size_t(np) * e.G * (e.row_len / 16) * 4, &e.dev_bytes));
   HC_TRY(dalloc((void**)&e.stats, size_t(np) * e.G * 2 * 4, &e.dev_bytes));
   HC_TRY(dalloc((void**)&e.rowbuf, size_t(np) * e.row_len * 4, &e.dev_bytes));
   HC_TRY(dalloc((void**)&e.top_idx, size_t(np) * e.lbase * 4, &e.dev_bytes));
@@ -424,6 +427,7 @@ AttnParams decode_params(EngineImpl& e, int t, const void* q, void* o) {
   p.out = o;
   p.partial = e.partial;
   p.logits = e.logits;
+  p.mref = e.mref;
   p.stats = e.stats;
   p.rows = e.n_piv ? e.rowbuf : nullptr;
   p.logit_stride = e.row_len;

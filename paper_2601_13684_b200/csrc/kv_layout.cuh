@@ -112,7 +112,8 @@ struct AttnParams {
   const void* q;         // bf16 [q_rows][128]
   void* out;             // bf16 [q_rows][128] (combine)
   float* partial;        // [slots][G][kPartStride]
-  float* logits;         // [pivot slots][G][logit_stride]  (log2-domain scaled scores)
+  void* logits;          // [pivot slots][G][logit_stride] fp16 e = 2^(x - m_ref), x = log2 score
+  float* mref;           // [pivot slots][G][logit_stride / 16] m_ref per 16-position group
   float* stats;          // [pivot slots][G][2]  (M, L) after combine
   float* rows;           // [pivot slots][row_stride]  GQA-mean probability rows
   int64_t logit_stride;
