@@ -213,22 +213,48 @@ def run_b200(args, rank, world):
     events = sum(len(s.raw_events) for s in dec.states)
 
     # ---- timed: end to end through the API with pinned host buffers ----
+    # Every step's Q / K_new / V_new cross H2D from pinned memory and its O
+    # comes back D2H inside the timed region; copies run on a side stream,
+    # double-buffered, so step t+1's upload and step t's download overlap the
+    # decode of step t (events order every buffer reuse).
     hq = [[x.cpu().pin_memory() for x in pool[ph][i]] for ph in (0, 1) for i in range(4)]
-    hout = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
-    dq, dkn, dvn = (torch.empty_like(x) for x in pool[0][0])
+    hout = [torch.empty(out.shape, dtype=out.dtype, pin_memory=True) for _ in range(2)]
+    dbuf = [tuple(torch.empty_like(x) for x in pool[0][0]) for _ in range(2)]
+    obuf = [torch.empty_like(out) for _ in range(2)]
+    copy = torch.cuda.Stream()
+    mk = lambda: torch.cuda.Event(enable_timing=False)  # noqa: E731
+    ev_in, ev_used, ev_out = [mk(), mk()], [mk(), mk()], [mk(), mk()]
     h2d = sum(x.numel() * x.element_size() for x in hq[0])
-    d2h = hout.numel() * hout.element_size()
+    d2h = hout[0].numel() * hout[0].element_size()
+
+    def upload(tt, slot):
+        src = hq[(sum(tt >= x for x in shifts) % 2) * 4 + tt % 4]
+        with torch.cuda.stream(copy):
+            copy.wait_event(ev_used[slot])  # the decode that last read this slot is done
+            for dst, x in zip(dbuf[slot], src):
+                dst.copy_(x, non_blocking=True)
+            ev_in[slot].record(copy)
+
+    for e in ev_used + ev_out:
+        e.record(stream)
     barrier()
     torch.cuda.synchronize()
     ev0.record(stream)
-    for _ in range(K):
+    upload(t + 1, 0)
+    for i in range(K):
         t += 1
-        src = hq[(sum(t >= x for x in shifts) % 2) * 4 + t % 4]
-        dq.copy_(src[0], non_blocking=True)
-        dkn.copy_(src[1], non_blocking=True)
-        dvn.copy_(src[2], non_blocking=True)
-        dec.decode_step(t, dq, dkn, dvn, out, rows=False)
-        hout.copy_(out, non_blocking=True)
+        slot = i % 2
+        if i + 1 < K:
+            upload(t + 1, 1 - slot)
+        stream.wait_event(ev_in[slot])
+        stream.wait_event(ev_out[slot])  # previous download of this output slot finished
+        dec.decode_step(t, *dbuf[slot], obuf[slot], rows=False)
+        ev_used[slot].record(stream)
+        with torch.cuda.stream(copy):
+            copy.wait_event(ev_used[slot])
+            hout[slot].copy_(obuf[slot], non_blocking=True)
+            ev_out[slot].record(copy)
+    stream.wait_stream(copy)
     ev1.record(stream)
     torch.cuda.synchronize()
     barrier()

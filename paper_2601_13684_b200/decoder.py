@@ -37,6 +37,16 @@ from .reporting import RetrievalRecord, SimulationReport, StepRow
 ROLE_CODE = {"volatile": 0, "anchor": 1, "pivot": 2, "satellite": 3}
 
 
+def window_median(v: np.ndarray) -> np.ndarray:
+    """Column medians of a [W, m] float64 window, bit-identical to np.median(axis=0)
+    (middle element, or (a + b) / 2 of the middle pair: numpy's mean of two)."""
+    s = np.sort(v, axis=0)
+    n = s.shape[0]
+    if n % 2:
+        return s[n // 2]
+    return (s[n // 2 - 1] + s[n // 2]) / 2
+
+
 @dataclass
 class _Event:
     """A fired retrieval; fetched sets arrive asynchronously (pinned D2H)."""
@@ -299,6 +309,7 @@ class HeteroCacheDecoder:
         _lib.check(self.lib.hc_engine_overlaps(self.handle, first, t, counts.ctypes.data, sh))
         vals = counts / self.l_base_int  # float64, == int / int in Python
         fire_units, fire_done = [], []
+        med = None if cfg.eval_every_step else window_median(vals) < cfg.tau_drift
         for b, st in enumerate(self.states):
             cols = self._cols[b]
             if cfg.eval_every_step:
@@ -312,7 +323,7 @@ class HeteroCacheDecoder:
                         st.buffers[p] = []
                     fired_mask.append(fired)
             else:
-                fired_mask = (np.median(vals[:, cols], axis=0) < cfg.tau_drift).tolist()
+                fired_mask = med[cols].tolist()
             for j, p in enumerate(self.pivots):
                 if not fired_mask[j]:
                     continue

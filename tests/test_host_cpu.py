@@ -124,3 +124,18 @@ def test_sass_proves_blackwell_native_kernels():
     assert re.search(r"UTC\w*MMA", out), "no tcgen05 MMA in the SASS"
     assert "LDTM" in out, "no tcgen05.ld (TMEM load) in the SASS"
     assert "UTMALDG" in out, "no TMA tensor load in the SASS"
+
+
+def test_window_median_bit_identical_to_numpy():
+    from paper_2601_13684_b200.decoder import window_median
+
+    rng = np.random.default_rng(0)
+    for W in (1, 2, 3, 4, 7, 8, 9, 16):
+        for _ in range(50):
+            v = rng.integers(0, 6555, size=(W, 37)) / 6554  # overlap counts / l_base_int
+            v[rng.random(v.shape) < 0.3] = 0.5
+            got = window_median(v)
+            exp = np.median(v, axis=0)
+            assert np.array_equal(got, exp)
+            for j in range(v.shape[1]):  # the reference's per-list call (engine.py:250)
+                assert got[j] == np.median(list(v[:, j]))
