@@ -472,11 +472,11 @@ int engine_decode_step(EngineImpl& e, int t, const void* q, const void* kn, cons
   e.last_t = t;
   if (e.n_piv) {
     // K1+K2: top-l_base threshold and |top & K_base| per pivot (engine.py:305-311)
+    // counts land directly in the overlap ring row of this step
     HC_TRY(launch_monitor(e.rowbuf, e.row_len, e.d_piv_slots, e.n_piv, uint32_t(e.L + t),
-                          uint32_t(e.lbase), e.kbase, e.words, e.thr, e.ovl_cur, st));
+                          uint32_t(e.lbase), e.kbase, e.words, e.thr,
+                          e.ovl_ring + size_t(t % kRing) * e.n_piv, st));
     if (ev) HC_CUDA_TRY(cudaEventRecord(ev[5], st));
-    HC_CUDA_TRY(cudaMemcpyAsync(e.ovl_ring + size_t(t % kRing) * e.n_piv, e.ovl_cur,
-                                size_t(e.n_piv) * 4, cudaMemcpyDeviceToDevice, st));
   } else if (ev) {
     HC_CUDA_TRY(cudaEventRecord(ev[5], st));
   }

@@ -154,8 +154,10 @@ class SyntheticKV:
             q = torch.stack([self.queries(layer, -1 - i) for i in range(window)][::-1], dim=1)
         return k.to(torch.bfloat16).contiguous(), v.to(torch.bfloat16).contiguous(), q.contiguous()
 
-    def queries(self, layer: int, step: int, shift_step: int | None = None):
-        """[B, H*G, D] bf16 queries of one layer at a decode step."""
+    def queries(self, layer: int, step: int, shift_step=None):
+        """[B, H*G, D] bf16 queries of one layer at a decode step.  shift_step: the
+        step of the planted topic shift, or a sequence of shift steps (the cluster
+        topic toggles at each)."""
         torch = self.torch
         g = torch.Generator(device=self.dev).manual_seed((self.seed * 7919 + layer) * 100003 + step)
         B, H, G, D = self.B, self.H, self.G, self.D
@@ -164,8 +166,9 @@ class SyntheticKV:
             tp = self._head_topic(h)
             if tp < 0:
                 continue
-            if tp == 0 and shift_step is not None and step >= shift_step:
-                tp = 1
+            if tp == 0 and shift_step is not None:
+                shifts = shift_step if isinstance(shift_step, (list, tuple)) else (shift_step,)
+                tp = sum(step >= x for x in shifts) % 2
             q[:, h] += self.beta * self.u[:, layer, tp][:, None, :]
         return q.view(B, H * G, D).to(torch.bfloat16).contiguous()
 

@@ -31,7 +31,7 @@ ROW_RTOL = 2e-3
 
 def _build(variant="heterocache", delay=1, bandwidth=1 << 30, B=2, NL=2, L=700, T=40,
            chunk=256, host_pool=True, window=8, eval_every_step=False, shift=13, seed=3,
-           obs_window=1):
+           obs_window=1, sinks=4, recency=8):
     import torch
 
     from paper_2601_13684_b200.decoder import HeteroCacheDecoder
@@ -43,7 +43,8 @@ def _build(variant="heterocache", delay=1, bandwidth=1 << 30, B=2, NL=2, L=700, 
     tax, plan = plan_for(w)
     cfg = EngineConfig(tau_drift=0.5, window=window, update_delay_steps=delay,
                        transfer_bandwidth=bandwidth, variant=variant,
-                       eval_every_step=eval_every_step)
+                       eval_every_step=eval_every_step, sink_count=sinks,
+                       recency_window=recency)
     dec = HeteroCacheDecoder(tax, plan, cfg, batch=B, group=model.group, max_decode=T,
                              chunk=chunk, host_pool=host_pool, obs_window=obs_window)
     gen = SyntheticKV(model, batch=B, prefill_len=L, num_layers=NL, hot=plan.l_base_int,
@@ -198,6 +199,15 @@ def test_prefill_rows_match_oracle():
     dict(delay=3), dict(bandwidth=20000, delay=2), dict(variant="no_allocation"),
     dict(eval_every_step=True), dict(window=4, shift=9), dict(host_pool=False),
     dict(obs_window=8),
+    # transfers queue behind each other per satellite (completion far beyond the
+    # trigger), several land in the same step: FIFO staging + deferred gathers
+    dict(bandwidth=3000, window=4, shift=(6, 11, 19, 27), T=36),
+    dict(bandwidth=5000, window=4, shift=(5, 9, 13, 17, 21), eval_every_step=True, T=30),
+    # tiny prompt: L below one tile, recency tail reaching the sinks
+    dict(L=60, T=24, window=4, shift=9, chunk=64),
+    dict(L=700, T=20, window=4, shift=9, chunk=192, B=3),
+    dict(sinks=0, recency=0, window=4, shift=9, T=20),
+    dict(sinks=16, recency=32, window=4, shift=9, T=40),
 ])
 def test_decoder_variants_match_oracle(kw):
     ctx = _build(**kw)
@@ -225,3 +235,21 @@ def test_resident_rows_match_cache_view_sizes():
             want += len(O.resident_positions(ctx["L"], 12, base, cfg.sink_count,
                                              cfg.recency_window))
     assert got == want
+
+
+def test_queued_transfers_per_satellite_land_in_fifo_order():
+    """A starved host link (3000 B/step) keeps a pivot's earlier transfer in flight
+    when it fires again: the satellite's staging buffer is busy, the second gather
+    is deferred until the first lands (engine.py:293-299 FIFO), and the event log
+    still equals the oracle's."""
+    ctx = _build(bandwidth=3000, window=4, shift=(6, 11, 19, 27), T=36)
+    rows, _, _, _ = _run(ctx)
+    _check_events(ctx, rows)
+    queued = 0
+    for st in ctx["dec"].states:
+        ev = st.events
+        for a in ev:
+            for b in ev:
+                if b.pivot == a.pivot and a.trigger_step < b.trigger_step < a.completion_step:
+                    queued += 1
+    assert queued >= 1, "scenario must put two transfers of one pivot in flight at once"
