@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--chunk", type=int, default=1024)
+    ap.add_argument("--policy", choices=("heterocache", "full"), default="heterocache",
+                    help="full: FullAttention baseline through the same engine (all heads full)")
     ap.add_argument("--obs-window", type=int, default=0,
                     help="prefill observation window (0: min(32, 128 // G))")
     ap.add_argument("--link-mib-per-step", type=float, default=64.0,
@@ -132,7 +134,7 @@ def run_b200(args, rank, world):
         from dataclasses import replace
         w = replace(w, layers=args.layers)
     m = w.model
-    tax, plan = plan_for(w)
+    tax, plan = plan_for(w, args.policy)
     K, W = args.steps, args.warmup
     # one planted topic shift mid-run per timed loop (cfg4: every
     # ~1.5 windows) -- every pivot of every layer and sequence drifts at that step
@@ -272,7 +274,7 @@ def run_b200(args, rank, world):
     achieved = attn_bytes / (attn_avg_ms * 1e-3) / 1e9 if attn_avg_ms > 0 else 0.0
     traffic = None
     tf = ROOT / "profiles" / f"traffic_{args.workload}.json"
-    if tf.exists():
+    if tf.exists() and args.policy == "heterocache":
         traffic = json.loads(tf.read_text()).get("dram_bytes_per_launch")
     res = {
         "metric": METRIC,
@@ -292,7 +294,9 @@ def run_b200(args, rank, world):
                         f"{m.q_heads}q/{m.kv_heads}kv, d={m.head_dim})",
             "prefill_len": w.prefill_len, "batch_per_gpu": w.batch, "layers": w.num_layers,
             "compression": w.compression, "rho": plan.rho, "l_base_int": plan.l_base_int,
-            "roles_per_layer": list(m.layer_roles()),
+            "roles_per_layer": list(m.layer_roles()) if args.policy == "heterocache"
+            else ["volatile"] * m.kv_heads,
+            "policy": args.policy,
             "decode_window": cfg.window, "tau_drift": cfg.tau_drift,
             "topic_shifts_at_steps": shifts, "split_k_chunk": args.chunk,
             "transfer_bandwidth_bytes_per_step": cfg.transfer_bandwidth,

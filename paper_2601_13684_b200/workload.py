@@ -91,7 +91,21 @@ def rho_for(model: ModelShape, c: float) -> float:
     return (n_full + c * (len(per) - n_full)) / len(per)
 
 
-def plan_for(w: Workload):
+def plan_for(w: Workload, policy: str = "heterocache"):
+    """Taxonomy + plan of a workload.  policy "full" is the FullAttention
+    baseline (evaluation.py:165-190 full_oracle): every head keeps its whole
+    cache, nothing is monitored or retrieved."""
+    if policy == "full":
+        from .budget import BudgetPlan
+
+        per = w.model.layer_roles()
+        roles = {(l, h): "volatile" for l in range(w.num_layers) for h in range(len(per))}
+        tax = taxonomy_from_roles(roles, [], num_layers=w.num_layers,
+                                  heads_per_layer=w.model.kv_heads)
+        plan = BudgetPlan(rho=1.0, prefill_len=w.prefill_len, num_heads=len(roles),
+                          num_full=len(roles), num_comp=0, l_base=float(w.prefill_len),
+                          l_base_int=w.prefill_len, lengths={})
+        return tax, plan
     tax = roles_for(w.model, w.num_layers)
     plan = plan_budget(tax, BudgetConfig(rho=rho_for(w.model, w.compression), min_length=16),
                        w.prefill_len)
