@@ -35,7 +35,7 @@ constexpr int kM = 128;                 // query rows per KV head (w*G padded)
 constexpr int kN = 128;                 // keys per tile
 constexpr int kBox = 128 * 128;         // bytes of one 64-col x 128-row swizzled box
 constexpr int kTile = 2 * kBox;         // one K tile (128 keys x 128 d bf16)
-constexpr int kStagesObs = 4;
+constexpr int kStagesObs = 2;  // 2 CTAs per SM keep 4 K tiles in flight per SM
 constexpr int kObsThreads = 192;
 constexpr int kSmemObs = 1024 + kTile /*Q*/ + kStagesObs * kTile + 256 /*barriers*/ +
                          4 * kN * 4 /*column partials*/;
@@ -111,7 +111,7 @@ __device__ __forceinline__ void umma_commit(uint32_t bar) {
                : "memory");
 }
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
-  uint32_t r[32];
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
       "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
@@ -121,9 +121,9 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
         "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
         "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
       : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
 // Sum 32 column values over the 32 lanes (rows) of a warp: afterwards lane c
@@ -143,7 +143,7 @@ __device__ __forceinline__ float transpose_reduce32(float (&v)[32]) {
   return v[0];
 }
 
-__global__ void __launch_bounds__(kObsThreads, 1)
+__global__ void __launch_bounds__(kObsThreads, 2)
 obs_score_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmQ,
                  const ObsParams p) {
   extern __shared__ uint8_t sm_raw[];
@@ -227,11 +227,11 @@ obs_score_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant_
     const int r = q4 * 32 + lane;            // query row
     const bool row_ok = r < p.rows;
     const int qpos = p.L - p.w + (row_ok ? r / p.G : 0);  // causal limit of this row
-    float m = -INFINITY, l = 0.f, Mr = 0.f, invL = 0.f;
+    float m = -INFINITY, l = 0.f, Mr = 0.f, log2L = 0.f;
     if (p.pass == 2 && row_ok) {
       Mr = p.stats[(size_t(unit) * kM + r) * 2 + 0];
       const float Lr = p.stats[(size_t(unit) * kM + r) * 2 + 1];
-      invL = Lr > 0.f ? 1.f / Lr : 0.f;
+      log2L = Lr > 0.f ? log2f(Lr) : INFINITY;  // empty row: every probability is 0
     }
     const float inv_rows = 1.f / float(p.rows);
     for (int i = 0; i < n_tiles; ++i) {
@@ -239,32 +239,52 @@ obs_score_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant_
       mb_wait(tfull + 8 * a, (i >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int key0 = (tile0 + i) * kN;
-      for (int c = 0; c < kN / 32; ++c) {
-        float v[32];
-        tmem_ld32(tmem + (uint32_t(q4 * 32) << 16) + a * kN + c * 32, v);
-        if (p.pass == 1) {
-          float tmax = -INFINITY;
+      // two 32-column TMEM loads in flight per wait (64 registers)
+      for (int c2 = 0; c2 < kN / 32; c2 += 2) {
+        float v2[2][32];
+        tmem_ld32(tmem + (uint32_t(q4 * 32) << 16) + a * kN + c2 * 32, v2[0]);
+        tmem_ld32(tmem + (uint32_t(q4 * 32) << 16) + a * kN + (c2 + 1) * 32, v2[1]);
+        tmem_wait_ld();
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int t = key0 + c * 32 + j;
-            v[j] = (row_ok && t <= qpos) ? v[j] * p.scale_log2 : -INFINITY;
-            tmax = fmaxf(tmax, v[j]);
+        for (int h = 0; h < 2; ++h) {
+          float (&v)[32] = v2[h];
+          const int c = c2 + h;
+          const int first = key0 + c * 32;
+          const bool unmasked = row_ok && first + 31 <= qpos;  // common case: no causal cut
+          if (p.pass == 1) {
+            // max on raw scores (scale > 0), then exp2(v*scale - m) as one FFMA + EX2
+            float tmax = -INFINITY;
+            if (unmasked) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) tmax = fmaxf(tmax, v[j]);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                v[j] = (row_ok && first + j <= qpos) ? v[j] : -INFINITY;
+                tmax = fmaxf(tmax, v[j]);
+              }
+            }
+            const float mn = fmaxf(m, tmax * p.scale_log2);
+            const float mb = mn == -INFINITY ? 0.f : mn;
+            float s = 0.f;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) s += exp2f(fmaf(v[j], p.scale_log2, -mb));
+            l = l * exp2f(m - mb) + s;
+            m = mn;
+          } else {
+            // exp2(v*scale - M) / L  ==  exp2(v*scale - (M + log2 L)): one FFMA + EX2
+            const float off = -(Mr + log2L);
+            if (unmasked) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = exp2f(fmaf(v[j], p.scale_log2, off));
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                v[j] = (row_ok && first + j <= qpos) ? exp2f(fmaf(v[j], p.scale_log2, off)) : 0.f;
+            }
+            const float col = transpose_reduce32(v);  // lane = column c*32 + lane
+            colsum[q4 * kN + c * 32 + lane] = col;
           }
-          const float mn = fmaxf(m, tmax);
-          const float mb = mn == -INFINITY ? 0.f : mn;
-          float s = 0.f;
-#pragma unroll
-          for (int j = 0; j < 32; ++j) s += exp2f(v[j] - mb);
-          l = l * exp2f(m - mb) + s;
-          m = mn;
-        } else {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int t = key0 + c * 32 + j;
-            v[j] = (row_ok && t <= qpos) ? exp2f(v[j] * p.scale_log2 - Mr) * invL : 0.f;
-          }
-          const float col = transpose_reduce32(v);  // lane = column c*32 + lane
-          colsum[q4 * kN + c * 32 + lane] = col;
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -323,6 +343,13 @@ __global__ void obs_pack_q_kernel(const __nv_bfloat16* __restrict__ q, int H, in
   qp[(size_t(unit) * kM + r) * 128 + d] = val;
 }
 
+// Key tiles per CTA: about two waves of 2 CTAs x 148 SMs over all units.
+int obs_tiles_per_cta(int n_units, int n_tiles) {
+  const long total = long(n_units) * n_tiles;
+  const long ctas = 2L * 2 * 148;
+  return int(std::max(4L, (total + ctas - 1) / ctas));
+}
+
 }  // namespace
 
 int make_kv_tensor_map_rows(CUtensorMap* map, const void* base, int64_t rows, int box_rows);
@@ -332,7 +359,7 @@ int make_kv_tensor_map_rows(CUtensorMap* map, const void* base, int64_t rows, in
 // must hold obs_scratch_bytes(); out rows have stride row_stride floats.
 size_t obs_scratch_bytes(int n_units, int L) {
   const int n_tiles = (L + kN - 1) / kN;
-  const int tiles_per_cta = 64;
+  const int tiles_per_cta = obs_tiles_per_cta(n_units, n_tiles);
   const int n_chunks = (n_tiles + tiles_per_cta - 1) / tiles_per_cta;
   return size_t(n_units) * kM * 128 * 2 /*packed Q*/ +
          size_t(n_units) * n_chunks * kM * 2 * 4 /*partials*/ + size_t(n_units) * kM * 2 * 4;
@@ -350,7 +377,7 @@ int launch_obs_scores(const void* k, const void* q_obs, int B, int H, int G, int
   }
   const int n_units = B * H;
   const int n_tiles = (L + kN - 1) / kN;
-  const int tiles_per_cta = 64;
+  const int tiles_per_cta = obs_tiles_per_cta(n_units, n_tiles);
   const int n_chunks = (n_tiles + tiles_per_cta - 1) / tiles_per_cta;
   char* sc = static_cast<char*>(scratch);
   __nv_bfloat16* qp = reinterpret_cast<__nv_bfloat16*>(sc);
