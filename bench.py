@@ -136,11 +136,16 @@ def run_b200(args, rank, world):
     m = w.model
     tax, plan = plan_for(w, args.policy)
     K, W = args.steps, args.warmup
-    # one planted topic shift mid-run per timed loop (cfg4: every
-    # ~1.5 windows) -- every pivot of every layer and sequence drifts at that step
-    shifts = [W + K // 2, W + K + K // 2]
+    # every (sequence, layer) cluster drifts once inside each timed
+    # loop, staggered across the loop (cfg4: every 12 steps, staggered phases)
+    from paper_2601_13684_b200.workload import decode_queries, staggered_shifts
+
     if w.shift_every:
-        shifts = list(range(W + w.shift_every, W + 2 * K + 1, w.shift_every))
+        shifts = staggered_shifts(w.batch, w.num_layers, W + 1, 2 * K, w.shift_every)
+    else:
+        a_ = staggered_shifts(w.batch, w.num_layers, W + 1, K)
+        b_ = staggered_shifts(w.batch, w.num_layers, W + K + 1, K)
+        shifts = {key: a_[key] + b_[key] for key in a_}
     cfg = EngineConfig(tau_drift=0.5, window=8, update_delay_steps=1,
                        transfer_bandwidth=int(args.link_mib_per_step * (1 << 20)))
     T = W + 2 * K + 8
@@ -164,14 +169,14 @@ def run_b200(args, rank, world):
     score_bytes = 2 * units_l * w.prefill_len * m.head_dim * 2
     score_flops = 2 * 2 * units_l * ((w.prefill_len + 127) // 128 * 128) * 128 * m.head_dim
     score_ms = pst["score_ms"] / max(1, pst["layers"])
-    # step inputs: 2 topics x 4 variants, cycled; topic flips every `period` steps
-    pool = {ph: [gen.step_inputs(100 + 10 * ph + i, 0 if ph else None) for i in range(4)]
-            for ph in (0, 1)}
+    # step inputs: per-step queries (staggered cluster topics), K/V appends cycled
+    qs = decode_queries(gen, T, shifts)
+    kv_pool = [gen.step_inputs(100 + i, None)[1:] for i in range(4)]
 
     def inputs(t):
-        return pool[sum(t >= x for x in shifts) % 2][t % 4]
+        return (qs[t],) + kv_pool[t % 4]
 
-    out = torch.empty_like(pool[0][0][0])
+    out = torch.empty_like(qs[0])
     stream = torch.cuda.current_stream()
     t = 0
     for _ in range(W):
@@ -219,18 +224,21 @@ def run_b200(args, rank, world):
     # comes back D2H inside the timed region; copies run on a side stream,
     # double-buffered, so step t+1's upload and step t's download overlap the
     # decode of step t (events order every buffer reuse).
-    hq = [[x.cpu().pin_memory() for x in pool[ph][i]] for ph in (0, 1) for i in range(4)]
+    hq_all = qs[t + 1:t + K + 1].cpu().pin_memory()  # this loop's queries, pinned host
+    hkv = [[x.cpu().pin_memory() for x in kv] for kv in kv_pool]
     hout = [torch.empty(out.shape, dtype=out.dtype, pin_memory=True) for _ in range(2)]
-    dbuf = [tuple(torch.empty_like(x) for x in pool[0][0]) for _ in range(2)]
+    dbuf = [tuple(torch.empty_like(x) for x in inputs(1)) for _ in range(2)]
+    t_e2e0 = t
     obuf = [torch.empty_like(out) for _ in range(2)]
     copy = torch.cuda.Stream()
     mk = lambda: torch.cuda.Event(enable_timing=False)  # noqa: E731
     ev_in, ev_used, ev_out = [mk(), mk()], [mk(), mk()], [mk(), mk()]
-    h2d = sum(x.numel() * x.element_size() for x in hq[0])
+    h2d = hq_all[0].numel() * hq_all[0].element_size() + sum(
+        x.numel() * x.element_size() for x in hkv[0])
     d2h = hout[0].numel() * hout[0].element_size()
 
     def upload(tt, slot):
-        src = hq[(sum(tt >= x for x in shifts) % 2) * 4 + tt % 4]
+        src = (hq_all[tt - t_e2e0 - 1],) + tuple(hkv[tt % 4])
         with torch.cuda.stream(copy):
             copy.wait_event(ev_used[slot])  # the decode that last read this slot is done
             for dst, x in zip(dbuf[slot], src):
@@ -298,7 +306,10 @@ def run_b200(args, rank, world):
             else ["volatile"] * m.kv_heads,
             "policy": args.policy,
             "decode_window": cfg.window, "tau_drift": cfg.tau_drift,
-            "topic_shifts_at_steps": shifts, "split_k_chunk": args.chunk,
+            "topic_shifts": ("every cluster (sequence, layer) once per timed loop, staggered"
+                             if not w.shift_every else
+                             f"every {w.shift_every} steps per cluster, staggered phases"),
+            "split_k_chunk": args.chunk,
             "transfer_bandwidth_bytes_per_step": cfg.transfer_bandwidth,
             "l2": f"inputs larger than L2: {step_bytes / 1e9:.2f} GB of resident K/V read per step",
             "parallelism": f"replicas x{world} (weak: each GPU decodes its own batch)",

@@ -197,6 +197,55 @@ class SyntheticKV:
                 vn.to(torch.bfloat16).contiguous())
 
 
+def staggered_shifts(batch: int, num_layers: int, start: int, span: int, every: int = 0):
+    """Per-(sequence, layer) cluster shift steps, spread evenly over [start, start+span).
+
+    every == 0: one shift per cluster inside the span (SURVEY.md section 8d,
+    "one shift mid-run"), staggered so drift bursts stay within what the host
+    link can retrieve; every > 0: a shift every `every` steps with staggered
+    phases (cfg4, frequent drift).  Returns {(b, l): [steps]}.
+    """
+    n = batch * num_layers
+    out = {}
+    for b in range(batch):
+        for l in range(num_layers):
+            i = b * num_layers + l
+            if every:
+                out[(b, l)] = list(range(start + i % every, start + span, every))
+            else:
+                out[(b, l)] = [start + (i * span) // n]
+    return out
+
+
+def decode_queries(gen: "SyntheticKV", steps: int, shifts: dict, n_noise: int = 4):
+    """Queries for decode steps 1..steps: [steps + 1, B, NL, H*G, D] bf16 (device).
+
+    Cluster heads (pivot, satellites) of (b, l) follow topic u0 or u1, toggling at
+    each of that cluster's shift steps; noise cycles through n_noise draws."""
+    torch = gen.torch
+    B, NL, H, G, D = gen.B, gen.NL, gen.H, gen.G, gen.D
+    noise = []
+    for i in range(n_noise):
+        g = torch.Generator(device=gen.dev).manual_seed(gen.seed * 131 + i)
+        noise.append(torch.randn(B, NL, H, G, D, device=gen.dev, generator=g))
+    cluster = torch.tensor([gen._head_topic(h) == 0 for h in range(H)], device=gen.dev)
+    anchor = torch.tensor([gen._head_topic(h) == 2 for h in range(H)], device=gen.dev)
+    u = gen.u  # [B, NL, 3, D]
+    out = torch.empty(steps + 1, B, NL, H * G, D, device=gen.dev, dtype=torch.bfloat16)
+    topic = torch.zeros(steps + 1, B, NL, dtype=torch.long, device=gen.dev)
+    for (b, l), xs in shifts.items():
+        for x in xs:
+            if 0 <= x <= steps:
+                topic[x:, b, l] ^= 1
+    for t in range(steps + 1):
+        ut = torch.gather(u, 2, topic[t][:, :, None, None].expand(B, NL, 1, D))[:, :, 0]  # [B,NL,D]
+        q = noise[t % n_noise].clone()
+        q += gen.beta * (cluster[None, None, :, None, None] * ut[:, :, None, None, :])
+        q += gen.beta * (anchor[None, None, :, None, None] * u[:, :, 2][:, :, None, None, :])
+        out[t] = q.view(B, NL, H * G, D).to(torch.bfloat16)
+    return out
+
+
 def algorithmic_bytes(resident_rows: int, batch: int, num_layers: int, q_heads: int,
                       head_dim: int = 128) -> int:
     """resident K+V (bf16) plus Q in / O out per step."""
