@@ -277,7 +277,9 @@ def run_b200(args, rank, world):
     rows_avg = (rows_first + rows_last) / 2.0
     step_bytes = algorithmic_bytes(int(rows_avg), w.batch, w.num_layers, m.q_heads)
     attn_bytes = rows_avg * 2 * m.head_dim * 2 + w.batch * w.num_layers * m.q_heads * m.head_dim * 2 * 2
-    attn_avg_ms = attn_ms / max(1, attn_n)
+    # K4 phase minus the residual landing waits recorded inside it (a landing
+    # step runs K4 on the other units, waits for its gathers, then the rest)
+    attn_avg_ms = max(0.0, attn_ms - retr["landing_stall_ms"]) / max(1, attn_n)
     peak, peak_src, _ = peaks()
     achieved = attn_bytes / (attn_avg_ms * 1e-3) / 1e9 if attn_avg_ms > 0 else 0.0
     traffic = None

@@ -24,6 +24,8 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include <functional>
+
 #include "hc_common.cuh"
 #include "kv_layout.cuh"
 
@@ -110,6 +112,7 @@ attn_tiles_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant
   const uint32_t bar_empty = bar_full + kStages * 8;
 
   const TileDesc tile = p.tiles[blockIdx.x];
+  if (p.skip && p.skip[tile.unit]) return;  // landing unit: its tiles run after the landing
   const UnitDesc unit = p.units[tile.unit];
   const TileRange rg = tile_range(unit, tile.seg_chunk, p.t, p.L, p.recency, p.chunk);
   const int G = p.group;
@@ -448,22 +451,37 @@ int make_bf16_tensor_map(CUtensorMap* map, const void* base, int64_t rows, int64
   return HC_OK;
 }
 
-int launch_attention(const CUtensorMap& tmK, const CUtensorMap& tmV, const AttnParams& p,
-                     int n_tiles, const int32_t* pivot_units_dev, int n_pivots,
-                     cudaStream_t st, const cudaEvent_t* ev) {
-  // ev (optional): events recorded before K4, after K4, after combine, after score rows
+static int configure_attn() {
   static bool configured = false;
   if (!configured) {
     HC_CUDA_TRY(cudaFuncSetAttribute(attn_tiles_kernel,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemAttn));
     configured = true;
   }
-  HC_REQUIRE(p.group >= 1 && p.group <= 8, HC_EINVAL, "GQA group must be 1..8");
-  if (ev) HC_CUDA_TRY(cudaEventRecord(ev[0], st));
+  return HC_OK;
+}
+
+// K4 over an explicit tile list (p.tiles, n_tiles entries).
+int launch_attn_tiles(const CUtensorMap& tmK, const CUtensorMap& tmV, const AttnParams& p,
+                      int n_tiles, cudaStream_t st) {
+  HC_TRY(configure_attn());
   if (n_tiles > 0) {
     attn_tiles_kernel<<<n_tiles, kThreadsAttn, kSmemAttn, st>>>(tmK, tmV, p);
     HC_CHECK_LAUNCH();
   }
+  return HC_OK;
+}
+
+int launch_attention(const CUtensorMap& tmK, const CUtensorMap& tmV, const AttnParams& p,
+                     int n_tiles, const int32_t* pivot_units_dev, int n_pivots,
+                     cudaStream_t st, const cudaEvent_t* ev, const std::function<int()>* mid) {
+  // ev (optional): events recorded before K4, after K4, after combine, after score rows
+  // mid (optional): runs after the K4 launch, before combine (deferred landings)
+  HC_TRY(configure_attn());
+  HC_REQUIRE(p.group >= 1 && p.group <= 8, HC_EINVAL, "GQA group must be 1..8");
+  if (ev) HC_CUDA_TRY(cudaEventRecord(ev[0], st));
+  HC_TRY(launch_attn_tiles(tmK, tmV, p, n_tiles, st));
+  if (mid) HC_TRY((*mid)());
   if (ev) HC_CUDA_TRY(cudaEventRecord(ev[1], st));
   if (p.n_units > 0) {
     combine_kernel<<<dim3(p.n_units, p.group), 128, 0, st>>>(p);

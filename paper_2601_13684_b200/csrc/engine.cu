@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <cstring>
 #include <deque>
+#include <functional>
 #include <new>
 #include <tuple>
 #include <vector>
@@ -29,7 +30,10 @@ namespace hc {
 int make_kv_tensor_map(CUtensorMap* map, const void* base, int64_t rows);
 int launch_attention(const CUtensorMap& tmK, const CUtensorMap& tmV, const AttnParams& p,
                      int n_tiles, const int32_t* pivot_units_dev, int n_pivots, cudaStream_t st,
-                     const cudaEvent_t* ev = nullptr);
+                     const cudaEvent_t* ev = nullptr,
+                     const std::function<int()>* mid = nullptr);
+int launch_attn_tiles(const CUtensorMap& tmK, const CUtensorMap& tmV, const AttnParams& p,
+                      int n_tiles, cudaStream_t st);
 int launch_topk(const hc_topk_job* jobs_dev, int n_jobs, uint32_t n_add, cudaStream_t st);
 size_t obs_scratch_bytes(int n_units, int L);
 int launch_obs_scores(const void* k, const void* q_obs, int B, int H, int G, int w, int L,
@@ -105,7 +109,14 @@ struct EngineImpl {
   __nv_bfloat16 *K = nullptr, *V = nullptr;
   CUtensorMap tmK{}, tmV{};
   std::vector<uint32_t> t_act;  // sorted activation steps of the tile table
+  std::vector<TileDesc> tiles_host;          // the tile table (host copy, same order)
+  std::vector<std::vector<int>> unit_tiles;  // per unit: its entries in the tile table
   TileDesc* d_tiles = nullptr;
+  uint8_t* d_skip = nullptr;                 // per unit: K4 tiles deferred past a landing
+  // landings requested by hc_engine_land_batch, applied inside the next decode
+  // step: K4 runs every other unit while the gathers finish (see decode_step)
+  std::vector<int> deferred;
+  cudaStream_t deferred_st = nullptr;
   int n_slots = 0;
   float* partial = nullptr;
   // pivots
@@ -195,7 +206,7 @@ int engine_destroy(EngineImpl& e) {
     if (e.pre_pos[u]) cudaFree(e.pre_pos[u]);
     if (e.pre_meta[u]) cudaFree(e.pre_meta[u]);
   }
-  void* ptrs[] = {e.d_units, e.K, e.V, e.d_tiles, e.partial, e.d_piv_units, e.logits, e.mref,
+  void* ptrs[] = {e.d_units, e.K, e.V, e.d_tiles, e.d_skip, e.partial, e.d_piv_units, e.logits, e.mref,
                   e.stats,
                   e.rowbuf, e.top_idx, e.top_cnt, e.kbase, e.ovl_cur, e.ovl_ring, e.d_piv_jobs,
                   e.thr, e.d_piv_slots,
@@ -328,6 +339,10 @@ int engine_create(EngineImpl& e, const hc_engine_desc& c, const int32_t* roles,
                    [](const TileDesc& a, const TileDesc& b) { return a.t_act < b.t_act; });
   e.t_act.resize(tiles.size());
   for (size_t i = 0; i < tiles.size(); ++i) e.t_act[i] = tiles[i].t_act;
+  e.tiles_host = tiles;
+  e.unit_tiles.assign(e.n_units, {});
+  for (size_t i = 0; i < tiles.size(); ++i) e.unit_tiles[tiles[i].unit].push_back(int(i));
+  HC_TRY(dalloc((void**)&e.d_skip, size_t(e.n_units), &e.dev_bytes));
 
   HC_TRY(dalloc((void**)&e.K, size_t(e.rows) * kHeadDim * 2, &e.dev_bytes));
   HC_TRY(dalloc((void**)&e.V, size_t(e.rows) * kHeadDim * 2, &e.dev_bytes));
@@ -446,9 +461,73 @@ int active_tiles(const EngineImpl& e, int t) {
   return int(std::upper_bound(e.t_act.begin(), e.t_act.end(), uint32_t(t)) - e.t_act.begin());
 }
 
+int new_event(EngineImpl& e, cudaEvent_t* out, bool timed = false) {
+  cudaEvent_t ev;
+  HC_CUDA_TRY(cudaEventCreateWithFlags(&ev, timed ? cudaEventDefault : cudaEventDisableTiming));
+  e.events.push_back(ev);
+  *out = ev;
+  return HC_OK;
+}
+
+int upload(EngineImpl& e, const void* src, size_t bytes, cudaStream_t st, void** dev);
+int apply_landings(EngineImpl& e, const std::vector<int>& ids, cudaStream_t st);
+
+// Apply landings requested earlier but not yet consumed by a decode step.
+int flush_deferred(EngineImpl& e) {
+  if (e.deferred.empty()) return HC_OK;
+  std::vector<int> ids;
+  ids.swap(e.deferred);
+  return apply_landings(e, ids, e.deferred_st);
+}
+
+__global__ void set_flags_kernel(uint8_t* flags, const int32_t* __restrict__ idx, int n,
+                                 uint8_t v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) flags[idx[i]] = v;
+}
+
 int engine_decode_step(EngineImpl& e, int t, const void* q, const void* kn, const void* vn,
                        void* o, cudaStream_t st) {
   HC_REQUIRE(t >= 1 && t <= e.T, HC_EINVAL, "step %d outside 1..%d", t, e.T);
+  // Landings due at this step.  Same stream: K4 first runs every unit that is
+  // not landing (flagged in d_skip) while the retrieval stream finishes the
+  // gathers, then the landing point (wait + descriptor swap), then K4 over
+  // the landing units' tiles -- the transfer hides behind the step's own
+  // attention instead of stalling it.  Other stream: plain landing first.
+  std::vector<int> land;
+  land.swap(e.deferred);
+  if (!land.empty() && e.deferred_st != st) {
+    HC_TRY(apply_landings(e, land, e.deferred_st));
+    cudaEvent_t ev;
+    HC_TRY(new_event(e, &ev));
+    HC_CUDA_TRY(cudaEventRecord(ev, e.deferred_st));
+    HC_CUDA_TRY(cudaStreamWaitEvent(st, ev, 0));
+    land.clear();
+  }
+  int32_t* d_land = nullptr;
+  int n_lu = 0, n_lt = 0;
+  if (!land.empty()) {
+    std::vector<int32_t> lu;
+    for (int id : land) {
+      const int u = e.xfers[id].unit;
+      if (std::find(lu.begin(), lu.end(), u) == lu.end()) lu.push_back(u);
+    }
+    n_lu = int(lu.size());
+    const size_t off = (lu.size() * 4 + 15) & ~size_t(15);
+    std::vector<char> blob(off);
+    std::memcpy(blob.data(), lu.data(), lu.size() * 4);
+    for (int u : lu)
+      for (int i : e.unit_tiles[u])
+        if (e.tiles_host[i].t_act <= uint32_t(t)) {
+          blob.resize(blob.size() + sizeof(TileDesc));
+          std::memcpy(blob.data() + blob.size() - sizeof(TileDesc), &e.tiles_host[i],
+                      sizeof(TileDesc));
+          ++n_lt;
+        }
+    HC_TRY(upload(e, blob.data(), blob.size(), st, (void**)&d_land));
+    set_flags_kernel<<<(n_lu + 127) / 128, 128, 0, st>>>(e.d_skip, d_land, n_lu, 1);
+    HC_CHECK_LAUNCH();
+  }
   cudaEvent_t* ev = nullptr;
   if (e.timing) {
     const size_t need = (e.tev_used + 1) * EngineImpl::kPhaseEvents;
@@ -467,8 +546,26 @@ int engine_decode_step(EngineImpl& e, int t, const void* q, const void* kn, cons
       reinterpret_cast<uint4*>(e.V));
   HC_CHECK_LAUNCH();
   AttnParams p = decode_params(e, t, q, o);
-  HC_TRY(launch_attention(e.tmK, e.tmV, p, active_tiles(e, t), e.d_piv_units, e.n_piv, st,
-                          ev ? ev + 1 : nullptr));
+  if (land.empty()) {
+    HC_TRY(launch_attention(e.tmK, e.tmV, p, active_tiles(e, t), e.d_piv_units, e.n_piv, st,
+                            ev ? ev + 1 : nullptr));
+  } else {
+    p.skip = e.d_skip;
+    const std::function<int()> mid = [&]() -> int {
+      HC_TRY(apply_landings(e, land, st));
+      AttnParams pl = p;
+      pl.skip = nullptr;
+      pl.tiles = reinterpret_cast<const TileDesc*>(
+          reinterpret_cast<const char*>(d_land) + ((size_t(n_lu) * 4 + 15) & ~size_t(15)));
+      HC_TRY(launch_attn_tiles(e.tmK, e.tmV, pl, n_lt, st));
+      set_flags_kernel<<<(n_lu + 127) / 128, 128, 0, st>>>(e.d_skip, d_land, n_lu, 0);
+      HC_CHECK_LAUNCH();
+      HC_CUDA_TRY(cudaFreeAsync(d_land, st));
+      return HC_OK;
+    };
+    HC_TRY(launch_attention(e.tmK, e.tmV, p, active_tiles(e, t), e.d_piv_units, e.n_piv, st,
+                            ev ? ev + 1 : nullptr, &mid));
+  }
   e.last_t = t;
   if (e.n_piv) {
     // K1+K2: top-l_base threshold and |top & K_base| per pivot (engine.py:305-311)
@@ -631,14 +728,6 @@ __global__ void restamp_batch_kernel(uint32_t* kbase, const uint32_t* top_idx,
     const uint32_t p = idx[i];
     if (int(p >> 5) < words) atomicOr(bm + (p >> 5), 1u << (p & 31));
   }
-}
-
-int new_event(EngineImpl& e, cudaEvent_t* out, bool timed = false) {
-  cudaEvent_t ev;
-  HC_CUDA_TRY(cudaEventCreateWithFlags(&ev, timed ? cudaEventDefault : cudaEventDisableTiming));
-  e.events.push_back(ev);
-  *out = ev;
-  return HC_OK;
 }
 
 // Issue the gathers of transfers `ids` (their units' staging buffers are free)
@@ -920,7 +1009,32 @@ int engine_fire_batch(EngineImpl& e, int n, const int32_t* pus, int t, const int
   return issue_gathers(e, now, selected);
 }
 
+// hc_engine_land_batch: validate now, apply inside the next decode step (or
+// at the next call that reads engine state).
 int engine_land_batch(EngineImpl& e, int n, const int32_t* ids, cudaStream_t st) {
+  HC_TRY(flush_deferred(e));
+  std::vector<std::pair<int, size_t>> seen;  // (unit, landings of it in this batch)
+  for (int q = 0; q < n; ++q) {
+    const int id = ids[q];
+    HC_REQUIRE(id >= 0 && id < int(e.xfers.size()), HC_EINVAL, "bad transfer id %d", id);
+    const Transfer& x = e.xfers[id];
+    HC_REQUIRE(!x.landed, HC_ESTATE, "transfer %d already landed", id);
+    HC_REQUIRE(std::find(ids, ids + q, id) == ids + q, HC_ESTATE, "transfer %d landed twice", id);
+    size_t k = 0;
+    for (auto& pr : seen)
+      if (pr.first == x.unit) k = ++pr.second;
+    if (k == 0) seen.emplace_back(x.unit, 0);
+    HC_REQUIRE(e.fifo[x.unit].size() > k && e.fifo[x.unit][k] == id, HC_ESTATE,
+               "transfer %d lands out of order", id);
+  }
+  e.deferred.assign(ids, ids + n);
+  e.deferred_st = st;
+  return HC_OK;
+}
+
+int apply_landings(EngineImpl& e, const std::vector<int>& idv, cudaStream_t st) {
+  const int n = int(idv.size());
+  const int32_t* ids = idv.data();
   std::vector<LandDev> lds;
   std::vector<int> landed_units;
   cudaEvent_t last_wait = nullptr;
@@ -1047,6 +1161,7 @@ extern "C" int hc_engine_info(const hc_engine* eng, int64_t* out4) {
 extern "C" int hc_engine_prefill_layer(hc_engine* eng, int32_t layer, const void* k_dev,
                                        const void* v_dev, const void* q_last_dev, void* stream) {
   HC_REQUIRE(eng && k_dev && v_dev && q_last_dev, HC_EINVAL, "null argument");
+  HC_TRY(hc::flush_deferred(eng->e));  // pending landings first
   return hc::engine_prefill_layer(eng->e, layer, (const __nv_bfloat16*)k_dev,
                                   (const __nv_bfloat16*)v_dev, (const __nv_bfloat16*)q_last_dev,
                                   (cudaStream_t)stream);
@@ -1063,6 +1178,7 @@ extern "C" int hc_engine_decode_step(hc_engine* eng, int32_t step, const void* q
 extern "C" int hc_engine_overlaps(hc_engine* eng, int32_t first, int32_t last, int32_t* out,
                                   void* stream) {
   HC_REQUIRE(eng && out, HC_EINVAL, "null argument");
+  HC_TRY(hc::flush_deferred(eng->e));  // pending landings first
   auto& e = eng->e;
   HC_REQUIRE(last >= first && last - first < hc::kRing, HC_EINVAL, "overlap window too long");
   cudaStream_t st = (cudaStream_t)stream;
@@ -1087,6 +1203,7 @@ extern "C" int hc_engine_overlaps(hc_engine* eng, int32_t first, int32_t last, i
 extern "C" int hc_engine_fire(hc_engine* eng, int32_t pivot_unit, int32_t step,
                               int32_t completion_step, int32_t* transfer_ids, void* stream) {
   HC_REQUIRE(eng && transfer_ids, HC_EINVAL, "null argument");
+  HC_TRY(hc::flush_deferred(eng->e));  // pending landings first
   return hc::engine_fire_batch(eng->e, 1, &pivot_unit, step, &completion_step, transfer_ids,
                                nullptr, (cudaStream_t)stream);
 }
@@ -1096,6 +1213,7 @@ extern "C" int hc_engine_fire_batch(hc_engine* eng, int32_t n, const int32_t* pi
                                     int32_t* transfer_ids, uint32_t* fetched_host, void* stream) {
   HC_REQUIRE(eng && (n == 0 || (pivot_units && completion_steps && transfer_ids)), HC_EINVAL,
              "null argument");
+  HC_TRY(hc::flush_deferred(eng->e));  // pending landings first
   return hc::engine_fire_batch(eng->e, n, pivot_units, step, completion_steps, transfer_ids,
                                fetched_host, (cudaStream_t)stream);
 }
@@ -1114,6 +1232,7 @@ extern "C" int hc_engine_land_batch(hc_engine* eng, int32_t n, const int32_t* tr
 extern "C" int hc_engine_read_indices(hc_engine* eng, int32_t kind, int32_t id, uint32_t* out,
                                       int32_t capacity, int32_t* n_out, void* stream) {
   HC_REQUIRE(eng && out && n_out, HC_EINVAL, "null argument");
+  HC_TRY(hc::flush_deferred(eng->e));  // pending landings first
   auto& e = eng->e;
   cudaStream_t st = (cudaStream_t)stream;
   const uint32_t* list = nullptr;
@@ -1167,6 +1286,7 @@ extern "C" int hc_engine_read_indices(hc_engine* eng, int32_t kind, int32_t id, 
 extern "C" int hc_engine_pivot_row(hc_engine* eng, int32_t pivot_unit, int32_t step, float* dst,
                                    void* stream) {
   HC_REQUIRE(eng && dst, HC_EINVAL, "null argument");
+  HC_TRY(hc::flush_deferred(eng->e));  // pending landings first
   auto& e = eng->e;
   HC_REQUIRE(pivot_unit >= 0 && pivot_unit < e.n_units && e.piv_slot[pivot_unit] >= 0,
              HC_EINVAL, "not a monitored pivot");
@@ -1179,6 +1299,7 @@ extern "C" int hc_engine_pivot_row(hc_engine* eng, int32_t pivot_unit, int32_t s
 extern "C" int hc_engine_resident_rows(hc_engine* eng, int32_t step, int64_t* rows_out,
                                        void* stream) {
   HC_REQUIRE(eng && rows_out, HC_EINVAL, "null argument");
+  HC_TRY(hc::flush_deferred(eng->e));  // pending landings first
   auto& e = eng->e;
   std::vector<hc::UnitDesc> u(e.n_units);
   cudaStream_t st = (cudaStream_t)stream;
