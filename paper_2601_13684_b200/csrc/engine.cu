@@ -40,7 +40,7 @@ int launch_obs_scores(const void* k, const void* q_obs, int B, int H, int G, int
                       float* out, int64_t row_stride, void* scratch, cudaStream_t st);
 int launch_monitor(const float* rows, int64_t row_stride, const int32_t* slots, int n_rows,
                    uint32_t n, uint32_t k, const uint32_t* kbase, int words, uint64_t* thr,
-                   uint32_t* ovl, cudaStream_t st);
+                   uint32_t* ovl, cudaStream_t st, uint32_t* ghist = nullptr);
 int launch_restamp_threshold(const float* rows, int64_t row_stride, const int32_t* slots,
                              int n_rows, uint32_t n, const uint64_t* thr, uint32_t* kbase,
                              int words, cudaStream_t st);
@@ -131,6 +131,7 @@ struct EngineImpl {
   uint32_t *ovl_cur = nullptr, *ovl_ring = nullptr;
   uint32_t* ovl_host = nullptr;     // pinned readback of the overlap window
   uint64_t* thr = nullptr;          // per pivot slot: composite-key threshold of its top set
+  uint32_t* ghist = nullptr;        // per pivot slot: first-digit key histogram (rows -> monitor)
   int32_t* d_piv_slots = nullptr;   // iota over pivot slots
   int last_t = 0;                   // last decode step run
   hc_topk_job* d_piv_jobs = nullptr;
@@ -209,7 +210,7 @@ int engine_destroy(EngineImpl& e) {
   void* ptrs[] = {e.d_units, e.K, e.V, e.d_tiles, e.d_skip, e.partial, e.d_piv_units, e.logits, e.mref,
                   e.stats,
                   e.rowbuf, e.top_idx, e.top_cnt, e.kbase, e.ovl_cur, e.ovl_ring, e.d_piv_jobs,
-                  e.thr, e.d_piv_slots,
+                  e.thr, e.ghist, e.d_piv_slots,
                   e.pf};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -372,6 +373,7 @@ int engine_create(EngineImpl& e, const hc_engine_desc& c, const int32_t* roles,
   HC_TRY(dalloc((void**)&e.ovl_cur, size_t(np) * 4, &e.dev_bytes));
   HC_TRY(dalloc((void**)&e.ovl_ring, size_t(np) * kRing * 4, &e.dev_bytes));
   HC_TRY(dalloc((void**)&e.thr, size_t(np) * 8, &e.dev_bytes));
+  HC_TRY(dalloc((void**)&e.ghist, size_t(np) * 8192 * 4, &e.dev_bytes));
   {
     std::vector<int32_t> iota(np);
     for (int i = 0; i < np; ++i) iota[i] = i;
@@ -445,6 +447,7 @@ AttnParams decode_params(EngineImpl& e, int t, const void* q, void* o) {
   p.mref = e.mref;
   p.stats = e.stats;
   p.rows = e.n_piv ? e.rowbuf : nullptr;
+  p.hist = e.n_piv ? e.ghist : nullptr;
   p.logit_stride = e.row_len;
   p.row_stride = e.row_len;
   p.group = e.G;
@@ -572,7 +575,7 @@ int engine_decode_step(EngineImpl& e, int t, const void* q, const void* kn, cons
     // counts land directly in the overlap ring row of this step
     HC_TRY(launch_monitor(e.rowbuf, e.row_len, e.d_piv_slots, e.n_piv, uint32_t(e.L + t),
                           uint32_t(e.lbase), e.kbase, e.words, e.thr,
-                          e.ovl_ring + size_t(t % kRing) * e.n_piv, st));
+                          e.ovl_ring + size_t(t % kRing) * e.n_piv, st, e.ghist));
     if (ev) HC_CUDA_TRY(cudaEventRecord(ev[5], st));
   } else if (ev) {
     HC_CUDA_TRY(cudaEventRecord(ev[5], st));

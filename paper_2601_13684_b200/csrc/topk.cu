@@ -347,7 +347,8 @@ __device__ void block_find_bucket(const uint32_t* hist, uint32_t rem, uint32_t* 
 __global__ void __launch_bounds__(kMonThreads, 1)
 monitor_kernel(const float* __restrict__ rows, int64_t row_stride, const int32_t* __restrict__ slots,
                uint32_t n, uint32_t k, const uint32_t* __restrict__ kbase, int words,
-               uint64_t* __restrict__ thr_out, uint32_t* __restrict__ ovl_out) {
+               uint64_t* __restrict__ thr_out, uint32_t* __restrict__ ovl_out,
+               uint32_t* __restrict__ ghist) {
   extern __shared__ __align__(16) uint8_t mon_smem[];
   uint32_t* hist = reinterpret_cast<uint32_t*>(mon_smem);
   uint64_t* cand = reinterpret_cast<uint64_t*>(mon_smem + kMonBins * 4);
@@ -359,7 +360,12 @@ monitor_kernel(const float* __restrict__ rows, int64_t row_stride, const int32_t
   const uint32_t* __restrict__ bm = kbase + size_t(s) * words;
   const int tid = threadIdx.x, lane = tid & 31;
 
+  // ghist (optional): this row's first-digit histogram, built by the kernel
+  // that wrote the row (score_rows_kernel); consumed and cleared here
+  uint32_t* gh = ghist ? ghist + size_t(s) * kMonBins : nullptr;
   if (k >= n) {  // everything is selected
+    if (gh)
+      for (int j = tid; j < kMonBins; j += kMonThreads) gh[j] = 0u;
     uint32_t c = 0;
     for (uint32_t i = tid; i < n; i += kMonThreads) c += (__ldg(bm + (i >> 5)) >> (i & 31)) & 1u;
     for (int off = 16; off; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
@@ -370,19 +376,28 @@ monitor_kernel(const float* __restrict__ rows, int64_t row_stride, const int32_t
     if (tid == 0) { thr_out[s] = 0; ovl_out[s] = sh[3]; }
     return;
   }
-  for (int j = tid; j < kMonBins; j += kMonThreads) hist[j] = 0;
   if (tid == 0) sh[3] = 0;  // candidate count
-  __syncthreads();
   const uint32_t n4 = n >> 2;
   const float4* __restrict__ row4 = reinterpret_cast<const float4*>(row);
-  for (uint32_t i = tid; i < n4; i += kMonThreads) {
+  if (gh) {  // all loads in flight at once; the clearing stores go out at the end
+    uint32_t hv[kMonBins / kMonThreads];
+#pragma unroll
+    for (int q = 0; q < kMonBins / kMonThreads; ++q) hv[q] = __ldcg(gh + tid + q * kMonThreads);
+#pragma unroll
+    for (int q = 0; q < kMonBins / kMonThreads; ++q) hist[tid + q * kMonThreads] = hv[q];
+  } else {
+    for (int j = tid; j < kMonBins; j += kMonThreads) hist[j] = 0;
+  }
+  __syncthreads();
+  for (uint32_t i = tid; !gh && i < n4; i += kMonThreads) {
     const float4 v = __ldg(row4 + i);
     atomicAdd(&hist[score_key(v.x) >> 19], 1u);
     atomicAdd(&hist[score_key(v.y) >> 19], 1u);
     atomicAdd(&hist[score_key(v.z) >> 19], 1u);
     atomicAdd(&hist[score_key(v.w) >> 19], 1u);
   }
-  for (uint32_t i = n4 * 4 + tid; i < n; i += kMonThreads) atomicAdd(&hist[score_key(__ldg(row + i)) >> 19], 1u);
+  for (uint32_t i = n4 * 4 + tid; !gh && i < n; i += kMonThreads)
+    atomicAdd(&hist[score_key(__ldg(row + i)) >> 19], 1u);
   __syncthreads();
   block_find_bucket<kMonBins>(hist, k, sh, warp_tot);
   const uint32_t b1 = sh[0];
@@ -390,26 +405,44 @@ monitor_kernel(const float* __restrict__ rows, int64_t row_stride, const int32_t
   const bool whole = (sh[2] == rem);
   __syncthreads();
 
-  // pass 2: K_base bits above b1, candidates inside b1
+  // pass 2: K_base bits above b1, candidates inside b1.  Four float4 loads
+  // are issued before any is consumed: with one CTA per row the pass is
+  // bound by bytes in flight per SM, not by DRAM.
   uint32_t ovl = 0;
-  auto visit = [&](uint32_t pos, float x) {
+  auto visit = [&](uint32_t pos, float x, uint32_t word) {
     const uint32_t k32 = score_key(x);
     const uint32_t d = k32 >> 19;
-    const uint32_t bit = (__ldg(bm + (pos >> 5)) >> (pos & 31)) & 1u;
+    const uint32_t bit = (word >> (pos & 31)) & 1u;
     if (d > b1 || (whole && d == b1)) ovl += bit;
     else if (!whole && d == b1) {
       const uint32_t at = atomicAdd(&sh[3], 1u);
       if (at < uint32_t(kMonCand)) cand[at] = ckey(k32, pos);
     }
   };
-  for (uint32_t i = tid; i < n4; i += kMonThreads) {
-    const float4 v = __ldg(row4 + i);
-    visit(4 * i, v.x);
-    visit(4 * i + 1, v.y);
-    visit(4 * i + 2, v.z);
-    visit(4 * i + 3, v.w);
+  constexpr int kU = 4;
+  for (uint32_t i0 = tid; i0 < n4; i0 += kMonThreads * kU) {
+    float4 v[kU];
+    uint32_t wd[kU];
+#pragma unroll
+    for (int q = 0; q < kU; ++q) {
+      const uint32_t i = i0 + q * kMonThreads;
+      if (i < n4) {
+        v[q] = __ldg(row4 + i);
+        wd[q] = __ldg(bm + (i >> 3));  // positions 4i..4i+3 share one bitmap word
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kU; ++q) {
+      const uint32_t i = i0 + q * kMonThreads;
+      if (i < n4) {
+        visit(4 * i, v[q].x, wd[q]);
+        visit(4 * i + 1, v[q].y, wd[q]);
+        visit(4 * i + 2, v[q].z, wd[q]);
+        visit(4 * i + 3, v[q].w, wd[q]);
+      }
+    }
   }
-  for (uint32_t i = n4 * 4 + tid; i < n; i += kMonThreads) visit(i, __ldg(row + i));
+  for (uint32_t i = n4 * 4 + tid; i < n; i += kMonThreads) visit(i, __ldg(row + i), __ldg(bm + (i >> 5)));
   __syncthreads();
 
   uint64_t T = uint64_t(b1) << 51;  // lowest composite key of bucket b1
@@ -470,6 +503,9 @@ monitor_kernel(const float* __restrict__ rows, int64_t row_stride, const int32_t
     thr_out[s] = T;
     ovl_out[s] = sh[3];
   }
+  if (gh)
+#pragma unroll
+    for (int q = 0; q < kMonBins / kMonThreads; ++q) gh[tid + q * kMonThreads] = 0u;
 }
 
 // K_base <- {p : key(p) >= T} over [0, n) for the listed pivot slots
@@ -496,7 +532,7 @@ __global__ void restamp_threshold_kernel(const float* __restrict__ rows, int64_t
 
 int launch_monitor(const float* rows, int64_t row_stride, const int32_t* slots, int n_rows,
                    uint32_t n, uint32_t k, const uint32_t* kbase, int words, uint64_t* thr,
-                   uint32_t* ovl, cudaStream_t st) {
+                   uint32_t* ovl, cudaStream_t st, uint32_t* ghist) {
   static bool configured = false;
   if (!configured) {
     HC_CUDA_TRY(cudaFuncSetAttribute(monitor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -505,7 +541,7 @@ int launch_monitor(const float* rows, int64_t row_stride, const int32_t* slots, 
   }
   if (n_rows <= 0) return HC_OK;
   monitor_kernel<<<n_rows, kMonThreads, kMonSmem, st>>>(rows, row_stride, slots, n, k, kbase,
-                                                        words, thr, ovl);
+                                                        words, thr, ovl, ghist);
   HC_CHECK_LAUNCH();
   return HC_OK;
 }
@@ -537,7 +573,7 @@ extern "C" int hc_monitor_rows(const float* rows_dev, int64_t row_stride, int32_
   for (int i = 0; i < n_rows; ++i) iota[i] = i;
   HC_CUDA_TRY(cudaMemcpyAsync(slots, iota.data(), iota.size() * 4, cudaMemcpyHostToDevice, st));
   int rc = hc::launch_monitor(rows_dev, row_stride, slots, n_rows, n, k, kbase_dev, words,
-                              thr_dev, ovl_dev, st);
+                              thr_dev, ovl_dev, st, nullptr);
   HC_CUDA_TRY(cudaFreeAsync(slots, st));
   HC_CUDA_TRY(cudaStreamSynchronize(st));
   return rc;
