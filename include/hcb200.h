@@ -214,6 +214,24 @@ int hc_engine_prefill_layer(hc_engine* eng, int32_t layer, const void* k_dev, co
 int hc_engine_decode_step(hc_engine* eng, int32_t step, const void* q_dev, const void* k_new_dev,
                           const void* v_new_dev, void* o_dev, void* stream);
 
+/* decode_step in two halves (decode_step = begin(hold 0) + end), so that the
+ * host's window decision of step-1 (engine.py:313-360, read with
+ * hc_engine_overlaps, acted on with hc_engine_fire_batch / land_batch) runs
+ * while the step's attention does:
+ *   begin  appends the token and launches attention over every unit except
+ *          the landing ones -- with hold_satellites != 0, except every
+ *          satellite (transfers fired by the open decision may land now);
+ *   end    applies the landings requested so far (landing point: wait for
+ *          the gathers, swap descriptors), attends the held units, then
+ *          combine, score rows and overlap counts.
+ * Between the halves, overlaps and fire_batch read the previous step's
+ * state on an internal side stream; land_batch is allowed only with
+ * hold_satellites.  Results equal decode_step's. */
+int hc_engine_decode_begin(hc_engine* eng, int32_t step, const void* q_dev,
+                           const void* k_new_dev, const void* v_new_dev, void* o_dev,
+                           int32_t hold_satellites, void* stream);
+int hc_engine_decode_end(hc_engine* eng, int32_t step, void* stream);
+
 /* Copy the overlap counts of steps [first, last] (<= 64 steps back) into
  * out [(last-first+1) x n_pivots] (pivot order = ascending unit), then sync. */
 int hc_engine_overlaps(hc_engine* eng, int32_t first, int32_t last, int32_t* out_host,
@@ -237,8 +255,10 @@ int hc_engine_fire_batch(hc_engine* eng, int32_t n, const int32_t* pivot_units, 
                          const int32_t* completion_steps, int32_t* transfer_ids,
                          uint32_t* fetched_host, void* stream);
 
-/* Landing of a due transfer (engine.py:293-299): the caller's stream waits
- * for the gather, then the satellite serves the new set from this step on. */
+/* Landing of a due transfer (engine.py:293-299): applied inside the next
+ * decode step (or before the next call that reads engine state), where the
+ * step's stream waits for the gather after attending every other unit; the
+ * satellite serves the new set from that step on. */
 int hc_engine_land(hc_engine* eng, int32_t transfer_id, void* stream);
 /* Land several due transfers in (completion, order) order with one launch. */
 int hc_engine_land_batch(hc_engine* eng, int32_t n, const int32_t* transfer_ids, void* stream);

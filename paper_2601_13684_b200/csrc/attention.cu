@@ -24,8 +24,6 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
-#include <functional>
-
 #include "hc_common.cuh"
 #include "kv_layout.cuh"
 
@@ -510,22 +508,17 @@ int launch_attn_tiles(const CUtensorMap& tmK, const CUtensorMap& tmV, const Attn
   return HC_OK;
 }
 
-int launch_attention(const CUtensorMap& tmK, const CUtensorMap& tmV, const AttnParams& p,
-                     int n_tiles, const int32_t* pivot_units_dev, int n_pivots,
-                     cudaStream_t st, const cudaEvent_t* ev, const std::function<int()>* mid) {
-  // ev (optional): events recorded before K4, after K4, after combine, after score rows
-  // mid (optional): runs after the K4 launch, before combine (deferred landings)
-  HC_TRY(configure_attn());
+// After K4: split-K combine, then the pivots' score rows (+ key histogram).
+// ev (optional): events recorded after K4, after combine, after score rows.
+int launch_attn_post(const AttnParams& p, const int32_t* pivot_units_dev, int n_pivots,
+                     cudaStream_t st, const cudaEvent_t* ev) {
   HC_REQUIRE(p.group >= 1 && p.group <= 8, HC_EINVAL, "GQA group must be 1..8");
   if (ev) HC_CUDA_TRY(cudaEventRecord(ev[0], st));
-  HC_TRY(launch_attn_tiles(tmK, tmV, p, n_tiles, st));
-  if (mid) HC_TRY((*mid)());
-  if (ev) HC_CUDA_TRY(cudaEventRecord(ev[1], st));
   if (p.n_units > 0) {
     combine_kernel<<<dim3(p.n_units, p.group), 128, 0, st>>>(p);
     HC_CHECK_LAUNCH();
   }
-  if (ev) HC_CUDA_TRY(cudaEventRecord(ev[2], st));
+  if (ev) HC_CUDA_TRY(cudaEventRecord(ev[1], st));
   if (n_pivots > 0 && p.rows) {
     HC_REQUIRE(p.logit_stride % 16 == 0 && p.row_stride % 8 == 0, HC_EINVAL,
                "score-row strides must be multiples of 16 / 8");
@@ -539,8 +532,18 @@ int launch_attention(const CUtensorMap& tmK, const CUtensorMap& tmV, const AttnP
     }
     HC_CHECK_LAUNCH();
   }
-  if (ev) HC_CUDA_TRY(cudaEventRecord(ev[3], st));
+  if (ev) HC_CUDA_TRY(cudaEventRecord(ev[2], st));
   return HC_OK;
+}
+
+// One-shot K4 + combine + score rows.
+// ev (optional): events recorded before K4, after K4, after combine, after score rows
+int launch_attention(const CUtensorMap& tmK, const CUtensorMap& tmV, const AttnParams& p,
+                     int n_tiles, const int32_t* pivot_units_dev, int n_pivots,
+                     cudaStream_t st, const cudaEvent_t* ev) {
+  if (ev) HC_CUDA_TRY(cudaEventRecord(ev[0], st));
+  HC_TRY(launch_attn_tiles(tmK, tmV, p, n_tiles, st));
+  return launch_attn_post(p, pivot_units_dev, n_pivots, st, ev ? ev + 1 : nullptr);
 }
 
 }  // namespace hc

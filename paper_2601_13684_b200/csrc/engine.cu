@@ -17,7 +17,6 @@
 #include <algorithm>
 #include <cstring>
 #include <deque>
-#include <functional>
 #include <new>
 #include <tuple>
 #include <vector>
@@ -30,8 +29,9 @@ namespace hc {
 int make_kv_tensor_map(CUtensorMap* map, const void* base, int64_t rows);
 int launch_attention(const CUtensorMap& tmK, const CUtensorMap& tmV, const AttnParams& p,
                      int n_tiles, const int32_t* pivot_units_dev, int n_pivots, cudaStream_t st,
-                     const cudaEvent_t* ev = nullptr,
-                     const std::function<int()>* mid = nullptr);
+                     const cudaEvent_t* ev = nullptr);
+int launch_attn_post(const AttnParams& p, const int32_t* pivot_units_dev, int n_pivots,
+                     cudaStream_t st, const cudaEvent_t* ev);
 int launch_attn_tiles(const CUtensorMap& tmK, const CUtensorMap& tmV, const AttnParams& p,
                       int n_tiles, cudaStream_t st);
 int launch_topk(const hc_topk_job* jobs_dev, int n_jobs, uint32_t n_add, cudaStream_t st);
@@ -40,7 +40,9 @@ int launch_obs_scores(const void* k, const void* q_obs, int B, int H, int G, int
                       float* out, int64_t row_stride, void* scratch, cudaStream_t st);
 int launch_monitor(const float* rows, int64_t row_stride, const int32_t* slots, int n_rows,
                    uint32_t n, uint32_t k, const uint32_t* kbase, int words, uint64_t* thr,
-                   uint32_t* ovl, cudaStream_t st, uint32_t* ghist = nullptr);
+                   uint32_t* ovl, cudaStream_t st, const uint32_t* ghist = nullptr,
+                   uint32_t* ghist_next = nullptr);
+int launch_fire_select(const FireJob* jobs_dev, int n_jobs, cudaStream_t st);
 int launch_restamp_threshold(const float* rows, int64_t row_stride, const int32_t* slots,
                              int n_rows, uint32_t n, const uint64_t* thr, uint32_t* kbase,
                              int words, cudaStream_t st);
@@ -117,6 +119,22 @@ struct EngineImpl {
   // step: K4 runs every other unit while the gathers finish (see decode_step)
   std::vector<int> deferred;
   cudaStream_t deferred_st = nullptr;
+  // satellites: static tile list + K4 skip flags for steps whose fire
+  // decision is still open (hold_satellites, see decode_begin)
+  TileDesc* d_sat_tiles = nullptr;
+  std::vector<uint32_t> sat_t_act;
+  uint8_t* d_sat_flags = nullptr;
+  // the open step between decode_begin and decode_end
+  int in_step = 0;
+  bool cur_hold = false;
+  cudaStream_t cur_st = nullptr;
+  AttnParams cur_p{};
+  cudaEvent_t* cur_ev = nullptr;
+  std::vector<int> cur_land;
+  int32_t* d_land = nullptr;
+  int n_lu = 0, n_lt = 0;
+  cudaEvent_t step_end = nullptr;  // end of the last completed step (rows, counts, K_base)
+  cudaStream_t side = nullptr;     // fire selection and control readbacks inside a step
   int n_slots = 0;
   float* partial = nullptr;
   // pivots
@@ -131,7 +149,8 @@ struct EngineImpl {
   uint32_t *ovl_cur = nullptr, *ovl_ring = nullptr;
   uint32_t* ovl_host = nullptr;     // pinned readback of the overlap window
   uint64_t* thr = nullptr;          // per pivot slot: composite-key threshold of its top set
-  uint32_t* ghist = nullptr;        // per pivot slot: first-digit key histogram (rows -> monitor)
+  uint32_t* ghist = nullptr;        // [2][pivot slot][8192] first-digit key histograms of the
+                                    // rows: step t fills buffer t&1 (rows -> monitor -> fire)
   int32_t* d_piv_slots = nullptr;   // iota over pivot slots
   int last_t = 0;                   // last decode step run
   hc_topk_job* d_piv_jobs = nullptr;
@@ -207,7 +226,8 @@ int engine_destroy(EngineImpl& e) {
     if (e.pre_pos[u]) cudaFree(e.pre_pos[u]);
     if (e.pre_meta[u]) cudaFree(e.pre_meta[u]);
   }
-  void* ptrs[] = {e.d_units, e.K, e.V, e.d_tiles, e.d_skip, e.partial, e.d_piv_units, e.logits, e.mref,
+  void* ptrs[] = {e.d_units, e.K, e.V, e.d_tiles, e.d_skip, e.d_sat_tiles, e.d_sat_flags,
+                  e.partial, e.d_piv_units, e.logits, e.mref,
                   e.stats,
                   e.rowbuf, e.top_idx, e.top_cnt, e.kbase, e.ovl_cur, e.ovl_ring, e.d_piv_jobs,
                   e.thr, e.ghist, e.d_piv_slots,
@@ -219,6 +239,7 @@ int engine_destroy(EngineImpl& e) {
     else cudaFree(e.pool);
   }
   if (e.retr) cudaStreamDestroy(e.retr);
+  if (e.side) cudaStreamDestroy(e.side);
   if (e.pf_ev0) cudaEventDestroy(e.pf_ev0);
   if (e.pf_ev1) cudaEventDestroy(e.pf_ev1);
   for (auto x : e.tev) cudaEventDestroy(x);
@@ -344,6 +365,22 @@ int engine_create(EngineImpl& e, const hc_engine_desc& c, const int32_t* roles,
   e.unit_tiles.assign(e.n_units, {});
   for (size_t i = 0; i < tiles.size(); ++i) e.unit_tiles[tiles[i].unit].push_back(int(i));
   HC_TRY(dalloc((void**)&e.d_skip, size_t(e.n_units), &e.dev_bytes));
+  {
+    std::vector<TileDesc> st;
+    std::vector<uint8_t> fl(e.n_units, 0);
+    for (int u = 0; u < e.n_units; ++u)
+      if (e.units[u].kind == kUnitComp && e.role[e.lh(u)] == HC_ROLE_SATELLITE) fl[u] = 1;
+    for (const TileDesc& d : tiles)
+      if (fl[d.unit]) st.push_back(d);  // keeps the t_act order
+    for (const TileDesc& d : st) e.sat_t_act.push_back(d.t_act);
+    HC_TRY(dalloc((void**)&e.d_sat_tiles, std::max<size_t>(1, st.size()) * sizeof(TileDesc),
+                  &e.dev_bytes));
+    if (!st.empty())
+      HC_CUDA_TRY(cudaMemcpy(e.d_sat_tiles, st.data(), st.size() * sizeof(TileDesc),
+                             cudaMemcpyHostToDevice));
+    HC_TRY(dalloc((void**)&e.d_sat_flags, size_t(e.n_units), &e.dev_bytes));
+    HC_CUDA_TRY(cudaMemcpy(e.d_sat_flags, fl.data(), fl.size(), cudaMemcpyHostToDevice));
+  }
 
   HC_TRY(dalloc((void**)&e.K, size_t(e.rows) * kHeadDim * 2, &e.dev_bytes));
   HC_TRY(dalloc((void**)&e.V, size_t(e.rows) * kHeadDim * 2, &e.dev_bytes));
@@ -373,7 +410,7 @@ int engine_create(EngineImpl& e, const hc_engine_desc& c, const int32_t* roles,
   HC_TRY(dalloc((void**)&e.ovl_cur, size_t(np) * 4, &e.dev_bytes));
   HC_TRY(dalloc((void**)&e.ovl_ring, size_t(np) * kRing * 4, &e.dev_bytes));
   HC_TRY(dalloc((void**)&e.thr, size_t(np) * 8, &e.dev_bytes));
-  HC_TRY(dalloc((void**)&e.ghist, size_t(np) * 8192 * 4, &e.dev_bytes));
+  HC_TRY(dalloc((void**)&e.ghist, 2 * size_t(np) * 8192 * 4, &e.dev_bytes));
   {
     std::vector<int32_t> iota(np);
     for (int i = 0; i < np; ++i) iota[i] = i;
@@ -433,6 +470,7 @@ int engine_create(EngineImpl& e, const hc_engine_desc& c, const int32_t* roles,
   int lo_prio = 0, hi_prio = 0;
   HC_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
   HC_CUDA_TRY(cudaStreamCreateWithPriority(&e.retr, cudaStreamNonBlocking, hi_prio));
+  HC_CUDA_TRY(cudaStreamCreateWithPriority(&e.side, cudaStreamNonBlocking, hi_prio));
   return HC_OK;
 }
 
@@ -447,7 +485,7 @@ AttnParams decode_params(EngineImpl& e, int t, const void* q, void* o) {
   p.mref = e.mref;
   p.stats = e.stats;
   p.rows = e.n_piv ? e.rowbuf : nullptr;
-  p.hist = e.n_piv ? e.ghist : nullptr;
+  p.hist = e.n_piv ? e.ghist + size_t(t & 1) * e.n_piv * 8192 : nullptr;
   p.logit_stride = e.row_len;
   p.row_stride = e.row_len;
   p.group = e.G;
@@ -477,7 +515,7 @@ int apply_landings(EngineImpl& e, const std::vector<int>& ids, cudaStream_t st);
 
 // Apply landings requested earlier but not yet consumed by a decode step.
 int flush_deferred(EngineImpl& e) {
-  if (e.deferred.empty()) return HC_OK;
+  if (e.deferred.empty() || e.in_step) return HC_OK;  // an open step lands them itself
   std::vector<int> ids;
   ids.swap(e.deferred);
   return apply_landings(e, ids, e.deferred_st);
@@ -489,33 +527,43 @@ __global__ void set_flags_kernel(uint8_t* flags, const int32_t* __restrict__ idx
   if (i < n) flags[idx[i]] = v;
 }
 
-int engine_decode_step(EngineImpl& e, int t, const void* q, const void* kn, const void* vn,
-                       void* o, cudaStream_t st) {
+// Decode step t, in two halves so a host decision can overlap the attention:
+//
+//   decode_begin  append the token; K4 over every unit except those that may
+//                 change this step (landing units, or -- hold_satellites --
+//                 every satellite, when the fire decision of step t-1 is still
+//                 open and may land transfers at t)
+//   (host)        overlaps / fire_batch / land_batch for the open decision:
+//                 they run on the side stream against step t-1's state
+//   decode_end    landing point (wait for the gathers, swap descriptors), K4
+//                 over the held units, combine, score rows, monitor
+//
+// The retrieval gathers of a landing overlap the step's main K4 instead of
+// stalling it; decode_step = begin(hold 0) + end.
+int engine_decode_begin(EngineImpl& e, int t, const void* q, const void* kn, const void* vn,
+                        void* o, bool hold, cudaStream_t st) {
   HC_REQUIRE(t >= 1 && t <= e.T, HC_EINVAL, "step %d outside 1..%d", t, e.T);
-  // Landings due at this step.  Same stream: K4 first runs every unit that is
-  // not landing (flagged in d_skip) while the retrieval stream finishes the
-  // gathers, then the landing point (wait + descriptor swap), then K4 over
-  // the landing units' tiles -- the transfer hides behind the step's own
-  // attention instead of stalling it.  Other stream: plain landing first.
-  std::vector<int> land;
-  land.swap(e.deferred);
-  if (!land.empty() && e.deferred_st != st) {
-    HC_TRY(apply_landings(e, land, e.deferred_st));
+  HC_REQUIRE(e.in_step == 0, HC_ESTATE, "decode_begin(%d) while step %d is open", t, e.in_step);
+  if (!e.deferred.empty() && e.deferred_st != st) {  // landings requested on another stream
+    std::vector<int> ids;
+    ids.swap(e.deferred);
+    HC_TRY(apply_landings(e, ids, e.deferred_st));
     cudaEvent_t ev;
     HC_TRY(new_event(e, &ev));
     HC_CUDA_TRY(cudaEventRecord(ev, e.deferred_st));
     HC_CUDA_TRY(cudaStreamWaitEvent(st, ev, 0));
-    land.clear();
   }
-  int32_t* d_land = nullptr;
-  int n_lu = 0, n_lt = 0;
+  std::vector<int> land;
+  if (!hold) land.swap(e.deferred);
+  e.d_land = nullptr;
+  e.n_lu = e.n_lt = 0;
   if (!land.empty()) {
     std::vector<int32_t> lu;
     for (int id : land) {
       const int u = e.xfers[id].unit;
       if (std::find(lu.begin(), lu.end(), u) == lu.end()) lu.push_back(u);
     }
-    n_lu = int(lu.size());
+    e.n_lu = int(lu.size());
     const size_t off = (lu.size() * 4 + 15) & ~size_t(15);
     std::vector<char> blob(off);
     std::memcpy(blob.data(), lu.data(), lu.size() * 4);
@@ -525,10 +573,10 @@ int engine_decode_step(EngineImpl& e, int t, const void* q, const void* kn, cons
           blob.resize(blob.size() + sizeof(TileDesc));
           std::memcpy(blob.data() + blob.size() - sizeof(TileDesc), &e.tiles_host[i],
                       sizeof(TileDesc));
-          ++n_lt;
+          ++e.n_lt;
         }
-    HC_TRY(upload(e, blob.data(), blob.size(), st, (void**)&d_land));
-    set_flags_kernel<<<(n_lu + 127) / 128, 128, 0, st>>>(e.d_skip, d_land, n_lu, 1);
+    HC_TRY(upload(e, blob.data(), blob.size(), st, (void**)&e.d_land));
+    set_flags_kernel<<<(e.n_lu + 127) / 128, 128, 0, st>>>(e.d_skip, e.d_land, e.n_lu, 1);
     HC_CHECK_LAUNCH();
   }
   cudaEvent_t* ev = nullptr;
@@ -548,40 +596,69 @@ int engine_decode_step(EngineImpl& e, int t, const void* q, const void* kn, cons
       reinterpret_cast<const uint4*>(vn), reinterpret_cast<uint4*>(e.K),
       reinterpret_cast<uint4*>(e.V));
   HC_CHECK_LAUNCH();
+  if (ev) HC_CUDA_TRY(cudaEventRecord(ev[1], st));
   AttnParams p = decode_params(e, t, q, o);
-  if (land.empty()) {
-    HC_TRY(launch_attention(e.tmK, e.tmV, p, active_tiles(e, t), e.d_piv_units, e.n_piv, st,
-                            ev ? ev + 1 : nullptr));
-  } else {
-    p.skip = e.d_skip;
-    const std::function<int()> mid = [&]() -> int {
-      HC_TRY(apply_landings(e, land, st));
-      AttnParams pl = p;
-      pl.skip = nullptr;
-      pl.tiles = reinterpret_cast<const TileDesc*>(
-          reinterpret_cast<const char*>(d_land) + ((size_t(n_lu) * 4 + 15) & ~size_t(15)));
-      HC_TRY(launch_attn_tiles(e.tmK, e.tmV, pl, n_lt, st));
-      set_flags_kernel<<<(n_lu + 127) / 128, 128, 0, st>>>(e.d_skip, d_land, n_lu, 0);
-      HC_CHECK_LAUNCH();
-      HC_CUDA_TRY(cudaFreeAsync(d_land, st));
-      return HC_OK;
-    };
-    HC_TRY(launch_attention(e.tmK, e.tmV, p, active_tiles(e, t), e.d_piv_units, e.n_piv, st,
-                            ev ? ev + 1 : nullptr, &mid));
+  p.skip = hold ? e.d_sat_flags : (land.empty() ? nullptr : e.d_skip);
+  HC_TRY(launch_attn_tiles(e.tmK, e.tmV, p, active_tiles(e, t), st));
+  e.in_step = t;
+  e.cur_hold = hold;
+  e.cur_st = st;
+  e.cur_p = p;
+  e.cur_ev = ev;
+  e.cur_land.swap(land);
+  return HC_OK;
+}
+
+int engine_decode_end(EngineImpl& e, int t, cudaStream_t st) {
+  HC_REQUIRE(e.in_step == t, HC_ESTATE, "decode_end(%d) without decode_begin(%d)", t, t);
+  HC_REQUIRE(st == e.cur_st, HC_EINVAL, "decode_end on another stream than decode_begin");
+  e.in_step = 0;  // landings below are applied for real
+  AttnParams pl = e.cur_p;
+  pl.skip = nullptr;
+  if (e.cur_hold) {
+    std::vector<int> land;
+    land.swap(e.deferred);
+    if (!land.empty()) HC_TRY(apply_landings(e, land, st));
+    const int n = int(std::upper_bound(e.sat_t_act.begin(), e.sat_t_act.end(), uint32_t(t)) -
+                      e.sat_t_act.begin());
+    pl.tiles = e.d_sat_tiles;
+    HC_TRY(launch_attn_tiles(e.tmK, e.tmV, pl, n, st));
+  } else if (!e.cur_land.empty()) {
+    HC_TRY(apply_landings(e, e.cur_land, st));
+    pl.tiles = reinterpret_cast<const TileDesc*>(reinterpret_cast<const char*>(e.d_land) +
+                                                 ((size_t(e.n_lu) * 4 + 15) & ~size_t(15)));
+    HC_TRY(launch_attn_tiles(e.tmK, e.tmV, pl, e.n_lt, st));
+    set_flags_kernel<<<(e.n_lu + 127) / 128, 128, 0, st>>>(e.d_skip, e.d_land, e.n_lu, 0);
+    HC_CHECK_LAUNCH();
+    HC_CUDA_TRY(cudaFreeAsync(e.d_land, st));
+    e.d_land = nullptr;
   }
+  e.cur_land.clear();
+  cudaEvent_t* ev = e.cur_ev;
+  HC_TRY(launch_attn_post(e.cur_p, e.d_piv_units, e.n_piv, st, ev ? ev + 2 : nullptr));
   e.last_t = t;
   if (e.n_piv) {
     // K1+K2: top-l_base threshold and |top & K_base| per pivot (engine.py:305-311)
     // counts land directly in the overlap ring row of this step
     HC_TRY(launch_monitor(e.rowbuf, e.row_len, e.d_piv_slots, e.n_piv, uint32_t(e.L + t),
                           uint32_t(e.lbase), e.kbase, e.words, e.thr,
-                          e.ovl_ring + size_t(t % kRing) * e.n_piv, st, e.ghist));
-    if (ev) HC_CUDA_TRY(cudaEventRecord(ev[5], st));
-  } else if (ev) {
-    HC_CUDA_TRY(cudaEventRecord(ev[5], st));
+                          e.ovl_ring + size_t(t % kRing) * e.n_piv, st,
+                          e.ghist + size_t(t & 1) * e.n_piv * 8192,
+                          e.ghist + size_t((t + 1) & 1) * e.n_piv * 8192));
   }
-  if (ev) HC_CUDA_TRY(cudaEventRecord(ev[6], st));
+  if (ev) {
+    HC_CUDA_TRY(cudaEventRecord(ev[5], st));
+    HC_CUDA_TRY(cudaEventRecord(ev[6], st));
+  }
+  if (!e.step_end) HC_TRY(new_event(e, &e.step_end));
+  HC_CUDA_TRY(cudaEventRecord(e.step_end, st));
   return HC_OK;
+}
+
+int engine_decode_step(EngineImpl& e, int t, const void* q, const void* kn, const void* vn,
+                       void* o, cudaStream_t st) {
+  HC_TRY(engine_decode_begin(e, t, q, kn, vn, o, false, st));
+  return engine_decode_end(e, t, st);
 }
 
 // Stream-ordered upload of a small host array: copy into the pinned staging
@@ -940,8 +1017,25 @@ int engine_prefill_layer(EngineImpl& e, int layer, const __nv_bfloat16* k,
 }
 
 int engine_fire_batch(EngineImpl& e, int n, const int32_t* pus, int t, const int32_t* completion,
-                      int32_t* ids, uint32_t* fetched_host, cudaStream_t st) {
+                      int32_t* ids, uint32_t* fetched_host, cudaStream_t caller) {
+  // Selection, K_base restamp and the fetched-set copies run on the side
+  // stream after the rows they read: inside an open step (decode_begin) that
+  // is the end of the previous step, so they overlap the step's K4; outside,
+  // everything queued on the caller's stream so far.  The caller's stream
+  // then waits for them (later score rows overwrite the rows, the monitor
+  // reads K_base).
+  cudaEvent_t dep = e.in_step ? e.step_end : nullptr;
+  if (!dep) {
+    HC_TRY(new_event(e, &dep));
+    HC_CUDA_TRY(cudaEventRecord(dep, caller));
+  }
+  cudaStream_t st = e.side;
+  HC_CUDA_TRY(cudaStreamWaitEvent(st, dep, 0));
   std::vector<hc_topk_job> jobs;
+  std::vector<FireJob> fjobs;
+  // the rows of step t still have their key histograms (buffer t&1) until
+  // step t+1's monitor: fast two-pass selection (fire_select_kernel)
+  const bool fast = e.ghist && t >= 1 && t == e.last_t;
   std::vector<int> new_ids;
   std::vector<int32_t> slots;
   const int LH = e.NL * e.H;
@@ -964,13 +1058,19 @@ int engine_fire_batch(EngineImpl& e, int n, const int32_t* pus, int t, const int
       HC_CUDA_TRY(cudaMallocAsync((void**)&x.cnt, 4, st));
       HC_CUDA_TRY(cudaMallocAsync((void**)&x.pos, size_t(std::max(1, e.cap[u])) * 4, st));
       HC_CUDA_TRY(cudaMallocAsync((void**)&x.meta, 16, st));
-      hc_topk_job jb{};
-      jb.scores = e.rowbuf + size_t(s) * e.row_len;
-      jb.n = uint32_t(e.L + t);
-      jb.k = uint32_t(x.k);
-      jb.out_idx = x.sel;
-      jb.out_count = x.cnt;
-      jobs.push_back(jb);
+      if (fast) {
+        fjobs.push_back(FireJob{e.rowbuf + size_t(s) * e.row_len,
+                                e.ghist + (size_t(t & 1) * e.n_piv + s) * 8192, uint32_t(e.L + t),
+                                uint32_t(x.k), x.sel, x.cnt});
+      } else {
+        hc_topk_job jb{};
+        jb.scores = e.rowbuf + size_t(s) * e.row_len;
+        jb.n = uint32_t(e.L + t);
+        jb.k = uint32_t(x.k);
+        jb.out_idx = x.sel;
+        jb.out_count = x.cnt;
+        jobs.push_back(jb);
+      }
       new_ids.push_back(int(e.xfers.size()));
       e.xfers.push_back(x);
     }
@@ -980,6 +1080,12 @@ int engine_fire_batch(EngineImpl& e, int n, const int32_t* pus, int t, const int
     hc_topk_job* dj = nullptr;
     HC_TRY(upload(e, jobs.data(), jobs.size() * sizeof(hc_topk_job), st, (void**)&dj));
     HC_TRY(launch_topk(dj, int(jobs.size()), 0, st));
+    HC_CUDA_TRY(cudaFreeAsync(dj, st));
+  }
+  if (!fjobs.empty()) {
+    FireJob* dj = nullptr;
+    HC_TRY(upload(e, fjobs.data(), fjobs.size() * sizeof(FireJob), st, (void**)&dj));
+    HC_TRY(launch_fire_select(dj, int(fjobs.size()), st));
     HC_CUDA_TRY(cudaFreeAsync(dj, st));
   }
   if (n > 0) {  // K_base <- current top set (engine.py:357), from the monitor threshold
@@ -1002,6 +1108,7 @@ int engine_fire_batch(EngineImpl& e, int n, const int32_t* pus, int t, const int
   cudaEvent_t selected;
   HC_TRY(new_event(e, &selected));
   HC_CUDA_TRY(cudaEventRecord(selected, st));
+  HC_CUDA_TRY(cudaStreamWaitEvent(caller, selected, 0));
   std::vector<int> now;
   for (int id : new_ids) {
     Transfer& x = e.xfers[id];
@@ -1015,22 +1122,38 @@ int engine_fire_batch(EngineImpl& e, int n, const int32_t* pus, int t, const int
 // hc_engine_land_batch: validate now, apply inside the next decode step (or
 // at the next call that reads engine state).
 int engine_land_batch(EngineImpl& e, int n, const int32_t* ids, cudaStream_t st) {
-  HC_TRY(flush_deferred(e));
-  std::vector<std::pair<int, size_t>> seen;  // (unit, landings of it in this batch)
+  if (e.in_step) {
+    HC_REQUIRE(e.cur_hold, HC_ESTATE,
+               "landing inside an open step needs decode_begin(hold_satellites=1)");
+    HC_REQUIRE(st == e.cur_st, HC_EINVAL, "landing on another stream than the open step");
+  } else {
+    HC_TRY(flush_deferred(e));
+  }
+  std::vector<std::pair<int, size_t>> seen;  // (unit, landings already requested)
+  for (int id : e.deferred) {
+    const int u = e.xfers[id].unit;
+    bool found = false;
+    for (auto& pr : seen)
+      if (pr.first == u) ++pr.second, found = true;
+    if (!found) seen.emplace_back(u, 1);
+  }
   for (int q = 0; q < n; ++q) {
     const int id = ids[q];
     HC_REQUIRE(id >= 0 && id < int(e.xfers.size()), HC_EINVAL, "bad transfer id %d", id);
     const Transfer& x = e.xfers[id];
     HC_REQUIRE(!x.landed, HC_ESTATE, "transfer %d already landed", id);
-    HC_REQUIRE(std::find(ids, ids + q, id) == ids + q, HC_ESTATE, "transfer %d landed twice", id);
+    HC_REQUIRE(std::find(ids, ids + q, id) == ids + q &&
+                   std::find(e.deferred.begin(), e.deferred.end(), id) == e.deferred.end(),
+               HC_ESTATE, "transfer %d landed twice", id);
     size_t k = 0;
+    bool found = false;
     for (auto& pr : seen)
-      if (pr.first == x.unit) k = ++pr.second;
-    if (k == 0) seen.emplace_back(x.unit, 0);
+      if (pr.first == x.unit) k = pr.second++, found = true;
+    if (!found) seen.emplace_back(x.unit, 1);
     HC_REQUIRE(e.fifo[x.unit].size() > k && e.fifo[x.unit][k] == id, HC_ESTATE,
                "transfer %d lands out of order", id);
   }
-  e.deferred.assign(ids, ids + n);
+  e.deferred.insert(e.deferred.end(), ids, ids + n);
   e.deferred_st = st;
   return HC_OK;
 }
@@ -1178,6 +1301,19 @@ extern "C" int hc_engine_decode_step(hc_engine* eng, int32_t step, const void* q
                                 (cudaStream_t)stream);
 }
 
+extern "C" int hc_engine_decode_begin(hc_engine* eng, int32_t step, const void* q_dev,
+                                      const void* k_new_dev, const void* v_new_dev, void* o_dev,
+                                      int32_t hold_satellites, void* stream) {
+  HC_REQUIRE(eng && q_dev && k_new_dev && v_new_dev && o_dev, HC_EINVAL, "null argument");
+  return hc::engine_decode_begin(eng->e, step, q_dev, k_new_dev, v_new_dev, o_dev,
+                                 hold_satellites != 0, (cudaStream_t)stream);
+}
+
+extern "C" int hc_engine_decode_end(hc_engine* eng, int32_t step, void* stream) {
+  HC_REQUIRE(eng, HC_EINVAL, "null argument");
+  return hc::engine_decode_end(eng->e, step, (cudaStream_t)stream);
+}
+
 extern "C" int hc_engine_overlaps(hc_engine* eng, int32_t first, int32_t last, int32_t* out,
                                   void* stream) {
   HC_REQUIRE(eng && out, HC_EINVAL, "null argument");
@@ -1185,6 +1321,12 @@ extern "C" int hc_engine_overlaps(hc_engine* eng, int32_t first, int32_t last, i
   auto& e = eng->e;
   HC_REQUIRE(last >= first && last - first < hc::kRing, HC_EINVAL, "overlap window too long");
   cudaStream_t st = (cudaStream_t)stream;
+  if (e.in_step) {  // inside an open step: read the finished rows beside its K4
+    HC_REQUIRE(last < e.in_step && e.step_end, HC_ESTATE, "overlaps of the open step %d",
+               e.in_step);
+    st = e.side;
+    HC_CUDA_TRY(cudaStreamWaitEvent(st, e.step_end, 0));
+  }
   if (!e.ovl_host)
     HC_CUDA_TRY(cudaHostAlloc((void**)&e.ovl_host, size_t(hc::kRing) * std::max(1, e.n_piv) * 4,
                               cudaHostAllocDefault));

@@ -69,4 +69,14 @@ __host__ __device__ __forceinline__ uint32_t ceil_div_u32(uint32_t a, uint32_t b
   return (a + b - 1) / b;
 }
 
+// Fire selection job (engine fire_batch -> fire_select_kernel): top-k of a
+// dense pivot row whose 13-bit first-digit key histogram is already known.
+struct FireJob {
+  const float* row;       // [n] probability row
+  const uint32_t* hist;   // [8192] histogram of score_key(row) >> 19
+  uint32_t n, k;
+  uint32_t* out_idx;      // [k] selected positions, ascending
+  uint32_t* out_count;
+};
+
 }  // namespace hc

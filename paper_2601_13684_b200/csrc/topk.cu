@@ -344,11 +344,50 @@ __device__ void block_find_bucket(const uint32_t* hist, uint32_t rem, uint32_t* 
   __syncthreads();
 }
 
+// Exact composite threshold T of a row's top set, given the 13-bit bucket b1
+// holding the rem-th largest key: an 8-bit radix over bits 50..0 of the
+// composite key among the bucket's keys -- the m candidates in shared memory,
+// or (cand == nullptr, bucket overflowed) streamed from the row.  Selected
+// <=> key >= T.  hist: >= kMonThreads words of shared scratch.
+__device__ uint64_t radix_threshold(const float* __restrict__ row, uint32_t n, uint32_t b1,
+                                    uint32_t rem, const uint64_t* cand, uint32_t m,
+                                    uint32_t* hist, uint32_t* sh, uint32_t* warp_tot) {
+  const int tid = threadIdx.x;
+  uint64_t prefix = uint64_t(b1) << 51, mask = uint64_t(0x1fff) << 51;
+  for (int shift = 43; ; shift -= 8) {
+    const int sh_eff = shift < 0 ? 0 : shift;
+    const uint64_t dmask = shift < 0 ? ((uint64_t(1) << (shift + 8)) - 1) : uint64_t(255);
+    for (int j = tid; j < kMonThreads; j += kMonThreads) hist[j] = 0;  // 1024-bin scan below
+    __syncthreads();
+    if (cand) {
+      for (uint32_t i = tid; i < m; i += kMonThreads) {
+        const uint64_t key = cand[i];
+        if ((key & mask) == prefix) atomicAdd(&hist[uint32_t((key >> sh_eff) & dmask)], 1u);
+      }
+    } else {
+      for (uint32_t i = tid; i < n; i += kMonThreads) {
+        const uint64_t key = ckey(score_key(__ldg(row + i)), i);
+        if ((key & mask) == prefix) atomicAdd(&hist[uint32_t((key >> sh_eff) & dmask)], 1u);
+      }
+    }
+    __syncthreads();
+    block_find_bucket<kMonThreads>(hist, rem, sh, warp_tot);  // 1024 >= 256 bins (zeros above)
+    const uint32_t b = sh[0];
+    rem = sh[1];
+    const bool done = (sh[2] == rem) || shift <= 0;
+    prefix |= uint64_t(b) << sh_eff;
+    mask |= dmask << sh_eff;
+    __syncthreads();
+    if (done) break;
+  }
+  return prefix;  // bucket fully taken, or keys unique
+}
+
 __global__ void __launch_bounds__(kMonThreads, 1)
 monitor_kernel(const float* __restrict__ rows, int64_t row_stride, const int32_t* __restrict__ slots,
                uint32_t n, uint32_t k, const uint32_t* __restrict__ kbase, int words,
                uint64_t* __restrict__ thr_out, uint32_t* __restrict__ ovl_out,
-               uint32_t* __restrict__ ghist) {
+               const uint32_t* __restrict__ ghist, uint32_t* __restrict__ ghist_next) {
   extern __shared__ __align__(16) uint8_t mon_smem[];
   uint32_t* hist = reinterpret_cast<uint32_t*>(mon_smem);
   uint64_t* cand = reinterpret_cast<uint64_t*>(mon_smem + kMonBins * 4);
@@ -361,11 +400,14 @@ monitor_kernel(const float* __restrict__ rows, int64_t row_stride, const int32_t
   const int tid = threadIdx.x, lane = tid & 31;
 
   // ghist (optional): this row's first-digit histogram, built by the kernel
-  // that wrote the row (score_rows_kernel); consumed and cleared here
-  uint32_t* gh = ghist ? ghist + size_t(s) * kMonBins : nullptr;
+  // that wrote the row (score_rows_kernel).  It stays valid for one more step
+  // (fire selection reads it); the other buffer is cleared for the next step.
+  const uint32_t* gh = ghist ? ghist + size_t(s) * kMonBins : nullptr;
+  uint32_t* gh_next = ghist_next ? ghist_next + size_t(s) * kMonBins : nullptr;
+  if (gh_next)
+#pragma unroll
+    for (int q = 0; q < kMonBins / kMonThreads; ++q) gh_next[tid + q * kMonThreads] = 0u;
   if (k >= n) {  // everything is selected
-    if (gh)
-      for (int j = tid; j < kMonBins; j += kMonThreads) gh[j] = 0u;
     uint32_t c = 0;
     for (uint32_t i = tid; i < n; i += kMonThreads) c += (__ldg(bm + (i >> 5)) >> (i & 31)) & 1u;
     for (int off = 16; off; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
@@ -449,35 +491,7 @@ monitor_kernel(const float* __restrict__ rows, int64_t row_stride, const int32_t
   if (!whole) {
     const uint32_t m = sh[3];
     const bool in_smem = m <= uint32_t(kMonCand);
-    uint64_t prefix = uint64_t(b1) << 51, mask = uint64_t(0x1fff) << 51;
-    // 8-bit radix over bits 50..0 of the composite key among the candidates
-    for (int shift = 43; ; shift -= 8) {
-      const int sh_eff = shift < 0 ? 0 : shift;
-      const uint64_t dmask = shift < 0 ? ((uint64_t(1) << (shift + 8)) - 1) : uint64_t(255);
-      for (int j = tid; j < kMonThreads; j += kMonThreads) hist[j] = 0;  // 1024-bin scan below
-      __syncthreads();
-      if (in_smem) {
-        for (uint32_t i = tid; i < m; i += kMonThreads) {
-          const uint64_t key = cand[i];
-          if ((key & mask) == prefix) atomicAdd(&hist[uint32_t((key >> sh_eff) & dmask)], 1u);
-        }
-      } else {
-        for (uint32_t i = tid; i < n; i += kMonThreads) {
-          const uint64_t key = ckey(score_key(__ldg(row + i)), i);
-          if ((key & mask) == prefix) atomicAdd(&hist[uint32_t((key >> sh_eff) & dmask)], 1u);
-        }
-      }
-      __syncthreads();
-      block_find_bucket<kMonThreads>(hist, rem, sh, warp_tot);  // 1024 >= 256 bins (zeros above)
-      const uint32_t b = sh[0];
-      rem = sh[1];
-      const bool done = (sh[2] == rem) || shift <= 0;
-      prefix |= uint64_t(b) << sh_eff;
-      mask |= dmask << sh_eff;
-      __syncthreads();
-      if (done) break;
-    }
-    T = prefix;  // selected <=> key >= prefix (bucket fully taken, or keys unique)
+    T = radix_threshold(row, n, b1, rem, in_smem ? cand : nullptr, m, hist, sh, warp_tot);
     // candidates at or above T add their K_base bits
     if (in_smem) {
       for (uint32_t i = tid; i < m; i += kMonThreads) {
@@ -503,9 +517,6 @@ monitor_kernel(const float* __restrict__ rows, int64_t row_stride, const int32_t
     thr_out[s] = T;
     ovl_out[s] = sh[3];
   }
-  if (gh)
-#pragma unroll
-    for (int q = 0; q < kMonBins / kMonThreads; ++q) gh[tid + q * kMonThreads] = 0u;
 }
 
 // K_base <- {p : key(p) >= T} over [0, n) for the listed pivot slots
@@ -528,11 +539,167 @@ __global__ void restamp_threshold_kernel(const float* __restrict__ rows, int64_t
   }
 }
 
+// K1 for fire selection (engine.py:326-329): top-k positions of a pivot row
+// whose first-digit histogram the score-row kernel already built.  One CTA
+// per satellite job, two passes over the (L2-resident) row instead of up to
+// nine: (A) each warp scans its contiguous segment, counting keys above the
+// threshold bucket and collecting the bucket's keys as candidates; a radix
+// select over the candidates gives the exact composite threshold T, and the
+// candidates >= T are added to their segments' counts; (C) after one scan
+// over the 32 segment counts every warp writes its selected positions in
+// ascending order (warp prefix sums, no block barriers in the loop).
+constexpr int kFireCand = 12288;
+constexpr int kFireSmem = kFireCand * 8 + kMonThreads * 4 + 96 * 4;
+
+__global__ void __launch_bounds__(kMonThreads, 2) fire_select_kernel(const FireJob* __restrict__ jobs) {
+  extern __shared__ __align__(16) uint8_t fs_smem[];
+  uint64_t* cand = reinterpret_cast<uint64_t*>(fs_smem);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(fs_smem + kFireCand * 8);  // radix scratch
+  uint32_t* sh = hist + kMonThreads;  // [0..7]
+  uint32_t* warp_tot = sh + 8;        // [32]
+  uint32_t* seg = sh + 40;            // [32] per-warp selected counts -> offsets
+  const FireJob job = jobs[blockIdx.x];
+  const uint32_t n = job.n, k = job.k;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (k >= n || k == 0) {  // everything / nothing
+    const uint32_t c = k >= n ? n : 0u;
+    for (uint32_t i = tid; i < c; i += kMonThreads) job.out_idx[i] = i;
+    if (tid == 0) *job.out_count = c;
+    return;
+  }
+  block_find_bucket<kMonBins>(job.hist, k, sh, warp_tot);
+  const uint32_t b1 = sh[0];
+  const uint32_t rem = sh[1];
+  const bool whole = (sh[2] == rem);
+  __syncthreads();
+  if (tid == 0) sh[3] = 0;
+  if (tid < 32) seg[tid] = 0;
+  __syncthreads();
+
+  const float4* __restrict__ row4 = reinterpret_cast<const float4*>(job.row);
+  const uint32_t nv = (n + 3) / 4;
+  const uint32_t segv = (nv + 31) / 32;
+  const uint32_t wbeg = min(nv, uint32_t(warp) * segv), wend = min(nv, wbeg + segv);
+  constexpr int kU = 4;
+  // ---- pass A: keys above bucket b1, candidates inside it ----
+  uint32_t above = 0;
+  for (uint32_t v0 = wbeg + lane; v0 < wend; v0 += 32 * kU) {
+    float4 x[kU];
+#pragma unroll
+    for (int q = 0; q < kU; ++q)
+      if (v0 + q * 32 < wend) x[q] = __ldg(row4 + v0 + q * 32);
+#pragma unroll
+    for (int q = 0; q < kU; ++q) {
+      const uint32_t v = v0 + q * 32;
+      if (v >= wend) break;
+      const float xs[4] = {x[q].x, x[q].y, x[q].z, x[q].w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint32_t pos = 4 * v + e;
+        if (pos >= n) break;
+        const uint32_t k32 = score_key(xs[e]);
+        const uint32_t d = k32 >> 19;
+        if (d > b1 || (whole && d == b1)) {
+          ++above;
+        } else if (d == b1) {
+          const uint32_t at = atomicAdd(&sh[3], 1u);
+          if (at < uint32_t(kFireCand)) cand[at] = ckey(k32, pos);
+        }
+      }
+    }
+  }
+  for (int off = 16; off; off >>= 1) above += __shfl_xor_sync(0xffffffffu, above, off);
+  if (lane == 0) atomicAdd(&seg[warp], above);
+  __syncthreads();
+  uint64_t T = uint64_t(b1) << 51;
+  if (!whole) {
+    const uint32_t m = sh[3];
+    const bool in_smem = m <= uint32_t(kFireCand);
+    T = radix_threshold(job.row, n, b1, rem, in_smem ? cand : nullptr, m, hist, sh, warp_tot);
+    if (in_smem) {
+      for (uint32_t i = tid; i < m; i += kMonThreads) {
+        const uint64_t key = cand[i];
+        if (key >= T) atomicAdd(&seg[min((~uint32_t(key) >> 2) / segv, 31u)], 1u);
+      }
+    } else {
+      for (uint32_t i = tid; i < n; i += kMonThreads) {
+        const uint64_t key = ckey(score_key(__ldg(job.row + i)), i);
+        if ((key >> 51) == b1 && key >= T) atomicAdd(&seg[min((i >> 2) / segv, 31u)], 1u);
+      }
+    }
+    __syncthreads();
+  }
+  if (warp == 0) {  // exclusive scan of the segment counts
+    const uint32_t c = seg[lane];
+    uint32_t incl = c;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += u;
+    }
+    seg[lane] = incl - c;
+  }
+  __syncthreads();
+  // ---- pass C: ordered write of the selected positions ----
+  uint32_t off = seg[warp];
+  for (uint32_t v0 = wbeg; v0 < wend; v0 += 32 * kU) {
+    float4 x[kU];
+#pragma unroll
+    for (int q = 0; q < kU; ++q) {
+      const uint32_t v = v0 + q * 32 + lane;
+      if (v < wend) x[q] = __ldg(row4 + v);
+    }
+#pragma unroll
+    for (int q = 0; q < kU; ++q) {
+      const uint32_t vb = v0 + q * 32;
+      if (vb >= wend) break;  // warp-uniform
+      const uint32_t v = vb + lane;
+      const float xs[4] = {x[q].x, x[q].y, x[q].z, x[q].w};
+      uint32_t selm = 0, c = 0;
+      if (v < wend) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t pos = 4 * v + e;
+          if (pos < n && ckey(score_key(xs[e]), pos) >= T) {
+            selm |= 1u << e;
+            ++c;
+          }
+        }
+      }
+      uint32_t incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+      }
+      uint32_t p = off + incl - c;
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (selm & (1u << e)) job.out_idx[p++] = 4 * v + e;
+      off += __shfl_sync(0xffffffffu, incl, 31);
+    }
+  }
+  if (tid == 0) *job.out_count = k;
+}
+
 }  // namespace
+
+int launch_fire_select(const FireJob* jobs_dev, int n_jobs, cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    HC_CUDA_TRY(cudaFuncSetAttribute(fire_select_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kFireSmem));
+    configured = true;
+  }
+  if (n_jobs <= 0) return HC_OK;
+  fire_select_kernel<<<n_jobs, kMonThreads, kFireSmem, st>>>(jobs_dev);
+  HC_CHECK_LAUNCH();
+  return HC_OK;
+}
 
 int launch_monitor(const float* rows, int64_t row_stride, const int32_t* slots, int n_rows,
                    uint32_t n, uint32_t k, const uint32_t* kbase, int words, uint64_t* thr,
-                   uint32_t* ovl, cudaStream_t st, uint32_t* ghist) {
+                   uint32_t* ovl, cudaStream_t st, const uint32_t* ghist, uint32_t* ghist_next) {
   static bool configured = false;
   if (!configured) {
     HC_CUDA_TRY(cudaFuncSetAttribute(monitor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -541,7 +708,7 @@ int launch_monitor(const float* rows, int64_t row_stride, const int32_t* slots, 
   }
   if (n_rows <= 0) return HC_OK;
   monitor_kernel<<<n_rows, kMonThreads, kMonSmem, st>>>(rows, row_stride, slots, n, k, kbase,
-                                                        words, thr, ovl, ghist);
+                                                        words, thr, ovl, ghist, ghist_next);
   HC_CHECK_LAUNCH();
   return HC_OK;
 }
@@ -573,7 +740,7 @@ extern "C" int hc_monitor_rows(const float* rows_dev, int64_t row_stride, int32_
   for (int i = 0; i < n_rows; ++i) iota[i] = i;
   HC_CUDA_TRY(cudaMemcpyAsync(slots, iota.data(), iota.size() * 4, cudaMemcpyHostToDevice, st));
   int rc = hc::launch_monitor(rows_dev, row_stride, slots, n_rows, n, k, kbase_dev, words,
-                              thr_dev, ovl_dev, st, nullptr);
+                              thr_dev, ovl_dev, st, nullptr, nullptr);
   HC_CUDA_TRY(cudaFreeAsync(slots, st));
   HC_CUDA_TRY(cudaStreamSynchronize(st));
   return rc;

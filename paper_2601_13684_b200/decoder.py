@@ -97,7 +97,7 @@ class HeteroCacheDecoder:
     def __init__(self, taxonomy, plan, config: EngineConfig = EngineConfig(), *, batch: int,
                  group: int, max_decode: int, head_dim: int = 128, chunk: int = 1024,
                  host_pool: bool = True, bytes_per_kv_entry: int | None = None,
-                 track_sets: bool = True, obs_window: int = 1):
+                 track_sets: bool = True, obs_window: int = 1, overlap_decisions: bool = True):
         _lib.require_cuda()
         self.lib = _lib.load()
         self.taxonomy, self.plan, self.config = taxonomy, plan, config
@@ -153,6 +153,10 @@ class HeteroCacheDecoder:
         np.median(np.zeros((2, 2)), axis=0)  # first call imports numpy.ma (~30 ms): not mid-run
         self._fire_events = []
         self._prefilled = set()
+        # boundary decision taken while the next step's attention runs (see
+        # decode_step); (step, first, per-sequence (charged, extra)) or None
+        self.overlap_decisions = overlap_decisions
+        self._open = None
 
     # ---- helpers -------------------------------------------------------------
 
@@ -248,23 +252,24 @@ class HeteroCacheDecoder:
         inter = int(np.isin(np.fromiter(extras, dtype=np.int64, count=len(extras)), dyn).sum())
         return len(dyn) + len(extras) - inter + t
 
-    def _row(self, st: SequenceState, t: int, flag: int) -> StepRow:
+    def _row_sizes(self, st: SequenceState, t: int):
         charged = len(self.full) * self.L + sum(st.dyn_count.values())
         if self.track_sets:
             total = len(self.full) * (self.L + t) + sum(self._size_of(st, hd, t) for hd in self.comp)
             extra = total - charged
         else:
             extra = -1
+        return charged, extra
+
+    def _row(self, st: SequenceState, t: int, flag: int, sizes=None) -> StepRow:
+        charged, extra = sizes if sizes is not None else self._row_sizes(st, t)
         return StepRow(step=t, recall=math.nan, gpu_entries=charged, extra_entries=extra,
                        bytes_in_flight=st.bytes_in_flight(t), cumulative_bytes=st.cumulative_bytes,
                        retrieval_flag=flag)
 
-    def decode_step(self, t: int, q, k_new, v_new, out, stream=None, *, rows: bool = True):
-        """q/out: [B, NL, H*G, D] bf16; k_new/v_new: [B, NL, H, D] bf16 (device)."""
-        cfg = self.config
-        sh = _lib.stream_handle(stream)
-        # 1. land due transfers (engine.py:293-299): per sequence in (completion,
-        #    order) order, all sequences in one batched call
+    def _land_due(self, t: int, sh) -> None:
+        """Land due transfers (engine.py:293-299): per sequence in (completion,
+        order) order, all sequences in one batched call."""
         land = []
         for st in self.states:
             if st.pending and st.pending[0][0] <= t:  # pending is kept sorted
@@ -281,19 +286,57 @@ class HeteroCacheDecoder:
         if land:
             ids = np.asarray(land, dtype=np.int32)
             _lib.check(self.lib.hc_engine_land_batch(self.handle, len(ids), ids.ctypes.data, sh))
-        # 2-4. append, attention, pivot rows, top-l_base + overlap counts
-        _lib.check(self.lib.hc_engine_decode_step(self.handle, t, _lib.ptr(q), _lib.ptr(k_new),
-                                                  _lib.ptr(v_new), _lib.ptr(out), sh))
+
+    def decode_step(self, t: int, q, k_new, v_new, out, stream=None, *, rows: bool = True):
+        """q/out: [B, NL, H*G, D] bf16; k_new/v_new: [B, NL, H, D] bf16 (device).
+
+        With overlap_decisions (default) a window boundary's decision (median
+        test, firing, engine.py:313-360) is taken inside the NEXT step, after
+        that step's attention over every non-satellite head is queued: the
+        host work and the fetch selection then overlap the GPU instead of
+        idling it.  Semantics are unchanged -- the decision reads step t's
+        counts and rows, its transfers land at their completion steps -- but
+        the StepRow / events of boundary step t appear when step t+1 runs (or
+        at finish()).
+        """
+        cfg = self.config
+        sh = _lib.stream_handle(stream)
+        hold = self._open is not None
+        self._land_due(t, sh)
+        if hold:
+            _lib.check(self.lib.hc_engine_decode_begin(self.handle, t, _lib.ptr(q),
+                                                       _lib.ptr(k_new), _lib.ptr(v_new),
+                                                       _lib.ptr(out), 1, sh))
+            self._close_decision(sh)
+            self._land_due(t, sh)  # transfers the decision completes at t
+            _lib.check(self.lib.hc_engine_decode_end(self.handle, t, sh))
+        else:
+            _lib.check(self.lib.hc_engine_decode_step(self.handle, t, _lib.ptr(q), _lib.ptr(k_new),
+                                                      _lib.ptr(v_new), _lib.ptr(out), sh))
+        boundary = self.monitor and (cfg.eval_every_step or t % cfg.window == 0)
+        if boundary:
+            first = t if cfg.eval_every_step else max(1, t - cfg.window + 1)
+            self._open = (t, first, [self._row_sizes(st, t) for st in self.states]
+                          if rows else None)
+            if not self.overlap_decisions:
+                self._close_decision(sh)
+        elif rows:
+            for st in self.states:
+                st.rows.append(self._row(st, t, 0))
+
+    def _close_decision(self, sh) -> None:
+        t, first, sizes = self._open
+        self._open = None
         flags = [0] * self.B
-        if self.monitor:
-            boundary = cfg.eval_every_step or (t % cfg.window == 0)
-            if boundary:
-                first = t if cfg.eval_every_step else max(1, t - cfg.window + 1)
-                self._decide(t, first, flags, sh)
-        if rows:
+        self._decide(t, first, flags, sh)
+        if sizes is not None:
             for b, st in enumerate(self.states):
-                st.rows.append(self._row(st, t, flags[b]))
-        return flags
+                st.rows.append(self._row(st, t, flags[b], sizes[b]))
+
+    def finish(self, stream=None) -> None:
+        """Take a still-open boundary decision (the last decoded step's)."""
+        if self._open is not None:
+            self._close_decision(_lib.stream_handle(stream))
 
     def _decide(self, t: int, first: int, flags: list, sh) -> None:
         """Window median test and firing (engine.py:305-360), vectorised over pivots.
@@ -401,6 +444,7 @@ class HeteroCacheDecoder:
     def sync(self, stream=None) -> None:
         import torch
 
+        self.finish(stream)
         torch.cuda.current_stream().synchronize() if stream is None else stream.synchronize()
         self._collect_fetched()
 

@@ -31,7 +31,7 @@ ROW_RTOL = 2e-3
 
 def _build(variant="heterocache", delay=1, bandwidth=1 << 30, B=2, NL=2, L=700, T=40,
            chunk=256, host_pool=True, window=8, eval_every_step=False, shift=13, seed=3,
-           obs_window=1, sinks=4, recency=8):
+           obs_window=1, sinks=4, recency=8, overlap_decisions=True):
     import torch
 
     from paper_2601_13684_b200.decoder import HeteroCacheDecoder
@@ -46,7 +46,8 @@ def _build(variant="heterocache", delay=1, bandwidth=1 << 30, B=2, NL=2, L=700, 
                        eval_every_step=eval_every_step, sink_count=sinks,
                        recency_window=recency)
     dec = HeteroCacheDecoder(tax, plan, cfg, batch=B, group=model.group, max_decode=T,
-                             chunk=chunk, host_pool=host_pool, obs_window=obs_window)
+                             chunk=chunk, host_pool=host_pool, obs_window=obs_window,
+                             overlap_decisions=overlap_decisions)
     gen = SyntheticKV(model, batch=B, prefill_len=L, num_layers=NL, hot=plan.l_base_int,
                       seed=seed)
     dump = torch.zeros(NL, B * model.kv_heads, L, device="cuda")
@@ -84,6 +85,7 @@ def _run(ctx, check_steps=()):
         if t in check_steps:
             outs[t] = o.clone()
             dyn_seen[t] = {(b, hd): dec.dynamic_set(b, hd) for b in range(B) for hd in dec.comp}
+    dec.finish()  # the last boundary's decision
     torch.cuda.synchronize()
     rows = {k: v.cpu().numpy() for k, v in rows.items()}
     return rows, outs, news, dyn_seen
@@ -208,6 +210,11 @@ def test_prefill_rows_match_oracle():
     dict(L=700, T=20, window=4, shift=9, chunk=192, B=3),
     dict(sinks=0, recency=0, window=4, shift=9, T=20),
     dict(sinks=16, recency=32, window=4, shift=9, T=40),
+    # boundary decisions taken synchronously (hc_engine_decode_step path) instead
+    # of inside the next step's attention
+    dict(overlap_decisions=False),
+    dict(overlap_decisions=False, bandwidth=3000, window=4, shift=(6, 11, 19, 27), T=36),
+    dict(overlap_decisions=False, eval_every_step=True),
 ])
 def test_decoder_variants_match_oracle(kw):
     ctx = _build(**kw)
