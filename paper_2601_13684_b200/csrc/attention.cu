@@ -362,77 +362,59 @@ __global__ void __launch_bounds__(128) combine_kernel(const AttnParams p) {
 // GQA-mean probability row of every pivot over [0, L + t):
 //   row[pos] = (sum_j e_j(pos) * 2^(m_j(pos/16) - M_j) * (1 / L_j)) / G
 // i.e. (sum_j exp(s_j - max_j) / sum_j) / G in head order (model.ts:283-289).
-// A block covers kRowsSpan positions of one pivot; each thread takes 8
-// consecutive positions per pass (one 16-B load of fp16 material per head,
-// one m_ref and one exp2 per head).  With p.hist set, the block also builds
-// the 13-bit first-digit histogram of the row's composite keys in shared
-// memory and adds it to the pivot's global histogram, so the monitor's first
-// pass over the row disappears (monitor_kernel reads and clears it).
+// One thread per 8 consecutive positions: all G 16-B loads of fp16 material
+// and G m_ref loads are issued before any is consumed (latency-bound
+// otherwise), then one exp2 per head and 8 FMAs.
 constexpr int kRowsThreads = 256;
-constexpr int kRowsPasses = 4;
-constexpr int kRowsSpan = kRowsThreads * 8 * kRowsPasses;  // 8192 positions per block
-constexpr int kHistBins = 8192;                            // key32 >> 19
+constexpr int kRowsSpan = kRowsThreads * 8;  // positions per block
 
 template <int G>
 __global__ void __launch_bounds__(kRowsThreads) score_rows_kernel(const AttnParams p,
                                                                   const int32_t* __restrict__ pivot_units) {
-  extern __shared__ uint32_t rows_hist[];  // [kHistBins] when p.hist
   __shared__ float s_m[G], s_inv[G];
   const UnitDesc u = p.units[pivot_units[blockIdx.y]];
   const int slot = u.pivot_slot;
   const int len = p.L + p.t;
   const int tid = threadIdx.x;
-  uint32_t* gh = p.hist ? p.hist + size_t(slot) * kHistBins : nullptr;
-  if (gh)
-    for (int b = tid; b < kHistBins; b += kRowsThreads) rows_hist[b] = 0u;
   if (tid < G) {
     s_m[tid] = p.stats[(size_t(slot) * G + tid) * 2 + 0];
     s_inv[tid] = 1.0f / p.stats[(size_t(slot) * G + tid) * 2 + 1];
   }
   __syncthreads();
+  const int pos = blockIdx.x * kRowsSpan + tid * 8;
+  if (pos >= len) return;
   const __half* lg = reinterpret_cast<const __half*>(p.logits) + size_t(slot) * G * p.logit_stride;
   const float* mr = p.mref + size_t(slot) * G * (p.logit_stride / 16);
-  float* row = p.rows + size_t(slot) * p.row_stride;
-  const float rg = float(G);
-#pragma unroll 1
-  for (int it = 0; it < kRowsPasses; ++it) {
-    const int pos = blockIdx.x * kRowsSpan + (it * kRowsThreads + tid) * 8;
-    if (pos >= len) break;
-    float acc[8];
+  uint4 raw[G];
+  float mv[G];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+  for (int j = 0; j < G; ++j) {
+    raw[j] = __ldcs(reinterpret_cast<const uint4*>(lg + size_t(j) * p.logit_stride + pos));
+    mv[j] = __ldg(mr + size_t(j) * (p.logit_stride / 16) + pos / 16);
+  }
+  float acc[8];
 #pragma unroll
-    for (int j = 0; j < G; ++j) {
-      const float cj = exp2f(mr[size_t(j) * (p.logit_stride / 16) + pos / 16] - s_m[j]) * s_inv[j];
-      const uint4 raw = *reinterpret_cast<const uint4*>(lg + size_t(j) * p.logit_stride + pos);
-      const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+  for (int e = 0; e < 8; ++e) acc[e] = 0.f;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[q]));
-        acc[2 * q] += f.x * cj;
-        acc[2 * q + 1] += f.y * cj;
-      }
-    }
+  for (int j = 0; j < G; ++j) {
+    const float cj = exp2f(mv[j] - s_m[j]) * s_inv[j];
+    const uint32_t w[4] = {raw[j].x, raw[j].y, raw[j].z, raw[j].w};
 #pragma unroll
-    for (int e = 0; e < 8; ++e) acc[e] = acc[e] / rg;
-    if (pos + 7 < len) {
-      reinterpret_cast<float4*>(row + pos)[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
-      reinterpret_cast<float4*>(row + pos)[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
-    } else {
-      for (int e = 0; pos + e < len; ++e) row[pos + e] = acc[e];
-    }
-    if (gh) {
-#pragma unroll
-      for (int e = 0; e < 8; ++e)
-        if (pos + e < len) atomicAdd(&rows_hist[score_key(acc[e]) >> 19], 1u);
+    for (int q = 0; q < 4; ++q) {
+      const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[q]));
+      acc[2 * q] += f.x * cj;
+      acc[2 * q + 1] += f.y * cj;
     }
   }
-  if (gh) {
-    __syncthreads();
-    for (int b = tid; b < kHistBins; b += kRowsThreads) {
-      const uint32_t c = rows_hist[b];
-      if (c) atomicAdd(gh + b, c);
-    }
+  const float rg = float(G);
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = acc[e] / rg;
+  float* row = p.rows + size_t(slot) * p.row_stride;
+  if (pos + 7 < len) {
+    reinterpret_cast<float4*>(row + pos)[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    reinterpret_cast<float4*>(row + pos)[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+  } else {
+    for (int e = 0; pos + e < len; ++e) row[pos + e] = acc[e];
   }
 }
 
@@ -524,9 +506,8 @@ int launch_attn_post(const AttnParams& p, const int32_t* pivot_units_dev, int n_
                "score-row strides must be multiples of 16 / 8");
     const int len = p.L + p.t;
     dim3 grid((len + kRowsSpan - 1) / kRowsSpan, n_pivots);
-    const size_t smem = p.hist ? kHistBins * 4 : 0;
     switch (p.group) {
-#define HC_ROWS(GG) case GG: score_rows_kernel<GG><<<grid, kRowsThreads, smem, st>>>(p, pivot_units_dev); break;
+#define HC_ROWS(GG) case GG: score_rows_kernel<GG><<<grid, kRowsThreads, 0, st>>>(p, pivot_units_dev); break;
       HC_ROWS(1) HC_ROWS(2) HC_ROWS(3) HC_ROWS(4) HC_ROWS(5) HC_ROWS(6) HC_ROWS(7) HC_ROWS(8)
 #undef HC_ROWS
     }

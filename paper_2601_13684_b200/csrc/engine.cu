@@ -40,8 +40,7 @@ int launch_obs_scores(const void* k, const void* q_obs, int B, int H, int G, int
                       float* out, int64_t row_stride, void* scratch, cudaStream_t st);
 int launch_monitor(const float* rows, int64_t row_stride, const int32_t* slots, int n_rows,
                    uint32_t n, uint32_t k, const uint32_t* kbase, int words, uint64_t* thr,
-                   uint32_t* ovl, cudaStream_t st, const uint32_t* ghist = nullptr,
-                   uint32_t* ghist_next = nullptr);
+                   uint32_t* ovl, cudaStream_t st, uint32_t* hist_out = nullptr);
 int launch_fire_select(const FireJob* jobs_dev, int n_jobs, cudaStream_t st);
 int launch_restamp_threshold(const float* rows, int64_t row_stride, const int32_t* slots,
                              int n_rows, uint32_t n, const uint64_t* thr, uint32_t* kbase,
@@ -150,7 +149,7 @@ struct EngineImpl {
   uint32_t* ovl_host = nullptr;     // pinned readback of the overlap window
   uint64_t* thr = nullptr;          // per pivot slot: composite-key threshold of its top set
   uint32_t* ghist = nullptr;        // [2][pivot slot][8192] first-digit key histograms of the
-                                    // rows: step t fills buffer t&1 (rows -> monitor -> fire)
+                                    // rows: step t's monitor fills buffer t&1 for its fires
   int32_t* d_piv_slots = nullptr;   // iota over pivot slots
   int last_t = 0;                   // last decode step run
   hc_topk_job* d_piv_jobs = nullptr;
@@ -485,7 +484,6 @@ AttnParams decode_params(EngineImpl& e, int t, const void* q, void* o) {
   p.mref = e.mref;
   p.stats = e.stats;
   p.rows = e.n_piv ? e.rowbuf : nullptr;
-  p.hist = e.n_piv ? e.ghist + size_t(t & 1) * e.n_piv * 8192 : nullptr;
   p.logit_stride = e.row_len;
   p.row_stride = e.row_len;
   p.group = e.G;
@@ -643,8 +641,7 @@ int engine_decode_end(EngineImpl& e, int t, cudaStream_t st) {
     HC_TRY(launch_monitor(e.rowbuf, e.row_len, e.d_piv_slots, e.n_piv, uint32_t(e.L + t),
                           uint32_t(e.lbase), e.kbase, e.words, e.thr,
                           e.ovl_ring + size_t(t % kRing) * e.n_piv, st,
-                          e.ghist + size_t(t & 1) * e.n_piv * 8192,
-                          e.ghist + size_t((t + 1) & 1) * e.n_piv * 8192));
+                          e.ghist + size_t(t & 1) * e.n_piv * 8192));
   }
   if (ev) {
     HC_CUDA_TRY(cudaEventRecord(ev[5], st));

@@ -126,7 +126,6 @@ struct AttnParams {
   int32_t n_units;
   float scale_log2;      // log2(e) / sqrt(d)
   const uint8_t* skip;   // per unit: 1 = tiles deferred to a later launch (landing units), or null
-  uint32_t* hist;        // [pivot slots][8192] first-digit key histogram of the rows, or null
 };
 
 constexpr int kPartStride = 132;  // M, L, pad, pad, O[128]

@@ -387,7 +387,7 @@ __global__ void __launch_bounds__(kMonThreads, 1)
 monitor_kernel(const float* __restrict__ rows, int64_t row_stride, const int32_t* __restrict__ slots,
                uint32_t n, uint32_t k, const uint32_t* __restrict__ kbase, int words,
                uint64_t* __restrict__ thr_out, uint32_t* __restrict__ ovl_out,
-               const uint32_t* __restrict__ ghist, uint32_t* __restrict__ ghist_next) {
+               uint32_t* __restrict__ hist_out) {
   extern __shared__ __align__(16) uint8_t mon_smem[];
   uint32_t* hist = reinterpret_cast<uint32_t*>(mon_smem);
   uint64_t* cand = reinterpret_cast<uint64_t*>(mon_smem + kMonBins * 4);
@@ -399,14 +399,9 @@ monitor_kernel(const float* __restrict__ rows, int64_t row_stride, const int32_t
   const uint32_t* __restrict__ bm = kbase + size_t(s) * words;
   const int tid = threadIdx.x, lane = tid & 31;
 
-  // ghist (optional): this row's first-digit histogram, built by the kernel
-  // that wrote the row (score_rows_kernel).  It stays valid for one more step
-  // (fire selection reads it); the other buffer is cleared for the next step.
-  const uint32_t* gh = ghist ? ghist + size_t(s) * kMonBins : nullptr;
-  uint32_t* gh_next = ghist_next ? ghist_next + size_t(s) * kMonBins : nullptr;
-  if (gh_next)
-#pragma unroll
-    for (int q = 0; q < kMonBins / kMonThreads; ++q) gh_next[tid + q * kMonThreads] = 0u;
+  // hist_out (optional): the row's first-digit histogram is published for
+  // the fire selection of this step (fire_select_kernel)
+  uint32_t* gh = hist_out ? hist_out + size_t(s) * kMonBins : nullptr;
   if (k >= n) {  // everything is selected
     uint32_t c = 0;
     for (uint32_t i = tid; i < n; i += kMonThreads) c += (__ldg(bm + (i >> 5)) >> (i & 31)) & 1u;
@@ -421,35 +416,39 @@ monitor_kernel(const float* __restrict__ rows, int64_t row_stride, const int32_t
   if (tid == 0) sh[3] = 0;  // candidate count
   const uint32_t n4 = n >> 2;
   const float4* __restrict__ row4 = reinterpret_cast<const float4*>(row);
-  if (gh) {  // all loads in flight at once; the clearing stores go out at the end
-    uint32_t hv[kMonBins / kMonThreads];
-#pragma unroll
-    for (int q = 0; q < kMonBins / kMonThreads; ++q) hv[q] = __ldcg(gh + tid + q * kMonThreads);
-#pragma unroll
-    for (int q = 0; q < kMonBins / kMonThreads; ++q) hist[tid + q * kMonThreads] = hv[q];
-  } else {
-    for (int j = tid; j < kMonBins; j += kMonThreads) hist[j] = 0;
-  }
+  for (int j = tid; j < kMonBins; j += kMonThreads) hist[j] = 0;
   __syncthreads();
-  for (uint32_t i = tid; !gh && i < n4; i += kMonThreads) {
-    const float4 v = __ldg(row4 + i);
-    atomicAdd(&hist[score_key(v.x) >> 19], 1u);
-    atomicAdd(&hist[score_key(v.y) >> 19], 1u);
-    atomicAdd(&hist[score_key(v.z) >> 19], 1u);
-    atomicAdd(&hist[score_key(v.w) >> 19], 1u);
+  // pass 1: 13-bit histogram; four float4 loads in flight per thread (one
+  // CTA per row: the pass is bound by bytes in flight per SM)
+  constexpr int kU = 4;
+  for (uint32_t i0 = tid; i0 < n4; i0 += kMonThreads * kU) {
+    float4 v[kU];
+#pragma unroll
+    for (int q = 0; q < kU; ++q)
+      if (i0 + q * kMonThreads < n4) v[q] = __ldg(row4 + i0 + q * kMonThreads);
+#pragma unroll
+    for (int q = 0; q < kU; ++q) {
+      if (i0 + q * kMonThreads >= n4) break;
+      atomicAdd(&hist[score_key(v[q].x) >> 19], 1u);
+      atomicAdd(&hist[score_key(v[q].y) >> 19], 1u);
+      atomicAdd(&hist[score_key(v[q].z) >> 19], 1u);
+      atomicAdd(&hist[score_key(v[q].w) >> 19], 1u);
+    }
   }
-  for (uint32_t i = n4 * 4 + tid; !gh && i < n; i += kMonThreads)
+  for (uint32_t i = n4 * 4 + tid; i < n; i += kMonThreads)
     atomicAdd(&hist[score_key(__ldg(row + i)) >> 19], 1u);
   __syncthreads();
+  if (gh)
+#pragma unroll
+    for (int q = 0; q < kMonBins / kMonThreads; ++q)
+      gh[tid + q * kMonThreads] = hist[tid + q * kMonThreads];
   block_find_bucket<kMonBins>(hist, k, sh, warp_tot);
   const uint32_t b1 = sh[0];
   uint32_t rem = sh[1];
   const bool whole = (sh[2] == rem);
   __syncthreads();
 
-  // pass 2: K_base bits above b1, candidates inside b1.  Four float4 loads
-  // are issued before any is consumed: with one CTA per row the pass is
-  // bound by bytes in flight per SM, not by DRAM.
+  // pass 2: K_base bits above b1, candidates inside b1
   uint32_t ovl = 0;
   auto visit = [&](uint32_t pos, float x, uint32_t word) {
     const uint32_t k32 = score_key(x);
@@ -461,7 +460,6 @@ monitor_kernel(const float* __restrict__ rows, int64_t row_stride, const int32_t
       if (at < uint32_t(kMonCand)) cand[at] = ckey(k32, pos);
     }
   };
-  constexpr int kU = 4;
   for (uint32_t i0 = tid; i0 < n4; i0 += kMonThreads * kU) {
     float4 v[kU];
     uint32_t wd[kU];
@@ -699,7 +697,7 @@ int launch_fire_select(const FireJob* jobs_dev, int n_jobs, cudaStream_t st) {
 
 int launch_monitor(const float* rows, int64_t row_stride, const int32_t* slots, int n_rows,
                    uint32_t n, uint32_t k, const uint32_t* kbase, int words, uint64_t* thr,
-                   uint32_t* ovl, cudaStream_t st, const uint32_t* ghist, uint32_t* ghist_next) {
+                   uint32_t* ovl, cudaStream_t st, uint32_t* hist_out) {
   static bool configured = false;
   if (!configured) {
     HC_CUDA_TRY(cudaFuncSetAttribute(monitor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -708,7 +706,7 @@ int launch_monitor(const float* rows, int64_t row_stride, const int32_t* slots, 
   }
   if (n_rows <= 0) return HC_OK;
   monitor_kernel<<<n_rows, kMonThreads, kMonSmem, st>>>(rows, row_stride, slots, n, k, kbase,
-                                                        words, thr, ovl, ghist, ghist_next);
+                                                        words, thr, ovl, hist_out);
   HC_CHECK_LAUNCH();
   return HC_OK;
 }
@@ -740,7 +738,7 @@ extern "C" int hc_monitor_rows(const float* rows_dev, int64_t row_stride, int32_
   for (int i = 0; i < n_rows; ++i) iota[i] = i;
   HC_CUDA_TRY(cudaMemcpyAsync(slots, iota.data(), iota.size() * 4, cudaMemcpyHostToDevice, st));
   int rc = hc::launch_monitor(rows_dev, row_stride, slots, n_rows, n, k, kbase_dev, words,
-                              thr_dev, ovl_dev, st, nullptr, nullptr);
+                              thr_dev, ovl_dev, st, nullptr);
   HC_CUDA_TRY(cudaFreeAsync(slots, st));
   HC_CUDA_TRY(cudaStreamSynchronize(st));
   return rc;
