@@ -310,13 +310,12 @@ attn_tiles_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant
 }
 
 // Merge a unit's split-K partials for one query head (block = (unit, g));
-// write O (bf16) and, for pivots, (M, L).  Block max of the slot maxima,
-// then warp w folds slots w, w+4, ... with lane l owning output dims
-// 4l..4l+3 (512 B coalesced per slot, 4 slots in flight per warp), and the
-// four warp partials meet in shared memory.
+// write O (bf16) and, for pivots, (M, L).  One pass: warp w folds slots
+// w, w+4, ... with an online max (lane l owns output dims 4l..4l+3, 512 B
+// coalesced per slot), eight slots' loads in flight per warp; the four warp
+// states meet in shared memory.
 __global__ void __launch_bounds__(128) combine_kernel(const AttnParams p) {
-  __shared__ float red[4];
-  __shared__ float rls[4];
+  __shared__ float wm[4], wl[4];
   __shared__ __align__(16) float racc[4][128];
   const UnitDesc u = p.units[blockIdx.x];
   const int g = blockIdx.y;
@@ -325,32 +324,51 @@ __global__ void __launch_bounds__(128) combine_kernel(const AttnParams p) {
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   const float* base = p.partial + (size_t(u.slot0) * G + g) * kPartStride;
   const size_t sstride = size_t(G) * kPartStride;
-  float m = -INFINITY;
-  for (int i = tid; i < n; i += 128) m = fmaxf(m, base[i * sstride]);
-  for (int off = 16; off; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
-  if (lane == 0) red[w] = m;
-  __syncthreads();
-  const float M = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
-  const float mb = (M == -INFINITY) ? 0.f : M;
+  constexpr int kU = 8;
+  float m = -INFINITY, l = 0.f;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  float ls = 0.f;
-#pragma unroll 4
-  for (int i = w; i < n; i += 4) {
-    const float* src = base + i * sstride;
-    const float li = src[1];
-    const float f = li == 0.f ? 0.f : exp2f(src[0] - mb);  // empty tile: O never written
-    const float4 o = reinterpret_cast<const float4*>(src + 4)[lane];
-    acc.x += f == 0.f ? 0.f : f * o.x;
-    acc.y += f == 0.f ? 0.f : f * o.y;
-    acc.z += f == 0.f ? 0.f : f * o.z;
-    acc.w += f == 0.f ? 0.f : f * o.w;
-    ls += f * li;
+  for (int i0 = w; i0 < n; i0 += 4 * kU) {
+    float mi[kU], li[kU];
+    float4 oi[kU];
+#pragma unroll
+    for (int q = 0; q < kU; ++q) {
+      const int i = i0 + 4 * q;
+      li[q] = 0.f;
+      mi[q] = -INFINITY;
+      if (i < n) {
+        const float* src = base + i * sstride;
+        mi[q] = src[0];
+        li[q] = src[1];
+        oi[q] = reinterpret_cast<const float4*>(src + 4)[lane];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kU; ++q) {
+      if (li[q] == 0.f) continue;  // empty tile: O never written
+      const float mn = fmaxf(m, mi[q]);
+      const float a = exp2f(m - mn), f = exp2f(mi[q] - mn);
+      acc.x = acc.x * a + f * oi[q].x;
+      acc.y = acc.y * a + f * oi[q].y;
+      acc.z = acc.z * a + f * oi[q].z;
+      acc.w = acc.w * a + f * oi[q].w;
+      l = l * a + f * li[q];
+      m = mn;
+    }
   }
   reinterpret_cast<float4*>(racc[w])[lane] = acc;
-  if (lane == 0) rls[w] = ls;
+  if (lane == 0) {
+    wm[w] = m;
+    wl[w] = l;
+  }
   __syncthreads();
-  const float Ls = (rls[0] + rls[1]) + (rls[2] + rls[3]);
-  const float a = (racc[0][tid] + racc[1][tid]) + (racc[2][tid] + racc[3][tid]);
+  const float M = fmaxf(fmaxf(wm[0], wm[1]), fmaxf(wm[2], wm[3]));
+  const float mb = (M == -INFINITY) ? 0.f : M;
+  float sw[4];
+#pragma unroll
+  for (int v = 0; v < 4; ++v) sw[v] = wl[v] == 0.f ? 0.f : exp2f(wm[v] - mb);
+  const float Ls = (wl[0] * sw[0] + wl[1] * sw[1]) + (wl[2] * sw[2] + wl[3] * sw[3]);
+  const float a = (racc[0][tid] * sw[0] + racc[1][tid] * sw[1]) +
+                  (racc[2][tid] * sw[2] + racc[3][tid] * sw[3]);
   __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.out);
   if (out) out[(size_t(u.q_row) + g) * kHeadDim + tid] = __float2bfloat16_rn(a / Ls);
   if (u.pivot_slot >= 0 && tid == 0) {
