@@ -206,6 +206,7 @@ def run_b200(args, rank, world):
         t += 1
         q, kn, vn = inputs(t)
         dec.decode_step(t, q, kn, vn, out, rows=False)
+    dec.join()  # the last step's monitor runs on the engine's side stream
     ev1.record(stream)
     torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
@@ -265,6 +266,7 @@ def run_b200(args, rank, world):
             hout[slot].copy_(obuf[slot], non_blocking=True)
             ev_out[slot].record(copy)
     stream.wait_stream(copy)
+    dec.join()
     ev1.record(stream)
     torch.cuda.synchronize()
     barrier()

@@ -232,6 +232,12 @@ int hc_engine_decode_begin(hc_engine* eng, int32_t step, const void* q_dev,
                            int32_t hold_satellites, void* stream);
 int hc_engine_decode_end(hc_engine* eng, int32_t step, void* stream);
 
+/* The per-step drift monitor (overlap counts, thresholds) runs on an
+ * internal stream beside the next step's attention; engine calls that read
+ * its results wait for it.  hc_engine_join makes `stream` wait for the last
+ * step's monitor (e.g. before timing or reading engine memory directly). */
+int hc_engine_join(hc_engine* eng, void* stream);
+
 /* Copy the overlap counts of steps [first, last] (<= 64 steps back) into
  * out [(last-first+1) x n_pivots] (pivot order = ascending unit), then sync. */
 int hc_engine_overlaps(hc_engine* eng, int32_t first, int32_t last, int32_t* out_host,

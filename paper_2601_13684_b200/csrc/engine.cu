@@ -132,7 +132,10 @@ struct EngineImpl {
   std::vector<int> cur_land;
   int32_t* d_land = nullptr;
   int n_lu = 0, n_lt = 0;
-  cudaEvent_t step_end = nullptr;  // end of the last completed step (rows, counts, K_base)
+  cudaEvent_t step_end = nullptr;  // monitor of the last completed step done (rows free again,
+                                   // overlap counts, thresholds and histograms valid)
+  cudaEvent_t rows_done = nullptr;
+  cudaStream_t mon = nullptr;      // the monitor runs beside the next step's attention
   cudaStream_t side = nullptr;     // fire selection and control readbacks inside a step
   int n_slots = 0;
   float* partial = nullptr;
@@ -176,8 +179,9 @@ struct EngineImpl {
   size_t stage_cap = 0, stage_head = 0;
   std::deque<std::tuple<size_t, size_t, cudaEvent_t>> stage_busy;  // (lo, hi, copy done)
   cudaStream_t retr = nullptr;
-  // per-step phase timeline (bench roofline): 7 events per step on the
-  // launching stream: start | append | K4 | combine | score rows | K1 | end
+  // per-step phase timeline (bench roofline): 7 events per step: start |
+  // append | K4 | combine | score rows (step stream) | monitor (its own
+  // stream) | end (step stream)
   static constexpr int kPhaseEvents = 7;
   bool timing = false;
   std::vector<cudaEvent_t> tev;
@@ -239,6 +243,7 @@ int engine_destroy(EngineImpl& e) {
   }
   if (e.retr) cudaStreamDestroy(e.retr);
   if (e.side) cudaStreamDestroy(e.side);
+  if (e.mon) cudaStreamDestroy(e.mon);
   if (e.pf_ev0) cudaEventDestroy(e.pf_ev0);
   if (e.pf_ev1) cudaEventDestroy(e.pf_ev1);
   for (auto x : e.tev) cudaEventDestroy(x);
@@ -470,6 +475,7 @@ int engine_create(EngineImpl& e, const hc_engine_desc& c, const int32_t* roles,
   HC_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
   HC_CUDA_TRY(cudaStreamCreateWithPriority(&e.retr, cudaStreamNonBlocking, hi_prio));
   HC_CUDA_TRY(cudaStreamCreateWithPriority(&e.side, cudaStreamNonBlocking, hi_prio));
+  HC_CUDA_TRY(cudaStreamCreateWithPriority(&e.mon, cudaStreamNonBlocking, hi_prio));
   return HC_OK;
 }
 
@@ -633,22 +639,31 @@ int engine_decode_end(EngineImpl& e, int t, cudaStream_t st) {
   }
   e.cur_land.clear();
   cudaEvent_t* ev = e.cur_ev;
+  // the previous step's monitor (own stream) must be done with the rows
+  if (e.step_end) HC_CUDA_TRY(cudaStreamWaitEvent(st, e.step_end, 0));
   HC_TRY(launch_attn_post(e.cur_p, e.d_piv_units, e.n_piv, st, ev ? ev + 2 : nullptr));
   e.last_t = t;
+  if (!e.step_end) HC_TRY(new_event(e, &e.step_end));
   if (e.n_piv) {
-    // K1+K2: top-l_base threshold and |top & K_base| per pivot (engine.py:305-311)
-    // counts land directly in the overlap ring row of this step
+    // K1+K2: top-l_base threshold and |top & K_base| per pivot (engine.py:305-311);
+    // counts land directly in the overlap ring row of this step.  Nothing in
+    // the next step's attention depends on it, so it runs on its own stream
+    // beside that attention; readers (overlaps, fire, the next score rows)
+    // wait for step_end.
+    if (!e.rows_done) HC_TRY(new_event(e, &e.rows_done));
+    HC_CUDA_TRY(cudaEventRecord(e.rows_done, st));
+    HC_CUDA_TRY(cudaStreamWaitEvent(e.mon, e.rows_done, 0));
     HC_TRY(launch_monitor(e.rowbuf, e.row_len, e.d_piv_slots, e.n_piv, uint32_t(e.L + t),
                           uint32_t(e.lbase), e.kbase, e.words, e.thr,
-                          e.ovl_ring + size_t(t % kRing) * e.n_piv, st,
+                          e.ovl_ring + size_t(t % kRing) * e.n_piv, e.mon,
                           e.ghist + size_t(t & 1) * e.n_piv * 8192));
   }
+  cudaStream_t ms = e.n_piv ? e.mon : st;
   if (ev) {
-    HC_CUDA_TRY(cudaEventRecord(ev[5], st));
+    HC_CUDA_TRY(cudaEventRecord(ev[5], ms));
     HC_CUDA_TRY(cudaEventRecord(ev[6], st));
   }
-  if (!e.step_end) HC_TRY(new_event(e, &e.step_end));
-  HC_CUDA_TRY(cudaEventRecord(e.step_end, st));
+  HC_CUDA_TRY(cudaEventRecord(e.step_end, ms));
   return HC_OK;
 }
 
@@ -1021,13 +1036,14 @@ int engine_fire_batch(EngineImpl& e, int n, const int32_t* pus, int t, const int
   // everything queued on the caller's stream so far.  The caller's stream
   // then waits for them (later score rows overwrite the rows, the monitor
   // reads K_base).
-  cudaEvent_t dep = e.in_step ? e.step_end : nullptr;
-  if (!dep) {
+  cudaStream_t st = e.side;
+  if (e.step_end) HC_CUDA_TRY(cudaStreamWaitEvent(st, e.step_end, 0));
+  if (!e.in_step) {
+    cudaEvent_t dep;
     HC_TRY(new_event(e, &dep));
     HC_CUDA_TRY(cudaEventRecord(dep, caller));
+    HC_CUDA_TRY(cudaStreamWaitEvent(st, dep, 0));
   }
-  cudaStream_t st = e.side;
-  HC_CUDA_TRY(cudaStreamWaitEvent(st, dep, 0));
   std::vector<hc_topk_job> jobs;
   std::vector<FireJob> fjobs;
   // the rows of step t still have their key histograms (buffer t&1) until
@@ -1311,6 +1327,13 @@ extern "C" int hc_engine_decode_end(hc_engine* eng, int32_t step, void* stream) 
   return hc::engine_decode_end(eng->e, step, (cudaStream_t)stream);
 }
 
+extern "C" int hc_engine_join(hc_engine* eng, void* stream) {
+  HC_REQUIRE(eng, HC_EINVAL, "null argument");
+  if (eng->e.step_end)
+    HC_CUDA_TRY(cudaStreamWaitEvent((cudaStream_t)stream, eng->e.step_end, 0));
+  return HC_OK;
+}
+
 extern "C" int hc_engine_overlaps(hc_engine* eng, int32_t first, int32_t last, int32_t* out,
                                   void* stream) {
   HC_REQUIRE(eng && out, HC_EINVAL, "null argument");
@@ -1322,8 +1345,8 @@ extern "C" int hc_engine_overlaps(hc_engine* eng, int32_t first, int32_t last, i
     HC_REQUIRE(last < e.in_step && e.step_end, HC_ESTATE, "overlaps of the open step %d",
                e.in_step);
     st = e.side;
-    HC_CUDA_TRY(cudaStreamWaitEvent(st, e.step_end, 0));
   }
+  if (e.step_end) HC_CUDA_TRY(cudaStreamWaitEvent(st, e.step_end, 0));  // counts written
   if (!e.ovl_host)
     HC_CUDA_TRY(cudaHostAlloc((void**)&e.ovl_host, size_t(hc::kRing) * std::max(1, e.n_piv) * 4,
                               cudaHostAllocDefault));
@@ -1479,9 +1502,13 @@ extern "C" int hc_engine_timing(hc_engine* eng, int32_t enable, double* phase_ms
     for (size_t i = 0; i < e.tev_used; ++i) {
       const cudaEvent_t* ev = e.tev.data() + i * P;
       HC_CUDA_TRY(cudaEventSynchronize(ev[P - 1]));
+      HC_CUDA_TRY(cudaEventSynchronize(ev[5]));
+      // append | attention | combine | score rows on the step's stream; the
+      // monitor (ev4 -> ev5) on its own stream beside the next step; tail =
+      // the step stream after the score rows (ev4 -> ev6)
       for (int k = 1; k < P; ++k) {
         float ms = 0;
-        HC_CUDA_TRY(cudaEventElapsedTime(&ms, ev[k - 1], ev[k]));
+        HC_CUDA_TRY(cudaEventElapsedTime(&ms, ev[k < 6 ? k - 1 : 4], ev[k]));
         phase_ms[k - 1] += ms;
       }
       float tot = 0;

@@ -441,10 +441,15 @@ class HeteroCacheDecoder:
             ev.fetched = [store[o:o + k] for o, k in ev.offsets]
         self._uncollected = []
 
+    def join(self, stream=None) -> None:
+        """Order `stream` after the engine's side-stream work (the last monitor)."""
+        _lib.check(self.lib.hc_engine_join(self.handle, _lib.stream_handle(stream)))
+
     def sync(self, stream=None) -> None:
         import torch
 
         self.finish(stream)
+        self.join(stream)
         torch.cuda.current_stream().synchronize() if stream is None else stream.synchronize()
         self._collect_fetched()
 
@@ -456,7 +461,7 @@ class HeteroCacheDecoder:
                                                     _lib.stream_handle(stream)))
         return out.value
 
-    PHASES = ("append", "attention", "combine", "score_rows", "monitor", "ovl_copy", "step",
+    PHASES = ("append", "attention", "combine", "score_rows", "monitor", "tail", "step",
               "inter_step_gap")
 
     def kernel_timing(self, enable: bool = True) -> dict:
