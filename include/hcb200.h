@@ -238,6 +238,24 @@ int hc_engine_decode_end(hc_engine* eng, int32_t step, void* stream);
  * step's monitor (e.g. before timing or reading engine memory directly). */
 int hc_engine_join(hc_engine* eng, void* stream);
 
+/* Measure mode: attention-mass recall at scale (CacheEngine._measure,
+ * engine.py:276-288, attention_recall evaluation.py:41-59).  Enable before
+ * prefill; the engine then keeps a full-context copy of every head's K and,
+ * per hc_engine_measure call (right after decode step `step`; step 0 = after
+ * prefill), forms every head's dense GQA-mean row (K5 for non-pivots; pivots
+ * keep their own decision rows), its top records (recall_topk per head,
+ * at step 0 and for pivots max(recall_topk, l_base_int, every l_h) -- enough
+ * for every selection the reference makes from them; HCTRACE1 order: score
+ * descending, index ascending, PAD tail) and each head's recall of the recorded mass against its CacheView
+ * resident set, in float64 in record order.  recall_out_host (optional):
+ * one double per unit u = (b*NL + layer)*H + head. */
+int hc_engine_enable_measure(hc_engine* eng, int32_t recall_topk);
+int hc_engine_measure(hc_engine* eng, int32_t step, const void* q_dev, double* recall_out_host,
+                      void* stream);
+/* The records of unit u from the last hc_engine_measure (capacity >= records). */
+int hc_engine_measure_records(hc_engine* eng, int32_t unit, uint32_t* idx_host,
+                              float* scores_host, int32_t capacity, void* stream);
+
 /* Copy the overlap counts of steps [first, last] (<= 64 steps back) into
  * out [(last-first+1) x n_pivots] (pivot order = ascending unit), then sync. */
 int hc_engine_overlaps(hc_engine* eng, int32_t first, int32_t last, int32_t* out_host,

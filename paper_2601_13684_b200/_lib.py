@@ -69,6 +69,9 @@ def _declare(lib):
         "hc_engine_decode_begin": (i32, [vp, i32, vp, vp, vp, vp, i32, vp]),
         "hc_engine_decode_end": (i32, [vp, i32, vp]),
         "hc_engine_join": (i32, [vp, vp]),
+        "hc_engine_enable_measure": (i32, [vp, i32]),
+        "hc_engine_measure": (i32, [vp, i32, vp, vp, vp]),
+        "hc_engine_measure_records": (i32, [vp, i32, vp, vp, i32, vp]),
         "hc_engine_overlaps": (i32, [vp, i32, i32, vp, vp]),
         "hc_engine_fire": (i32, [vp, i32, i32, i32, vp, vp]),
         "hc_engine_land": (i32, [vp, i32, vp]),

@@ -37,11 +37,13 @@ int launch_attn_tiles(const CUtensorMap& tmK, const CUtensorMap& tmV, const Attn
 int launch_topk(const hc_topk_job* jobs_dev, int n_jobs, uint32_t n_add, cudaStream_t st);
 size_t obs_scratch_bytes(int n_units, int L);
 int launch_obs_scores(const void* k, const void* q_obs, int B, int H, int G, int w, int L,
-                      float* out, int64_t row_stride, void* scratch, cudaStream_t st);
+                      float* out, int64_t row_stride, void* scratch, cudaStream_t st, int64_t kstride = 0);
 int launch_monitor(const float* rows, int64_t row_stride, const int32_t* slots, int n_rows,
                    uint32_t n, uint32_t k, const uint32_t* kbase, int words, uint64_t* thr,
                    uint32_t* ovl, cudaStream_t st, uint32_t* hist_out = nullptr);
 int launch_fire_select(const FireJob* jobs_dev, int n_jobs, cudaStream_t st);
+int segmented_sort_desc_u64(void* temp, size_t* temp_bytes, const uint64_t* in, uint64_t* out,
+                            int n_items, int n_segments, const int* offsets, cudaStream_t st);
 int launch_restamp_threshold(const float* rows, int64_t row_stride, const int32_t* slots,
                              int n_rows, uint32_t n, const uint64_t* thr, uint32_t* kbase,
                              int words, cudaStream_t st);
@@ -55,15 +57,26 @@ constexpr int kRing = 64;  // overlap-count ring (steps), read back at window bo
 // Append the decode token of step t (position L+t-1) to every unit.
 __global__ void append_kernel(const UnitDesc* __restrict__ units, int n_units, int L, int t,
                               const uint4* __restrict__ k_new, const uint4* __restrict__ v_new,
-                              uint4* __restrict__ K, uint4* __restrict__ V) {
+                              uint4* __restrict__ K, uint4* __restrict__ V,
+                              uint4* __restrict__ shadow, int NL, int H, int64_t srows) {
   const int u = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (u >= n_units) return;
   const UnitDesc d = units[u];
   const int64_t row = d.kind == kUnitFull ? d.row0 + L + t - 1 : d.app_row + t - 1;
   // 256 B per row = 16 x uint4; lanes 0-15 move K, 16-31 move V
-  if (lane < 16) K[row * 16 + lane] = k_new[size_t(u) * 16 + lane];
-  else V[row * 16 + lane - 16] = v_new[size_t(u) * 16 + lane - 16];
+  if (lane < 16) {
+    const uint4 x = k_new[size_t(u) * 16 + lane];
+    K[row * 16 + lane] = x;
+    if (shadow) {  // measure mode: full-context K, layout [layer][b*H + h][srows]
+      const int h = u % H, l = (u / H) % NL, b = u / (NL * H);
+      const int64_t B = n_units / (NL * H);
+      const int64_t srow = ((int64_t(l) * B + b) * H + h) * srows + L + t - 1;
+      shadow[srow * 16 + lane] = x;
+    }
+  } else {
+    V[row * 16 + lane - 16] = v_new[size_t(u) * 16 + lane - 16];
+  }
 }
 
 
@@ -198,7 +211,34 @@ struct EngineImpl {
   char* pf = nullptr;
   size_t pf_bytes = 0;
 
+  // measure mode: attention-mass recall at scale (CacheEngine._measure,
+  // engine.py:276-288).  Every head's dense GQA-mean row
+  // per step (K5 over a full-context K copy; pivots keep their own K4 rows),
+  // its top records, and recall against the resident sets, all on the GPU.
+  int rec_k = 0;                       // records per head (0 = off)
+  int rec_kmax = 0;                    // record capacity: max(rec_k, l_base_int, l_h)
+  __nv_bfloat16* shadowK = nullptr;    // [NL][B*H][L+T][128]
+  float* mrows = nullptr;              // [NL*B*H][row_len], measure index mu = (l*B + b)*H + h
+  uint32_t* rec_idx = nullptr;         // [NL*B*H][rec_kmax] records (ascending position, PAD tail)
+  float* rec_sc = nullptr;             // [NL*B*H][rec_kmax]
+  uint32_t* rec_cnt = nullptr;         // [NL*B*H]
+  uint32_t* dynbm = nullptr;           // [n_units][words] dynamic-set bitmaps
+  double* rec_out = nullptr;           // [NL*B*H] per-head recall
+  hc_topk_job* d_mjobs = nullptr;      // static K1 jobs over mrows (n grows with n_add);
+                                       // [0, nm): steps >= 1, [nm, 2 nm): step 0
+  hc_recall_head* d_rheads = nullptr;  // static recall heads
+  int32_t* d_piv_mu = nullptr;         // pivot slot -> mu
+  uint64_t* rec_keys = nullptr;        // [2][NL*B*H][rec_kmax] composite keys (sort in/out)
+  int* rec_off = nullptr;              // [NL*B*H + 1] segment offsets
+  void* sort_tmp = nullptr;
+  size_t sort_tmp_bytes = 0;
+  char* mscratch = nullptr;            // packed queries + K5 scratch of one layer
+  size_t mscratch_bytes = 0;
+  int measured_t = -1;
+
   int lh(int u) const { return u % (NL * H); }
+  int mu_of(int u) const { const int b = u / (NL * H), l = (u / H) % NL, h = u % H;
+                           return (l * B + b) * H + h; }
   int head(int u) const { return u % H; }
 };
 
@@ -229,7 +269,10 @@ int engine_destroy(EngineImpl& e) {
     if (e.pre_pos[u]) cudaFree(e.pre_pos[u]);
     if (e.pre_meta[u]) cudaFree(e.pre_meta[u]);
   }
-  void* ptrs[] = {e.d_units, e.K, e.V, e.d_tiles, e.d_skip, e.d_sat_tiles, e.d_sat_flags,
+  void* ptrs[] = {e.shadowK, e.mrows, e.rec_idx, e.rec_sc, e.rec_cnt, e.dynbm, e.rec_out,
+                  e.d_mjobs, e.d_rheads, e.d_piv_mu, e.mscratch, e.rec_keys, e.rec_off,
+                  e.sort_tmp,
+                  e.d_units, e.K, e.V, e.d_tiles, e.d_skip, e.d_sat_tiles, e.d_sat_flags,
                   e.partial, e.d_piv_units, e.logits, e.mref,
                   e.stats,
                   e.rowbuf, e.top_idx, e.top_cnt, e.kbase, e.ovl_cur, e.ovl_ring, e.d_piv_jobs,
@@ -598,7 +641,8 @@ int engine_decode_begin(EngineImpl& e, int t, const void* q, const void* kn, con
   append_kernel<<<(e.n_units + 7) / 8, 256, 0, st>>>(
       e.d_units, e.n_units, e.L, t, reinterpret_cast<const uint4*>(kn),
       reinterpret_cast<const uint4*>(vn), reinterpret_cast<uint4*>(e.K),
-      reinterpret_cast<uint4*>(e.V));
+      reinterpret_cast<uint4*>(e.V), reinterpret_cast<uint4*>(e.shadowK), e.NL, e.H,
+      int64_t(e.L) + e.T);
   HC_CHECK_LAUNCH();
   if (ev) HC_CUDA_TRY(cudaEventRecord(ev[1], st));
   AttnParams p = decode_params(e, t, q, o);
@@ -923,6 +967,15 @@ int engine_prefill_layer(EngineImpl& e, int layer, const __nv_bfloat16* k,
     HC_CUDA_TRY(cudaEventElapsedTime(&ms, e.pf_ev0, e.pf_ev1));
     e.pf_score_ms += ms;
     e.pf_layers += 1;
+  }
+  if (e.rec_k) {  // measure mode: full-context K copy and the step-0 rows
+    const int64_t srows = int64_t(e.L) + e.T;
+    HC_CUDA_TRY(cudaMemcpy2DAsync(e.shadowK + size_t(layer) * nu * srows * kHeadDim,
+                                  size_t(srows) * kHeadDim * 2, k, size_t(e.L) * kHeadDim * 2,
+                                  size_t(e.L) * kHeadDim * 2, nu, cudaMemcpyDeviceToDevice, st));
+    HC_CUDA_TRY(cudaMemcpy2DAsync(e.mrows + size_t(layer) * nu * e.row_len, size_t(e.row_len) * 4,
+                                  rows, size_t(Lp) * 4, size_t(e.L) * 4, nu,
+                                  cudaMemcpyDeviceToDevice, st));
   }
   if (e.prefill_dump)  // test hook: step-0 rows [NL][B*H][L]
     HC_CUDA_TRY(cudaMemcpy2DAsync(e.prefill_dump + size_t(layer) * nu * e.L, size_t(e.L) * 4,
@@ -1258,6 +1311,215 @@ const uint32_t* dyn_list(const EngineImpl& e, int u, const uint32_t** cnt) {
   return e.dyn_sel[u];
 }
 
+// ---- measure mode ----------------------------------------------------------
+
+__global__ void copy_pivot_rows_kernel(float* __restrict__ mrows, const float* __restrict__ rows,
+                                       const int32_t* __restrict__ piv_mu, int64_t stride,
+                                       int n) {
+  const int s = blockIdx.y;
+  const float4* src = reinterpret_cast<const float4*>(rows + size_t(s) * stride);
+  float4* dst = reinterpret_cast<float4*>(mrows + size_t(piv_mu[s]) * stride);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < (n + 3) / 4; i += gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
+// records -> composite keys (score_key << 32 | ~index); 0 past the count
+__global__ void record_keys_kernel(const float* __restrict__ mrows, int64_t stride,
+                                   const uint32_t* __restrict__ idx,
+                                   const uint32_t* __restrict__ cnt, int kmax,
+                                   uint64_t* __restrict__ keys) {
+  const int m = blockIdx.y;
+  const uint32_t c = cnt[m];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < kmax; i += gridDim.x * blockDim.x) {
+    const size_t o = size_t(m) * kmax + i;
+    uint64_t k = 0;
+    if (uint32_t(i) < c) {
+      const uint32_t p = idx[o];
+      k = (uint64_t(score_key(mrows[size_t(m) * stride + p])) << 32) | uint64_t(~p);
+    }
+    keys[o] = k;
+  }
+}
+
+// sorted keys -> records in (score desc, index asc) order, PAD tail
+__global__ void record_unpack_kernel(const float* __restrict__ mrows, int64_t stride,
+                                     const uint64_t* __restrict__ keys, int kmax,
+                                     uint32_t* __restrict__ idx, float* __restrict__ sc) {
+  const int m = blockIdx.y;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < kmax; i += gridDim.x * blockDim.x) {
+    const size_t o = size_t(m) * kmax + i;
+    const uint64_t k = keys[o];
+    if (k) {
+      const uint32_t p = ~uint32_t(k);
+      idx[o] = p;
+      sc[o] = mrows[size_t(m) * stride + p];
+    } else {
+      idx[o] = HC_PAD_INDEX;
+      sc[o] = 0.f;
+    }
+  }
+}
+
+struct BitmapJob {
+  const uint32_t* sel;
+  const uint32_t* cnt;
+  uint32_t* bm;
+};
+
+__global__ void bitmaps_kernel(const BitmapJob* __restrict__ jobs, int words) {
+  const BitmapJob j = jobs[blockIdx.x];
+  for (int w = threadIdx.x; w < words; w += blockDim.x) j.bm[w] = 0u;
+  __syncthreads();
+  const uint32_t c = *j.cnt;
+  for (uint32_t i = threadIdx.x; i < c; i += blockDim.x) {
+    const uint32_t p = j.sel[i];
+    if (int(p >> 5) < words) atomicOr(j.bm + (p >> 5), 1u << (p & 31));
+  }
+}
+
+int engine_enable_measure(EngineImpl& e, int recall_topk) {
+  HC_REQUIRE(recall_topk >= 1, HC_EINVAL, "recall_topk must be >= 1");
+  HC_REQUIRE(!e.rec_k && e.pf_layers == 0, HC_ESTATE, "enable measure once, before prefill");
+  const int nm = e.NL * e.B * e.H;
+  const int64_t srows = int64_t(e.L) + e.T;
+  e.rec_k = recall_topk;
+  // enough records for every selection the reference makes from them: step 0
+  // (all heads) feeds prefill_init's top-l_h (engine.py:263-271); pivots'
+  // records feed the monitor (l_base_int) and every fetch of their
+  // satellites (top-l_s of the pivot row, engine.py:326-329)
+  int kmax = e.n_piv ? e.lbase : 0;
+  for (int j = 0; j < e.NL * e.H; ++j)
+    if (e.role[j] == HC_ROLE_ANCHOR || e.role[j] == HC_ROLE_SATELLITE)
+      kmax = std::max(kmax, e.length[j]);
+  e.rec_kmax = std::max(recall_topk, kmax);
+  HC_TRY(dalloc((void**)&e.shadowK, size_t(nm) * srows * kHeadDim * 2, &e.dev_bytes));
+  HC_TRY(dalloc((void**)&e.mrows, size_t(nm) * e.row_len * 4, &e.dev_bytes));
+  HC_TRY(dalloc((void**)&e.rec_idx, size_t(nm) * e.rec_kmax * 4, &e.dev_bytes));
+  HC_TRY(dalloc((void**)&e.rec_sc, size_t(nm) * e.rec_kmax * 4, &e.dev_bytes));
+  HC_TRY(dalloc((void**)&e.rec_cnt, size_t(nm) * 4, &e.dev_bytes));
+  HC_TRY(dalloc((void**)&e.dynbm, size_t(e.n_units) * e.words * 4, &e.dev_bytes));
+  HC_TRY(dalloc((void**)&e.rec_out, size_t(nm) * 8, &e.dev_bytes));
+  std::vector<hc_topk_job> jobs(2 * nm);
+  std::vector<hc_recall_head> heads(nm);
+  for (int u = 0; u < e.n_units; ++u) {
+    const int m = e.mu_of(u);
+    const bool piv = e.piv_slot[u] >= 0;
+    hc_topk_job& j = jobs[m];
+    j = hc_topk_job{};
+    j.scores = e.mrows + size_t(m) * e.row_len;
+    j.n = uint32_t(e.L);  // + step (n_add)
+    j.k = uint32_t(piv ? e.rec_kmax : e.rec_k);
+    j.out_idx = e.rec_idx + size_t(m) * e.rec_kmax;
+    j.out_count = e.rec_cnt + m;
+    jobs[nm + m] = j;
+    jobs[nm + m].k = uint32_t(e.rec_kmax);
+    heads[m].idx = e.rec_idx + size_t(m) * e.rec_kmax;
+    heads[m].scores = e.rec_sc + size_t(m) * e.rec_kmax;
+    heads[m].dynamic = e.units[u].kind == kUnitComp ? e.dynbm + size_t(u) * e.words : nullptr;
+  }
+  HC_TRY(dalloc((void**)&e.rec_keys, 2 * size_t(nm) * e.rec_kmax * 8, &e.dev_bytes));
+  {
+    std::vector<int> off(nm + 1);
+    for (int m = 0; m <= nm; ++m) off[m] = m * e.rec_kmax;
+    HC_REQUIRE(int64_t(nm) * e.rec_kmax < (int64_t(1) << 31), HC_EINVAL, "too many records");
+    HC_TRY(dalloc((void**)&e.rec_off, off.size() * 4, &e.dev_bytes));
+    HC_CUDA_TRY(cudaMemcpy(e.rec_off, off.data(), off.size() * 4, cudaMemcpyHostToDevice));
+    HC_TRY(segmented_sort_desc_u64(nullptr, &e.sort_tmp_bytes, e.rec_keys,
+                                   e.rec_keys + size_t(nm) * e.rec_kmax, nm * e.rec_kmax, nm,
+                                   e.rec_off, 0));
+    HC_TRY(dalloc(&e.sort_tmp, e.sort_tmp_bytes, &e.dev_bytes));
+  }
+  HC_TRY(dalloc((void**)&e.d_mjobs, jobs.size() * sizeof(hc_topk_job), &e.dev_bytes));
+  HC_CUDA_TRY(cudaMemcpy(e.d_mjobs, jobs.data(), jobs.size() * sizeof(hc_topk_job),
+                         cudaMemcpyHostToDevice));
+  HC_TRY(dalloc((void**)&e.d_rheads, heads.size() * sizeof(hc_recall_head), &e.dev_bytes));
+  HC_CUDA_TRY(cudaMemcpy(e.d_rheads, heads.data(), heads.size() * sizeof(hc_recall_head),
+                         cudaMemcpyHostToDevice));
+  std::vector<int32_t> pm(std::max(1, e.n_piv));
+  for (int s2 = 0; s2 < e.n_piv; ++s2) pm[s2] = e.mu_of(e.piv_units[s2]);
+  HC_TRY(dalloc((void**)&e.d_piv_mu, pm.size() * 4, &e.dev_bytes));
+  HC_CUDA_TRY(cudaMemcpy(e.d_piv_mu, pm.data(), pm.size() * 4, cudaMemcpyHostToDevice));
+  const int nu = e.B * e.H;
+  size_t obs = 0;
+  for (int64_t n = e.L; n <= srows; n += std::max<int64_t>(1, (srows - e.L) / 8 + 1))
+    obs = std::max(obs, obs_scratch_bytes(nu, int(n)));
+  obs = std::max(obs, obs_scratch_bytes(nu, int(srows)));
+  e.mscratch_bytes = ((size_t(nu) * e.G * kHeadDim * 2 + 255) & ~size_t(255)) + obs;
+  HC_TRY(dalloc((void**)&e.mscratch, e.mscratch_bytes, &e.dev_bytes));
+  return HC_OK;
+}
+
+// Recall of every head at step t (after decode step t; t = 0: after prefill).
+// q: the step's queries [B][NL][H*G][128] (unused at t = 0: the step-0 rows
+// are the prefill rows).  recall_out (host, optional): per unit u.
+int engine_measure(EngineImpl& e, int t, const void* q, double* recall_out, cudaStream_t st) {
+  HC_REQUIRE(e.rec_k, HC_ESTATE, "measure mode is off (hc_engine_enable_measure)");
+  HC_REQUIRE(e.in_step == 0, HC_ESTATE, "measure inside an open step");
+  HC_REQUIRE(t == 0 ? e.pf_layers >= e.NL : (t == e.last_t && q), HC_EINVAL,
+             "measure(%d): run it right after that step", t);
+  const int nu = e.B * e.H, nm = e.NL * nu;
+  const int64_t srows = int64_t(e.L) + e.T;
+  const int len = e.L + t;
+  if (t > 0) {
+    __nv_bfloat16* qp = reinterpret_cast<__nv_bfloat16*>(e.mscratch);
+    char* obs = e.mscratch + ((size_t(nu) * e.G * kHeadDim * 2 + 255) & ~size_t(255));
+    HC_REQUIRE(obs_scratch_bytes(nu, len) + (obs - e.mscratch) <= e.mscratch_bytes, HC_EINVAL,
+               "measure scratch too small");
+    const size_t qrow = size_t(e.H) * e.G * kHeadDim * 2;  // one (b, layer) block of queries
+    for (int l = 0; l < e.NL; ++l) {
+      HC_CUDA_TRY(cudaMemcpy2DAsync(qp, qrow, static_cast<const char*>(q) + size_t(l) * qrow,
+                                    qrow * e.NL, qrow, e.B, cudaMemcpyDeviceToDevice, st));
+      HC_TRY(launch_obs_scores(e.shadowK + size_t(l) * nu * srows * kHeadDim, qp, e.B, e.H, e.G,
+                               1, len, e.mrows + size_t(l) * nu * e.row_len, e.row_len, obs, st,
+                               srows));
+    }
+    if (e.n_piv) {  // the pivots' rows are the engine's own (the decision rows)
+      if (e.step_end) HC_CUDA_TRY(cudaStreamWaitEvent(st, e.step_end, 0));
+      copy_pivot_rows_kernel<<<dim3(64, e.n_piv), 256, 0, st>>>(e.mrows, e.rowbuf, e.d_piv_mu,
+                                                                e.row_len, len);
+      HC_CHECK_LAUNCH();
+    }
+  }
+  HC_TRY(launch_topk(e.d_mjobs + (t == 0 ? nm : 0), nm, uint32_t(t), st));
+  {  // records in HCTRACE1 order: score descending, index ascending
+    const dim3 g(std::max(1, std::min(64, (e.rec_kmax + 255) / 256)), nm);
+    uint64_t* kin = e.rec_keys;
+    uint64_t* kout = e.rec_keys + size_t(nm) * e.rec_kmax;
+    record_keys_kernel<<<g, 256, 0, st>>>(e.mrows, e.row_len, e.rec_idx, e.rec_cnt, e.rec_kmax,
+                                          kin);
+    HC_CHECK_LAUNCH();
+    HC_TRY(segmented_sort_desc_u64(e.sort_tmp, &e.sort_tmp_bytes, kin, kout, nm * e.rec_kmax, nm,
+                                   e.rec_off, st));
+    record_unpack_kernel<<<g, 256, 0, st>>>(e.mrows, e.row_len, kout, e.rec_kmax, e.rec_idx,
+                                            e.rec_sc);
+    HC_CHECK_LAUNCH();
+  }
+  std::vector<BitmapJob> bj;
+  for (int u = 0; u < e.n_units; ++u) {
+    if (e.units[u].kind != kUnitComp) continue;
+    const uint32_t* cnt = nullptr;
+    const uint32_t* sel = dyn_list(e, u, &cnt);
+    bj.push_back(BitmapJob{sel, cnt, e.dynbm + size_t(u) * e.words});
+  }
+  if (!bj.empty()) {
+    BitmapJob* d = nullptr;
+    HC_TRY(upload(e, bj.data(), bj.size() * sizeof(BitmapJob), st, (void**)&d));
+    bitmaps_kernel<<<int(bj.size()), 256, 0, st>>>(d, e.words);
+    HC_CHECK_LAUNCH();
+    HC_CUDA_TRY(cudaFreeAsync(d, st));
+  }
+  HC_TRY_RC(hc_trace_recall(e.d_rheads, nm, uint32_t(e.rec_kmax), 0, uint32_t(e.L), uint32_t(t),
+                            uint32_t(e.S), uint32_t(e.R), e.rec_out, st));
+  e.measured_t = t;
+  if (recall_out) {
+    std::vector<double> r(nm);
+    HC_CUDA_TRY(cudaMemcpyAsync(r.data(), e.rec_out, size_t(nm) * 8, cudaMemcpyDeviceToHost, st));
+    HC_CUDA_TRY(cudaStreamSynchronize(st));
+    for (int u = 0; u < e.n_units; ++u) recall_out[u] = r[e.mu_of(u)];
+  }
+  return HC_OK;
+}
+
 }  // namespace
 }  // namespace hc
 
@@ -1325,6 +1587,35 @@ extern "C" int hc_engine_decode_begin(hc_engine* eng, int32_t step, const void* 
 extern "C" int hc_engine_decode_end(hc_engine* eng, int32_t step, void* stream) {
   HC_REQUIRE(eng, HC_EINVAL, "null argument");
   return hc::engine_decode_end(eng->e, step, (cudaStream_t)stream);
+}
+
+extern "C" int hc_engine_enable_measure(hc_engine* eng, int32_t recall_topk) {
+  HC_REQUIRE(eng, HC_EINVAL, "null argument");
+  return hc::engine_enable_measure(eng->e, recall_topk);
+}
+
+extern "C" int hc_engine_measure(hc_engine* eng, int32_t step, const void* q_dev,
+                                 double* recall_out_host, void* stream) {
+  HC_REQUIRE(eng, HC_EINVAL, "null argument");
+  HC_TRY(hc::flush_deferred(eng->e));
+  return hc::engine_measure(eng->e, step, q_dev, recall_out_host, (cudaStream_t)stream);
+}
+
+extern "C" int hc_engine_measure_records(hc_engine* eng, int32_t unit, uint32_t* idx_host,
+                                         float* scores_host, int32_t capacity, void* stream) {
+  HC_REQUIRE(eng && idx_host && scores_host, HC_EINVAL, "null argument");
+  auto& e = eng->e;
+  HC_REQUIRE(e.rec_k && e.measured_t >= 0, HC_ESTATE, "nothing measured yet");
+  HC_REQUIRE(unit >= 0 && unit < e.n_units, HC_EINVAL, "bad unit %d", unit);
+  HC_REQUIRE(capacity >= e.rec_kmax, HC_EINVAL, "capacity %d < %d records", capacity, e.rec_kmax);
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t o = size_t(e.mu_of(unit)) * e.rec_kmax;
+  HC_CUDA_TRY(cudaMemcpyAsync(idx_host, e.rec_idx + o, size_t(e.rec_kmax) * 4,
+                              cudaMemcpyDeviceToHost, st));
+  HC_CUDA_TRY(cudaMemcpyAsync(scores_host, e.rec_sc + o, size_t(e.rec_kmax) * 4,
+                              cudaMemcpyDeviceToHost, st));
+  HC_CUDA_TRY(cudaStreamSynchronize(st));
+  return HC_OK;
 }
 
 extern "C" int hc_engine_join(hc_engine* eng, void* stream) {

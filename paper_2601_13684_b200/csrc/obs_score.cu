@@ -42,6 +42,7 @@ constexpr int kSmemObs = 1024 + kTile /*Q*/ + kStagesObs * kTile + 256 /*barrier
 
 struct ObsParams {
   int L;             // keys per unit
+  int64_t kstride;   // rows between consecutive units' keys (>= L)
   int rows;          // valid query rows (w * G)
   int G;
   int w;
@@ -196,7 +197,7 @@ obs_score_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant_
         const int s = i % kStagesObs;
         mb_wait(empty + 8 * s, ((i / kStagesObs) & 1) ^ 1);
         mb_expect(full + 8 * s, kTile);
-        const int row = unit * p.L + (tile0 + i) * kN;
+        const int row = int(unit * p.kstride) + (tile0 + i) * kN;
         tma2d(sK + s * kTile, &tmK, 0, row, full + 8 * s);
         tma2d(sK + s * kTile + kBox, &tmK, 64, row, full + 8 * s);
       }
@@ -366,7 +367,11 @@ size_t obs_scratch_bytes(int n_units, int L) {
 }
 
 int launch_obs_scores(const void* k, const void* q_obs, int B, int H, int G, int w, int L,
-                      float* out, int64_t row_stride, void* scratch, cudaStream_t st) {
+                      float* out, int64_t row_stride, void* scratch, cudaStream_t st,
+                      int64_t kstride) {
+  if (kstride <= 0) kstride = L;
+  HC_REQUIRE(kstride >= L && int64_t(B) * H * kstride < (int64_t(1) << 31), HC_EINVAL,
+             "key stride %lld out of range", (long long)kstride);
   HC_REQUIRE(w >= 1 && w * G <= kM, HC_EINVAL, "observation window %d x group %d > 128 rows", w,
              G);
   static bool configured = false;
@@ -387,10 +392,11 @@ int launch_obs_scores(const void* k, const void* q_obs, int B, int H, int G, int
       static_cast<const __nv_bfloat16*>(q_obs), H, G, w, qp);
   HC_CHECK_LAUNCH();
   CUtensorMap tk, tq;
-  HC_TRY_RC(make_kv_tensor_map_rows(&tk, k, int64_t(n_units) * L, 128));
+  HC_TRY_RC(make_kv_tensor_map_rows(&tk, k, int64_t(n_units) * kstride, 128));
   HC_TRY_RC(make_kv_tensor_map_rows(&tq, qp, int64_t(n_units) * kM, 128));
   ObsParams p{};
   p.L = L;
+  p.kstride = kstride;
   p.rows = w * G;
   p.G = G;
   p.w = w;
@@ -425,7 +431,7 @@ extern "C" int hc_obs_scores(const void* k_dev, const void* q_obs_dev, int32_t b
   void* scratch = nullptr;
   HC_CUDA_TRY(cudaMallocAsync(&scratch, bytes, st));
   const int rc = hc::launch_obs_scores(k_dev, q_obs_dev, batch, kv_heads, group, window, L,
-                                       rows_dev, row_stride, scratch, st);
+                                       rows_dev, row_stride, scratch, st, 0);
   HC_CUDA_TRY(cudaFreeAsync(scratch, st));
   return rc;
 }

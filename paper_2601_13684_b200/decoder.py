@@ -17,8 +17,15 @@ and the StepRow / RetrievalRecord records (reporting.py).  Host <-> device
 synchronisation happens only at window boundaries (or every step with
 eval_every_step), where the overlap counts are read back.
 
-StepRow.recall is NaN here: attention-mass recall is a trace-replay
-diagnostic that needs every head's full attention (evaluation.py:41-59).
+StepRow.recall is NaN unless measure mode is on (recall_topk > 0):
+attention-mass recall (evaluation.py:41-59) needs every head's full attention,
+which the compressed path by design never computes.  In measure mode the
+engine keeps a full-context K copy, forms every head's dense row per step,
+records its top recall_topk positions (pivots: their own decision rows, at
+least l_base_int records) and computes each head's recall of the recorded
+mass against its resident set on the GPU -- the records are exactly an
+HCTRACE1 trace of the run (tools/export_trace.py), so the reference engine
+replaying it reproduces the StepRows bit for bit.
 """
 
 from __future__ import annotations
@@ -97,7 +104,8 @@ class HeteroCacheDecoder:
     def __init__(self, taxonomy, plan, config: EngineConfig = EngineConfig(), *, batch: int,
                  group: int, max_decode: int, head_dim: int = 128, chunk: int = 1024,
                  host_pool: bool = True, bytes_per_kv_entry: int | None = None,
-                 track_sets: bool = True, obs_window: int = 1, overlap_decisions: bool = True):
+                 track_sets: bool = True, obs_window: int = 1, overlap_decisions: bool = True,
+                 recall_topk: int = 0):
         _lib.require_cuda()
         self.lib = _lib.load()
         self.taxonomy, self.plan, self.config = taxonomy, plan, config
@@ -136,6 +144,12 @@ class HeteroCacheDecoder:
         _lib.check(self.lib.hc_engine_create(C.byref(desc), roles.ctypes.data, lengths.ctypes.data,
                                              cpiv.ctypes.data, C.byref(h)))
         self.handle = h
+        # measure mode (recall at scale): every head's top-recall_topk records per step
+        self.recall_topk = recall_topk
+        self.record_k = max([recall_topk, self.l_base_int if self.monitor else 0] +
+                            [self.effective_length(hd) for hd in self.comp])
+        if recall_topk:
+            _lib.check(self.lib.hc_engine_enable_measure(self.handle, recall_topk))
         info = (C.c_int64 * 4)()
         _lib.check(self.lib.hc_engine_info(self.handle, info))
         self.device_bytes, self.host_bytes, self.arena_rows, self.n_pivot_units = list(info)
@@ -230,7 +244,9 @@ class HeteroCacheDecoder:
             if self.monitor:
                 for p in self.pivots:
                     st.buffers[p] = []
-            st.rows.append(self._row(st, 0, 0))
+        rec = self._measure(0, None)
+        for b, st in enumerate(self.states):
+            st.rows.append(self._row(st, 0, 0, self._row_sizes(st, 0, rec[b])))
         if self.monitor:  # pinned landing zone for fetched sets: every satellite firing at once
             import torch
 
@@ -252,18 +268,41 @@ class HeteroCacheDecoder:
         inter = int(np.isin(np.fromiter(extras, dtype=np.int64, count=len(extras)), dyn).sum())
         return len(dyn) + len(extras) - inter + t
 
-    def _row_sizes(self, st: SequenceState, t: int):
+    def _row_sizes(self, st: SequenceState, t: int, recall: float = math.nan):
         charged = len(self.full) * self.L + sum(st.dyn_count.values())
         if self.track_sets:
             total = len(self.full) * (self.L + t) + sum(self._size_of(st, hd, t) for hd in self.comp)
             extra = total - charged
         else:
             extra = -1
-        return charged, extra
+        return charged, extra, recall
+
+    def _measure(self, t: int, q, sh=None) -> list:
+        """Per-sequence recall at step t (CacheEngine._measure, engine.py:276-288):
+        the mean over heads in (layer, head) order of each head's recall of its
+        recorded mass; NaN when measure mode is off."""
+        if not self.recall_topk:
+            return [math.nan] * self.B
+        out = np.empty(self.B * self.NL * self.H, dtype=np.float64)
+        _lib.check(self.lib.hc_engine_measure(self.handle, t, _lib.ptr(q) if q is not None else None,
+                                              out.ctypes.data,
+                                              sh if sh is not None else _lib.stream_handle()))
+        per = out.reshape(self.B, self.NL * self.H)
+        return [sum(per[b].tolist()) / (self.NL * self.H) for b in range(self.B)]
+
+    def measure_records(self, b: int, head_id):
+        """(indices, scores) recorded for one head at the last measured step."""
+        cap = self.record_k
+        idx = np.empty(cap, dtype=np.uint32)
+        sc = np.empty(cap, dtype=np.float32)
+        _lib.check(self.lib.hc_engine_measure_records(self.handle, self.unit(b, head_id),
+                                                      idx.ctypes.data, sc.ctypes.data, cap,
+                                                      _lib.stream_handle()))
+        return idx, sc
 
     def _row(self, st: SequenceState, t: int, flag: int, sizes=None) -> StepRow:
-        charged, extra = sizes if sizes is not None else self._row_sizes(st, t)
-        return StepRow(step=t, recall=math.nan, gpu_entries=charged, extra_entries=extra,
+        charged, extra, recall = sizes if sizes is not None else self._row_sizes(st, t)
+        return StepRow(step=t, recall=recall, gpu_entries=charged, extra_entries=extra,
                        bytes_in_flight=st.bytes_in_flight(t), cumulative_bytes=st.cumulative_bytes,
                        retrieval_flag=flag)
 
@@ -313,16 +352,17 @@ class HeteroCacheDecoder:
         else:
             _lib.check(self.lib.hc_engine_decode_step(self.handle, t, _lib.ptr(q), _lib.ptr(k_new),
                                                       _lib.ptr(v_new), _lib.ptr(out), sh))
+        rec = self._measure(t, q, sh) if self.recall_topk else [math.nan] * self.B
         boundary = self.monitor and (cfg.eval_every_step or t % cfg.window == 0)
         if boundary:
             first = t if cfg.eval_every_step else max(1, t - cfg.window + 1)
-            self._open = (t, first, [self._row_sizes(st, t) for st in self.states]
-                          if rows else None)
+            self._open = (t, first, [self._row_sizes(st, t, rec[b])
+                                     for b, st in enumerate(self.states)] if rows else None)
             if not self.overlap_decisions:
                 self._close_decision(sh)
         elif rows:
-            for st in self.states:
-                st.rows.append(self._row(st, t, 0))
+            for b, st in enumerate(self.states):
+                st.rows.append(self._row(st, t, 0, self._row_sizes(st, t, rec[b])))
 
     def _close_decision(self, sh) -> None:
         t, first, sizes = self._open

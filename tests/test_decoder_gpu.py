@@ -31,7 +31,7 @@ ROW_RTOL = 2e-3
 
 def _build(variant="heterocache", delay=1, bandwidth=1 << 30, B=2, NL=2, L=700, T=40,
            chunk=256, host_pool=True, window=8, eval_every_step=False, shift=13, seed=3,
-           obs_window=1, sinks=4, recency=8, overlap_decisions=True):
+           obs_window=1, sinks=4, recency=8, overlap_decisions=True, recall_topk=0):
     import torch
 
     from paper_2601_13684_b200.decoder import HeteroCacheDecoder
@@ -47,7 +47,7 @@ def _build(variant="heterocache", delay=1, bandwidth=1 << 30, B=2, NL=2, L=700, 
                        recency_window=recency)
     dec = HeteroCacheDecoder(tax, plan, cfg, batch=B, group=model.group, max_decode=T,
                              chunk=chunk, host_pool=host_pool, obs_window=obs_window,
-                             overlap_decisions=overlap_decisions)
+                             overlap_decisions=overlap_decisions, recall_topk=recall_topk)
     gen = SyntheticKV(model, batch=B, prefill_len=L, num_layers=NL, hot=plan.l_base_int,
                       seed=seed)
     dump = torch.zeros(NL, B * model.kv_heads, L, device="cuda")
@@ -260,3 +260,57 @@ def test_queued_transfers_per_satellite_land_in_fifo_order():
                 if b.pivot == a.pivot and a.trigger_step < b.trigger_step < a.completion_step:
                     queued += 1
     assert queued >= 1, "scenario must put two transfers of one pivot in flight at once"
+
+
+@pytest.mark.parametrize("kw", [dict(), dict(bandwidth=3000, window=4, shift=(6, 11, 19, 27), T=36),
+                                dict(overlap_decisions=False, delay=2)])
+def test_measure_mode_recall_matches_oracle_replay(kw):
+    """Measure mode: every head's records per step (GPU dense rows, pivots' own
+    decision rows) replayed by the oracle engine with measurement on give the
+    same events and the same StepRows -- recall included, bit for bit."""
+    import math
+
+    import torch
+
+    ctx = _build(recall_topk=96, **kw)
+    dec, gen = ctx["dec"], ctx["gen"]
+    B, NL, L, T, H = ctx["B"], ctx["NL"], ctx["L"], ctx["T"], ctx["model"].kv_heads
+    K = dec.record_k
+    idx = np.full((B, T + 1, NL, H, K), O.PAD_INDEX, dtype=np.uint32)
+    sc = np.zeros((B, T + 1, NL, H, K), dtype=np.float32)
+
+    def grab(t):
+        for b in range(B):
+            for l in range(NL):
+                for h in range(H):
+                    idx[b, t, l, h], sc[b, t, l, h] = dec.measure_records(b, (l, h))
+
+    grab(0)  # finish_prefill measured step 0
+    for t in range(1, T + 1):
+        q, kn, vn = gen.step_inputs(t, ctx["shift"])
+        o = torch.empty_like(q)
+        dec.decode_step(t, q, kn, vn, o)
+        grab(t)
+    dec.sync()
+    cfg = ctx["cfg"]
+    roles = {hd: pr.role for hd, pr in ctx["tax"].heads.items()}
+    clusters = [(c.pivot, tuple(c.satellites)) for c in ctx["tax"].clusters]
+    for b in range(B):
+        ref = O.replay(idx[b], sc[b], prefill_len=L, bytes_per_kv_entry=512, roles=roles,
+                       clusters=clusters, lengths=dict(ctx["plan"].lengths),
+                       l_base_int=ctx["plan"].l_base_int, tau_drift=cfg.tau_drift,
+                       window=cfg.window, transfer_bandwidth=cfg.transfer_bandwidth,
+                       update_delay_steps=cfg.update_delay_steps, sink_count=cfg.sink_count,
+                       recency_window=cfg.recency_window, variant=cfg.variant,
+                       eval_every_step=cfg.eval_every_step, measure=True)
+        st = dec.states[b]
+        got = [dict(trigger_step=e.trigger_step, pivot=e.pivot, completion_step=e.completion_step,
+                    transfer_bytes=e.transfer_bytes, fetches=e.fetches) for e in st.events]
+        assert got == ref["events"]
+        assert len(st.rows) == len(ref["rows"]) == T + 1
+        for g, e in zip(st.rows, ref["rows"]):
+            assert not math.isnan(g.recall)
+            assert (g.step, g.recall, g.gpu_entries, g.extra_entries, g.bytes_in_flight,
+                    g.cumulative_bytes, g.retrieval_flag) == (
+                e["step"], e["recall"], e["gpu_entries"], e["extra_entries"],
+                e["bytes_in_flight"], e["cumulative_bytes"], e["retrieval_flag"]), (b, g.step)

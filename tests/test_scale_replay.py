@@ -1,13 +1,15 @@
 """Parity closed at 128K context -- CPU only.
 
 tests/golden/scale_128k/ holds an HCTRACE1-shaped export of a tensor-mode GPU
-run (tools/export_trace.py on a B200: Qwen2.5-7B-shaped, 131,072-token
-prefill, 2 layers, planted topic shift): the top-K records of the GPU's own
-fp32 step-0 rows (every head) and per-step pivot rows, plus the GPU engine's
-event log, StepRow integers and final dynamic sets.  Replaying the trace
-through the REFERENCE engine (heterocache.engine.CacheEngine, imported from
-/root/reference when it is mounted) and through the pinned oracle must
-reproduce the GPU's decisions exactly.
+run in measure mode (tools/export_trace.py on a B200: Qwen2.5-7B-shaped,
+131,072-token prefill, 2 layers, planted topic shift): every head's records
+at every step (pivots: top-l_base_int of their own decision rows; the others:
+top-1024 of their dense GPU rows), plus the GPU engine's event log, full
+StepRows (recall computed on the GPU) and final dynamic
+sets.  Replaying the trace through the REFERENCE engine
+(heterocache.engine.CacheEngine, imported from /root/reference when it is
+mounted) and through the pinned oracle must reproduce the GPU's decisions
+and StepRows -- recall included -- exactly.
 """
 
 import json
@@ -45,11 +47,12 @@ def test_oracle_replay_of_gpu_trace_at_128k():
                    roles={key(h): r for h, r in run["roles"].items()},
                    clusters=[(tuple(p), tuple(tuple(s) for s in sats)) for p, sats in run["clusters"]],
                    lengths={key(h): n for h, n in run["plan"]["lengths"].items()},
-                   l_base_int=run["plan"]["l_base_int"], measure=False, **cfg)
+                   l_base_int=run["plan"]["l_base_int"], measure=True, **cfg)
     assert run["gpu_events"], "the planted shift must fire"
     assert out["events"] == _gpu_events(run)
+    assert len(run["gpu_rows"]) == len(out["rows"])
     for g, e in zip(run["gpu_rows"], out["rows"]):
-        assert g == {k: v for k, v in e.items() if k != "recall"}
+        assert g == e
     assert {f"{h[0]},{h[1]}": sorted(v) for h, v in out["dynamic"].items()} == run["gpu_dynamic"]
 
 
@@ -94,6 +97,8 @@ def test_reference_engine_replays_gpu_trace_at_128k():
     got = [dict(trigger_step=e.trigger_step, pivot=e.pivot, completion_step=e.completion_step,
                 transfer_bytes=e.transfer_bytes, fetches=e.fetches) for e in ref.report.events]
     assert got == _gpu_events(run)
+    assert len(run["gpu_rows"]) == len(ref.report.rows)
+    assert any(r["recall"] < 1.0 for r in run["gpu_rows"]), "compressed heads must miss some mass"
     for g, r in zip(run["gpu_rows"], ref.report.rows):
-        assert g == {k: v for k, v in r.to_json_dict().items() if k != "recall"}
+        assert g == r.to_json_dict()
     assert {f"{h[0]},{h[1]}": sorted(v) for h, v in ref.state.dynamic.items()} == run["gpu_dynamic"]

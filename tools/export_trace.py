@@ -2,13 +2,15 @@
 
 Runs on the GPU box: a 128K-context Qwen2.5-7B-shaped decode (2 layers,
 batch 1, observation window 1 = the reference's step-0 semantics) with a
-planted topic shift, then writes
+planted topic shift, in measure mode, then writes
 
-  <out>/scale_trace.npz   trace arrays: per-step top-K (index, score) records
-                          of the GPU's own fp32 rows -- every head at step 0,
-                          pivots at every decode step (other heads PAD)
+  <out>/scale_trace.npz   trace arrays: per-step records of every head -- the
+                          engine's measure-mode records (step 0 and pivots:
+                          top-max(l_base_int, l_h) -- pivots from their own
+                          decision rows; other heads: top-1024 of their dense
+                          GPU rows) in HCTRACE1 order, PAD tail
   <out>/scale_run.json    manifest, roles/clusters/plan/config and the GPU
-                          engine's event log and StepRow integers
+                          engine's event log and StepRows (recall included)
 
 tests/test_scale_replay.py replays the trace through the reference engine
 (heterocache.engine.CacheEngine, when /root/reference is present) and the
@@ -32,13 +34,6 @@ from paper_2601_13684_b200.trace import PAD_INDEX  # noqa: E402
 from paper_2601_13684_b200.workload import CONFIGS, SyntheticKV, plan_for  # noqa: E402
 
 
-def topk_records(row: np.ndarray, K: int):
-    """Top-K (index, score) of a dense row in (score desc, index asc) order."""
-    n = row.size
-    order = np.lexsort((np.arange(n), -row.astype(np.float64)))[:K]
-    return order.astype(np.uint32), row[order].astype(np.float32)
-
-
 def main(out_dir: str, T: int = 16, shift: int = 7):
     out = Path(out_dir)
     out.mkdir(parents=True, exist_ok=True)
@@ -48,30 +43,29 @@ def main(out_dir: str, T: int = 16, shift: int = 7):
     cfg = EngineConfig(tau_drift=0.5, window=4, update_delay_steps=1,
                        transfer_bandwidth=64 << 20)
     L, NL, H, G = w.prefill_len, w.num_layers, m.kv_heads, m.group
-    dec = HeteroCacheDecoder(tax, plan, cfg, batch=1, group=G, max_decode=T, obs_window=1)
+    dec = HeteroCacheDecoder(tax, plan, cfg, batch=1, group=G, max_decode=T, obs_window=1,
+                             recall_topk=1024)
     gen = SyntheticKV(m, batch=1, prefill_len=L, num_layers=NL, hot=plan.l_base_int, seed=77)
-    dump = torch.zeros(NL, H, L, device="cuda")
-    dec.lib.hc_engine_set_prefill_dump(dec.handle, dump.data_ptr())
     for l in range(NL):
         k, v, q = gen.layer_kv(l)
         dec.prefill_layer(l, k, v, q)
     torch.cuda.synchronize()
     dec.finish_prefill()
-    K = max(list(plan.lengths.values()) + [plan.l_base_int])
+    K = dec.record_k
     idx = np.full((T + 1, NL, H, K), PAD_INDEX, dtype=np.uint32)
     sc = np.zeros((T + 1, NL, H, K), dtype=np.float32)
-    d0 = dump.cpu().numpy()
-    for l in range(NL):
-        for h in range(H):
-            idx[0, l, h], sc[0, l, h] = topk_records(d0[l, h], K)
+
+    def grab(t):
+        for l in range(NL):
+            for h in range(H):
+                idx[t, l, h], sc[t, l, h] = dec.measure_records(0, (l, h))
+
+    grab(0)
     for t in range(1, T + 1):
         q, kn, vn = gen.step_inputs(t, shift)
         o = torch.empty_like(q)
         dec.decode_step(t, q, kn, vn, o)
-        for p in dec.pivots:
-            row = torch.empty(L + t, device="cuda")
-            dec.pivot_row(0, p, t, row)
-            idx[t, p[0], p[1]], sc[t, p[0], p[1]] = topk_records(row.cpu().numpy(), K)
+        grab(t)
     dec.sync()
     st = dec.states[0]
     np.savez_compressed(out / "scale_trace.npz", indices=idx, scores=sc)
@@ -92,8 +86,7 @@ def main(out_dir: str, T: int = 16, shift: int = 7):
                    "recency_window": cfg.recency_window, "variant": cfg.variant,
                    "eval_every_step": cfg.eval_every_step},
         "gpu_events": [e.to_json_dict() for e in st.events],
-        "gpu_rows": [{k: v for k, v in r.to_json_dict().items() if k != "recall"}
-                     for r in st.rows],
+        "gpu_rows": [r.to_json_dict() for r in st.rows],
         "gpu_dynamic": {f"{l},{h}": dec.dynamic_set(0, (l, h)).tolist() for (l, h) in dec.comp},
     }
     (out / "scale_run.json").write_text(json.dumps(run))
