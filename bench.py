@@ -53,8 +53,11 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--chunk", type=int, default=1024)
-    ap.add_argument("--policy", choices=("heterocache", "full"), default="heterocache",
-                    help="full: FullAttention baseline through the same engine (all heads full)")
+    ap.add_argument("--policy", choices=("heterocache", "full", "static_topk", "sink_window"),
+                    default="heterocache",
+                    help="baseline residency policies through the same engine (evaluation.py): "
+                         "full = FullAttention (every head keeps its whole cache); static_topk / "
+                         "sink_window at the heterocache plan's budget rho")
     ap.add_argument("--obs-window", type=int, default=0,
                     help="prefill observation window (0: min(32, 128 // G))")
     ap.add_argument("--link-mib-per-step", type=float, default=64.0,
@@ -134,7 +137,9 @@ def run_b200(args, rank, world):
         from dataclasses import replace
         w = replace(w, layers=args.layers)
     m = w.model
-    tax, plan = plan_for(w, args.policy)
+    htax, hplan = plan_for(w)  # the synthetic data is the same for every policy
+    tax, plan = plan_for(w, args.policy) if args.policy in ("heterocache", "full") \
+        else (None, None)
     K, W = args.steps, args.warmup
     # every (sequence, layer) cluster drifts once inside each timed
     # loop, staggered across the loop (cfg4: every 12 steps, staggered phases)
@@ -151,10 +156,19 @@ def run_b200(args, rank, world):
     T = W + 2 * K + 8
     lib = _lib.load()
     obs = args.obs_window or max(1, min(32, 128 // m.group))  # w_obs = 32 (Llama)
-    dec = HeteroCacheDecoder(tax, plan, cfg, batch=w.batch, group=m.group, max_decode=T,
-                             chunk=args.chunk, host_pool=True, track_sets=False, obs_window=obs)
+    dkw = dict(batch=w.batch, group=m.group, max_decode=T, chunk=args.chunk, host_pool=True,
+               track_sets=False, obs_window=obs)
+    if plan is None:  # static baseline policy at the heterocache budget (evaluation.py:198-228)
+        from paper_2601_13684_b200.evaluation import PolicySpec, policy_decoder
+
+        dec = policy_decoder(PolicySpec(args.policy, rho=hplan.rho), num_layers=w.num_layers,
+                             heads_per_layer=m.kv_heads, prefill_len=w.prefill_len,
+                             engine_config=cfg, **dkw)
+        tax, plan = dec.taxonomy, dec.plan
+    else:
+        dec = HeteroCacheDecoder(tax, plan, cfg, **dkw)
     gen = SyntheticKV(m, batch=w.batch, prefill_len=w.prefill_len, num_layers=w.num_layers,
-                      hot=plan.l_base_int, seed=20261018 + 3 + rank)
+                      hot=hplan.l_base_int, seed=20261018 + 3 + rank)
     t0 = time.time()
     for l in range(w.num_layers):
         k, v, q = gen.layer_kv(l, obs)
@@ -306,8 +320,7 @@ def run_b200(args, rank, world):
                         f"{m.q_heads}q/{m.kv_heads}kv, d={m.head_dim})",
             "prefill_len": w.prefill_len, "batch_per_gpu": w.batch, "layers": w.num_layers,
             "compression": w.compression, "rho": plan.rho, "l_base_int": plan.l_base_int,
-            "roles_per_layer": list(m.layer_roles()) if args.policy == "heterocache"
-            else ["volatile"] * m.kv_heads,
+            "roles_per_layer": [tax.heads[(0, h)].role for h in range(m.kv_heads)],
             "policy": args.policy,
             "decode_window": cfg.window, "tau_drift": cfg.tau_drift,
             "topic_shifts": ("every cluster (sequence, layer) once per timed loop, staggered"
@@ -461,7 +474,7 @@ def main():
             from paper_2601_13684_b200.workload import plan_for
 
             tax, plan = plan_for(w)
-            per_step, cores, sample, _ = cpu_step_timer(w, plan, tax, seconds=args.cpu_seconds)
+            per_step, cores, sample, _ = cpu_step_timer(w, hplan, htax, seconds=args.cpu_seconds)
             res["cpu_baseline"] = {"value": 1.0 / per_step, "unit": "steps/s", "cores": cores,
                                    "kind": "port", "sample": sample}
         else:

@@ -407,3 +407,70 @@ def replay(indices, scores, *, prefill_len, bytes_per_kv_entry, roles, clusters,
                                               sink_count, recency_window)) for hd in heads}
     return {"rows": rows, "events": events, "final_gpu": final, "dynamic": dynamic,
             "k_base": k_base, "dynamic_trace": dyn_trace}
+
+
+# ---- baseline policies (evaluation.py:60-228) --------------------------------
+
+
+class PolicyError(ValueError):
+    """evaluation.py:33-34 EvaluationError."""
+
+
+def policy_window(rho, sink_count, window, prefill_len) -> int:
+    """PolicySpec.effective_window (evaluation.py:85-94)."""
+    if window is not None:
+        return window
+    w = floor(rho * prefill_len) - sink_count
+    if w < 0:
+        raise PolicyError("sink_count exceeds the budget")
+    return w
+
+
+def policy_budget_ceiling(name, rho, sink_count, window, num_heads, prefill_len) -> float:
+    """PolicySpec.budget_ceiling (evaluation.py:96-102)."""
+    if name == "full_oracle":
+        return float(num_heads * prefill_len)
+    if name == "sink_window":
+        per_head = min(sink_count + policy_window(rho, sink_count, window, prefill_len),
+                       prefill_len)
+        return float(num_heads * per_head)
+    return rho * num_heads * prefill_len
+
+
+def static_policy_report(indices, scores, *, prefill_len, name, rho=0.5, sink_count=4,
+                         window=None, engine_sink_count=4, engine_recency_window=8) -> dict:
+    """run_policy for full_oracle / static_topk / sink_window (evaluation.py:165-228)
+    through _static_rows (evaluation.py:110-162): per-head sets frozen for the
+    whole decode.  Returns the SimulationReport fields that depend on the trace
+    (rows, budget_ceiling, update_delay_steps, events)."""
+    T1, NL, H, _ = indices.shape
+    L = prefill_len
+    heads = [(l, h) for l in range(NL) for h in range(H)]
+    if name == "full_oracle":
+        base, S, R = {hd: None for hd in heads}, 0, 0
+    elif name == "static_topk":
+        k = floor(rho * L)
+        if k < 1:
+            raise PolicyError("rho leaves no budget for static_topk")
+        base = {(l, h): frozenset(int(x) for x in top_k_sparse(indices[0, l, h],
+                                                               scores[0, l, h], k))
+                for l, h in heads}
+        S, R = engine_sink_count, engine_recency_window
+    elif name == "sink_window":
+        R = policy_window(rho, sink_count, window, L)
+        base, S = {hd: frozenset() for hd in heads}, sink_count
+    else:
+        raise PolicyError(f"not a static policy: {name}")
+    charged = sum(L if base[hd] is None else len(base[hd]) for hd in heads)
+    rows = []
+    for t in range(T1):
+        recalls, total = [], 0
+        for l, h in heads:
+            b = base[(l, h)]
+            recalls.append(_recall(L, t, b, S, R, indices[t, l, h], scores[t, l, h]))
+            total += cache_view_size(L, t, b, S, R)
+        rows.append(dict(step=t, recall=sum(recalls) / len(recalls), gpu_entries=charged,
+                         extra_entries=total - charged, bytes_in_flight=0, cumulative_bytes=0,
+                         retrieval_flag=0))
+    return {"policy": name, "rows": rows, "events": [], "update_delay_steps": 0,
+            "budget_ceiling": policy_budget_ceiling(name, rho, sink_count, window, len(heads), L)}

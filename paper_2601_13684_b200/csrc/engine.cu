@@ -299,8 +299,7 @@ int engine_create(EngineImpl& e, const hc_engine_desc& c, const int32_t* roles,
   HC_REQUIRE(c.group >= 1 && c.group <= 8, HC_EINVAL, "group must be 1..8");
   HC_REQUIRE(c.batch >= 1 && c.num_layers >= 1 && c.kv_heads >= 1, HC_EINVAL, "bad geometry");
   HC_REQUIRE(c.prefill_len >= 1 && c.max_decode >= 1, HC_EINVAL, "bad lengths");
-  HC_REQUIRE(c.recency_window >= 0 && c.recency_window <= 32, HC_EINVAL,
-             "recency_window must be in [0, 32]");
+  HC_REQUIRE(c.recency_window >= 0, HC_EINVAL, "recency_window must be >= 0");
   HC_REQUIRE(c.sink_count >= 0, HC_EINVAL, "sink_count must be >= 0");
   HC_REQUIRE(c.l_base_int >= 1, HC_EINFEASIBLE, "l_base_int must be >= 1");
   e.cfg = c;
@@ -321,6 +320,11 @@ int engine_create(EngineImpl& e, const hc_engine_desc& c, const int32_t* roles,
     HC_REQUIRE(e.role[i] >= 0 && e.role[i] <= 3, HC_EINVAL, "bad role at %d", i);
     const bool comp = e.role[i] == HC_ROLE_ANCHOR || e.role[i] == HC_ROLE_SATELLITE;
     if (comp) HC_REQUIRE(e.length[i] >= 0 && e.length[i] <= e.L, HC_EINVAL, "bad length at %d", i);
+    // recency tails longer than 32 rows are held as a contiguous block
+    // (kv_layout.cuh tail_lo): only without a dynamic set (sink_window)
+    if (comp && e.R > 32)
+      HC_REQUIRE(e.length[i] == 0, HC_EINVAL,
+                 "recency_window %d > 32 needs compressed heads without a dynamic set", e.R);
     if (e.role[i] == HC_ROLE_SATELLITE) {
       const int p = e.cpivot[i];
       HC_REQUIRE(p >= 0 && p < e.H && e.role[(i / e.H) * e.H + p] == HC_ROLE_PIVOT, HC_EINVAL,
@@ -784,9 +788,10 @@ __global__ void build_positions_batch_kernel(const XferDev* __restrict__ xs, int
       while (u < v) { const int m = (u + v) >> 1; if (int(sel[m]) < p) u = m + 1; else v = m; }
       if (!(u < hi && int(sel[u]) == p)) {
         x.pos[nt++] = uint32_t(p);
-        mask |= 1u << (p - (L - R));
+        if (R <= 32) mask |= 1u << (p - (L - R));
       }
     }
+    if (R > 32) mask = uint32_t(nt);  // contiguous tail block [L - nt, L) (no dynamic set)
     s_lo = lo;
     s_hi = hi;
     s_ntail = nt;

@@ -34,7 +34,8 @@ struct UnitDesc {
   int64_t app_row;     // comp: row of decode position L; full: row0 + L
   int32_t kind;        // UnitKind
   int32_t n_prefix;    // comp: rows in the active prefix buffer; full: L
-  uint32_t tail_mask;  // comp: bit i set <=> position L-R+i is a tail-only row
+  uint32_t tail_mask;  // comp: bit i set <=> position L-R+i is a tail-only row (R <= 32),
+                       // or the tail-only row count (R > 32, see tail_lo)
   int32_t q_row;       // first query row (of G) for this unit
   int32_t pivot_slot;  // >= 0: emit logits / score row into this slot
   int32_t slot0;       // first split-K partial slot
@@ -68,7 +69,15 @@ __host__ __device__ inline int popc32(uint32_t x) {
 }
 
 // lo(t): tail-only prefix rows that left the recency window by step t.
+// recency <= 32: bit i of tail_mask <=> position L-R+i is a tail-only row.
+// recency > 32 (heads without a dynamic set): tail_mask = n, the tail-only
+// rows are the contiguous positions [L-n, L), of which those below L+t-R left.
 __host__ __device__ inline int32_t tail_lo(uint32_t tail_mask, int32_t t, int32_t recency) {
+  if (recency > 32) {
+    const int32_t n = int32_t(tail_mask);
+    const int32_t v = n + t - recency;
+    return v < 0 ? 0 : (v > n ? n : v);
+  }
   const int32_t w = t < recency ? t : recency;
   const uint32_t m = w >= 32 ? 0xffffffffu : ((1u << w) - 1u);
   return popc32(tail_mask & m);

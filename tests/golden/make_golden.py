@@ -14,6 +14,8 @@ outputs, not to our reading of it.  Outputs:
   topk_cases.json                          reference top_k_indices answers
   budget_cases.json                        reference plan_budget / allocate
   taxonomy_cases.json                      reference run_taxonomy results
+  policy_cases.json                        reference run_policy reports of the
+                                           baseline policies (evaluation.py)
   golden_replay.json                       the reference's own golden file
 """
 
@@ -33,6 +35,7 @@ sys.dont_write_bytecode = True
 
 from heterocache.budget import BudgetConfig, allocate, plan_budget  # noqa: E402
 from heterocache.engine import CacheEngine, EngineConfig  # noqa: E402
+from heterocache.evaluation import PolicySpec, run_policy  # noqa: E402
 from heterocache.metrics import top_k_indices  # noqa: E402
 from heterocache.profiling import (  # noqa: E402
     Cluster, HeadProfile, ProfileConfig, TaxonomyResult, run_taxonomy,
@@ -364,8 +367,47 @@ def taxonomy_cases(arrays):
     return out
 
 
+POLICY_TRACES = ("demo", "drift_seed5", "drift_t0_21", "replay_00", "replay_01", "replay_05",
+                 "multilayer_21", "dense_31", "dense_32")
+
+
+def policy_cases(cases, arrays):
+    """run_policy (evaluation.py:165-228) for the baseline policies over engine-case traces."""
+    from heterocache.trace import TraceManifest
+
+    out = []
+    for c in cases:
+        if c["name"] not in POLICY_TRACES:
+            continue
+        m = TraceManifest(**c["manifest"])
+        tr = make_trace(m, arrays[c["name"] + "/indices"], arrays[c["name"] + "/scores"])
+        specs = [
+            (PolicySpec("full_oracle"), None),
+            (PolicySpec("static_topk", rho=0.1), None),
+            (PolicySpec("static_topk", rho=0.35), EngineConfig(sink_count=8, recency_window=16)),
+            (PolicySpec("static_topk", rho=0.6), EngineConfig(sink_count=0, recency_window=0)),
+            (PolicySpec("sink_window", rho=0.3), None),
+            (PolicySpec("sink_window", rho=0.5, sink_count=2, window=10), None),
+            (PolicySpec("sink_window", rho=0.25, sink_count=0), None),
+            (PolicySpec("static_topk", rho=0.01), None),   # k = floor(rho L) < 1 on short L
+            (PolicySpec("sink_window", rho=0.05), None),   # sinks exceed floor(rho L)
+        ]
+        for spec, ecfg in specs:
+            try:
+                rep_ = run_policy(tr, spec, engine_config=ecfg)
+                expected = rep_.to_json_dict()
+            except Exception as exc:  # noqa: BLE001 -- record the reference's refusal
+                expected = {"error": type(exc).__name__}
+            out.append({"trace": c["name"], "policy": spec.name, "rho": spec.rho,
+                        "sink_count": spec.sink_count, "window": spec.window,
+                        "engine": None if ecfg is None else cfg_json(ecfg),
+                        "expected": expected})
+    return out
+
+
 def main():
     cases, arrays = engine_cases()
+    (OUT / "policy_cases.json").write_text(json.dumps(policy_cases(cases, arrays)))
     tax = taxonomy_cases(arrays)
     np.savez_compressed(OUT / "engine_traces.npz", **arrays)
     (OUT / "engine_cases.json").write_text(json.dumps(cases))

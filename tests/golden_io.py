@@ -71,3 +71,16 @@ def json_fixture(name):
 def taxonomy_arrays(name):
     t = _traces()
     return t[name + "/indices"], t[name + "/scores"]
+
+
+@lru_cache(maxsize=None)
+def policy_cases():
+    return json.loads((GOLDEN / "policy_cases.json").read_text())
+
+
+def policy_kwargs(pc, prefill_len):
+    """kwargs of oracle.static_policy_report for one policy case."""
+    eng = pc["engine"] or {"sink_count": 4, "recency_window": 8}  # EngineConfig() defaults
+    return dict(prefill_len=prefill_len, name=pc["policy"], rho=pc["rho"],
+                sink_count=pc["sink_count"], window=pc["window"],
+                engine_sink_count=eng["sink_count"], engine_recency_window=eng["recency_window"])

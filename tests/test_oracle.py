@@ -122,3 +122,27 @@ def test_attention_oracle_semantics():
     assert torch.allclose(o.double(), ref @ v[[0, 3, 7, 9]].double(), atol=1e-5)
     row = gqa_mean_row(p)
     assert torch.allclose(row.double(), ref.mean(0), atol=1e-6)
+
+
+def test_oracle_static_policies_match_reference_run_policy():
+    """Baseline policies: the oracle's run_policy restatement
+    reproduces the reference's reports (evaluation.py:165-228), refusals included."""
+    from golden_io import case_arrays, engine_cases, policy_cases, policy_kwargs
+
+    L = {c["name"]: c["manifest"]["prefill_len"] for c in engine_cases()}
+    n = 0
+    for pc in policy_cases():
+        idx, sc = case_arrays(pc["trace"])
+        kw = policy_kwargs(pc, L[pc["trace"]])
+        exp = pc["expected"]
+        if "error" in exp:
+            with pytest.raises(O.PolicyError):
+                O.static_policy_report(idx, sc, **kw)
+            continue
+        got = O.static_policy_report(idx, sc, **kw)
+        assert got["rows"] == exp["rows"], (pc["trace"], pc["policy"], pc["rho"])
+        assert got["budget_ceiling"] == exp["budget_ceiling"]
+        assert got["update_delay_steps"] == exp["update_delay_steps"]
+        assert got["events"] == list(exp["events"]) and got["policy"] == exp["policy"]
+        n += 1
+    assert n >= 50
