@@ -838,6 +838,47 @@ __global__ void gather_rows_batch_kernel(const XferDev* __restrict__ xs, uint4* 
   }
 }
 
+// Retrieval gather from the pinned host pool (zero-copy over the host link).
+// A small fixed grid (kGatherCtas CTAs, one per SM at most) loops over all
+// transfers of the batch: the link needs only ~100 KB in flight, and a
+// light footprint (32 registers, no shared memory) leaves room for the two
+// attention CTAs on every SM it shares -- a large grid of high-priority
+// gather CTAs would evict attention occupancy for the whole transfer.
+constexpr int kGatherCtas = 128;
+
+__global__ void __launch_bounds__(256) gather_host_rows_kernel(const XferDev* __restrict__ xs,
+                                                               int n_x, uint4* __restrict__ K,
+                                                               uint4* __restrict__ V) {
+  const int lane = threadIdx.x & 31;
+  const int nw = gridDim.x * (blockDim.x >> 5);
+  const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  constexpr int kUnroll = 4;
+  for (int xi = 0; xi < n_x; ++xi) {
+    const XferDev x = xs[xi];
+    const int n = x.meta[0];
+    for (int j0 = gw * kUnroll; j0 < n; j0 += nw * kUnroll) {
+      uint4 v[kUnroll];
+#pragma unroll
+      for (int q = 0; q < kUnroll; ++q) {
+        const int j = j0 + q;
+        if (j < n) {
+          const size_t p = x.pos[j];
+          v[q] = lane < 16 ? x.srcK[p * 16 + lane] : x.srcV[p * 16 + lane - 16];
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < kUnroll; ++q) {
+        const int j = j0 + q;
+        if (j < n) {
+          const int64_t r = x.dst_row + j;
+          if (lane < 16) K[r * 16 + lane] = v[q];
+          else V[r * 16 + lane - 16] = v[q];
+        }
+      }
+    }
+  }
+}
+
 struct LandDev {
   int32_t unit;
   int32_t pad_;
@@ -911,9 +952,9 @@ int issue_gathers(EngineImpl& e, const std::vector<int>& ids_in, cudaEvent_t aft
       HC_TRY(new_event(e, &t1, true));
       HC_CUDA_TRY(cudaEventRecord(t0, e.retr));
     }
-    const int per = std::max(1, std::min(16, (max_cap + 127) / 128));
-    gather_rows_batch_kernel<<<dim3(per, int(xd.size())), 256, 0, e.retr>>>(
-        d, reinterpret_cast<uint4*>(e.K), reinterpret_cast<uint4*>(e.V));
+    (void)max_cap;
+    gather_host_rows_kernel<<<kGatherCtas, 256, 0, e.retr>>>(
+        d, int(xd.size()), reinterpret_cast<uint4*>(e.K), reinterpret_cast<uint4*>(e.V));
     HC_CHECK_LAUNCH();
     if (e.timing) {
       HC_CUDA_TRY(cudaEventRecord(t1, e.retr));

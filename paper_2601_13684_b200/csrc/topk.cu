@@ -287,9 +287,13 @@ extern "C" int hc_bitmap_from_indices(uint32_t* bitmap_dev, uint32_t n_words,
 namespace hc {
 namespace {
 
-constexpr int kMonThreads = 1024;
+// The monitor runs beside the next step's attention: 512 threads (<= 64
+// registers) and ~97 KB of shared memory let one monitor CTA share an SM
+// with one attention CTA instead of owning it.
+constexpr int kMonThreads = 512;
+constexpr int kSelThreads = 1024;   // fire selection (runs beside K4 on its own)
 constexpr int kMonBins = 8192;      // 13-bit first digit: key32 >> 19
-constexpr int kMonCand = 16384;     // shared-memory candidate capacity
+constexpr int kMonCand = 8192;      // shared-memory candidate capacity
 constexpr int kMonSmem = kMonBins * 4 + kMonCand * 8 + 64 * 4;
 
 __device__ __forceinline__ uint64_t ckey(uint32_t k32, uint32_t pos) {
@@ -299,10 +303,11 @@ __device__ __forceinline__ uint64_t ckey(uint32_t k32, uint32_t pos) {
 // Block-wide: find the bin (scanning from the top of `hist[nb]`) that holds
 // the rem-th largest entry.  Returns via sh[0] = bin, sh[1] = rank in bin,
 // sh[2] = bin count.  Every thread owns nb / blockDim.x consecutive bins.
-template <int NB>
+template <int NB, int NT>
 __device__ void block_find_bucket(const uint32_t* hist, uint32_t rem, uint32_t* sh,
                                   uint32_t* warp_tot) {
-  constexpr int per = NB / kMonThreads;
+  constexpr int per = NB / NT;
+  constexpr int NW = NT / 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint32_t local = 0;
 #pragma unroll
@@ -316,14 +321,14 @@ __device__ void block_find_bucket(const uint32_t* hist, uint32_t rem, uint32_t* 
   if (lane == 31) warp_tot[warp] = incl;
   __syncthreads();
   if (warp == 0) {
-    const uint32_t v = warp_tot[lane];
+    const uint32_t v = lane < NW ? warp_tot[lane] : 0u;
     uint32_t wi = v;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
       const uint32_t u = __shfl_up_sync(0xffffffffu, wi, off);
       if (lane >= off) wi += u;
     }
-    warp_tot[lane] = wi - v;
+    if (lane < NW) warp_tot[lane] = wi - v;
   }
   __syncthreads();
   const uint32_t excl = warp_tot[warp] + incl - local;
@@ -348,7 +353,8 @@ __device__ void block_find_bucket(const uint32_t* hist, uint32_t rem, uint32_t* 
 // holding the rem-th largest key: an 8-bit radix over bits 50..0 of the
 // composite key among the bucket's keys -- the m candidates in shared memory,
 // or (cand == nullptr, bucket overflowed) streamed from the row.  Selected
-// <=> key >= T.  hist: >= kMonThreads words of shared scratch.
+// <=> key >= T.  hist: >= 1024 words of shared scratch.
+template <int NT>
 __device__ uint64_t radix_threshold(const float* __restrict__ row, uint32_t n, uint32_t b1,
                                     uint32_t rem, const uint64_t* cand, uint32_t m,
                                     uint32_t* hist, uint32_t* sh, uint32_t* warp_tot) {
@@ -357,21 +363,21 @@ __device__ uint64_t radix_threshold(const float* __restrict__ row, uint32_t n, u
   for (int shift = 43; ; shift -= 8) {
     const int sh_eff = shift < 0 ? 0 : shift;
     const uint64_t dmask = shift < 0 ? ((uint64_t(1) << (shift + 8)) - 1) : uint64_t(255);
-    for (int j = tid; j < kMonThreads; j += kMonThreads) hist[j] = 0;  // 1024-bin scan below
+    for (int j = tid; j < 1024; j += NT) hist[j] = 0;  // 1024-bin scan below
     __syncthreads();
     if (cand) {
-      for (uint32_t i = tid; i < m; i += kMonThreads) {
+      for (uint32_t i = tid; i < m; i += NT) {
         const uint64_t key = cand[i];
         if ((key & mask) == prefix) atomicAdd(&hist[uint32_t((key >> sh_eff) & dmask)], 1u);
       }
     } else {
-      for (uint32_t i = tid; i < n; i += kMonThreads) {
+      for (uint32_t i = tid; i < n; i += NT) {
         const uint64_t key = ckey(score_key(__ldg(row + i)), i);
         if ((key & mask) == prefix) atomicAdd(&hist[uint32_t((key >> sh_eff) & dmask)], 1u);
       }
     }
     __syncthreads();
-    block_find_bucket<kMonThreads>(hist, rem, sh, warp_tot);  // 1024 >= 256 bins (zeros above)
+    block_find_bucket<1024, NT>(hist, rem, sh, warp_tot);  // 1024 >= 256 bins (zeros above)
     const uint32_t b = sh[0];
     rem = sh[1];
     const bool done = (sh[2] == rem) || shift <= 0;
@@ -383,7 +389,7 @@ __device__ uint64_t radix_threshold(const float* __restrict__ row, uint32_t n, u
   return prefix;  // bucket fully taken, or keys unique
 }
 
-__global__ void __launch_bounds__(kMonThreads, 1)
+__global__ void __launch_bounds__(kMonThreads, 2)
 monitor_kernel(const float* __restrict__ rows, int64_t row_stride, const int32_t* __restrict__ slots,
                uint32_t n, uint32_t k, const uint32_t* __restrict__ kbase, int words,
                uint64_t* __restrict__ thr_out, uint32_t* __restrict__ ovl_out,
@@ -442,7 +448,7 @@ monitor_kernel(const float* __restrict__ rows, int64_t row_stride, const int32_t
 #pragma unroll
     for (int q = 0; q < kMonBins / kMonThreads; ++q)
       gh[tid + q * kMonThreads] = hist[tid + q * kMonThreads];
-  block_find_bucket<kMonBins>(hist, k, sh, warp_tot);
+  block_find_bucket<kMonBins, kMonThreads>(hist, k, sh, warp_tot);
   const uint32_t b1 = sh[0];
   uint32_t rem = sh[1];
   const bool whole = (sh[2] == rem);
@@ -489,7 +495,8 @@ monitor_kernel(const float* __restrict__ rows, int64_t row_stride, const int32_t
   if (!whole) {
     const uint32_t m = sh[3];
     const bool in_smem = m <= uint32_t(kMonCand);
-    T = radix_threshold(row, n, b1, rem, in_smem ? cand : nullptr, m, hist, sh, warp_tot);
+    T = radix_threshold<kMonThreads>(row, n, b1, rem, in_smem ? cand : nullptr, m, hist, sh,
+                                     warp_tot);
     // candidates at or above T add their K_base bits
     if (in_smem) {
       for (uint32_t i = tid; i < m; i += kMonThreads) {
@@ -547,13 +554,13 @@ __global__ void restamp_threshold_kernel(const float* __restrict__ rows, int64_t
 // over the 32 segment counts every warp writes its selected positions in
 // ascending order (warp prefix sums, no block barriers in the loop).
 constexpr int kFireCand = 12288;
-constexpr int kFireSmem = kFireCand * 8 + kMonThreads * 4 + 96 * 4;
+constexpr int kFireSmem = kFireCand * 8 + kSelThreads * 4 + 96 * 4;
 
-__global__ void __launch_bounds__(kMonThreads, 2) fire_select_kernel(const FireJob* __restrict__ jobs) {
+__global__ void __launch_bounds__(kSelThreads, 2) fire_select_kernel(const FireJob* __restrict__ jobs) {
   extern __shared__ __align__(16) uint8_t fs_smem[];
   uint64_t* cand = reinterpret_cast<uint64_t*>(fs_smem);
   uint32_t* hist = reinterpret_cast<uint32_t*>(fs_smem + kFireCand * 8);  // radix scratch
-  uint32_t* sh = hist + kMonThreads;  // [0..7]
+  uint32_t* sh = hist + kSelThreads;  // [0..7]
   uint32_t* warp_tot = sh + 8;        // [32]
   uint32_t* seg = sh + 40;            // [32] per-warp selected counts -> offsets
   const FireJob job = jobs[blockIdx.x];
@@ -561,11 +568,11 @@ __global__ void __launch_bounds__(kMonThreads, 2) fire_select_kernel(const FireJ
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (k >= n || k == 0) {  // everything / nothing
     const uint32_t c = k >= n ? n : 0u;
-    for (uint32_t i = tid; i < c; i += kMonThreads) job.out_idx[i] = i;
+    for (uint32_t i = tid; i < c; i += kSelThreads) job.out_idx[i] = i;
     if (tid == 0) *job.out_count = c;
     return;
   }
-  block_find_bucket<kMonBins>(job.hist, k, sh, warp_tot);
+  block_find_bucket<kMonBins, kSelThreads>(job.hist, k, sh, warp_tot);
   const uint32_t b1 = sh[0];
   const uint32_t rem = sh[1];
   const bool whole = (sh[2] == rem);
@@ -613,14 +620,15 @@ __global__ void __launch_bounds__(kMonThreads, 2) fire_select_kernel(const FireJ
   if (!whole) {
     const uint32_t m = sh[3];
     const bool in_smem = m <= uint32_t(kFireCand);
-    T = radix_threshold(job.row, n, b1, rem, in_smem ? cand : nullptr, m, hist, sh, warp_tot);
+    T = radix_threshold<kSelThreads>(job.row, n, b1, rem, in_smem ? cand : nullptr, m, hist, sh,
+                                     warp_tot);
     if (in_smem) {
-      for (uint32_t i = tid; i < m; i += kMonThreads) {
+      for (uint32_t i = tid; i < m; i += kSelThreads) {
         const uint64_t key = cand[i];
         if (key >= T) atomicAdd(&seg[min((~uint32_t(key) >> 2) / segv, 31u)], 1u);
       }
     } else {
-      for (uint32_t i = tid; i < n; i += kMonThreads) {
+      for (uint32_t i = tid; i < n; i += kSelThreads) {
         const uint64_t key = ckey(score_key(__ldg(job.row + i)), i);
         if ((key >> 51) == b1 && key >= T) atomicAdd(&seg[min((i >> 2) / segv, 31u)], 1u);
       }
@@ -690,7 +698,7 @@ int launch_fire_select(const FireJob* jobs_dev, int n_jobs, cudaStream_t st) {
     configured = true;
   }
   if (n_jobs <= 0) return HC_OK;
-  fire_select_kernel<<<n_jobs, kMonThreads, kFireSmem, st>>>(jobs_dev);
+  fire_select_kernel<<<n_jobs, kSelThreads, kFireSmem, st>>>(jobs_dev);
   HC_CHECK_LAUNCH();
   return HC_OK;
 }
