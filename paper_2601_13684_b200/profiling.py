@@ -192,12 +192,6 @@ def aggregate_gqa(query_scores, group_size: int) -> np.ndarray:
     return s.reshape(s.shape[0] // group_size, group_size, -1).mean(axis=1)
 
 
-def _overlap(a: set, b: set) -> float:
-    if not a or not b:
-        raise ValueError("overlap coefficient is undefined for empty index sets")
-    return len(a & b) / min(len(a), len(b))
-
-
 def step_set_gram(trace, k: int):
     """Per-layer intersection counts of all per-step top-k sets, on the GPU.
 
@@ -231,13 +225,6 @@ def step_set_gram(trace, k: int):
     return g, cnt4.astype(np.int64)
 
 
-def _ovl(inter: int, a: int, b: int) -> float:
-    """metrics.py:74-79 from counts: |A & B| / min(|A|, |B|)."""
-    if a == 0 or b == 0:
-        raise ValueError("overlap coefficient is undefined for empty index sets")
-    return int(inter) / min(int(a), int(b))
-
-
 def _geometry(traces):
     if not traces:
         raise TaxonomyError("profiling requires at least one trace")
@@ -250,44 +237,63 @@ def _geometry(traces):
 
 
 def _profile_and_pairs(traces, config: ProfileConfig):
+    """Stability / similarity scores and the agreement graph (profiling.py:286-367).
+
+    Per trace, every intersection count comes from one Gram matrix per layer
+    (step_set_gram, K1 + K6 on the GPU); the overlap coefficients, per-head
+    medians over decode steps and the sums over traces are then numpy array
+    operations with the reference's exact arithmetic: int / int in float64,
+    np.median (same partition and middle-pair mean as the reference's
+    per-list np.median), max over peers, and float64 accumulation in trace
+    order.
+    """
     NL, H = _geometry(traces)
-    acc = {(l, h): [0.0, 0.0] for l in range(NL) for h in range(H)}
-    pair = {}
+    acc_st = np.zeros((NL, H))
+    acc_sim = np.zeros((NL, H))
+    pair = np.zeros((NL, H, H))
+    empty = "overlap coefficient is undefined for empty index sets"
     for tr in traces:
         m = tr.manifest
         gram, size = step_set_gram(tr, config.effective_topk(m.prefill_len))
         T = m.decode_steps
         if T < 1:
             raise ValueError("stability requires at least one decode step")
-
-        def ov(l, t1, h1, t2, h2):
-            return _ovl(gram[l, t1 * H + h1, t2 * H + h2], size[t1, l, h1], size[t2, l, h2])
-
-        for l in range(NL):
-            for h in range(H):
-                acc[(l, h)][0] += float(np.median([ov(l, t, h, 0, h) for t in range(1, T + 1)]))
-                if H > 1:
-                    acc[(l, h)][1] += float(np.median(
-                        [max(ov(l, t, h, t, p) for p in range(H) if p != h)
-                         for t in range(1, T + 1)]))
+        T1 = T + 1
+        g = gram.reshape(NL, T1, H, T1, H)
+        sz = size.transpose(1, 0, 2)  # [NL, T1, H]
+        if (sz == 0).any():
+            raise ValueError(empty)
+        # stability: overlap of each decode-step set with the step-0 set (metrics.py:82-87)
+        inter = np.stack([g[:, 1:, h, 0, h] for h in range(H)], axis=-1)  # [NL, T, H]
+        den = np.minimum(sz[:, 1:, :], sz[:, :1, :])
+        acc_st += np.median(inter.astype(np.float64) / den.astype(np.float64), axis=1)
+        # same-step overlaps of every head pair: [NL, T1, H, H]
+        tt = np.arange(T1)
+        same = np.moveaxis(g[:, tt, :, tt, :], 0, 1).astype(np.float64)
+        den2 = np.minimum(sz[:, :, :, None], sz[:, :, None, :]).astype(np.float64)
+        ovp = same / den2
+        if H > 1:  # similarity: best peer per step, median over steps (metrics.py:90-106)
+            peers = ovp[:, 1:].copy()
+            peers[:, :, np.arange(H), np.arange(H)] = -np.inf
+            acc_sim += np.median(peers.max(axis=-1), axis=1)
         if config.adjacency_step is not None:
             if not 1 <= config.adjacency_step <= T:
                 raise TaxonomyError(f"adjacency step {config.adjacency_step} outside 1..{T}")
             steps = [config.adjacency_step]
         else:
-            steps = range(1, T + 1)
-        for l in range(NL):
-            for h1 in range(H):
-                for h2 in range(h1 + 1, H):
-                    v = float(np.median([ov(l, t, h1, t, h2) for t in steps]))
-                    pair[(l, h1, h2)] = pair.get((l, h1, h2), 0.0) + v
+            steps = list(range(1, T + 1))
+        pair += np.median(ovp[:, steps], axis=1)  # [NL, H, H], used for h1 < h2
     n = len(traces)
-    scores = {hd: HeadScores(s_stable=a[0] / n, s_sim=a[1] / n) for hd, a in acc.items()}
-    adjacency = {hd: set() for hd in acc}
-    for (l, h1, h2), tot in pair.items():
-        if tot / n >= config.tau_sim:
-            adjacency[(l, h1)].add((l, h2))
-            adjacency[(l, h2)].add((l, h1))
+    scores = {(l, h): HeadScores(s_stable=float(acc_st[l, h]) / n,
+                                 s_sim=float(acc_sim[l, h]) / n)
+              for l in range(NL) for h in range(H)}
+    adjacency = {(l, h): set() for l in range(NL) for h in range(H)}
+    for l in range(NL):
+        for h1 in range(H):
+            for h2 in range(h1 + 1, H):
+                if float(pair[l, h1, h2]) / n >= config.tau_sim:
+                    adjacency[(l, h1)].add((l, h2))
+                    adjacency[(l, h2)].add((l, h1))
     return scores, {hd: frozenset(v) for hd, v in adjacency.items()}
 
 

@@ -364,6 +364,22 @@ def taxonomy_cases(arrays):
                     "config": {"tau_stable": prof.tau_stable, "tau_sim": prof.tau_sim,
                                "profiling_topk": prof.profiling_topk},
                     "expected": taxonomy_json(tax)})
+    # multi-trace calibration (profiling.py:286-367: medians per trace, mean over traces;
+    # SURVEY 8f rank 4): several traces of one geometry
+    for name, seeds, prof in (("calib3", (4100, 4101, 4102), ProfileConfig(tau_sim=0.7)),
+                              ("calib5", (4200, 4201, 4202, 4203, 4204),
+                               ProfileConfig(tau_sim=0.6, profiling_topk=12))):
+        trs = [generate_synthetic(mixed_spec(sd))[0] for sd in seeds]
+        tax = run_taxonomy(trs, prof)
+        names = []
+        for i, tr in enumerate(trs):
+            arrays[f"{name}/t{i}/indices"] = tr.indices
+            arrays[f"{name}/t{i}/scores"] = tr.scores
+            names.append(f"{name}/t{i}")
+        out.append({"name": name, "traces": names, "prefill_len": trs[0].manifest.prefill_len,
+                    "config": {"tau_stable": prof.tau_stable, "tau_sim": prof.tau_sim,
+                               "profiling_topk": prof.profiling_topk},
+                    "expected": taxonomy_json(tax)})
     return out
 
 

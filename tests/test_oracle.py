@@ -94,10 +94,10 @@ def test_oracle_budget_matches_reference():
 
 def test_oracle_taxonomy_matches_reference():
     for c in json_fixture("taxonomy_cases.json"):
-        idx, sc = taxonomy_arrays(c["name"])
+        traces = [(*taxonomy_arrays(n), c["prefill_len"]) for n in c.get("traces", [c["name"]])]
         cfg = c["config"]
         roles, cluster_of, clusters, s_stable, s_sim = O.run_taxonomy(
-            [(idx, sc, c["prefill_len"])], tau_stable=cfg["tau_stable"], tau_sim=cfg["tau_sim"],
+            traces, tau_stable=cfg["tau_stable"], tau_sim=cfg["tau_sim"],
             profiling_topk=cfg["profiling_topk"])
         exp = c["expected"]
         assert {f"{h[0]},{h[1]}": r for h, r in roles.items()} == exp["roles"]

@@ -163,10 +163,13 @@ def test_profiling_matches_reference_taxonomy():
     from paper_2601_13684_b200.trace import TraceManifest, make_trace
 
     for c in json_fixture("taxonomy_cases.json"):
-        idx, sc = taxonomy_arrays(c["name"])
-        T1, NL, H, K = idx.shape
-        m = TraceManifest("t", NL, H, c["prefill_len"], T1 - 1, K, 0, 256)
-        tax = run_taxonomy([make_trace(m, idx, sc)], ProfileConfig(**c["config"]))
+        traces = []
+        for name in c.get("traces", [c["name"]]):  # multi-trace calibration cases
+            idx, sc = taxonomy_arrays(name)
+            T1, NL, H, K = idx.shape
+            m = TraceManifest("t", NL, H, c["prefill_len"], T1 - 1, K, 0, 256)
+            traces.append(make_trace(m, idx, sc))
+        tax = run_taxonomy(traces, ProfileConfig(**c["config"]))
         exp = c["expected"]
         assert {f"{l},{h}": p.role for (l, h), p in tax.heads.items()} == exp["roles"]
         assert [[list(cl.pivot), [list(s) for s in cl.satellites]] for cl in tax.clusters] \
