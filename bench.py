@@ -141,16 +141,12 @@ def run_b200(args, rank, world):
     tax, plan = plan_for(w, args.policy) if args.policy in ("heterocache", "full") \
         else (None, None)
     K, W = args.steps, args.warmup
-    # every (sequence, layer) cluster drifts once inside each timed
-    # loop, staggered across the loop (cfg4: every 12 steps, staggered phases)
-    from paper_2601_13684_b200.workload import decode_queries, staggered_shifts
+    # every (sequence, layer) cluster drifts once per 300 steps
+    # (cfg4: every 12 steps), phases staggered over the period: a fixed drift rate,
+    # whatever the length of the timed loops
+    from paper_2601_13684_b200.workload import DRIFT_PERIOD, decode_queries, staggered_shifts
 
-    if w.shift_every:
-        shifts = staggered_shifts(w.batch, w.num_layers, W + 1, 2 * K, w.shift_every)
-    else:
-        a_ = staggered_shifts(w.batch, w.num_layers, W + 1, K)
-        b_ = staggered_shifts(w.batch, w.num_layers, W + K + 1, K)
-        shifts = {key: a_[key] + b_[key] for key in a_}
+    shifts = staggered_shifts(w.batch, w.num_layers, W + 1, 2 * K + 8, w.shift_every)
     cfg = EngineConfig(tau_drift=0.5, window=8, update_delay_steps=1,
                        transfer_bandwidth=int(args.link_mib_per_step * (1 << 20)))
     T = W + 2 * K + 8
@@ -323,9 +319,8 @@ def run_b200(args, rank, world):
             "roles_per_layer": [tax.heads[(0, h)].role for h in range(m.kv_heads)],
             "policy": args.policy,
             "decode_window": cfg.window, "tau_drift": cfg.tau_drift,
-            "topic_shifts": ("every cluster (sequence, layer) once per timed loop, staggered"
-                             if not w.shift_every else
-                             f"every {w.shift_every} steps per cluster, staggered phases"),
+            "topic_shifts": (f"every cluster (sequence, layer) once per "
+                             f"{w.shift_every or DRIFT_PERIOD} steps, staggered phases"),
             "split_k_chunk": args.chunk,
             "transfer_bandwidth_bytes_per_step": cfg.transfer_bandwidth,
             "l2": f"inputs larger than L2: {step_bytes / 1e9:.2f} GB of resident K/V read per step",

@@ -53,7 +53,7 @@ class Workload:
     batch: int
     compression: float   # c: L_base = c * L
     decode_steps: int
-    shift_every: int     # planted topic shift period (steps); 0 = one shift mid-run
+    shift_every: int     # planted topic shift period (steps); 0 = DRIFT_PERIOD
     layers: int | None = None  # override (bench subsets); None = all layers
 
     @property
@@ -197,23 +197,25 @@ class SyntheticKV:
                 vn.to(torch.bfloat16).contiguous())
 
 
-def staggered_shifts(batch: int, num_layers: int, start: int, span: int, every: int = 0):
-    """Per-(sequence, layer) cluster shift steps, spread evenly over [start, start+span).
+DRIFT_PERIOD = 300  # steps between a cluster's topic shifts (one per run)
 
-    every == 0: one shift per cluster inside the span (SURVEY.md section 8d,
-    "one shift mid-run"), staggered so drift bursts stay within what the host
-    link can retrieve; every > 0: a shift every `every` steps with staggered
-    phases (cfg4, frequent drift).  Returns {(b, l): [steps]}.
+
+def staggered_shifts(batch: int, num_layers: int, start: int, span: int, every: int = 0):
+    """Per-(sequence, layer) cluster shift steps over [start, start + span).
+
+    Every cluster's topic shifts once per `every` steps (0: DRIFT_PERIOD, the
+    survey's "one shift per run" of 300 steps; cfg4: every 12 steps), with the
+    clusters' phases spread evenly over the period.  The drift rate per step
+    is therefore fixed by the workload, not by the length of the timed loop.
+    Returns {(b, l): [steps]}.
     """
+    every = every or DRIFT_PERIOD
     n = batch * num_layers
     out = {}
     for b in range(batch):
         for l in range(num_layers):
             i = b * num_layers + l
-            if every:
-                out[(b, l)] = list(range(start + i % every, start + span, every))
-            else:
-                out[(b, l)] = [start + (i * span) // n]
+            out[(b, l)] = list(range(start + (i * every) // n, start + span, every))
     return out
 
 
