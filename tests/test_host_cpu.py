@@ -139,3 +139,54 @@ def test_window_median_bit_identical_to_numpy():
             assert np.array_equal(got, exp)
             for j in range(v.shape[1]):  # the reference's per-list call (engine.py:250)
                 assert got[j] == np.median(list(v[:, j]))
+
+
+def test_policy_spec_mirrors_reference_rules():
+    """evaluation.PolicySpec / run_policies / compare host logic (evaluation.py:62-335),
+    checked against the oracle's restatement of the budget rules -- no GPU needed."""
+    from paper_2601_13684_b200.evaluation import (BudgetMismatchError, EvaluationError,
+                                                  PolicySpec, compare, comparison_csv,
+                                                  static_roles)
+    from paper_2601_13684_b200.reporting import SimulationReport, StepRow
+    from oracle import hc_oracle as O
+
+    with pytest.raises(EvaluationError):
+        PolicySpec("lru")
+    with pytest.raises(EvaluationError):
+        PolicySpec("static_topk", rho=0.0)
+    with pytest.raises(EvaluationError):
+        PolicySpec("sink_window", window=-1)
+    for name, rho, sinks, window, L in [("sink_window", 0.3, 4, None, 400),
+                                        ("sink_window", 0.5, 2, 10, 60),
+                                        ("static_topk", 0.35, 4, None, 96),
+                                        ("full_oracle", 0.5, 4, None, 400)]:
+        spec = PolicySpec(name, rho=rho, sink_count=sinks, window=window)
+        assert spec.budget_ceiling(12, L) == O.policy_budget_ceiling(name, rho, sinks, window,
+                                                                      12, L)
+    with pytest.raises(EvaluationError):
+        PolicySpec("sink_window", rho=0.05).effective_window(60)
+    with pytest.raises(EvaluationError):
+        static_roles(PolicySpec("static_topk", rho=0.01), 1, 4, 60)
+    tax, plan, cfg = static_roles(PolicySpec("sink_window", rho=0.3), 2, 4, 400)
+    assert set(tax.compressed_heads()) == set(plan.lengths) and not any(plan.lengths.values())
+    assert (cfg.sink_count, cfg.recency_window, cfg.variant) == (4, 116, "no_retrieval")
+
+    def rep(policy, recalls, ceiling, sha="x"):
+        rows = tuple(StepRow(step=t, recall=r, gpu_entries=10, extra_entries=0,
+                             bytes_in_flight=0, cumulative_bytes=0, retrieval_flag=0)
+                     for t, r in enumerate(recalls))
+        return SimulationReport(policy=policy, trace_sha256=sha, num_layers=1,
+                                heads_per_layer=4, prefill_len=100, decode_steps=len(rows) - 1,
+                                budget_ceiling=ceiling, update_delay_steps=0, rows=rows,
+                                events=())
+
+    table = compare([rep("static_topk", [1.0, 0.5], 40.0), rep("heterocache", [1.0, 0.9], 40.0),
+                     rep("full_oracle", [1.0, 1.0], 400.0)])
+    assert [r["policy"] for r in table["policies"]] == ["full_oracle", "heterocache",
+                                                        "static_topk"]
+    assert table["mean_recall_delta_vs_heterocache"]["static_topk"] == 0.95 - 0.75
+    assert comparison_csv(table).splitlines()[0].startswith("policy,mean_recall")
+    with pytest.raises(BudgetMismatchError):
+        compare([rep("static_topk", [1.0], 40.0), rep("sink_window", [1.0], 80.0)])
+    with pytest.raises(EvaluationError):
+        compare([rep("static_topk", [1.0], 40.0), rep("heterocache", [1.0], 40.0, sha="y")])
