@@ -185,7 +185,9 @@ struct EngineImpl {
   __nv_bfloat16* pool = nullptr;          // [n_sat][2][L][128]
   bool pool_host = true;
   std::vector<Transfer> xfers;
-  std::vector<cudaEvent_t> events;  // owned events (retrieval / landing ordering)
+  // owned ordering events (fires, gathers, landings), with the step that made
+  // them; gc_events() retires the completed, unreferenced ones
+  std::deque<std::pair<cudaEvent_t, int>> events;
   // pinned staging ring for small host->device descriptor uploads: keeps every
   // cudaMemcpyAsync truly asynchronous (pageable sources may sync the stream)
   char* stage = nullptr;
@@ -256,7 +258,9 @@ int engine_destroy(EngineImpl& e) {
   for (auto& pr : e.stage_busy) cudaEventDestroy(std::get<2>(pr));
   if (e.stage) cudaFreeHost(e.stage);
   if (e.ovl_host) cudaFreeHost(e.ovl_host);
-  for (auto ev : e.events) cudaEventDestroy(ev);
+  for (auto& ev : e.events) cudaEventDestroy(ev.first);
+  if (e.step_end) cudaEventDestroy(e.step_end);
+  if (e.rows_done) cudaEventDestroy(e.rows_done);
   for (auto& x : e.xfers) {
     if (x.sel) cudaFree(x.sel);
     if (x.cnt) cudaFree(x.cnt);
@@ -556,8 +560,34 @@ int active_tiles(const EngineImpl& e, int t) {
 int new_event(EngineImpl& e, cudaEvent_t* out, bool timed = false) {
   cudaEvent_t ev;
   HC_CUDA_TRY(cudaEventCreateWithFlags(&ev, timed ? cudaEventDefault : cudaEventDisableTiming));
-  e.events.push_back(ev);
+  e.events.emplace_back(ev, e.last_t);
   *out = ev;
+  return HC_OK;
+}
+
+// Retire ordering events older than kRing steps that have completed and that
+// no pending transfer or timing record still refers to (a long decode would
+// otherwise accumulate one per fire / gather / landing).
+int gc_events(EngineImpl& e, int t) {
+  if (t % kRing || e.events.empty()) return HC_OK;
+  std::vector<cudaEvent_t> live;
+  for (const auto& q : e.fifo)
+    for (int id : q) {
+      live.push_back(e.xfers[id].selected);
+      live.push_back(e.xfers[id].done);
+    }
+  for (const auto& pr : e.gather_ev) live.push_back(pr.first), live.push_back(pr.second);
+  for (const auto& pr : e.land_ev) live.push_back(pr.first), live.push_back(pr.second);
+  std::sort(live.begin(), live.end());
+  while (!e.events.empty() && e.events.front().second < t - kRing) {
+    const cudaEvent_t ev = e.events.front().first;
+    if (std::binary_search(live.begin(), live.end(), ev)) break;
+    const cudaError_t q = cudaEventQuery(ev);
+    if (q == cudaErrorNotReady) break;
+    HC_CUDA_TRY(q);
+    HC_CUDA_TRY(cudaEventDestroy(ev));
+    e.events.pop_front();
+  }
   return HC_OK;
 }
 
@@ -691,14 +721,16 @@ int engine_decode_end(EngineImpl& e, int t, cudaStream_t st) {
   if (e.step_end) HC_CUDA_TRY(cudaStreamWaitEvent(st, e.step_end, 0));
   HC_TRY(launch_attn_post(e.cur_p, e.d_piv_units, e.n_piv, st, ev ? ev + 2 : nullptr));
   e.last_t = t;
-  if (!e.step_end) HC_TRY(new_event(e, &e.step_end));
+  if (!e.step_end)
+    HC_CUDA_TRY(cudaEventCreateWithFlags(&e.step_end, cudaEventDisableTiming));
   if (e.n_piv) {
     // K1+K2: top-l_base threshold and |top & K_base| per pivot (engine.py:305-311);
     // counts land directly in the overlap ring row of this step.  Nothing in
     // the next step's attention depends on it, so it runs on its own stream
     // beside that attention; readers (overlaps, fire, the next score rows)
     // wait for step_end.
-    if (!e.rows_done) HC_TRY(new_event(e, &e.rows_done));
+    if (!e.rows_done)
+      HC_CUDA_TRY(cudaEventCreateWithFlags(&e.rows_done, cudaEventDisableTiming));
     HC_CUDA_TRY(cudaEventRecord(e.rows_done, st));
     HC_CUDA_TRY(cudaStreamWaitEvent(e.mon, e.rows_done, 0));
     HC_TRY(launch_monitor(e.rowbuf, e.row_len, e.d_piv_slots, e.n_piv, uint32_t(e.L + t),
@@ -712,7 +744,7 @@ int engine_decode_end(EngineImpl& e, int t, cudaStream_t st) {
     HC_CUDA_TRY(cudaEventRecord(ev[6], st));
   }
   HC_CUDA_TRY(cudaEventRecord(e.step_end, ms));
-  return HC_OK;
+  return gc_events(e, t);
 }
 
 int engine_decode_step(EngineImpl& e, int t, const void* q, const void* kn, const void* vn,
