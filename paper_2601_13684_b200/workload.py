@@ -55,6 +55,10 @@ class Workload:
     decode_steps: int
     shift_every: int     # planted topic shift period (steps); 0 = DRIFT_PERIOD
     layers: int | None = None  # override (bench subsets); None = all layers
+    # EngineConfig.transfer_bandwidth of timing runs ("set from the
+    # measured host link"): the B200 box's measured link (~48 GB/s, zero-copy
+    # gather) times the workload's measured decode step, in MiB per step
+    link_mib_per_step: float = 64.0
 
     @property
     def num_layers(self) -> int:
@@ -63,11 +67,17 @@ class Workload:
 
 # BASELINE.json configs
 CONFIGS = {
-    "cfg1": Workload("llama3-8b-layer-4k-b1", LLAMA3_8B, 4096, 1, 0.10, 64, 0, layers=1),
-    "cfg2": Workload("llama3.1-8b-32k-b1", LLAMA3_8B, 32768, 1, 0.10, 256, 0),
-    "cfg3": Workload("qwen2.5-7b-128k-b4", QWEN25_7B, 131072, 4, 0.05, 128, 0),
-    "cfg4": Workload("r1-distill-llama-8b-64k+8k-b1", R1_LLAMA_8B, 65536, 1, 0.10, 8192, 12),
-    "cfg5": Workload("llama3.1-8b-224k-b8", LLAMA3_8B, 229376, 8, 0.10, 64, 0),
+    # link MiB/step = 48 GB/s x step: cfg1 0.05 ms, cfg2 0.27, cfg3 1.41, cfg4 0.57, cfg5 11.6
+    "cfg1": Workload("llama3-8b-layer-4k-b1", LLAMA3_8B, 4096, 1, 0.10, 64, 0, layers=1,
+                     link_mib_per_step=2.0),
+    "cfg2": Workload("llama3.1-8b-32k-b1", LLAMA3_8B, 32768, 1, 0.10, 256, 0,
+                     link_mib_per_step=12.0),
+    "cfg3": Workload("qwen2.5-7b-128k-b4", QWEN25_7B, 131072, 4, 0.05, 128, 0,
+                     link_mib_per_step=64.0),
+    "cfg4": Workload("r1-distill-llama-8b-64k+8k-b1", R1_LLAMA_8B, 65536, 1, 0.10, 8192, 12,
+                     link_mib_per_step=26.0),
+    "cfg5": Workload("llama3.1-8b-224k-b8", LLAMA3_8B, 229376, 8, 0.10, 64, 0,
+                     link_mib_per_step=530.0),
 }
 
 
