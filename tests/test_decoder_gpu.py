@@ -31,14 +31,17 @@ ROW_RTOL = 2e-3
 
 def _build(variant="heterocache", delay=1, bandwidth=1 << 30, B=2, NL=2, L=700, T=40,
            chunk=256, host_pool=True, window=8, eval_every_step=False, shift=13, seed=3,
-           obs_window=1, sinks=4, recency=8, overlap_decisions=True, recall_topk=0):
+           obs_window=1, sinks=4, recency=8, overlap_decisions=True, recall_topk=0,
+           heads=(16, 4)):
     import torch
 
     from paper_2601_13684_b200.decoder import HeteroCacheDecoder
     from paper_2601_13684_b200.engine import EngineConfig
     from paper_2601_13684_b200.workload import ModelShape, SyntheticKV, plan_for, Workload
 
-    model = ModelShape("tiny-qwen", NL, 16, 4)
+    # (q heads, kv heads): 4 KV heads -> the Qwen role mix (pivot, 2 satellites, anchor);
+    # 8 -> the Llama mix (pivot, 4 satellites, 2 anchors, volatile)
+    model = ModelShape("tiny", NL, *heads)
     w = Workload("tiny", model, L, B, 0.10, T, 0, layers=NL)
     tax, plan = plan_for(w)
     cfg = EngineConfig(tau_drift=0.5, window=window, update_delay_steps=delay,
@@ -149,9 +152,14 @@ def _unit_kv(ctx, news, b, l, h, t):
     return torch.cat(ks), torch.cat(vs)
 
 
-def test_decoder_events_rows_and_outputs_match_oracle():
-    ctx = _build()
-    rows, outs, news, dyn_seen = _run(ctx, check_steps=(1, 7, 16, 26, 40))
+@pytest.mark.parametrize("heads,kw", [((16, 4), {}),
+                                      ((28, 4), dict(B=1, T=24, shift=9)),   # Qwen2.5 G=7
+                                      ((32, 8), dict(B=1, T=24, shift=9))])  # Llama-3 mix
+def test_decoder_events_rows_and_outputs_match_oracle(heads, kw):
+    ctx = _build(heads=heads, **kw)
+    T = ctx["T"]
+    rows, outs, news, dyn_seen = _run(ctx, check_steps=tuple(
+        t for t in (1, 7, 16, 26, 40) if t <= T))
     fired = _check_events(ctx, rows)
     assert fired >= 1, "planted topic shift must trigger a retrieval"
     dec, L, H, G = ctx["dec"], ctx["L"], ctx["model"].kv_heads, ctx["model"].group
@@ -215,6 +223,11 @@ def test_prefill_rows_match_oracle():
     dict(overlap_decisions=False),
     dict(overlap_decisions=False, bandwidth=3000, window=4, shift=(6, 11, 19, 27), T=36),
     dict(overlap_decisions=False, eval_every_step=True),
+    # GQA groups of the target models: Qwen2.5 (G=7) and Llama-3 (G=4, 8 KV heads with
+    # four satellites per pivot, two anchors and a volatile head), and G=8
+    dict(heads=(28, 4), shift=11, T=30),
+    dict(heads=(32, 8), B=1, shift=11, T=30),
+    dict(heads=(32, 4), B=1, shift=9, T=24, window=4),
 ])
 def test_decoder_variants_match_oracle(kw):
     ctx = _build(**kw)
