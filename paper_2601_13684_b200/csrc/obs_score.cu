@@ -36,9 +36,10 @@ constexpr int kN = 128;                 // keys per tile
 constexpr int kBox = 128 * 128;         // bytes of one 64-col x 128-row swizzled box
 constexpr int kTile = 2 * kBox;         // one K tile (128 keys x 128 d bf16)
 constexpr int kStagesObs = 2;  // 2 CTAs per SM keep 4 K tiles in flight per SM
-constexpr int kObsThreads = 192;
+constexpr int kEpiWarps = 8;  // two per TMEM lane quarter: each owns half of a tile's columns
+constexpr int kObsThreads = (2 + kEpiWarps) * 32;
 constexpr int kSmemObs = 1024 + kTile /*Q*/ + kStagesObs * kTile + 256 /*barriers*/ +
-                         4 * kN * 4 /*column partials*/;
+                         2 * 4 * kN * 4 /*column partials, double-buffered*/;
 
 struct ObsParams {
   int L;             // keys per unit
@@ -156,7 +157,7 @@ obs_score_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant_
   const uint32_t full = bars, empty = bars + 8 * kStagesObs;
   const uint32_t tfull = bars + 16 * kStagesObs, tempty = tfull + 16, qfull = tempty + 16;
   const uint32_t tmem_slot = qfull + 8;
-  float* colsum = reinterpret_cast<float*>(gbase + (bars - base) + 256);  // [4][128]
+  float* colsum = reinterpret_cast<float*>(gbase + (bars - base) + 256);  // [2][4][128]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(gbase + (tmem_slot - base));
 
   const int unit = blockIdx.y, chunk = blockIdx.x;
@@ -172,7 +173,7 @@ obs_score_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant_
     }
     for (int a = 0; a < 2; ++a) {
       mb_init(tfull + 8 * a, 1);
-      mb_init(tempty + 8 * a, 4);  // one arrive per epilogue warp
+      mb_init(tempty + 8 * a, kEpiWarps);  // one arrive per epilogue warp
     }
     mb_init(qfull, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -223,8 +224,9 @@ obs_score_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant_
     }
     __syncwarp();
   } else {
-    // ---------------- epilogue: thread = query row ----------------
-    const int q4 = warp & 3;                // TMEM lane quarter this warp may access
+    // ---------------- epilogue: thread = query row, warp = half of the columns ----------------
+    const int q4 = warp & 3;                 // TMEM lane quarter this warp may access
+    const int half = (warp - 2) >> 2;        // columns [64 * half, 64 * half + 64) of each tile
     const int r = q4 * 32 + lane;            // query row
     const bool row_ok = r < p.rows;
     const int qpos = p.L - p.w + (row_ok ? r / p.G : 0);  // causal limit of this row
@@ -240,67 +242,72 @@ obs_score_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant_
       mb_wait(tfull + 8 * a, (i >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int key0 = (tile0 + i) * kN;
-      // two 32-column TMEM loads in flight per wait (64 registers)
-      for (int c2 = 0; c2 < kN / 32; c2 += 2) {
-        float v2[2][32];
-        tmem_ld32(tmem + (uint32_t(q4 * 32) << 16) + a * kN + c2 * 32, v2[0]);
-        tmem_ld32(tmem + (uint32_t(q4 * 32) << 16) + a * kN + (c2 + 1) * 32, v2[1]);
-        tmem_wait_ld();
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          float (&v)[32] = v2[h];
-          const int c = c2 + h;
-          const int first = key0 + c * 32;
-          const bool unmasked = row_ok && first + 31 <= qpos;  // common case: no causal cut
-          if (p.pass == 1) {
-            // max on raw scores (scale > 0), then exp2(v*scale - m) as one FFMA + EX2
-            float tmax = -INFINITY;
-            if (unmasked) {
-#pragma unroll
-              for (int j = 0; j < 32; ++j) tmax = fmaxf(tmax, v[j]);
-            } else {
-#pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                v[j] = (row_ok && first + j <= qpos) ? v[j] : -INFINITY;
-                tmax = fmaxf(tmax, v[j]);
-              }
-            }
-            const float mn = fmaxf(m, tmax * p.scale_log2);
-            const float mb = mn == -INFINITY ? 0.f : mn;
-            float s = 0.f;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) s += exp2f(fmaf(v[j], p.scale_log2, -mb));
-            l = l * exp2f(m - mb) + s;
-            m = mn;
-          } else {
-            // exp2(v*scale - M) / L  ==  exp2(v*scale - (M + log2 L)): one FFMA + EX2
-            const float off = -(Mr + log2L);
-            if (unmasked) {
-#pragma unroll
-              for (int j = 0; j < 32; ++j) v[j] = exp2f(fmaf(v[j], p.scale_log2, off));
-            } else {
-#pragma unroll
-              for (int j = 0; j < 32; ++j)
-                v[j] = (row_ok && first + j <= qpos) ? exp2f(fmaf(v[j], p.scale_log2, off)) : 0.f;
-            }
-            const float col = transpose_reduce32(v);  // lane = column c*32 + lane
-            colsum[q4 * kN + c * 32 + lane] = col;
-          }
-        }
-      }
+      // this warp's two 32-column TMEM loads in flight per wait (64 registers)
+      float v2[2][32];
+      const int c0 = half * 2;
+      tmem_ld32(tmem + (uint32_t(q4 * 32) << 16) + a * kN + c0 * 32, v2[0]);
+      tmem_ld32(tmem + (uint32_t(q4 * 32) << 16) + a * kN + (c0 + 1) * 32, v2[1]);
+      tmem_wait_ld();
+      // the accumulator may be overwritten as soon as every warp holds its columns
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mb_arrive(tempty + 8 * a);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float (&v)[32] = v2[h];
+        const int c = c0 + h;
+        const int first = key0 + c * 32;
+        const bool unmasked = row_ok && first + 31 <= qpos;  // common case: no causal cut
+        if (p.pass == 1) {
+          // max on raw scores (scale > 0), then exp2(v*scale - m) as one FFMA + EX2
+          float tmax = -INFINITY;
+          if (unmasked) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) tmax = fmaxf(tmax, v[j]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              v[j] = (row_ok && first + j <= qpos) ? v[j] : -INFINITY;
+              tmax = fmaxf(tmax, v[j]);
+            }
+          }
+          const float mn = fmaxf(m, tmax * p.scale_log2);
+          const float mb = mn == -INFINITY ? 0.f : mn;
+          float s = 0.f;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) s += exp2f(fmaf(v[j], p.scale_log2, -mb));
+          l = l * exp2f(m - mb) + s;
+          m = mn;
+        } else {
+          // exp2(v*scale - M) / L  ==  exp2(v*scale - (M + log2 L)): one FFMA + EX2
+          const float off = -(Mr + log2L);
+          if (unmasked) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = exp2f(fmaf(v[j], p.scale_log2, off));
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              v[j] = (row_ok && first + j <= qpos) ? exp2f(fmaf(v[j], p.scale_log2, off)) : 0.f;
+          }
+          const float col = transpose_reduce32(v);  // lane = column c*32 + lane
+          colsum[(a * 4 + q4) * kN + c * 32 + lane] = col;
+        }
+      }
       if (p.pass == 2) {
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        // one barrier per tile: the partials of tile i live in buffer i&1, which
+        // tile i+2 overwrites only after tile i+1's barrier (every thread has
+        // read tile i's columns by then)
+        asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
         const int t = threadIdx.x - 64;  // 0..127: one key column each
-        const float sum = (colsum[t] + colsum[kN + t]) + (colsum[2 * kN + t] + colsum[3 * kN + t]);
-        if (key0 + t < p.L) p.out[size_t(unit) * p.row_stride + key0 + t] = sum * inv_rows;
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (t < kN) {
+          const float* cs = colsum + a * 4 * kN;
+          const float sum = (cs[t] + cs[kN + t]) + (cs[2 * kN + t] + cs[3 * kN + t]);
+          if (key0 + t < p.L) p.out[size_t(unit) * p.row_stride + key0 + t] = sum * inv_rows;
+        }
       }
     }
-    if (p.pass == 1) {
-      float* dst = p.part + ((size_t(unit) * p.n_chunks + chunk) * kM + r) * 2;
+    if (p.pass == 1) {  // one (m, l) per row and column half: 2 x n_chunks partials per row
+      float* dst = p.part + ((size_t(unit) * 2 * p.n_chunks + 2 * chunk + half) * kM + r) * 2;
       dst[0] = m;
       dst[1] = l;
     }
@@ -363,7 +370,7 @@ size_t obs_scratch_bytes(int n_units, int L) {
   const int tiles_per_cta = obs_tiles_per_cta(n_units, n_tiles);
   const int n_chunks = (n_tiles + tiles_per_cta - 1) / tiles_per_cta;
   return size_t(n_units) * kM * 128 * 2 /*packed Q*/ +
-         size_t(n_units) * n_chunks * kM * 2 * 4 /*partials*/ + size_t(n_units) * kM * 2 * 4;
+         size_t(n_units) * 2 * n_chunks * kM * 2 * 4 /*partials*/ + size_t(n_units) * kM * 2 * 4;
 }
 
 int launch_obs_scores(const void* k, const void* q_obs, int B, int H, int G, int w, int L,
@@ -387,7 +394,7 @@ int launch_obs_scores(const void* k, const void* q_obs, int B, int H, int G, int
   char* sc = static_cast<char*>(scratch);
   __nv_bfloat16* qp = reinterpret_cast<__nv_bfloat16*>(sc);
   float* part = reinterpret_cast<float*>(sc + size_t(n_units) * kM * 128 * 2);
-  float* stats = part + size_t(n_units) * n_chunks * kM * 2;
+  float* stats = part + size_t(n_units) * 2 * n_chunks * kM * 2;
   obs_pack_q_kernel<<<dim3(n_units, kM), 128, 0, st>>>(
       static_cast<const __nv_bfloat16*>(q_obs), H, G, w, qp);
   HC_CHECK_LAUNCH();
@@ -411,7 +418,7 @@ int launch_obs_scores(const void* k, const void* q_obs, int B, int H, int G, int
   p.pass = 1;
   obs_score_kernel<<<grid, kObsThreads, kSmemObs, st>>>(tk, tq, p);
   HC_CHECK_LAUNCH();
-  obs_merge_kernel<<<n_units, kM, 0, st>>>(part, n_chunks, stats);
+  obs_merge_kernel<<<n_units, kM, 0, st>>>(part, 2 * n_chunks, stats);
   HC_CHECK_LAUNCH();
   p.pass = 2;
   obs_score_kernel<<<grid, kObsThreads, kSmemObs, st>>>(tk, tq, p);
