@@ -480,7 +480,7 @@ def main():
             from paper_2601_13684_b200.workload import plan_for
 
             tax, plan = plan_for(w)
-            per_step, cores, sample, _ = cpu_step_timer(w, hplan, htax, seconds=args.cpu_seconds)
+            per_step, cores, sample, _ = cpu_step_timer(w, plan, tax, seconds=args.cpu_seconds)
             res["cpu_baseline"] = {"value": 1.0 / per_step, "unit": "steps/s", "cores": cores,
                                    "kind": "port", "sample": sample}
         else:
