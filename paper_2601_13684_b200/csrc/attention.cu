@@ -535,14 +535,4 @@ int launch_attn_post(const AttnParams& p, const int32_t* pivot_units_dev, int n_
   return HC_OK;
 }
 
-// One-shot K4 + combine + score rows.
-// ev (optional): events recorded before K4, after K4, after combine, after score rows
-int launch_attention(const CUtensorMap& tmK, const CUtensorMap& tmV, const AttnParams& p,
-                     int n_tiles, const int32_t* pivot_units_dev, int n_pivots,
-                     cudaStream_t st, const cudaEvent_t* ev) {
-  if (ev) HC_CUDA_TRY(cudaEventRecord(ev[0], st));
-  HC_TRY(launch_attn_tiles(tmK, tmV, p, n_tiles, st));
-  return launch_attn_post(p, pivot_units_dev, n_pivots, st, ev ? ev + 1 : nullptr);
-}
-
 }  // namespace hc

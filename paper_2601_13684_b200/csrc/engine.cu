@@ -27,9 +27,6 @@
 namespace hc {
 
 int make_kv_tensor_map(CUtensorMap* map, const void* base, int64_t rows);
-int launch_attention(const CUtensorMap& tmK, const CUtensorMap& tmV, const AttnParams& p,
-                     int n_tiles, const int32_t* pivot_units_dev, int n_pivots, cudaStream_t st,
-                     const cudaEvent_t* ev = nullptr);
 int launch_attn_post(const AttnParams& p, const int32_t* pivot_units_dev, int n_pivots,
                      cudaStream_t st, const cudaEvent_t* ev);
 int launch_attn_tiles(const CUtensorMap& tmK, const CUtensorMap& tmV, const AttnParams& p,
