@@ -327,3 +327,42 @@ def test_measure_mode_recall_matches_oracle_replay(kw):
                     g.cumulative_bytes, g.retrieval_flag) == (
                 e["step"], e["recall"], e["gpu_entries"], e["extra_entries"],
                 e["bytes_in_flight"], e["cumulative_bytes"], e["retrieval_flag"]), (b, g.step)
+
+
+def test_single_call_fire_and_land_abi():
+    """hc_engine_fire / hc_engine_land (one pivot, one transfer per call) driven
+    directly through the C ABI: the satellite serves exactly the fetched set from
+    the landing step on, and its prefix buffer holds that set plus sinks/tail."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2601_13684_b200 import _lib
+
+    ctx = _build(T=12, B=1)
+    dec, gen = ctx["dec"], ctx["gen"]
+    lib, h, sh = dec.lib, dec.handle, _lib.stream_handle()
+    p = dec.pivots[0]
+    sat = dec.satellites_of[p][0]
+    for t in (1, 2):
+        q, kn, vn = gen.step_inputs(t, 1)
+        o = torch.empty_like(q)
+        _lib.check(lib.hc_engine_decode_step(h, t, _lib.ptr(q), _lib.ptr(kn), _lib.ptr(vn),
+                                             _lib.ptr(o), sh))
+    ids = (C.c_int32 * len(dec.satellites_of[p]))()
+    _lib.check(lib.hc_engine_fire(h, dec.unit(0, p), 2, 3, ids, sh))
+    fetched = dec.read_indices(0, ids[0], ctx["L"] + ctx["T"])
+    before = dec.dynamic_set(0, sat)
+    for tid in ids:
+        _lib.check(lib.hc_engine_land(h, tid, sh))
+    q, kn, vn = gen.step_inputs(3, 1)
+    o = torch.empty_like(q)
+    _lib.check(lib.hc_engine_decode_step(h, 3, _lib.ptr(q), _lib.ptr(kn), _lib.ptr(vn),
+                                         _lib.ptr(o), sh))
+    after = dec.dynamic_set(0, sat)
+    assert np.array_equal(after, fetched) and not np.array_equal(after, before)
+    pre = set(dec.prefix_positions(0, sat).tolist())
+    cfg = ctx["cfg"]
+    want = set(O.resident_positions(ctx["L"], 3, set(fetched.tolist()), cfg.sink_count,
+                                    cfg.recency_window)) - set(range(ctx["L"], ctx["L"] + 3))
+    assert want <= pre
