@@ -15,14 +15,19 @@ buffers and median test (engine.py:305-321), byte accounting and completion
 steps (engine.py:322-347), FIFO landing of due transfers (engine.py:293-299)
 and the StepRow / RetrievalRecord records (reporting.py).  Host <-> device
 synchronisation happens only at window boundaries (or every step with
-eval_every_step), where the overlap counts are read back.
+eval_every_step), where the overlap counts are read back -- and, with
+overlap_decisions (default), not even there on the GPU's critical path: the
+boundary decision of step t is taken inside step t+1, while that step's
+attention over every non-satellite head already runs (decode_begin /
+decode_end), so its StepRow and events appear one step later or at finish().
 
 StepRow.recall is NaN unless measure mode is on (recall_topk > 0):
 attention-mass recall (evaluation.py:41-59) needs every head's full attention,
 which the compressed path by design never computes.  In measure mode the
 engine keeps a full-context K copy, forms every head's dense row per step,
-records its top recall_topk positions (pivots: their own decision rows, at
-least l_base_int records) and computes each head's recall of the recorded
+records its top recall_topk positions (step 0 and pivots: enough records for
+every selection the reference makes from them; pivots use their own decision
+rows) and computes each head's recall of the recorded
 mass against its resident set on the GPU -- the records are exactly an
 HCTRACE1 trace of the run (tools/export_trace.py), so the reference engine
 replaying it reproduces the StepRows bit for bit.
