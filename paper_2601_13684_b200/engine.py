@@ -99,7 +99,10 @@ class CacheView:
     def size(self) -> int:
         if self.base is None:
             return self.prefill_len + self.step
-        return len(self.base | self.extras()) + self.step
+        # |base U extras| without materialising the union (base holds thousands of
+        # positions, extras only sinks + the recency tail)
+        extras = self.extras()
+        return len(self.base) + sum(1 for x in extras if x not in self.base) + self.step
 
 
 @dataclass
