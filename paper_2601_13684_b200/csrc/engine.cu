@@ -3,13 +3,21 @@
 // drift monitor) and K3 retrieval from the pinned host pool.
 //
 // Mirrors the reference engine's lifecycle (engine.py:153-416):
-//   hc_engine_create        CacheEngine.__init__ geometry / plan  (engine.py:156-214)
-//   hc_engine_prefill_layer prefill_init                          (engine.py:263-274)
-//   hc_engine_decode_step   decode_step steps 2-4                 (engine.py:301-311)
-//   hc_engine_fire          fetch loop + K_base restamp           (engine.py:322-357)
-//   hc_engine_land          landing of a due transfer             (engine.py:293-299)
+//   hc_engine_create         CacheEngine.__init__ geometry / plan  (engine.py:156-214)
+//   hc_engine_prefill_layer  prefill_init                          (engine.py:263-274)
+//   hc_engine_decode_step    decode_step steps 2-4                 (engine.py:301-311)
+//     = decode_begin + decode_end, split so the previous boundary's decision
+//     can run beside the step's attention
+//   hc_engine_fire[_batch]   fetch loop + K_base restamp           (engine.py:322-357)
+//   hc_engine_land[_batch]   landing of due transfers              (engine.py:293-299)
+//   hc_engine_measure        _measure / attention_recall           (engine.py:276-288)
 // The window median / completion-step arithmetic stays in the Python mirror
 // (decoder.py), exactly as the reference writes it.
+//
+// Streams: the caller's stream runs the step; `mon` runs each step's monitor
+// beside the next step's attention; `side` runs fire selection and in-step
+// readbacks; `retr` (high priority) runs the retrieval gathers.  Events
+// (step_end, rows_done, selected, gather done) order every hand-off.
 
 #include <cuda.h>
 #include <cuda_bf16.h>
