@@ -27,6 +27,7 @@
 #include <deque>
 #include <new>
 #include <tuple>
+#include <unordered_map>
 #include <vector>
 
 #include "hc_common.cuh"
@@ -189,7 +190,18 @@ struct EngineImpl {
   int n_sat = 0;
   __nv_bfloat16* pool = nullptr;          // [n_sat][2][L][128]
   bool pool_host = true;
-  std::vector<Transfer> xfers;
+  // transfers by id (ids increase monotonically); a record is dropped once a
+  // later landing supersedes it, so the table holds only pending transfers and
+  // the ones serving a satellite right now -- bounded over any decode length
+  struct TransferTable {
+    std::unordered_map<int, Transfer> m;
+    int next = 0;
+    Transfer& operator[](int id) { return m.at(id); }
+    const Transfer& operator[](int id) const { return m.at(id); }
+    bool contains(int id) const { return m.count(id) != 0; }
+    int add(const Transfer& x) { m.emplace(next, x); return next++; }
+    void erase(int id) { m.erase(id); }
+  } xfers;
   // owned ordering events (fires, gathers, landings), with the step that made
   // them; gc_events() retires the completed, unreferenced ones
   std::deque<std::pair<cudaEvent_t, int>> events;
@@ -266,7 +278,8 @@ int engine_destroy(EngineImpl& e) {
   for (auto& ev : e.events) cudaEventDestroy(ev.first);
   if (e.step_end) cudaEventDestroy(e.step_end);
   if (e.rows_done) cudaEventDestroy(e.rows_done);
-  for (auto& x : e.xfers) {
+  for (auto& kv : e.xfers.m) {
+    auto& x = kv.second;
     if (x.sel) cudaFree(x.sel);
     if (x.cnt) cudaFree(x.cnt);
     if (x.pos) cudaFree(x.pos);
@@ -1220,8 +1233,7 @@ int engine_fire_batch(EngineImpl& e, int n, const int32_t* pus, int t, const int
         jb.out_count = x.cnt;
         jobs.push_back(jb);
       }
-      new_ids.push_back(int(e.xfers.size()));
-      e.xfers.push_back(x);
+      new_ids.push_back(e.xfers.add(x));
     }
   }
   if (!jobs.empty()) {
@@ -1288,7 +1300,7 @@ int engine_land_batch(EngineImpl& e, int n, const int32_t* ids, cudaStream_t st)
   }
   for (int q = 0; q < n; ++q) {
     const int id = ids[q];
-    HC_REQUIRE(id >= 0 && id < int(e.xfers.size()), HC_EINVAL, "bad transfer id %d", id);
+    HC_REQUIRE(e.xfers.contains(id), HC_EINVAL, "bad transfer id %d", id);
     const Transfer& x = e.xfers[id];
     HC_REQUIRE(!x.landed, HC_ESTATE, "transfer %d already landed", id);
     HC_REQUIRE(std::find(ids, ids + q, id) == ids + q &&
@@ -1326,7 +1338,7 @@ int apply_landings(EngineImpl& e, const std::vector<int>& idv, cudaStream_t st) 
   };
   for (int q = 0; q < n; ++q) {
     const int id = ids[q];
-    HC_REQUIRE(id >= 0 && id < int(e.xfers.size()), HC_EINVAL, "bad transfer id %d", id);
+    HC_REQUIRE(e.xfers.contains(id), HC_EINVAL, "bad transfer id %d", id);
     Transfer& x = e.xfers[id];
     HC_REQUIRE(!x.landed, HC_ESTATE, "transfer %d already landed", id);
     const int u = x.unit;
@@ -1361,7 +1373,7 @@ int apply_landings(EngineImpl& e, const std::vector<int>& idv, cudaStream_t st) 
       Transfer& old = e.xfers[e.dyn_owner[u]];
       for (void* ptr : {(void*)old.sel, (void*)old.cnt, (void*)old.pos, (void*)old.meta})
         HC_CUDA_TRY(cudaFreeAsync(ptr, st));
-      old.sel = nullptr, old.cnt = nullptr, old.pos = nullptr, old.meta = nullptr;
+      e.xfers.erase(e.dyn_owner[u]);
     }
     e.dyn_owner[u] = id;
     x.landed = true;
@@ -1778,7 +1790,7 @@ extern "C" int hc_engine_read_indices(hc_engine* eng, int32_t kind, int32_t id, 
   const uint32_t* cnt = nullptr;
   const int32_t* meta = nullptr;
   if (kind == 0) {
-    HC_REQUIRE(id >= 0 && id < int(e.xfers.size()) && e.xfers[id].sel, HC_EINVAL, "bad transfer");
+    HC_REQUIRE(e.xfers.contains(id) && e.xfers[id].sel, HC_EINVAL, "bad transfer");
     list = e.xfers[id].sel;
     cnt = e.xfers[id].cnt;
   } else if (kind == 1 || kind == 3) {
