@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--chunk", type=int, default=1024)
+    ap.add_argument("--start-step", type=int, default=0,
+                    help="decode this many steps untimed before warm-up (e.g. cfg4 at t = 8K)")
     ap.add_argument("--policy", choices=("heterocache", "full", "static_topk", "sink_window"),
                     default="heterocache",
                     help="baseline residency policies through the same engine (evaluation.py): "
@@ -147,11 +149,15 @@ def run_b200(args, rank, world):
     # whatever the length of the timed loops
     from paper_2601_13684_b200.workload import DRIFT_PERIOD, decode_queries, staggered_shifts
 
-    shifts = staggered_shifts(w.batch, w.num_layers, W + 1, 2 * K + 8, w.shift_every)
+    S0 = args.start_step
+    shifts = staggered_shifts(w.batch, w.num_layers, S0 + W + 1, 2 * K + 8, w.shift_every)
+    if S0:  # the fast-forward drifts too
+        pre = staggered_shifts(w.batch, w.num_layers, 1, S0 + W, w.shift_every)
+        shifts = {key: pre[key] + shifts[key] for key in shifts}
     cfg = EngineConfig(tau_drift=0.5, window=8, update_delay_steps=1,
                        transfer_bandwidth=int((args.link_mib_per_step or w.link_mib_per_step)
                                               * (1 << 20)))
-    T = W + 2 * K + 8
+    T = S0 + W + 2 * K + 8
     lib = _lib.load()
     obs = args.obs_window or max(1, min(32, 128 // m.group))  # w_obs = 32 (Llama)
     dkw = dict(batch=w.batch, group=m.group, max_decode=T, chunk=args.chunk, host_pool=True,
@@ -191,7 +197,7 @@ def run_b200(args, rank, world):
     out = torch.empty_like(qs[0])
     stream = torch.cuda.current_stream()
     t = 0
-    for _ in range(W):
+    for _ in range(S0 + W):
         t += 1
         q, kn, vn = inputs(t)
         dec.decode_step(t, q, kn, vn, out, rows=False)
@@ -331,7 +337,7 @@ def run_b200(args, rank, world):
             "decode_window": cfg.window, "tau_drift": cfg.tau_drift,
             "topic_shifts": (f"every cluster (sequence, layer) once per "
                              f"{w.shift_every or DRIFT_PERIOD} steps, staggered phases"),
-            "split_k_chunk": args.chunk,
+            "split_k_chunk": args.chunk, "start_step": S0,
             "transfer_bandwidth_bytes_per_step": cfg.transfer_bandwidth,
             "l2": f"inputs larger than L2: {step_bytes / 1e9:.2f} GB of resident K/V read per step",
             "parallelism": f"replicas x{world} (weak: each GPU decodes its own batch)",
