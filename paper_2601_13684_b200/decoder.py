@@ -445,6 +445,7 @@ class HeteroCacheDecoder:
                                                  self._pinned.data_ptr() + 4 * base, sh))
         q = 0
         off = base
+        unsorted = []
         for st, ev in evs:
             ev.tids = ids[q:q + len(ev.sats)].tolist()
             ev.offsets = []
@@ -453,13 +454,17 @@ class HeteroCacheDecoder:
                 off += k
             q += len(ev.sats)
             for s, k, tid in zip(ev.sats, ev.ks, ev.tids):
+                if st.pending and st.pending[-1][0] > ev.completion_step and \
+                        all(x is not st for x in unsorted):
+                    unsorted.append(st)
                 st.pending.append((ev.completion_step, st.order, s, tid, k, ev))
                 st.order += 1
             self._uncollected.append(ev)
         self._pin_head = off
-        # completion steps are nondecreasing in firing order, but keep the
-        # (completion, order) landing order explicit (engine.py:293-296)
-        for st in self.states:
+        # completion steps are nondecreasing in firing order (cumulative bytes only
+        # grow), so appends keep the (completion, order) landing order of
+        # engine.py:293-296; re-sort only if that ever does not hold
+        for st in unsorted:
             st.pending.sort(key=lambda x: (x[0], x[1]))
         if self.track_sets:
             self.sync()
