@@ -63,10 +63,16 @@ def launches(path, out):
                 agg[d["Kernel Name"]][0] += 1
                 agg[d["Kernel Name"]][1] += _us(d["Metric Value"], d.get("Metric Unit", ""))
     tot = sum(v for _, v in agg.values()) or 1.0
+    # kernels of the retrieval stream run beside the step (host-link bound); the
+    # step's own share is the one to compare with the bench's phase timeline
+    side = ("gather_host_rows_kernel", "build_positions_batch_kernel")
+    tot_step = sum(v for k, (_, v) in agg.items() if not any(x in k for x in side)) or 1.0
     lines = [f"# ncu launch list (gpu__time_duration.sum; serialised, cold caches): `{path}`", "",
-             "| kernel | launches | total us | avg us | share |", "|---|---|---|---|---|"]
+             "| kernel | launches | total us | avg us | share | share of the step (excl. retrieval stream) |",
+             "|---|---|---|---|---|---|"]
     for k, (n, s) in sorted(agg.items(), key=lambda x: -x[1][1]):
-        lines.append(f"| {k[:90]} | {n} | {s:.1f} | {s / n:.1f} | {s / tot:.1%} |")
+        st = "—" if any(x in k for x in side) else f"{s / tot_step:.1%}"
+        lines.append(f"| {k[:90]} | {n} | {s:.1f} | {s / n:.1f} | {s / tot:.1%} | {st} |")
     open(out, "w").write("\n".join(lines) + "\n")
 
 
