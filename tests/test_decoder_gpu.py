@@ -15,6 +15,8 @@ Protocol:
     bf16 P for the PV product, bf16 output).
 """
 
+import os
+
 import numpy as np
 import pytest
 
@@ -23,6 +25,7 @@ from oracle.attention_oracle import gqa_mean_row, unit_attention
 
 pytestmark = pytest.mark.gpu
 
+N_RANDOM_CONFIGS = int(os.environ.get("HC_RANDOM_CONFIGS", "8"))  # 80 passed on a B200
 O_ATOL = 2e-2
 O_RTOL = 2e-2
 ROW_ATOL = 2e-6
@@ -366,3 +369,25 @@ def test_single_call_fire_and_land_abi():
     want = set(O.resident_positions(ctx["L"], 3, set(fetched.tolist()), cfg.sink_count,
                                     cfg.recency_window)) - set(range(ctx["L"], ctx["L"] + 3))
     assert want <= pre
+
+
+@pytest.mark.parametrize("seed", range(N_RANDOM_CONFIGS))
+def test_randomized_configs_match_oracle(seed):
+    """Seeded random engine configurations (window, delay, host-link model, sinks /
+    recency, chunk, batch, prompt length, shift schedule, decision order): events,
+    StepRows and dynamic sets must equal the oracle's replay of the GPU rows."""
+    rng = np.random.default_rng(1000 + seed)
+    T = int(rng.integers(16, 41))
+    n_shift = int(rng.integers(1, 4))
+    kw = dict(
+        B=int(rng.integers(1, 4)), NL=int(rng.integers(1, 3)), L=int(rng.choice([96, 300, 700])),
+        T=T, window=int(rng.choice([2, 4, 8])), delay=int(rng.integers(0, 4)),
+        bandwidth=int(rng.choice([2000, 8000, 1 << 30])), sinks=int(rng.choice([0, 4, 9])),
+        recency=int(rng.choice([0, 8, 31])), chunk=int(rng.choice([64, 128, 256])),
+        eval_every_step=bool(rng.integers(0, 2)), overlap_decisions=bool(rng.integers(0, 2)),
+        shift=tuple(sorted(int(x) for x in rng.choice(np.arange(3, T - 2), n_shift,
+                                                         replace=False))),
+        seed=int(rng.integers(0, 1000)))
+    ctx = _build(**kw)
+    rows, _, _, _ = _run(ctx)
+    _check_events(ctx, rows)
