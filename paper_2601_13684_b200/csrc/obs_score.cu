@@ -39,7 +39,7 @@ constexpr int kStagesObs = 2;  // 2 CTAs per SM keep 4 K tiles in flight per SM
 constexpr int kEpiWarps = 8;  // two per TMEM lane quarter: each owns half of a tile's columns
 constexpr int kObsThreads = (2 + kEpiWarps) * 32;
 constexpr int kSmemObs = 1024 + kTile /*Q*/ + kStagesObs * kTile + 256 /*barriers*/ +
-                         2 * 4 * kN * 4 /*column partials, double-buffered*/;
+                         4 * 4 * kN * 4 /*column partials of 4 tiles*/;
 
 struct ObsParams {
   int L;             // keys per unit
@@ -157,7 +157,7 @@ obs_score_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant_
   const uint32_t full = bars, empty = bars + 8 * kStagesObs;
   const uint32_t tfull = bars + 16 * kStagesObs, tempty = tfull + 16, qfull = tempty + 16;
   const uint32_t tmem_slot = qfull + 8;
-  float* colsum = reinterpret_cast<float*>(gbase + (bars - base) + 256);  // [2][4][128]
+  float* colsum = reinterpret_cast<float*>(gbase + (bars - base) + 256);  // [4][4][128]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(gbase + (tmem_slot - base));
 
   const int unit = blockIdx.y, chunk = blockIdx.x;
@@ -290,19 +290,23 @@ obs_score_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant_
               v[j] = (row_ok && first + j <= qpos) ? exp2f(fmaf(v[j], p.scale_log2, off)) : 0.f;
           }
           const float col = transpose_reduce32(v);  // lane = column c*32 + lane
-          colsum[(a * 4 + q4) * kN + c * 32 + lane] = col;
+          colsum[((i & 3) * 4 + q4) * kN + c * 32 + lane] = col;
         }
       }
-      if (p.pass == 2) {
-        // one barrier per tile: the partials of tile i live in buffer i&1, which
-        // tile i+2 overwrites only after tile i+1's barrier (every thread has
-        // read tile i's columns by then)
+      if (p.pass == 2 && ((i & 1) || i == n_tiles - 1)) {
+        // one barrier per PAIR of tiles: the partials of tile i live in buffer
+        // i&3, which tile i+4 overwrites only after the next pair's barrier
+        // (every thread has read this pair's columns by then); the 256
+        // epilogue threads then sum one (tile, column) each
         asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
-        const int t = threadIdx.x - 64;  // 0..127: one key column each
-        if (t < kN) {
-          const float* cs = colsum + a * 4 * kN;
-          const float sum = (cs[t] + cs[kN + t]) + (cs[2 * kN + t] + cs[3 * kN + t]);
-          if (key0 + t < p.L) p.out[size_t(unit) * p.row_stride + key0 + t] = sum * inv_rows;
+        const int t = threadIdx.x - 64;  // 0..255
+        const int ti = (i & 1) ? i - 1 + (t >> 7) : i;
+        const int col = t & (kN - 1);
+        if ((i & 1) || t < kN) {
+          const float* cs = colsum + (ti & 3) * 4 * kN;
+          const float sum = (cs[col] + cs[kN + col]) + (cs[2 * kN + col] + cs[3 * kN + col]);
+          const int kt = (tile0 + ti) * kN + col;
+          if (kt < p.L) p.out[size_t(unit) * p.row_stride + kt] = sum * inv_rows;
         }
       }
     }
