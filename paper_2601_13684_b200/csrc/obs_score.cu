@@ -128,21 +128,28 @@ __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-// Sum 32 column values over the 32 lanes (rows) of a warp: afterwards lane c
-// holds the total of column c (halving butterfly, 31 shuffles).
-__device__ __forceinline__ float transpose_reduce32(float (&v)[32]) {
+// Sum 32 column values over the 32 lanes (rows) of a warp -- afterwards lane c
+// holds the total of column c (halving butterfly, 31 shuffles) -- for two
+// independent 32x32 blocks, stage-interleaved so every
+// shuffle stage has twice the independent work (the chains are latency-bound).
+__device__ __forceinline__ void transpose_reduce32x2(float (&a)[32], float (&b)[32], float& ca,
+                                                     float& cb) {
   const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int off = 16; off >= 1; off >>= 1) {
     const bool upper = (lane & off) != 0;
 #pragma unroll
     for (int j = 0; j < off; ++j) {
-      const float keep = upper ? v[j + off] : v[j];
-      const float send = upper ? v[j] : v[j + off];
-      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+      const float ka = upper ? a[j + off] : a[j], sa = upper ? a[j] : a[j + off];
+      const float kb = upper ? b[j + off] : b[j], sb = upper ? b[j] : b[j + off];
+      const float ra = __shfl_xor_sync(0xffffffffu, sa, off);
+      const float rb = __shfl_xor_sync(0xffffffffu, sb, off);
+      a[j] = ka + ra;
+      b[j] = kb + rb;
     }
   }
-  return v[0];
+  ca = a[0];
+  cb = b[0];
 }
 
 __global__ void __launch_bounds__(kObsThreads, 2)
@@ -289,9 +296,13 @@ obs_score_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant_
             for (int j = 0; j < 32; ++j)
               v[j] = (row_ok && first + j <= qpos) ? exp2f(fmaf(v[j], p.scale_log2, off)) : 0.f;
           }
-          const float col = transpose_reduce32(v);  // lane = column c*32 + lane
-          colsum[((i & 3) * 4 + q4) * kN + c * 32 + lane] = col;
         }
+      }
+      if (p.pass == 2) {  // column sums of both 32-column chunks (lane = column)
+        float ca, cb;
+        transpose_reduce32x2(v2[0], v2[1], ca, cb);
+        colsum[((i & 3) * 4 + q4) * kN + c0 * 32 + lane] = ca;
+        colsum[((i & 3) * 4 + q4) * kN + (c0 + 1) * 32 + lane] = cb;
       }
       if (p.pass == 2 && ((i & 1) || i == n_tiles - 1)) {
         // one barrier per PAIR of tiles: the partials of tile i live in buffer
