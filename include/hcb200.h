@@ -78,6 +78,14 @@ typedef struct hc_topk_job {
  * (dense rows that grow by one position per decode step). */
 int hc_topk_batched(const hc_topk_job* jobs_dev, int n_jobs, uint32_t n_add, void* stream);
 
+/* Pooled dense top-k (metrics.py:26-39 with pool_kernel > 0): float64 row
+ * w_dev[n], odd pool_kernel <= n; writes the first min(k, n) indices of the
+ * order (zero-padded moving average desc, raw desc, index asc).  The engine
+ * never pools; this backs top_k_indices(scores, k, pool_kernel) for dense
+ * profiling. */
+int hc_pooled_topk(const double* w_dev, uint32_t n, uint32_t pool_kernel, uint32_t k,
+                   uint32_t* out_idx_dev, void* stream);
+
 /* Single-row convenience wrapper around the same kernel. */
 int hc_select_topk(const float* scores_dev, const uint32_t* idx_dev, uint32_t n, uint32_t k,
                    uint32_t* out_idx_dev, uint32_t* out_count_dev, void* stream);

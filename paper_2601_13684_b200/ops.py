@@ -97,16 +97,17 @@ def topk_rows(idx, scores, k, base_bitmaps=None):
 def top_k_indices(scores, k: int, pool_kernel: int = 0) -> frozenset:
     """Drop-in for heterocache.metrics.top_k_indices (metrics.py:48-71), on the GPU.
 
-    Dense 1-D arrays and (index, score) pair sequences are supported;
-    pooling (pool_kernel > 0) is not offloaded (the engine never pools,
-    engine.py:229-230) and raises.
+    Dense 1-D arrays and (index, score) pair sequences are supported.  Dense
+    rows with pool_kernel > 0 take the pooled path (hc_pooled_topk: float64
+    moving sums in numpy's order, then the (pooled, raw, index) order of
+    metrics.py:26-39); the engine itself never pools (engine.py:229-230).
     """
     if k < 0:
         raise ValueError(f"k must be nonnegative, got {k}")
     if k == 0:
         return frozenset()
     if pool_kernel:
-        raise NotImplementedError("pooled dense top-k is not on the B200 path")
+        return _pooled_top_k(scores, k, pool_kernel)
     if isinstance(scores, np.ndarray):
         row = np.asarray(scores, dtype=np.float64)
         if row.ndim != 1:
@@ -125,6 +126,23 @@ def top_k_indices(scores, k: int, pool_kernel: int = 0) -> frozenset:
         sel, cnt = topk_rows(idx[None, :], sc[None, :], k)
         return frozenset(int(x) for x in sel[0, :cnt[0]])
     return top_k_indices(np.asarray(seq, dtype=np.float64), k)
+
+
+def _pooled_top_k(scores, k: int, pool_kernel: int) -> frozenset:
+    w = np.asarray(scores, dtype=np.float64)
+    if w.ndim != 1:
+        raise ValueError(f"dense scores must be 1-D, got shape {w.shape}")
+    if pool_kernel < 1 or pool_kernel % 2 == 0:
+        raise ValueError(f"pool kernel must be odd and positive, got {pool_kernel}")
+    if pool_kernel > w.size:  # np.convolve 'same' returns max(n, kernel) values: lexsort refuses
+        raise ValueError("all keys need to be the same shape")
+    torch = _torch()
+    _lib.require_cuda()
+    d = torch.from_numpy(np.ascontiguousarray(w)).cuda()
+    out = torch.empty(min(k, w.size), dtype=torch.int32, device="cuda")
+    _lib.check(_lib.load().hc_pooled_topk(_lib.ptr(d), w.size, pool_kernel, k, _lib.ptr(out),
+                                          _lib.stream_handle()))
+    return frozenset(int(x) for x in out.cpu().numpy())
 
 
 def monitor_rows(rows, k: int, base_bitmaps):

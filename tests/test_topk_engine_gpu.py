@@ -97,6 +97,34 @@ def test_topk_matches_reference_known_answers():
         assert sorted(sel[0, :cnt[0]].tolist()) == c["expected"]
 
 
+def test_pooled_dense_topk_matches_reference():
+    """top_k_indices(dense, k, pool_kernel) on the GPU (hc_pooled_topk): the
+    reference's known answers, then larger rows with ties and zeros against the
+    oracle (np.convolve + lexsort, metrics.py:26-39)."""
+    from paper_2601_13684_b200.ops import top_k_indices
+
+    n = 0
+    for c in json_fixture("topk_cases.json"):
+        if c["kind"] == "dense" and c["pool"]:
+            w = np.asarray(c["w"], dtype=np.float64)
+            assert sorted(top_k_indices(w, c["k"], pool_kernel=c["pool"])) == c["expected"]
+            n += 1
+    assert n >= 20
+    rng = np.random.default_rng(77)
+    for size, pool in ((20000, 13), (131072, 5), (4097, 3), (50000, 13)):
+        w = rng.random(size)
+        w[rng.choice(size, size // 10)] = 0.0               # zero runs: pooled ties
+        w[: size // 50] = np.round(w[: size // 50] * 4) / 4  # quantised: raw ties
+        w[5] = -0.0
+        for k in (1, 37, size // 3):
+            want = O.top_k_dense(w, k, pool_kernel=pool)
+            assert top_k_indices(w, k, pool_kernel=pool) == frozenset(int(x) for x in want)
+    with pytest.raises(ValueError):
+        top_k_indices(np.ones(5), 2, pool_kernel=7)
+    with pytest.raises(ValueError):
+        top_k_indices(np.ones(50), 2, pool_kernel=4)
+
+
 def test_top_k_indices_dropin():
     from paper_2601_13684_b200.ops import top_k_indices
 
