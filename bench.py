@@ -476,6 +476,8 @@ def main():
 
     import torch
 
+    from paper_2601_13684_b200 import build as _build
+    _build.ensure_built()  # no-op when the in-tree library shipped with the checkout
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)

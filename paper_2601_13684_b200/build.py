@@ -42,10 +42,15 @@ def needs_build() -> bool:
     return any(p.stat().st_mtime > t for p in deps)
 
 
+def ensure_built() -> Path:
+    """Build only if the library is absent (a fresh checkout); never on mtime skew."""
+    return LIB if LIB.exists() else build(force=True)
+
+
 def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not needs_build():
         return LIB
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = LIB.with_suffix(f".so.{os.getpid()}.tmp")  # concurrent builders never share a tmp
     cmd = [nvcc(), *ARCH, *FLAGS, "-o", str(tmp), *map(str, sources())]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = res.stdout + res.stderr
