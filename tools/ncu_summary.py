@@ -36,8 +36,9 @@ def full(rep, out):
         lines += [f"## {name}", "", "| metric | value | unit |", "|---|---|---|"]
         rec = {"kernel": name}
         for m in METRICS:
-            if m in hdr:
-                i = hdr.index(m)
+            hits = [j for j, h in enumerate(hdr) if h == m or h.endswith("." + m)]
+            if hits:
+                i = hits[0]
                 lines.append(f"| {m} | {r[i]} | {units[i]} |")
                 rec[m] = r[i]
         js.append(rec)
