@@ -497,28 +497,19 @@ static int configure_attn() {
   return HC_OK;
 }
 
-// K4 over an explicit tile list (p.tiles, n_tiles entries).
-int launch_attn_tiles(const CUtensorMap& tmK, const CUtensorMap& tmV, const AttnParams& p,
-                      int n_tiles, cudaStream_t st) {
-  HC_TRY(configure_attn());
-  if (n_tiles > 0) {
-    attn_tiles_kernel<<<n_tiles, kThreadsAttn, kSmemAttn, st>>>(tmK, tmV, p);
+// Split-K combine (O and the pivots' softmax statistics).
+int launch_combine(const AttnParams& p, cudaStream_t st) {
+  HC_REQUIRE(p.group >= 1 && p.group <= 8, HC_EINVAL, "GQA group must be 1..8");
+  if (p.n_units > 0) {
+    combine_kernel<<<dim3(p.n_units, p.group), 128, 0, st>>>(p);
     HC_CHECK_LAUNCH();
   }
   return HC_OK;
 }
 
-// After K4: split-K combine, then the pivots' score rows (+ key histogram).
-// ev (optional): events recorded after K4, after combine, after score rows.
-int launch_attn_post(const AttnParams& p, const int32_t* pivot_units_dev, int n_pivots,
-                     cudaStream_t st, const cudaEvent_t* ev) {
-  HC_REQUIRE(p.group >= 1 && p.group <= 8, HC_EINVAL, "GQA group must be 1..8");
-  if (ev) HC_CUDA_TRY(cudaEventRecord(ev[0], st));
-  if (p.n_units > 0) {
-    combine_kernel<<<dim3(p.n_units, p.group), 128, 0, st>>>(p);
-    HC_CHECK_LAUNCH();
-  }
-  if (ev) HC_CUDA_TRY(cudaEventRecord(ev[1], st));
+// The pivots' GQA-mean probability rows (needs combine's statistics).
+int launch_score_rows(const AttnParams& p, const int32_t* pivot_units_dev, int n_pivots,
+                      cudaStream_t st) {
   if (n_pivots > 0 && p.rows) {
     HC_REQUIRE(p.logit_stride % 16 == 0 && p.row_stride % 8 == 0, HC_EINVAL,
                "score-row strides must be multiples of 16 / 8");
@@ -531,8 +522,19 @@ int launch_attn_post(const AttnParams& p, const int32_t* pivot_units_dev, int n_
     }
     HC_CHECK_LAUNCH();
   }
-  if (ev) HC_CUDA_TRY(cudaEventRecord(ev[2], st));
   return HC_OK;
 }
+
+// K4 over an explicit tile list (p.tiles, n_tiles entries).
+int launch_attn_tiles(const CUtensorMap& tmK, const CUtensorMap& tmV, const AttnParams& p,
+                      int n_tiles, cudaStream_t st) {
+  HC_TRY(configure_attn());
+  if (n_tiles > 0) {
+    attn_tiles_kernel<<<n_tiles, kThreadsAttn, kSmemAttn, st>>>(tmK, tmV, p);
+    HC_CHECK_LAUNCH();
+  }
+  return HC_OK;
+}
+
 
 }  // namespace hc

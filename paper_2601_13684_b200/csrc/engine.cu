@@ -36,8 +36,9 @@
 namespace hc {
 
 int make_kv_tensor_map(CUtensorMap* map, const void* base, int64_t rows);
-int launch_attn_post(const AttnParams& p, const int32_t* pivot_units_dev, int n_pivots,
-                     cudaStream_t st, const cudaEvent_t* ev);
+int launch_combine(const AttnParams& p, cudaStream_t st);
+int launch_score_rows(const AttnParams& p, const int32_t* pivot_units_dev, int n_pivots,
+                      cudaStream_t st);
 int launch_attn_tiles(const CUtensorMap& tmK, const CUtensorMap& tmV, const AttnParams& p,
                       int n_tiles, cudaStream_t st);
 int launch_topk(const hc_topk_job* jobs_dev, int n_jobs, uint32_t n_add, cudaStream_t st);
@@ -153,7 +154,8 @@ struct EngineImpl {
   int n_lu = 0, n_lt = 0;
   cudaEvent_t step_end = nullptr;  // monitor of the last completed step done (rows free again,
                                    // overlap counts, thresholds and histograms valid)
-  cudaEvent_t rows_done = nullptr;
+  cudaEvent_t rows_done = nullptr;     // combine of the last step done (main stream)
+  cudaEvent_t rows_ev[2] = {nullptr, nullptr};  // score rows of steps with parity 0 / 1 done
   cudaStream_t mon = nullptr;      // the monitor runs beside the next step's attention
   cudaStream_t side = nullptr;     // fire selection and control readbacks inside a step
   int n_slots = 0;
@@ -278,6 +280,8 @@ int engine_destroy(EngineImpl& e) {
   for (auto& ev : e.events) cudaEventDestroy(ev.first);
   if (e.step_end) cudaEventDestroy(e.step_end);
   if (e.rows_done) cudaEventDestroy(e.rows_done);
+  for (auto x : e.rows_ev)
+    if (x) cudaEventDestroy(x);
   for (auto& kv : e.xfers.m) {
     auto& x = kv.second;
     if (x.sel) cudaFree(x.sel);
@@ -473,9 +477,11 @@ int engine_create(EngineImpl& e, const hc_engine_desc& c, const int32_t* roles,
   if (e.n_piv)
     HC_CUDA_TRY(cudaMemcpy(e.d_piv_units, e.piv_units.data(), size_t(e.n_piv) * 4,
                            cudaMemcpyHostToDevice));
-  HC_TRY(dalloc((void**)&e.logits, size_t(np) * e.G * e.row_len * 2, &e.dev_bytes));
-  HC_TRY(dalloc((void**)&e.mref, size_t(np) * e.G * (e.row_len / 16) * 4, &e.dev_bytes));
-  HC_TRY(dalloc((void**)&e.stats, size_t(np) * e.G * 2 * 4, &e.dev_bytes));
+  // pivot score material and statistics, double-buffered by step parity: the
+  // score rows of step t run beside step t+1's attention
+  HC_TRY(dalloc((void**)&e.logits, 2 * size_t(np) * e.G * e.row_len * 2, &e.dev_bytes));
+  HC_TRY(dalloc((void**)&e.mref, 2 * size_t(np) * e.G * (e.row_len / 16) * 4, &e.dev_bytes));
+  HC_TRY(dalloc((void**)&e.stats, 2 * size_t(np) * e.G * 2 * 4, &e.dev_bytes));
   HC_TRY(dalloc((void**)&e.rowbuf, size_t(np) * e.row_len * 4, &e.dev_bytes));
   HC_TRY(dalloc((void**)&e.top_idx, size_t(np) * e.lbase * 4, &e.dev_bytes));
   HC_TRY(dalloc((void**)&e.top_cnt, size_t(np) * 4, &e.dev_bytes));
@@ -555,9 +561,10 @@ AttnParams decode_params(EngineImpl& e, int t, const void* q, void* o) {
   p.q = q;
   p.out = o;
   p.partial = e.partial;
-  p.logits = e.logits;
-  p.mref = e.mref;
-  p.stats = e.stats;
+  const size_t np = size_t(std::max(1, e.n_piv));
+  p.logits = static_cast<char*>(e.logits) + size_t(t & 1) * np * e.G * e.row_len * 2;
+  p.mref = e.mref + size_t(t & 1) * np * e.G * (e.row_len / 16);
+  p.stats = e.stats + size_t(t & 1) * np * e.G * 2;
   p.rows = e.n_piv ? e.rowbuf : nullptr;
   p.logit_stride = e.row_len;
   p.row_stride = e.row_len;
@@ -698,6 +705,8 @@ int engine_decode_begin(EngineImpl& e, int t, const void* q, const void* kn, con
   HC_CHECK_LAUNCH();
   if (ev) HC_CUDA_TRY(cudaEventRecord(ev[1], st));
   AttnParams p = decode_params(e, t, q, o);
+  // K4 overwrites the score material of parity t&1: step t-2's rows must be done
+  if (e.rows_ev[t & 1]) HC_CUDA_TRY(cudaStreamWaitEvent(st, e.rows_ev[t & 1], 0));
   p.skip = hold ? e.d_sat_flags : (land.empty() ? nullptr : e.d_skip);
   HC_TRY(launch_attn_tiles(e.tmK, e.tmV, p, active_tiles(e, t), st));
   e.in_step = t;
@@ -735,26 +744,34 @@ int engine_decode_end(EngineImpl& e, int t, cudaStream_t st) {
   }
   e.cur_land.clear();
   cudaEvent_t* ev = e.cur_ev;
-  // the previous step's monitor (own stream) must be done with the rows
-  if (e.step_end) HC_CUDA_TRY(cudaStreamWaitEvent(st, e.step_end, 0));
-  HC_TRY(launch_attn_post(e.cur_p, e.d_piv_units, e.n_piv, st, ev ? ev + 2 : nullptr));
+  if (ev) HC_CUDA_TRY(cudaEventRecord(ev[2], st));
+  HC_TRY(launch_combine(e.cur_p, st));  // O: the step's output
+  if (ev) HC_CUDA_TRY(cudaEventRecord(ev[3], st));
   e.last_t = t;
   if (!e.step_end)
     HC_CUDA_TRY(cudaEventCreateWithFlags(&e.step_end, cudaEventDisableTiming));
   if (e.n_piv) {
-    // K1+K2: top-l_base threshold and |top & K_base| per pivot (engine.py:305-311);
-    // counts land directly in the overlap ring row of this step.  Nothing in
-    // the next step's attention depends on it, so it runs on its own stream
-    // beside that attention; readers (overlaps, fire, the next score rows)
-    // wait for step_end.
+    // Score rows and the K1+K2 monitor (top-l_base threshold and |top & K_base|
+    // per pivot, engine.py:305-311; counts land in the overlap ring row of the
+    // step) feed only the drift decision, so they run on their own stream
+    // beside the next step's attention.  Readers (overlaps, fire, measure,
+    // pivot_row) wait for step_end; the attention two steps later waits for
+    // this step's rows before it overwrites the score material of its parity.
     if (!e.rows_done)
       HC_CUDA_TRY(cudaEventCreateWithFlags(&e.rows_done, cudaEventDisableTiming));
     HC_CUDA_TRY(cudaEventRecord(e.rows_done, st));
     HC_CUDA_TRY(cudaStreamWaitEvent(e.mon, e.rows_done, 0));
+    HC_TRY(launch_score_rows(e.cur_p, e.d_piv_units, e.n_piv, e.mon));
+    cudaEvent_t& re = e.rows_ev[t & 1];
+    if (!re) HC_CUDA_TRY(cudaEventCreateWithFlags(&re, cudaEventDisableTiming));
+    HC_CUDA_TRY(cudaEventRecord(re, e.mon));
+    if (ev) HC_CUDA_TRY(cudaEventRecord(ev[4], e.mon));
     HC_TRY(launch_monitor(e.rowbuf, e.row_len, e.d_piv_slots, e.n_piv, uint32_t(e.L + t),
                           uint32_t(e.lbase), e.kbase, e.words, e.thr,
                           e.ovl_ring + size_t(t % kRing) * e.n_piv, e.mon,
                           e.ghist + size_t(t & 1) * e.n_piv * 8192));
+  } else if (ev) {
+    HC_CUDA_TRY(cudaEventRecord(ev[4], st));
   }
   cudaStream_t ms = e.n_piv ? e.mon : st;
   if (ev) {
@@ -1808,6 +1825,7 @@ extern "C" int hc_engine_read_indices(hc_engine* eng, int32_t kind, int32_t id, 
     const int s = e.piv_slot[id];
     list = e.top_idx + size_t(s) * e.lbase;
     cnt = e.top_cnt + s;
+    if (e.step_end) HC_CUDA_TRY(cudaStreamWaitEvent(st, e.step_end, 0));  // rows on `mon`
     if (e.last_t > 0) {  // the monitor keeps only a threshold: materialise the set
       hc_topk_job jb{};
       jb.scores = e.rowbuf + size_t(s) * e.row_len;
@@ -1841,6 +1859,8 @@ extern "C" int hc_engine_pivot_row(hc_engine* eng, int32_t pivot_unit, int32_t s
   auto& e = eng->e;
   HC_REQUIRE(pivot_unit >= 0 && pivot_unit < e.n_units && e.piv_slot[pivot_unit] >= 0,
              HC_EINVAL, "not a monitored pivot");
+  // the rows are written on the monitor stream
+  if (e.step_end) HC_CUDA_TRY(cudaStreamWaitEvent((cudaStream_t)stream, e.step_end, 0));
   HC_CUDA_TRY(cudaMemcpyAsync(dst, e.rowbuf + size_t(e.piv_slot[pivot_unit]) * e.row_len,
                               size_t(e.L + step) * 4, cudaMemcpyDeviceToDevice,
                               (cudaStream_t)stream));

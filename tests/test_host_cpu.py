@@ -190,3 +190,19 @@ def test_policy_spec_mirrors_reference_rules():
         compare([rep("static_topk", [1.0], 40.0), rep("sink_window", [1.0], 80.0)])
     with pytest.raises(EvaluationError):
         compare([rep("static_topk", [1.0], 40.0), rep("heterocache", [1.0], 40.0, sha="y")])
+
+
+def test_library_has_no_unresolved_internal_symbols():
+    """Every hc:: function the translation units call is defined in the library
+    (a missing definition would only surface as a dlopen failure on the GPU box)."""
+    import shutil
+    import subprocess
+
+    from paper_2601_13684_b200 import _lib
+
+    if not shutil.which("nm"):
+        pytest.skip("nm not available")
+    out = subprocess.run(["nm", "-D", "--undefined-only", str(_lib.LIB_PATH)],
+                         capture_output=True, text=True, check=True).stdout
+    missing = [ln.split()[-1] for ln in out.splitlines() if "_ZN2hc" in ln]
+    assert not missing, missing
