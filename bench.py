@@ -15,8 +15,13 @@ N=1 default workload is cfg3 (Qwen2.5-7B-shaped, 128K context, batch 4, 5%
 compressed-head budget): the largest BASELINE.json config whose satellite
 host pool (15 GB pinned) and resident cache fit one B200 box comfortably.
 For N>1 (torchrun, one rank per GPU) every rank runs its own batch of the
-same workload (weak scaling, no data-path collective: sequences are
-independent); value = all ranks' steps / max-over-ranks time.
+same workload (--shard sequences, the default: weak scaling, no data-path
+collective -- sequences are independent); value = all ranks' steps /
+max-over-ranks time.  --shard units splits ONE batch's (sequence, layer,
+cluster-or-loner) units over the ranks (strong scaling, parallel.assign_units):
+boundary fires are exchanged so completion steps stay the reference's
+(parallel.order_fires), and the e2e loop all-gathers the per-shard outputs
+over NCCL into the full O before its D2H.
 
 --impl reference times the reference algorithm's CPU restatement (the
 oracle port: fp32 attention over the same resident sets + the reference
@@ -62,6 +67,9 @@ def parse():
                          "sink_window at the heterocache plan's budget rho")
     ap.add_argument("--obs-window", type=int, default=0,
                     help="prefill observation window (0: min(32, 128 // G))")
+    ap.add_argument("--shard", choices=("sequences", "units"), default="sequences",
+                    help="N>1: sequences = every rank its own batch (weak); units = one batch's "
+                         "units bin-packed over the ranks (strong)")
     ap.add_argument("--link-mib-per-step", type=float, default=0.0,
                     help="EngineConfig.transfer_bandwidth in MiB per decode step (host link "
                          "model); 0: the workload's measured-link value")
@@ -162,6 +170,17 @@ def run_b200(args, rank, world):
     obs = args.obs_window or max(1, min(32, 128 // m.group))  # w_obs = 32 (Llama)
     dkw = dict(batch=w.batch, group=m.group, max_decode=T, chunk=args.chunk, host_pool=True,
                track_sets=False, obs_window=obs)
+    units_mode = args.shard == "units" and world > 1
+    owned_all = None
+    if units_mode:
+        import torch.distributed as dist
+
+        from paper_2601_13684_b200.parallel import FireExchange, assign_units
+
+        if plan is None:
+            raise SystemExit("--shard units supports the heterocache and full policies")
+        owned_all = assign_units(tax, plan, w.batch, world, T)
+        dkw.update(owned=owned_all[rank], exchange=FireExchange(dist.new_group(backend="gloo")))
     if plan is None:  # static baseline policy at the heterocache budget (evaluation.py:198-228)
         from paper_2601_13684_b200.evaluation import PolicySpec, policy_decoder
 
@@ -172,7 +191,7 @@ def run_b200(args, rank, world):
     else:
         dec = HeteroCacheDecoder(tax, plan, cfg, **dkw)
     gen = SyntheticKV(m, batch=w.batch, prefill_len=w.prefill_len, num_layers=w.num_layers,
-                      hot=hplan.l_base_int, seed=20261018 + 3 + rank)
+                      hot=hplan.l_base_int, seed=20261018 + 3 + (0 if units_mode else rank))
     t0 = time.time()
     for l in range(w.num_layers):
         k, v, q = gen.layer_kv(l, obs)
@@ -252,6 +271,14 @@ def run_b200(args, rank, world):
     copy = torch.cuda.Stream()
     mk = lambda: torch.cuda.Event(enable_timing=False)  # noqa: E731
     ev_in, ev_used, ev_out = [mk(), mk()], [mk(), mk()], [mk(), mk()]
+    if units_mode:  # the job's result is the full O: NCCL all-gather of the shards' outputs
+        import torch.distributed as dist
+
+        gath = torch.empty((world,) + tuple(out.shape), dtype=out.dtype, device=out.device)
+        own_q = torch.as_tensor(owned_all, device=out.device).repeat_interleave(m.group, dim=3)
+        src_rank = own_q.long().argmax(dim=0)  # [B, NL, Hq]: the rank holding each query row
+        bi, li, hi = torch.meshgrid(*(torch.arange(n, device=out.device) for n in src_rank.shape),
+                                    indexing="ij")
     h2d = hq_all[0].numel() * hq_all[0].element_size() + sum(
         x.numel() * x.element_size() for x in hkv[0])
     d2h = hout[0].numel() * hout[0].element_size()
@@ -277,7 +304,12 @@ def run_b200(args, rank, world):
             upload(t + 1, 1 - slot)
         stream.wait_event(ev_in[slot])
         stream.wait_event(ev_out[slot])  # previous download of this output slot finished
-        dec.decode_step(t, *dbuf[slot], obuf[slot], rows=False)
+        if units_mode:
+            dec.decode_step(t, *dbuf[slot], gath[rank], rows=False)
+            dist.all_gather_into_tensor(gath, gath[rank])
+            obuf[slot].copy_(gath[src_rank, bi, li, hi])
+        else:
+            dec.decode_step(t, *dbuf[slot], obuf[slot], rows=False)
         ev_used[slot].record(stream)
         with torch.cuda.stream(copy):
             copy.wait_event(ev_used[slot])
@@ -301,10 +333,22 @@ def run_b200(args, rank, world):
     if world > 1:
         from paper_2601_13684_b200.parallel import max_over_ranks
         ms, ms_e2e = max_over_ranks([ms, ms_e2e], device="cuda")
+    jobs = world  # batches decoded per step by the whole job
+    own_rows = (rows_first + rows_last) / 2.0  # this rank's (K4 bytes per launch)
+    if units_mode:  # one batch over all ranks: its resident rows and fires are the ranks' sum
+        import torch.distributed as dist
+
+        tot = torch.tensor([rows_first, rows_last, events, exposed], dtype=torch.float64,
+                           device="cuda")
+        dist.all_reduce(tot)
+        rows_first, rows_last, events, exposed = (int(x) for x in tot.tolist())
+        jobs = 1
 
     rows_avg = (rows_first + rows_last) / 2.0
     step_bytes = algorithmic_bytes(int(rows_avg), w.batch, w.num_layers, m.q_heads)
-    attn_bytes = rows_avg * 2 * m.head_dim * 2 + w.batch * w.num_layers * m.q_heads * m.head_dim * 2 * 2
+    # the dominant kernel's bytes per launch: this rank's own resident rows
+    q_rows = int(dec.owned.sum()) * m.group if units_mode else w.batch * w.num_layers * m.q_heads
+    attn_bytes = own_rows * 2 * m.head_dim * 2 + q_rows * m.head_dim * 2 * 2
     # K4 phase minus the residual landing waits recorded inside it (a landing
     # step runs K4 on the other units, waits for its gathers, then the rest)
     attn_avg_ms = max(0.0, attn_ms - retr["landing_stall_ms"]) / max(1, attn_n)
@@ -312,18 +356,18 @@ def run_b200(args, rank, world):
     achieved = attn_bytes / (attn_avg_ms * 1e-3) / 1e9 if attn_avg_ms > 0 else 0.0
     traffic = None
     tf = ROOT / "profiles" / f"traffic_{args.workload}.json"
-    if tf.exists() and args.policy == "heterocache":
+    if tf.exists() and args.policy == "heterocache" and not units_mode:
         traffic = json.loads(tf.read_text()).get("dram_bytes_per_launch")
     res = {
         "metric": METRIC,
-        "value": world * K / (ms * 1e-3),
+        "value": jobs * K / (ms * 1e-3),
         "unit": "steps/s",
         "n_gpus": world,
         "steps": K,
         "warmup": W,
         "ms_per_step": ms / K,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if units_mode else "weak",
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic: seeded bf16 K/V/Q with planted per-cluster hot sets and topic shifts",
@@ -340,11 +384,14 @@ def run_b200(args, rank, world):
             "split_k_chunk": args.chunk, "start_step": S0,
             "transfer_bandwidth_bytes_per_step": cfg.transfer_bandwidth,
             "l2": f"inputs larger than L2: {step_bytes / 1e9:.2f} GB of resident K/V read per step",
-            "parallelism": f"replicas x{world} (weak: each GPU decodes its own batch)",
+            "parallelism": (f"units x{world} (strong: one batch's (sequence, layer, cluster) "
+                            f"units bin-packed over the GPUs, fire exchange at boundaries, "
+                            f"NCCL all-gather of O in the e2e loop)") if units_mode else
+                           f"replicas x{world} (weak: each GPU decodes its own batch)",
         },
-        "hbm_gbs_step": step_bytes / (ms / K * 1e-3) / 1e9,
+        "hbm_gbs_step": jobs * step_bytes / (ms / K * 1e-3) / 1e9,
         "algorithmic_bytes_per_step": int(step_bytes),
-        "e2e": {"value": world * K / (ms_e2e * 1e-3), "unit": "steps/s",
+        "e2e": {"value": jobs * K / (ms_e2e * 1e-3), "unit": "steps/s",
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "kernel": "attn_tiles_kernel (K4)",

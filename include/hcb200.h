@@ -201,6 +201,16 @@ typedef struct hc_engine_desc {
  * (same layer, profiling.py:237-239), -1 otherwise. */
 int hc_engine_create(const hc_engine_desc* desc, const int32_t* roles, const int32_t* lengths,
                      const int32_t* cluster_pivot, hc_engine** out);
+/* Sharded store (units are (sequence, layer, cluster-or-loner
+ * head)): owned is a [batch * num_layers * kv_heads] host array, unit
+ * u = (b * num_layers + l) * kv_heads + h; units with owned[u] == 0 belong to
+ * another rank and get no rows, no tiles, no append and no output (O rows of
+ * absent units are left untouched).  A satellite must be owned together with
+ * its pivot (it is refilled from the pivot's row, engine.py:326-329).  Measure
+ * mode needs an unsharded engine.  owned == NULL: hc_engine_create. */
+int hc_engine_create_sharded(const hc_engine_desc* desc, const int32_t* roles,
+                             const int32_t* lengths, const int32_t* cluster_pivot,
+                             const uint8_t* owned, hc_engine** out);
 int hc_engine_destroy(hc_engine* eng);
 /* device bytes, pinned host bytes, arena rows, number of pivot units */
 int hc_engine_info(const hc_engine* eng, int64_t* out4);

@@ -62,6 +62,7 @@ def _declare(lib):
         "hc_gram_from_sets": (i32, [vp, vp, i32, i32, i32, i32, vp, vp]),
         "hc_trace_recall": (i32, [vp, i32, u32, C.c_uint64, u32, u32, u32, u32, vp, vp]),
         "hc_engine_create": (i32, [vp, vp, vp, vp, vp]),
+        "hc_engine_create_sharded": (i32, [vp, vp, vp, vp, vp, vp]),
         "hc_engine_destroy": (i32, [vp]),
         "hc_engine_info": (i32, [vp, vp]),
         "hc_engine_prefill_layer": (i32, [vp, i32, vp, vp, vp, vp]),

@@ -318,6 +318,7 @@ __global__ void __launch_bounds__(128) combine_kernel(const AttnParams p) {
   __shared__ float wm[4], wl[4];
   __shared__ __align__(16) float racc[4][128];
   const UnitDesc u = p.units[blockIdx.x];
+  if (u.kind == kUnitAbsent) return;  // owned by another shard
   const int g = blockIdx.y;
   const int G = p.group;
   const int n = unit_slots(u, p.t, p.L, p.chunk);

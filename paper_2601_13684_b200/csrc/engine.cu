@@ -70,6 +70,7 @@ __global__ void append_kernel(const UnitDesc* __restrict__ units, int n_units, i
   const int lane = threadIdx.x & 31;
   if (u >= n_units) return;
   const UnitDesc d = units[u];
+  if (d.kind == kUnitAbsent) return;
   const int64_t row = d.kind == kUnitFull ? d.row0 + L + t - 1 : d.app_row + t - 1;
   // 256 B per row = 16 x uint4; lanes 0-15 move K, 16-31 move V
   if (lane < 16) {
@@ -124,6 +125,8 @@ struct EngineImpl {
   int n_units = 0;
   int64_t dev_bytes = 0, host_bytes = 0;
   std::vector<int32_t> role, length, cpivot;
+  std::vector<uint8_t> owned;  // per unit: 0 = absent (another shard's)
+  int n_absent = 0;
   std::vector<UnitDesc> units;
   UnitDesc* d_units = nullptr;
   int64_t rows = 0;
@@ -214,7 +217,7 @@ struct EngineImpl {
   std::deque<std::tuple<size_t, size_t, cudaEvent_t>> stage_busy;  // (lo, hi, copy done)
   cudaStream_t retr = nullptr;
   // per-step phase timeline (bench roofline): 7 events per step: start |
-  // append | K4 | combine | score rows (step stream) | monitor (its own
+  // append | K4 | combine (step stream) | score rows | monitor (monitor
   // stream) | end (step stream)
   static constexpr int kPhaseEvents = 7;
   bool timing = false;
@@ -320,7 +323,7 @@ int engine_destroy(EngineImpl& e) {
 }
 
 int engine_create(EngineImpl& e, const hc_engine_desc& c, const int32_t* roles,
-                  const int32_t* lengths, const int32_t* cpiv) {
+                  const int32_t* lengths, const int32_t* cpiv, const uint8_t* owned) {
   HC_REQUIRE(c.head_dim == kHeadDim, HC_EINVAL, "head_dim must be 128");
   HC_REQUIRE(c.group >= 1 && c.group <= 8, HC_EINVAL, "group must be 1..8");
   HC_REQUIRE(c.batch >= 1 && c.num_layers >= 1 && c.kv_heads >= 1, HC_EINVAL, "bad geometry");
@@ -358,6 +361,20 @@ int engine_create(EngineImpl& e, const hc_engine_desc& c, const int32_t* roles,
     }
   }
   e.n_units = e.B * LH;
+  // sharded engines: units another rank owns are absent; a
+  // satellite always lives with its pivot (it is refilled from the pivot's
+  // row, engine.py:326-329)
+  e.owned.assign(e.n_units, 1);
+  if (owned) {
+    for (int u = 0; u < e.n_units; ++u) e.owned[u] = owned[u] ? 1 : 0;
+    for (int u = 0; u < e.n_units; ++u) {
+      const int i = u % LH;
+      if (e.role[i] != HC_ROLE_SATELLITE) continue;
+      const int pu = (u / e.H) * e.H + e.cpivot[i];
+      HC_REQUIRE(e.owned[u] == e.owned[pu], HC_EINVAL,
+                 "unit %d: a satellite must be owned together with its pivot", u);
+    }
+  }
   e.units.resize(e.n_units);
   e.cap.assign(e.n_units, 0);
   e.buf_row0.assign(e.n_units, -1);
@@ -388,7 +405,10 @@ int engine_create(EngineImpl& e, const hc_engine_desc& c, const int32_t* roles,
     d.pivot_slot = -1;
     d.slot0 = slot;
     const bool full = e.role[i] == HC_ROLE_VOLATILE || e.role[i] == HC_ROLE_PIVOT;
-    if (full) {
+    if (!e.owned[u]) {
+      d.kind = kUnitAbsent;
+      ++e.n_absent;
+    } else if (full) {
       d.kind = kUnitFull;
       d.row0 = row;
       d.app_row = row + e.L;
@@ -1103,6 +1123,7 @@ int engine_prefill_layer(EngineImpl& e, int layer, const __nv_bfloat16* k,
     const int b = i / e.H, h = i % e.H;
     const int u = (b * e.NL + layer) * e.H + h;
     const int r = e.role[layer * e.H + h];
+    if (!e.owned[u]) continue;
     hc_topk_job j{};
     j.scores = rows + size_t(i) * Lp;
     j.n = uint32_t(e.L);
@@ -1149,6 +1170,7 @@ int engine_prefill_layer(EngineImpl& e, int layer, const __nv_bfloat16* k,
     const __nv_bfloat16* sk = k + size_t(i) * e.L * kHeadDim;
     const __nv_bfloat16* sv = v + size_t(i) * e.L * kHeadDim;
     const UnitDesc& d = e.units[u];
+    if (d.kind == kUnitAbsent) continue;
     if (d.kind == kUnitFull) {
       HC_CUDA_TRY(cudaMemcpyAsync(e.K + size_t(d.row0) * kHeadDim, sk, rowb * e.L,
                                   cudaMemcpyDeviceToDevice, st));
@@ -1490,6 +1512,8 @@ __global__ void bitmaps_kernel(const BitmapJob* __restrict__ jobs, int words) {
 }
 
 int engine_enable_measure(EngineImpl& e, int recall_topk) {
+  HC_REQUIRE(e.n_absent == 0, HC_EINVAL,
+             "measure mode needs every head of every sequence (unsharded engine)");
   HC_REQUIRE(recall_topk >= 1, HC_EINVAL, "recall_topk must be >= 1");
   HC_REQUIRE(!e.rec_k && e.pf_layers == 0, HC_ESTATE, "enable measure once, before prefill");
   const int nm = e.NL * e.B * e.H;
@@ -1640,12 +1664,18 @@ int engine_measure(EngineImpl& e, int t, const void* q, double* recall_out, cuda
 extern "C" int hc_engine_create(const hc_engine_desc* desc, const int32_t* roles,
                                 const int32_t* lengths, const int32_t* cluster_pivot,
                                 hc_engine** out) {
+  return hc_engine_create_sharded(desc, roles, lengths, cluster_pivot, nullptr, out);
+}
+
+extern "C" int hc_engine_create_sharded(const hc_engine_desc* desc, const int32_t* roles,
+                                        const int32_t* lengths, const int32_t* cluster_pivot,
+                                        const uint8_t* owned, hc_engine** out) {
   HC_REQUIRE(desc && roles && lengths && cluster_pivot && out, HC_EINVAL,
              "hc_engine_create: null argument");
   *out = nullptr;
   hc_engine* h = new (std::nothrow) hc_engine();
   HC_REQUIRE(h, HC_ENOMEM, "out of host memory");
-  const int rc = hc::engine_create(h->e, *desc, roles, lengths, cluster_pivot);
+  const int rc = hc::engine_create(h->e, *desc, roles, lengths, cluster_pivot, owned);
   if (rc != HC_OK) {
     hc::engine_destroy(h->e);
     delete h;
@@ -1880,6 +1910,7 @@ extern "C" int hc_engine_resident_rows(hc_engine* eng, int32_t step, int64_t* ro
   int64_t total = 0;
   for (const auto& d : u) {
     if (d.kind == hc::kUnitFull) total += int64_t(e.L) + step;
+    else if (d.kind == hc::kUnitAbsent) continue;
     else total += int64_t(d.n_prefix) - hc::tail_lo(d.tail_mask, step, e.R) + step;
   }
   *rows_out = total;
@@ -1909,12 +1940,12 @@ extern "C" int hc_engine_timing(hc_engine* eng, int32_t enable, double* phase_ms
       const cudaEvent_t* ev = e.tev.data() + i * P;
       HC_CUDA_TRY(cudaEventSynchronize(ev[P - 1]));
       HC_CUDA_TRY(cudaEventSynchronize(ev[5]));
-      // append | attention | combine | score rows on the step's stream; the
-      // monitor (ev4 -> ev5) on its own stream beside the next step; tail =
-      // the step stream after the score rows (ev4 -> ev6)
+      // append | attention | combine on the step's stream; score rows (ev3 ->
+      // ev4) and the monitor (ev4 -> ev5) on the monitor stream beside the next
+      // step; tail = the step stream after the combine (ev3 -> ev6)
       for (int k = 1; k < P; ++k) {
         float ms = 0;
-        HC_CUDA_TRY(cudaEventElapsedTime(&ms, ev[k < 6 ? k - 1 : 4], ev[k]));
+        HC_CUDA_TRY(cudaEventElapsedTime(&ms, ev[k < 6 ? k - 1 : 3], ev[k]));
         phase_ms[k - 1] += ms;
       }
       float tot = 0;

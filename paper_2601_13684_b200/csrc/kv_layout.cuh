@@ -27,7 +27,9 @@ namespace hc {
 
 constexpr int kHeadDim = 128;
 
-enum UnitKind : int32_t { kUnitFull = 0, kUnitComp = 1 };
+// kUnitAbsent: a (sequence, layer, head) another rank owns (sharded engines,
+// hc_engine_create_sharded): no rows, no tiles, no output.
+enum UnitKind : int32_t { kUnitFull = 0, kUnitComp = 1, kUnitAbsent = 2 };
 
 struct UnitDesc {
   int64_t row0;        // full: row of position 0; comp: active prefix buffer
@@ -112,6 +114,7 @@ __host__ __device__ inline TileRange tile_range(const UnitDesc& u, uint32_t seg_
 // Number of split-K partial slots a unit uses at step t (combine side).
 __host__ __device__ inline int32_t unit_slots(const UnitDesc& u, int32_t t, int32_t L, int32_t chunk) {
   if (u.kind == kUnitFull) return (L + t + chunk - 1) / chunk;
+  if (u.kind == kUnitAbsent) return 0;
   return u.n_pchunks + (t + chunk - 1) / chunk;
 }
 

@@ -91,6 +91,7 @@ class SequenceState:
     pending: list = field(default_factory=list)       # (completion, order, sat, tid, k, event)
     raw_events: list = field(default_factory=list)    # _Event, trigger order
     cumulative_bytes: int = 0
+    ledger: list = field(default_factory=list)        # (completion, bytes) of every event, all ranks
     order: int = 0
     dyn_count: dict = field(default_factory=dict)     # compressed head -> |dynamic|
     dyn_sets: dict = field(default_factory=dict)      # compressed head -> sorted positions
@@ -102,7 +103,7 @@ class SequenceState:
         return [e.record() for e in self.raw_events]
 
     def bytes_in_flight(self, step: int) -> int:
-        return sum(e.transfer_bytes for e in self.raw_events if e.completion_step > step)
+        return sum(n for c, n in self.ledger if c > step)
 
 
 class HeteroCacheDecoder:
@@ -110,7 +111,11 @@ class HeteroCacheDecoder:
                  group: int, max_decode: int, head_dim: int = 128, chunk: int = 1024,
                  host_pool: bool = True, bytes_per_kv_entry: int | None = None,
                  track_sets: bool = True, obs_window: int = 1, overlap_decisions: bool = True,
-                 recall_topk: int = 0):
+                 recall_topk: int = 0, owned=None, exchange=None):
+        """owned: optional [batch, layers, kv_heads] bool mask of the units this
+        rank holds (parallel.assign_units; None = all).  exchange: the fire
+        exchange of a unit-sharded run (parallel.FireExchange); every rank of
+        the run must step in lockstep, since boundary decisions all_gather."""
         _lib.require_cuda()
         self.lib = _lib.load()
         self.taxonomy, self.plan, self.config = taxonomy, plan, config
@@ -146,9 +151,28 @@ class HeteroCacheDecoder:
                                host_pool=int(host_pool), obs_window=obs_window)
         self.W = obs_window
         h = C.c_void_p()
-        _lib.check(self.lib.hc_engine_create(C.byref(desc), roles.ctypes.data, lengths.ctypes.data,
-                                             cpiv.ctypes.data, C.byref(h)))
+        if owned is None:
+            self.owned = np.ones((batch, self.NL, self.H), dtype=bool)
+            _lib.check(self.lib.hc_engine_create(C.byref(desc), roles.ctypes.data,
+                                                 lengths.ctypes.data, cpiv.ctypes.data, C.byref(h)))
+        else:
+            self.owned = np.ascontiguousarray(np.asarray(owned, dtype=bool).reshape(
+                batch, self.NL, self.H))
+            om = self.owned.astype(np.uint8)
+            _lib.check(self.lib.hc_engine_create_sharded(C.byref(desc), roles.ctypes.data,
+                                                         lengths.ctypes.data, cpiv.ctypes.data,
+                                                         om.ctypes.data, C.byref(h)))
         self.handle = h
+        if exchange is None:
+            from .parallel import LocalExchange
+
+            exchange = LocalExchange()
+        self.exchange = exchange
+        # per sequence: the heads / pivots this rank holds (all of them unsharded)
+        own = self.owned
+        self.full_of = [[hd for hd in sorted(self.full) if own[b][hd]] for b in range(batch)]
+        self.comp_of = [[hd for hd in self.comp if own[b][hd]] for b in range(batch)]
+        self.piv_of = [[p for p in self.pivots if own[b][p]] for b in range(batch)]
         # measure mode (recall at scale): every head's top-recall_topk records per step
         self.recall_topk = recall_topk
         self.record_k = max([recall_topk, self.l_base_int if self.monitor else 0] +
@@ -159,12 +183,12 @@ class HeteroCacheDecoder:
         _lib.check(self.lib.hc_engine_info(self.handle, info))
         self.device_bytes, self.host_bytes, self.arena_rows, self.n_pivot_units = list(info)
         # pivot slot order == ascending unit order
-        self.pivot_units = [self.unit(b, p) for b in range(self.B) for p in self.pivots] \
+        self.pivot_units = [self.unit(b, p) for b in range(self.B) for p in self.piv_of[b]] \
             if self.monitor else []
         self.pivot_units.sort()
         self.pivot_slot = {u: i for i, u in enumerate(self.pivot_units)}
         self.states = [SequenceState() for _ in range(self.B)]
-        self._cols = [[self.pivot_slot[self.unit(b, p)] for p in self.pivots] if self.monitor
+        self._cols = [[self.pivot_slot[self.unit(b, p)] for p in self.piv_of[b]] if self.monitor
                       else [] for b in range(self.B)]
         self._pinned = None
         self._pin_head = 0
@@ -241,22 +265,22 @@ class HeteroCacheDecoder:
         if len(self._prefilled) != self.NL:
             raise EngineError("prefill every layer before decoding")
         for b, st in enumerate(self.states):
-            for hd in self.comp:
+            for hd in self.comp_of[b]:
                 k = self.effective_length(hd)
                 st.dyn_count[hd] = min(k, self.L)
                 if self.track_sets:
                     st.dyn_sets[hd] = self.dynamic_set(b, hd)
             if self.monitor:
-                for p in self.pivots:
+                for p in self.piv_of[b]:
                     st.buffers[p] = []
         rec = self._measure(0, None)
         for b, st in enumerate(self.states):
-            st.rows.append(self._row(st, 0, 0, self._row_sizes(st, 0, rec[b])))
+            st.rows.append(self._row(st, 0, 0, self._row_sizes(b, 0, rec[b])))
         if self.monitor:  # pinned landing zone for fetched sets: every satellite firing at once
             import torch
 
-            cap = sum(self.effective_length(s) for p in self.pivots
-                      for s in self.satellites_of[p]) * self.B
+            cap = sum(self.effective_length(s) for b in range(self.B) for p in self.piv_of[b]
+                      for s in self.satellites_of[p])
             self._pinned = torch.empty(max(4 * cap, 1 << 16), dtype=torch.int32,
                                        pin_memory=True)  # four full drift bursts
             self._pin_head = 0
@@ -273,10 +297,15 @@ class HeteroCacheDecoder:
         inter = int(np.isin(np.fromiter(extras, dtype=np.int64, count=len(extras)), dyn).sum())
         return len(dyn) + len(extras) - inter + t
 
-    def _row_sizes(self, st: SequenceState, t: int, recall: float = math.nan):
-        charged = len(self.full) * self.L + sum(st.dyn_count.values())
+    def _row_sizes(self, b: int, t: int, recall: float = math.nan):
+        """(charged, extra, recall) of sequence b at step t over the heads this
+        rank holds (engine.py:276-288); a unit-sharded run adds the ranks'
+        partials (parallel.merge_reports)."""
+        st = self.states[b]
+        nf = len(self.full_of[b])
+        charged = nf * self.L + sum(st.dyn_count.values())
         if self.track_sets:
-            total = len(self.full) * (self.L + t) + sum(self._size_of(st, hd, t) for hd in self.comp)
+            total = nf * (self.L + t) + sum(self._size_of(st, hd, t) for hd in self.comp_of[b])
             extra = total - charged
         else:
             extra = -1
@@ -305,8 +334,8 @@ class HeteroCacheDecoder:
                                                       _lib.stream_handle()))
         return idx, sc
 
-    def _row(self, st: SequenceState, t: int, flag: int, sizes=None) -> StepRow:
-        charged, extra, recall = sizes if sizes is not None else self._row_sizes(st, t)
+    def _row(self, st: SequenceState, t: int, flag: int, sizes) -> StepRow:
+        charged, extra, recall = sizes
         return StepRow(step=t, recall=recall, gpu_entries=charged, extra_entries=extra,
                        bytes_in_flight=st.bytes_in_flight(t), cumulative_bytes=st.cumulative_bytes,
                        retrieval_flag=flag)
@@ -361,13 +390,13 @@ class HeteroCacheDecoder:
         boundary = self.monitor and (cfg.eval_every_step or t % cfg.window == 0)
         if boundary:
             first = t if cfg.eval_every_step else max(1, t - cfg.window + 1)
-            self._open = (t, first, [self._row_sizes(st, t, rec[b])
-                                     for b, st in enumerate(self.states)] if rows else None)
+            self._open = (t, first, [self._row_sizes(b, t, rec[b])
+                                     for b in range(self.B)] if rows else None)
             if not self.overlap_decisions:
                 self._close_decision(sh)
         elif rows:
             for b, st in enumerate(self.states):
-                st.rows.append(self._row(st, t, 0, self._row_sizes(st, t, rec[b])))
+                st.rows.append(self._row(st, t, 0, self._row_sizes(b, t, rec[b])))
 
     def _close_decision(self, sh) -> None:
         t, first, sizes = self._open
@@ -389,20 +418,25 @@ class HeteroCacheDecoder:
         Boundary mode: the buffers hold exactly this window's values (they are
         cleared at every boundary), so medians are one np.median over axis 0
         (same partition + mean-of-middle-pair arithmetic as the reference's
-        per-list np.median).  Sliding mode keeps per-pivot lists.
+        per-list np.median).  Sliding mode keeps per-pivot lists.  The fires of
+        every rank (one rank unsharded) are then accounted in the reference's
+        sorted pivot order per sequence (parallel.order_fires).
         """
+        from .parallel import order_fires
+
         cfg = self.config
         n = t - first + 1
         counts = np.empty((n, len(self.pivot_units)), dtype=np.int32)
         _lib.check(self.lib.hc_engine_overlaps(self.handle, first, t, counts.ctypes.data, sh))
         vals = counts / self.l_base_int  # float64, == int / int in Python
-        fire_units, fire_done = [], []
         med = None if cfg.eval_every_step else window_median(vals) < cfg.tau_drift
+        local = []  # (b, pivot, sats, ks, bytes) in (b, sorted pivot) order
         for b, st in enumerate(self.states):
             cols = self._cols[b]
+            pivs = self.piv_of[b]
             if cfg.eval_every_step:
                 fired_mask = []
-                for j, p in enumerate(self.pivots):
+                for j, p in enumerate(pivs):
                     buf = st.buffers[p]
                     buf.extend(vals[:, cols[j]].tolist())
                     fired = len(buf) >= cfg.window and \
@@ -412,21 +446,32 @@ class HeteroCacheDecoder:
                     fired_mask.append(fired)
             else:
                 fired_mask = med[cols].tolist()
-            for j, p in enumerate(self.pivots):
-                if not fired_mask[j]:
-                    continue
-                flags[b] = 1
-                sats = self.satellites_of[p]
-                ks = [min(self.effective_length(s), self.L + t) for s in sats]
-                nbytes = sum(ks) * self.bytes_per_entry
-                st.cumulative_bytes += nbytes
-                done = completion_step(t, st.cumulative_bytes, cfg)
-                ev = _Event(trigger_step=t, pivot=p, completion_step=done, transfer_bytes=nbytes,
-                            sats=sats, ks=ks)
-                st.raw_events.append(ev)
-                fire_units.append(self.unit(b, p))
-                fire_done.append(done)
-                self._fire_events.append((st, ev))
+            for j, p in enumerate(pivs):
+                if fired_mask[j]:
+                    sats = self.satellites_of[p]
+                    ks = [min(self.effective_length(s), self.L + t) for s in sats]
+                    local.append((b, p, sats, ks, sum(ks) * self.bytes_per_entry))
+        gathered = self.exchange.all_gather([(b, p, nb) for b, p, _, _, nb in local])
+        if not any(gathered):
+            return
+        cum = [st.cumulative_bytes for st in self.states]
+        done_of = order_fires(t, gathered, cum, cfg)
+        for b, _ in done_of:
+            flags[b] = 1
+        for b, p, n_ in sorted((b, p, n_) for part in gathered for (b, p, n_) in part):
+            self.states[b].ledger.append((done_of[(b, p)][0], n_))
+        for b, st in enumerate(self.states):
+            st.cumulative_bytes = cum[b]
+        fire_units, fire_done = [], []
+        for b, p, sats, ks, nbytes in local:
+            st = self.states[b]
+            done = done_of[(b, p)][0]
+            ev = _Event(trigger_step=t, pivot=p, completion_step=done, transfer_bytes=nbytes,
+                        sats=sats, ks=ks)
+            st.raw_events.append(ev)
+            fire_units.append(self.unit(b, p))
+            fire_done.append(done)
+            self._fire_events.append((st, ev))
         if fire_units:
             self._fire_batch(t, fire_units, fire_done, sh)
 
