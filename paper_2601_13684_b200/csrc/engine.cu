@@ -926,12 +926,14 @@ __global__ void gather_rows_batch_kernel(const XferDev* __restrict__ xs, uint4* 
 }
 
 // Retrieval gather from the pinned host pool (zero-copy over the host link).
-// A small fixed grid (kGatherCtas CTAs, one per SM at most) loops over all
-// transfers of the batch: the link needs only ~100 KB in flight, and a
-// light footprint (32 registers, no shared memory) leaves room for the two
-// attention CTAs on every SM it shares -- a large grid of high-priority
-// gather CTAs would evict attention occupancy for the whole transfer.
-constexpr int kGatherCtas = 128;
+// A small fixed grid loops over all transfers of the batch: 40 CTAs of 256
+// threads (4 x 16-B loads in flight per thread, 640 KB in all) hold the link
+// at 47-48 GB/s, and each gather CTA that shares an SM with the attention
+// slows that SM's K4.  At cfg4, where gathers run most of every step, back to
+// back on one box: 128 CTAs 993 / 802 steps/s, 40 CTAs 1211 / 1188 (cfg5
+// unchanged within noise; 24 CTAs: the link drops to 42 GB/s; more loads in
+// flight per thread or fewer threads per CTA: slower).
+constexpr int kGatherCtas = 40;
 
 __global__ void __launch_bounds__(256) gather_host_rows_kernel(const XferDev* __restrict__ xs,
                                                                int n_x, uint4* __restrict__ K,
