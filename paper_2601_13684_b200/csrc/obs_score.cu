@@ -128,6 +128,15 @@ __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// exp2 as one MUFU.EX2 (ex2.approx.ftz: max relative error 2^-22, results
+// below 2^-126 flush to 0); exp2f() adds a subnormal-range fixup per call
+// (FSETP + 2 FMUL), which the SFU-bound epilogues cannot afford.
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // Sum 32 column values over the 32 lanes (rows) of a warp -- afterwards lane c
 // holds the total of column c (halving butterfly, 31 shuffles) -- for two
 // independent 32x32 blocks, stage-interleaved so every
@@ -282,7 +291,7 @@ obs_score_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant_
           const float mb = mn == -INFINITY ? 0.f : mn;
           float s = 0.f;
 #pragma unroll
-          for (int j = 0; j < 32; ++j) s += exp2f(fmaf(v[j], p.scale_log2, -mb));
+          for (int j = 0; j < 32; ++j) s += fast_exp2(fmaf(v[j], p.scale_log2, -mb));
           l = l * exp2f(m - mb) + s;
           m = mn;
         } else {
@@ -290,11 +299,11 @@ obs_score_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant_
           const float off = -(Mr + log2L);
           if (unmasked) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = exp2f(fmaf(v[j], p.scale_log2, off));
+            for (int j = 0; j < 32; ++j) v[j] = fast_exp2(fmaf(v[j], p.scale_log2, off));
           } else {
 #pragma unroll
             for (int j = 0; j < 32; ++j)
-              v[j] = (row_ok && first + j <= qpos) ? exp2f(fmaf(v[j], p.scale_log2, off)) : 0.f;
+              v[j] = (row_ok && first + j <= qpos) ? fast_exp2(fmaf(v[j], p.scale_log2, off)) : 0.f;
           }
         }
       }
