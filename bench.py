@@ -421,6 +421,17 @@ def run_b200(args, rank, world):
     return res, w
 
 
+def cpu_model() -> str:
+    """Host CPU model name (lscpu's "Model name"), for the baseline's record."""
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 # ---------------------------------------------------------------------------
 # CPU arm (oracle port): same resident sets, fp32 attention + reference selection
 # ---------------------------------------------------------------------------
@@ -514,6 +525,7 @@ def main():
             "config": {"workload": f"{args.workload}: {w.name}", "prefill_len": w.prefill_len,
                        "batch": w.batch, "layers": w.num_layers},
             "cpu_baseline": {"value": v, "unit": "steps/s", "cores": cores, "kind": "port",
+                             "cpu_model": cpu_model(),
                              "sample": sample},
             "e2e": {"value": v, "unit": "steps/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
@@ -537,6 +549,7 @@ def main():
             tax, plan = plan_for(w)
             per_step, cores, sample, _ = cpu_step_timer(w, plan, tax, seconds=args.cpu_seconds)
             res["cpu_baseline"] = {"value": 1.0 / per_step, "unit": "steps/s", "cores": cores,
+                                   "cpu_model": cpu_model(),
                                    "kind": "port", "sample": sample}
         else:
             res["cpu_baseline"] = None
