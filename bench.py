@@ -44,6 +44,11 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "decode attn steps/sec & HBM GB/s @128K/224K ctx, 1/2/4/8 B200 vs host-CPU ref"
+# process-group backend of a multi-rank run: NCCL (one GPU per rank).  gloo is
+# only for functional tests of the multi-rank paths on a single GPU
+# (tests/test_bench_contract.py): its numbers are not measurements.
+BACKEND = os.environ.get("HC_BENCH_BACKEND", "nccl")
+COLL_DEV = "cuda" if BACKEND == "nccl" else "cpu"
 FALLBACK_HBM_GBS = 6650.0
 
 
@@ -306,7 +311,12 @@ def run_b200(args, rank, world):
         stream.wait_event(ev_out[slot])  # previous download of this output slot finished
         if units_mode:
             dec.decode_step(t, *dbuf[slot], gath[rank], rows=False)
-            dist.all_gather_into_tensor(gath, gath[rank])
+            if BACKEND == "nccl":
+                dist.all_gather_into_tensor(gath, gath[rank])
+            else:  # gloo: host copies
+                parts = list(gath.cpu().unbind(0))
+                dist.all_gather(parts, parts[rank].contiguous())
+                gath.copy_(torch.stack(parts))
             obuf[slot].copy_(gath[src_rank, bi, li, hi])
         else:
             dec.decode_step(t, *dbuf[slot], obuf[slot], rows=False)
@@ -332,14 +342,14 @@ def run_b200(args, rank, world):
                   for e in timed_ev)
     if world > 1:
         from paper_2601_13684_b200.parallel import max_over_ranks
-        ms, ms_e2e = max_over_ranks([ms, ms_e2e], device="cuda")
+        ms, ms_e2e = max_over_ranks([ms, ms_e2e], device=COLL_DEV)
     jobs = world  # batches decoded per step by the whole job
     own_rows = (rows_first + rows_last) / 2.0  # this rank's (K4 bytes per launch)
     if units_mode:  # one batch over all ranks: its resident rows and fires are the ranks' sum
         import torch.distributed as dist
 
         tot = torch.tensor([rows_first, rows_last, events, exposed], dtype=torch.float64,
-                           device="cuda")
+                           device=COLL_DEV)
         dist.all_reduce(tot)
         rows_first, rows_last, events, exposed = (int(x) for x in tot.tolist())
         jobs = 1
@@ -539,8 +549,8 @@ def main():
     _build.ensure_built()  # no-op when the in-tree library shipped with the checkout
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(local % torch.cuda.device_count())
+        dist.init_process_group(BACKEND)
     res, w = run_b200(args, rank, world)
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:

@@ -8,15 +8,26 @@ from pathlib import Path
 
 import pytest
 
+
+def _free_port():
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
 ROOT = Path(__file__).resolve().parent.parent
 KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
         "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config", "e2e",
         "cpu_baseline"}
 
 
-def _run(args, timeout=900):
-    env = dict(os.environ, HC_BENCH_NO_CLOCKS="1")
-    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), *args], capture_output=True,
+def _run(args, timeout=900, ranks=1, **env_kw):
+    env = dict(os.environ, HC_BENCH_NO_CLOCKS="1", **env_kw)
+    launch = [sys.executable, str(ROOT / "bench.py")] if ranks == 1 else [
+        sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={ranks}",
+        "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(ROOT / "bench.py")]
+    out = subprocess.run([*launch, *args], capture_output=True,
                          text=True, timeout=timeout, env=env, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-3000:]
     lines = [ln for ln in out.stdout.splitlines() if ln.strip()]
@@ -38,3 +49,16 @@ def test_b200_arm_full_line_with_cpu_baseline():
     assert KEYS <= set(d) and {"roofline", "gpu_launches", "clocks"} <= set(d)
     assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
     assert d["cpu_baseline"]["value"] > 0 and d["roofline"]["bound"] == "hbm"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shard", ["sequences", "units"])
+def test_two_rank_paths_run_end_to_end(shard):
+    """Functional check of the N>1 bench paths on one GPU: two ranks over gloo
+    (HC_BENCH_BACKEND; the driver's runs use NCCL, one GPU per rank).  Units
+    mode exercises the fire exchange and the all-gather of O; the numbers of
+    such a run are not measurements."""
+    d = _run(["--gpus", "2", "--shard", shard, "--workload", "cfg1", "--steps", "16",
+              "--warmup", "3"], ranks=2, HC_BENCH_BACKEND="gloo")
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0
+    assert d["scaling"] == ("strong" if shard == "units" else "weak")
