@@ -172,14 +172,13 @@ struct EngineImpl {
   void* logits = nullptr;  // fp16 per-token pivot material
   float *mref = nullptr, *stats = nullptr, *rowbuf = nullptr;
   uint32_t *top_idx = nullptr, *top_cnt = nullptr, *kbase = nullptr;
-  uint32_t *ovl_cur = nullptr, *ovl_ring = nullptr;
+  uint32_t* ovl_ring = nullptr;
   uint32_t* ovl_host = nullptr;     // pinned readback of the overlap window
   uint64_t* thr = nullptr;          // per pivot slot: composite-key threshold of its top set
   uint32_t* ghist = nullptr;        // [2][pivot slot][8192] first-digit key histograms of the
                                     // rows: step t's monitor fills buffer t&1 for its fires
   int32_t* d_piv_slots = nullptr;   // iota over pivot slots
   int last_t = 0;                   // last decode step run
-  hc_topk_job* d_piv_jobs = nullptr;
   // compressed units
   std::vector<int32_t> cap;               // prefix capacity per unit (0 for full)
   std::vector<int64_t> buf_row0, buf_row1;
@@ -304,7 +303,7 @@ int engine_destroy(EngineImpl& e) {
                   e.d_units, e.K, e.V, e.d_tiles, e.d_skip, e.d_sat_tiles, e.d_sat_flags,
                   e.partial, e.d_piv_units, e.logits, e.mref,
                   e.stats,
-                  e.rowbuf, e.top_idx, e.top_cnt, e.kbase, e.ovl_cur, e.ovl_ring, e.d_piv_jobs,
+                  e.rowbuf, e.top_idx, e.top_cnt, e.kbase, e.ovl_ring,
                   e.thr, e.ghist, e.d_piv_slots,
                   e.pf};
   for (void* p : ptrs)
@@ -506,7 +505,6 @@ int engine_create(EngineImpl& e, const hc_engine_desc& c, const int32_t* roles,
   HC_TRY(dalloc((void**)&e.top_idx, size_t(np) * e.lbase * 4, &e.dev_bytes));
   HC_TRY(dalloc((void**)&e.top_cnt, size_t(np) * 4, &e.dev_bytes));
   HC_TRY(dalloc((void**)&e.kbase, size_t(np) * e.words * 4, &e.dev_bytes));
-  HC_TRY(dalloc((void**)&e.ovl_cur, size_t(np) * 4, &e.dev_bytes));
   HC_TRY(dalloc((void**)&e.ovl_ring, size_t(np) * kRing * 4, &e.dev_bytes));
   HC_TRY(dalloc((void**)&e.thr, size_t(np) * 8, &e.dev_bytes));
   HC_TRY(dalloc((void**)&e.ghist, 2 * size_t(np) * 8192 * 4, &e.dev_bytes));
@@ -516,21 +514,6 @@ int engine_create(EngineImpl& e, const hc_engine_desc& c, const int32_t* roles,
     HC_TRY(dalloc((void**)&e.d_piv_slots, size_t(np) * 4, &e.dev_bytes));
     HC_CUDA_TRY(cudaMemcpy(e.d_piv_slots, iota.data(), size_t(np) * 4, cudaMemcpyHostToDevice));
   }
-  std::vector<hc_topk_job> jobs(np);
-  for (int s = 0; s < e.n_piv; ++s) {
-    hc_topk_job& j = jobs[s];
-    j.scores = e.rowbuf + size_t(s) * e.row_len;
-    j.idx = nullptr;
-    j.n = uint32_t(e.L);  // + step (n_add)
-    j.k = uint32_t(e.lbase);
-    j.out_idx = e.top_idx + size_t(s) * e.lbase;
-    j.out_count = e.top_cnt + s;
-    j.base_bitmap = e.kbase + size_t(s) * e.words;
-    j.overlap_out = e.ovl_cur + s;
-  }
-  HC_TRY(dalloc((void**)&e.d_piv_jobs, size_t(np) * sizeof(hc_topk_job), &e.dev_bytes));
-  HC_CUDA_TRY(cudaMemcpy(e.d_piv_jobs, jobs.data(), size_t(np) * sizeof(hc_topk_job),
-                         cudaMemcpyHostToDevice));
 
   // ---- compressed-unit bookkeeping buffers ----
   for (int u = 0; u < e.n_units; ++u) {
