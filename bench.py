@@ -340,6 +340,7 @@ def run_b200(args, rank, world):
     events = len(timed_ev)
     exposed = sum(max(0, e.completion_step - (e.trigger_step + cfg.update_delay_steps))
                   for e in timed_ev)
+    ref_bytes = sum(e.transfer_bytes for e in timed_ev)  # engine.py:330-333 accounting
     if world > 1:
         from paper_2601_13684_b200.parallel import max_over_ranks
         ms, ms_e2e = max_over_ranks([ms, ms_e2e], device=COLL_DEV)
@@ -348,10 +349,10 @@ def run_b200(args, rank, world):
     if units_mode:  # one batch over all ranks: its resident rows and fires are the ranks' sum
         import torch.distributed as dist
 
-        tot = torch.tensor([rows_first, rows_last, events, exposed], dtype=torch.float64,
-                           device=COLL_DEV)
+        tot = torch.tensor([rows_first, rows_last, events, exposed, ref_bytes],
+                           dtype=torch.float64, device=COLL_DEV)
         dist.all_reduce(tot)
-        rows_first, rows_last, events, exposed = (int(x) for x in tot.tolist())
+        rows_first, rows_last, events, exposed, ref_bytes = (int(x) for x in tot.tolist())
         jobs = 1
 
     rows_avg = (rows_first + rows_last) / 2.0
@@ -421,7 +422,11 @@ def run_b200(args, rank, world):
         },
         "retrieval_events_timed_run": events,
         "exposed_transfer_steps_timed_run": exposed,
+        # bytes: rows the timed loop's gathers moved over the host link (fetched set +
+        # sinks + recency tail, an upper bound); reference_accounted_bytes: what the
+        # reference charges for the timed loop's fires (fetched indices x bytes_per_kv_entry)
         "retrieval": {"host_link_gbs": retr["host_link_gbs"], "bytes": retr["bytes"],
+                      "reference_accounted_bytes_timed_run": ref_bytes,
                       "gather_ms": retr["gather_ms"], "landing_stall_ms_total": retr["landing_stall_ms"],
                       "batches": retr["batches"]},
         "prefill_seconds": prefill_s,
