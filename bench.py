@@ -239,6 +239,7 @@ def run_b200(args, rank, world):
     if not os.environ.get("HC_BENCH_NO_CLOCKS"):
         clocks.start()
     launches0 = lib.hc_launch_count()
+    dec.retrieval_stats()  # start the retrieval counters with the timed loop
     dec.kernel_timing(not os.environ.get("HC_BENCH_NO_TIMING"))
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()

@@ -1032,7 +1032,7 @@ int issue_gathers(EngineImpl& e, const std::vector<int>& ids_in, cudaEvent_t aft
       HC_CUDA_TRY(cudaEventRecord(t1, e.retr));
       e.gather_ev.emplace_back(t0, t1);
     }
-    e.gather_rows_issued += rows;
+    if (e.timing) e.gather_rows_issued += rows;  // same window as gather_ev
     HC_CUDA_TRY(cudaFreeAsync(d, e.retr));
     cudaEvent_t done;
     HC_TRY(new_event(e, &done));
