@@ -127,10 +127,16 @@ def ptr(t) -> int:
 
 
 def stream_handle(stream=None) -> int:
+    """cudaStream_t of `stream`, or of torch's current stream (raw query: the public
+    torch.cuda.current_stream() costs ~15 us per call, a quarter of a small step's host time)."""
+    if stream is not None:
+        return int(stream.cuda_stream)
     import torch
 
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return int(s.cuda_stream)
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    if raw is not None:
+        return int(raw(torch._C._cuda_getDevice()))
+    return int(torch.cuda.current_stream().cuda_stream)
 
 
 def require_cuda():
