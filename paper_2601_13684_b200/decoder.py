@@ -458,6 +458,8 @@ class HeteroCacheDecoder:
         done_of = order_fires(t, gathered, cum, cfg)
         for b, _ in done_of:
             flags[b] = 1
+        for st in self.states:  # landed transfers never count as in flight again
+            st.ledger = [(c, n_) for c, n_ in st.ledger if c > t - 1]
         for b, p, n_ in sorted((b, p, n_) for part in gathered for (b, p, n_) in part):
             self.states[b].ledger.append((done_of[(b, p)][0], n_))
         for b, st in enumerate(self.states):
