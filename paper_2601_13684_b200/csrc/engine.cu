@@ -97,6 +97,7 @@ struct Transfer {
   uint32_t* cnt = nullptr;  // [1]
   uint32_t* pos = nullptr;  // [prefix capacity]
   int32_t* meta = nullptr;  // [3]
+  int block = -1;           // the fire batch's device allocation these point into
   bool gathered = false;
   bool landed = false;
   cudaEvent_t selected = nullptr;  // caller's stream, after selection (shared per batch)
@@ -197,6 +198,14 @@ struct EngineImpl {
   // transfers by id (ids increase monotonically); a record is dropped once a
   // later landing supersedes it, so the table holds only pending transfers and
   // the ones serving a satellite right now -- bounded over any decode length
+  // one device allocation per fire batch holds every transfer's buffers (all
+  // fetched sets contiguous first: one D2H copy); freed with its last transfer
+  struct XferBlock {
+    void* ptr;
+    int refs;
+  };
+  std::unordered_map<int, XferBlock> blocks;
+  int next_block = 0;
   struct TransferTable {
     std::unordered_map<int, Transfer> m;
     int next = 0;
@@ -284,13 +293,7 @@ int engine_destroy(EngineImpl& e) {
   if (e.rows_done) cudaEventDestroy(e.rows_done);
   for (auto x : e.rows_ev)
     if (x) cudaEventDestroy(x);
-  for (auto& kv : e.xfers.m) {
-    auto& x = kv.second;
-    if (x.sel) cudaFree(x.sel);
-    if (x.cnt) cudaFree(x.cnt);
-    if (x.pos) cudaFree(x.pos);
-    if (x.meta) cudaFree(x.meta);
-  }
+  for (auto& kv : e.blocks) cudaFree(kv.second.ptr);
   for (size_t u = 0; u < e.dyn_sel.size(); ++u) {
     if (e.dyn_sel[u]) cudaFree(e.dyn_sel[u]);
     if (e.dyn_cnt[u]) cudaFree(e.dyn_cnt[u]);
@@ -1225,6 +1228,12 @@ int engine_fire_batch(EngineImpl& e, int n, const int32_t* pus, int t, const int
   std::vector<int> new_ids;
   std::vector<int32_t> slots;
   const int LH = e.NL * e.H;
+  // pass 1: the transfers (one per satellite of each firing pivot) and their sizes
+  struct Pending {
+    Transfer x;
+    int slot;
+  };
+  std::vector<Pending> pend;
   for (int f = 0; f < n; ++f) {
     const int pu = pus[f];
     HC_REQUIRE(pu >= 0 && pu < e.n_units && e.piv_slot[pu] >= 0, HC_EINVAL,
@@ -1235,30 +1244,54 @@ int engine_fire_batch(EngineImpl& e, int n, const int32_t* pus, int t, const int
     for (int h = 0; h < e.H; ++h) {
       const int j = l * e.H + h;
       if (e.role[j] != HC_ROLE_SATELLITE || e.cpivot[j] != ph) continue;
-      const int u = (b * e.NL + l) * e.H + h;
       Transfer x;
-      x.unit = u;
+      x.unit = (b * e.NL + l) * e.H + h;
       x.k = std::min(e.length[j], e.L + t);
       x.completion = completion[f];
-      HC_CUDA_TRY(cudaMallocAsync((void**)&x.sel, size_t(std::max(1, x.k)) * 4, st));
-      HC_CUDA_TRY(cudaMallocAsync((void**)&x.cnt, 4, st));
-      HC_CUDA_TRY(cudaMallocAsync((void**)&x.pos, size_t(std::max(1, e.cap[u])) * 4, st));
-      HC_CUDA_TRY(cudaMallocAsync((void**)&x.meta, 16, st));
-      if (fast) {
-        fjobs.push_back(FireJob{e.rowbuf + size_t(s) * e.row_len,
-                                e.ghist + (size_t(t & 1) * e.n_piv + s) * 8192, uint32_t(e.L + t),
-                                uint32_t(x.k), x.sel, x.cnt});
-      } else {
-        hc_topk_job jb{};
-        jb.scores = e.rowbuf + size_t(s) * e.row_len;
-        jb.n = uint32_t(e.L + t);
-        jb.k = uint32_t(x.k);
-        jb.out_idx = x.sel;
-        jb.out_count = x.cnt;
-        jobs.push_back(jb);
-      }
-      new_ids.push_back(e.xfers.add(x));
+      pend.push_back({x, s});
     }
+  }
+  // pass 2: one allocation [sel_0 .. sel_m | cnt x m | pos_0 .. pos_m | meta x m]
+  // (fetched sets contiguous in firing order: a single D2H copy below)
+  size_t n_sel = 0, n_pos = 0;
+  for (const Pending& q : pend) {
+    n_sel += size_t(std::max(1, q.x.k));
+    n_pos += (size_t(std::max(1, e.cap[q.x.unit])) + 3) & ~size_t(3);
+  }
+  const size_t m = pend.size();
+  const size_t o_cnt = (n_sel + 3) & ~size_t(3), o_pos = o_cnt + ((m + 3) & ~size_t(3));
+  const size_t o_meta = o_pos + n_pos, words_total = o_meta + 4 * m;
+  uint32_t* blk = nullptr;
+  const int block_id = e.next_block++;
+  if (m) {
+    HC_CUDA_TRY(cudaMallocAsync((void**)&blk, words_total * 4, st));
+    e.blocks[block_id] = EngineImpl::XferBlock{blk, int(m)};
+  }
+  size_t a_sel = 0, a_pos = o_pos;
+  for (size_t q = 0; q < m; ++q) {
+    Transfer& x = pend[q].x;
+    const int s = pend[q].slot;
+    x.block = block_id;
+    x.sel = blk + a_sel;
+    x.cnt = blk + o_cnt + q;
+    x.pos = blk + a_pos;
+    x.meta = reinterpret_cast<int32_t*>(blk + o_meta + 4 * q);
+    a_sel += size_t(std::max(1, x.k));
+    a_pos += (size_t(std::max(1, e.cap[x.unit])) + 3) & ~size_t(3);
+    if (fast) {
+      fjobs.push_back(FireJob{e.rowbuf + size_t(s) * e.row_len,
+                              e.ghist + (size_t(t & 1) * e.n_piv + s) * 8192, uint32_t(e.L + t),
+                              uint32_t(x.k), x.sel, x.cnt});
+    } else {
+      hc_topk_job jb{};
+      jb.scores = e.rowbuf + size_t(s) * e.row_len;
+      jb.n = uint32_t(e.L + t);
+      jb.k = uint32_t(x.k);
+      jb.out_idx = x.sel;
+      jb.out_count = x.cnt;
+      jobs.push_back(jb);
+    }
+    new_ids.push_back(e.xfers.add(x));
   }
   if (!jobs.empty()) {
     // pageable -> device copies are staged before cudaMemcpyAsync returns
@@ -1280,15 +1313,27 @@ int engine_fire_batch(EngineImpl& e, int n, const int32_t* pus, int t, const int
                                     e.kbase, e.words, st));
     HC_CUDA_TRY(cudaFreeAsync(ds, st));
   }
+  // fetched sets, in firing order, packed at k per transfer (the block pads k = 0 to 1)
   size_t off = 0;
   for (size_t q = 0; q < new_ids.size(); ++q) {
-    const Transfer& x = e.xfers[new_ids[q]];
-    if (fetched_host) {
-      HC_CUDA_TRY(cudaMemcpyAsync(fetched_host + off, x.sel, size_t(x.k) * 4,
-                                  cudaMemcpyDeviceToHost, st));
-    }
-    off += size_t(x.k);
+    off += size_t(e.xfers[new_ids[q]].k);
     ids[q] = new_ids[q];
+  }
+  if (fetched_host && m) {
+    bool packed = true;  // k >= 1 for every transfer: device and host layouts coincide
+    for (const Pending& q : pend) packed &= q.x.k >= 1;
+    if (packed) {
+      HC_CUDA_TRY(cudaMemcpyAsync(fetched_host, blk, off * 4, cudaMemcpyDeviceToHost, st));
+    } else {
+      size_t ho = 0, dof = 0;
+      for (const Pending& q : pend) {
+        if (q.x.k > 0)
+          HC_CUDA_TRY(cudaMemcpyAsync(fetched_host + ho, blk + dof, size_t(q.x.k) * 4,
+                                      cudaMemcpyDeviceToHost, st));
+        ho += size_t(q.x.k);
+        dof += size_t(std::max(1, q.x.k));
+      }
+    }
   }
   cudaEvent_t selected;
   HC_TRY(new_event(e, &selected));
@@ -1395,8 +1440,11 @@ int apply_landings(EngineImpl& e, const std::vector<int>& idv, cudaStream_t st) 
     e.active[u] = x.buf;
     if (e.dyn_owner[u] >= 0) {  // superseded records
       Transfer& old = e.xfers[e.dyn_owner[u]];
-      for (void* ptr : {(void*)old.sel, (void*)old.cnt, (void*)old.pos, (void*)old.meta})
-        HC_CUDA_TRY(cudaFreeAsync(ptr, st));
+      auto bl = e.blocks.find(old.block);
+      if (bl != e.blocks.end() && --bl->second.refs == 0) {
+        HC_CUDA_TRY(cudaFreeAsync(bl->second.ptr, st));
+        e.blocks.erase(bl);
+      }
       e.xfers.erase(e.dyn_owner[u]);
     }
     e.dyn_owner[u] = id;
