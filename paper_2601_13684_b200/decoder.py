@@ -532,10 +532,13 @@ class HeteroCacheDecoder:
         """Copy fetched index sets out of the pinned staging buffer (after a sync)."""
         if not self._uncollected:
             return
-        end = max(o + k for ev in self._uncollected for o, k in ev.offsets)
-        store = self._pinned.numpy().view(np.uint32)[:end].copy()  # one bulk copy
+        spans = [(o, o + k) for ev in self._uncollected for o, k in ev.offsets]
+        lo = min(a for a, _ in spans) if spans else 0
+        end = max((b for _, b in spans), default=0)
+        # one bulk copy of just the uncollected span of the ring
+        store = self._pinned.numpy().view(np.uint32)[lo:end].copy()
         for ev in self._uncollected:  # K1 dense output is already ascending
-            ev.fetched = [store[o:o + k] for o, k in ev.offsets]
+            ev.fetched = [store[o - lo:o - lo + k] for o, k in ev.offsets]
         self._uncollected = []
 
     def join(self, stream=None) -> None:

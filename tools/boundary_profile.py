@@ -75,14 +75,23 @@ def main(name="cfg4", K=120, W=5):
     dec.kernel_timing(True)
     dec.retrieval_stats()
     real = dec.lib
+    import cProfile
+    import pstats
+    prof = cProfile.Profile()
     for t in range(W + 1, W + K + 1):
         log = defaultdict(float)
         dec.lib = Timed(real, names, log)
+        boundary_next = (t - 1) % 8 == 0
+        if boundary_next and "--cprofile" in sys.argv:
+            prof.enable()
         a = time.perf_counter()
         dec.decode_step(t, qs[t], kn, vn, out, rows=False)
         log["total"] = time.perf_counter() - a
+        prof.disable()
         dec.lib = real
         per_step.append((t, dict(log)))
+    if "--cprofile" in sys.argv:
+        pstats.Stats(prof).sort_stats("tottime").print_stats(14)
     dec.finish()
     torch.cuda.synchronize()
     ph = dec.kernel_timing(False)
@@ -103,5 +112,5 @@ def main(name="cfg4", K=120, W=5):
 
 
 if __name__ == "__main__":
-    a = sys.argv[1:]
+    a = [x for x in sys.argv[1:] if not x.startswith("--")]
     main(a[0] if a else "cfg4", int(a[1]) if len(a) > 1 else 120)
