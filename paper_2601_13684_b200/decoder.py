@@ -532,11 +532,16 @@ class HeteroCacheDecoder:
         """Copy fetched index sets out of the pinned staging buffer (after a sync)."""
         if not self._uncollected:
             return
+        import torch
+
         spans = [(o, o + k) for ev in self._uncollected for o, k in ev.offsets]
         lo = min(a for a, _ in spans) if spans else 0
         end = max((b for _, b in spans), default=0)
-        # one bulk copy of just the uncollected span of the ring
-        store = self._pinned.numpy().view(np.uint32)[lo:end].copy()
+        # one bulk copy of just the uncollected span of the ring (torch's copy is
+        # multithreaded: the ring can hold tens of MB)
+        buf = torch.empty(end - lo, dtype=torch.int32)
+        buf.copy_(self._pinned[lo:end])
+        store = buf.numpy().view(np.uint32)
         for ev in self._uncollected:  # K1 dense output is already ascending
             ev.fetched = [store[o - lo:o - lo + k] for o, k in ev.offsets]
         self._uncollected = []
