@@ -547,6 +547,12 @@ int engine_create(EngineImpl& e, const hc_engine_desc& c, const int32_t* roles,
     HC_CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, dev));
     uint64_t keep = ~uint64_t(0);
     HC_CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    // a block freed on one stream (a superseded transfer, on the caller's) must
+    // not be handed to an allocation on another (the fire selection's side
+    // stream) with an inserted wait on the free: that would hold the selection
+    // -- and the gathers behind it -- until the caller's stream got there
+    int no = 0;
+    HC_CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &no));
   }
   HC_CUDA_TRY(cudaHostAlloc((void**)&e.ovl_host, size_t(kRing) * std::max(1, e.n_piv) * 4,
                             cudaHostAllocDefault));
