@@ -165,3 +165,17 @@ def test_merge_reports_sums_partials_and_unions_events():
     assert [e.pivot for e in m.events] == [(0, 0), (1, 0)]
     with pytest.raises(ValueError):
         merge_reports([rep([row], []), rep([replace(row, cumulative_bytes=1)], [])])
+
+
+def test_combine_unit_outputs_takes_each_rank_rows():
+    import torch
+
+    from paper_2601_13684_b200.parallel import combine_unit_outputs
+
+    B, NL, H, G, D = 2, 3, 4, 2, 5
+    owned = np.zeros((2, B, NL, H), dtype=bool)
+    owned[0, :, :, :2] = True
+    owned[1, :, :, 2:] = True
+    parts = [torch.full((B, NL, H * G, D), float(r)) for r in range(2)]
+    out = combine_unit_outputs(parts, owned, G)
+    assert (out[:, :, :2 * G] == 0).all() and (out[:, :, 2 * G:] == 1).all()
