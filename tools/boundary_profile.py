@@ -39,8 +39,13 @@ class Timed:
 
         def call(*a):
             t0 = time.perf_counter()
+            if name == "hc_engine_fire_batch" and "overlaps_end" in self._log:
+                self._log["python_decision"] += t0 - self._log["overlaps_end"]
             r = fn(*a)
-            self._log[name] += time.perf_counter() - t0
+            t1 = time.perf_counter()
+            self._log[name] += t1 - t0
+            if name == "hc_engine_overlaps":
+                self._log["overlaps_end"] = t1
             return r
         return call
 
@@ -71,6 +76,7 @@ def main(name="cfg4", K=120, W=5):
     torch.cuda.synchronize()
     names = ["hc_engine_decode_begin", "hc_engine_overlaps", "hc_engine_fire_batch",
              "hc_engine_land_batch", "hc_engine_decode_end", "hc_engine_decode_step"]
+    shown = names + ["python_decision"]
     per_step = []
     dec.kernel_timing(True)
     dec.retrieval_stats()
@@ -87,6 +93,7 @@ def main(name="cfg4", K=120, W=5):
         a = time.perf_counter()
         dec.decode_step(t, qs[t], kn, vn, out, rows=False)
         log["total"] = time.perf_counter() - a
+        log.pop("overlaps_end", None)
         prof.disable()
         dec.lib = real
         per_step.append((t, dict(log)))
@@ -106,7 +113,7 @@ def main(name="cfg4", K=120, W=5):
           f" gathers {rs['gather_ms']:.1f} ms in {rs['batches']} batches")
     for label, ds in (("after boundary", after), ("other", other)):
         parts = ", ".join(f"{k.replace('hc_engine_', '')} {mean(ds, k):.3f}"
-                          for k in names + ["total"] if mean(ds, k) > 0)
+                          for k in shown + ["total"] if mean(ds, k) > 0)
         print(f"  {label} (n={len(ds)}) host ms: {parts}")
     dec.close()
 
