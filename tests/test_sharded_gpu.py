@@ -128,3 +128,25 @@ def test_unit_sharding_matches_unsharded(case):
         m = np.repeat(owned[r], G, axis=2)  # [B, NL, H*G]
         comb[:, m] = res[r][3][:, m]
     assert np.array_equal(comb, ref)
+
+
+def test_sharded_engine_refuses_measure_mode_and_split_clusters():
+    """Measure mode needs every head of every sequence; a satellite must live
+    with its pivot (hc_engine_create_sharded validation)."""
+    from paper_2601_13684_b200._lib import HCError
+    from paper_2601_13684_b200.decoder import HeteroCacheDecoder
+    from paper_2601_13684_b200.engine import EngineConfig
+    from paper_2601_13684_b200.parallel import assign_units
+    from paper_2601_13684_b200.workload import ModelShape, Workload, plan_for
+
+    model = ModelShape("tiny", NL, 32, 8)
+    tax, plan = plan_for(Workload("tiny", model, L, B, 0.10, T, 0, layers=NL))
+    owned = assign_units(tax, plan, B, 2, T)
+    kw = dict(batch=B, group=model.group, max_decode=T, chunk=256)
+    with pytest.raises(HCError):
+        HeteroCacheDecoder(tax, plan, EngineConfig(), owned=owned[0], recall_topk=64, **kw)
+    split = owned[0].copy()
+    c = tax.clusters[0]
+    split[0, c.satellites[0][0], c.satellites[0][1]] = not split[0, c.pivot[0], c.pivot[1]]
+    with pytest.raises(HCError):
+        HeteroCacheDecoder(tax, plan, EngineConfig(), owned=split, **kw)
