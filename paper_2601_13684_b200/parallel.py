@@ -154,6 +154,8 @@ def merge_reports(parts):
     from dataclasses import replace
 
     base = parts[0]
+    if len({len(p.rows) for p in parts}) != 1:
+        raise ValueError("ranks report different numbers of steps")
     rows = []
     for rs in zip(*(p.rows for p in parts)):
         r0 = rs[0]
