@@ -192,6 +192,7 @@ class HeteroCacheDecoder:
                       else [] for b in range(self.B)]
         self._pinned = None
         self._pin_head = 0
+        self._fetch_ev = None
         self._uncollected = []
         np.median(np.zeros((2, 2)), axis=0)  # first call imports numpy.ma (~30 ms): not mid-run
         self._fire_events = []
@@ -490,6 +491,13 @@ class HeteroCacheDecoder:
         _lib.check(self.lib.hc_engine_fire_batch(self.handle, len(u), u.ctypes.data, t,
                                                  d.ctypes.data, ids.ctypes.data,
                                                  self._pinned.data_ptr() + 4 * base, sh))
+        # the caller's stream waits for the fetched-set copies: an event on it from
+        # here marks this batch's part of the ring readable
+        import torch
+
+        self._fetch_ev = torch.cuda.Event()
+        self._fetch_ev.record(torch.cuda.default_stream() if not sh else
+                              torch.cuda.ExternalStream(sh))
         q = 0
         off = base
         unsorted = []
@@ -521,12 +529,19 @@ class HeteroCacheDecoder:
         import torch
 
         if self._pinned is None or self._pinned.numel() < total:
-            self.sync()
+            self._drain_fetched()
             self._pinned = torch.empty(max(total, 1 << 16), dtype=torch.int32, pin_memory=True)
             self._pin_head = 0
         if self._pin_head + total > self._pinned.numel():
-            self.sync()  # copy out what the ring still holds before overwriting it
+            self._drain_fetched()  # copy out what the ring still holds before overwriting it
             self._pin_head = 0
+
+    def _drain_fetched(self) -> None:
+        """Wait for the copies into the ring (the last batch's event), not for the
+        whole GPU queue, then copy the ring out."""
+        if self._fetch_ev is not None:
+            self._fetch_ev.synchronize()
+        self._collect_fetched()
 
     def _collect_fetched(self) -> None:
         """Copy fetched index sets out of the pinned staging buffer (after a sync)."""
