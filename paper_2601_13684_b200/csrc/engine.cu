@@ -553,6 +553,22 @@ int engine_create(EngineImpl& e, const hc_engine_desc& c, const int32_t* roles,
     // -- and the gathers behind it -- until the caller's stream got there
     int no = 0;
     HC_CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &no));
+    // grow the pool once, here, for the transfer blocks of ~16 fires per
+    // satellite in flight: growing it inside a decode step (a fire batch's
+    // cudaMallocAsync) costs milliseconds on the boundary's critical path
+    if (c.monitor && e.n_sat) {
+      size_t per = 0;
+      for (int u = 0; u < e.n_units; ++u)
+        if (e.sat_slot[u] >= 0) per += (2 * size_t(std::max(1, e.cap[u])) + 8) * 4;
+      const size_t want = std::min<size_t>(per * 16, size_t(1) << 30);
+      void* tmp = nullptr;
+      if (cudaMallocAsync(&tmp, want, 0) == cudaSuccess) {
+        HC_CUDA_TRY(cudaFreeAsync(tmp, 0));
+        HC_CUDA_TRY(cudaStreamSynchronize(0));
+      } else {
+        cudaGetLastError();  // no room to pre-grow: the pool grows on demand
+      }
+    }
   }
   HC_CUDA_TRY(cudaHostAlloc((void**)&e.ovl_host, size_t(kRing) * std::max(1, e.n_piv) * 4,
                             cudaHostAllocDefault));

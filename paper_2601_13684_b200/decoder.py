@@ -195,7 +195,6 @@ class HeteroCacheDecoder:
         self._fetch_ev = None
         self._uncollected = []
         np.median(np.zeros((2, 2)), axis=0)  # first call imports numpy.ma (~30 ms): not mid-run
-        self._fire_events = []
         self._prefilled = set()
         # boundary decision taken while the next step's attention runs (see
         # decode_step); (step, first, per-sequence (charged, extra)) or None
@@ -457,6 +456,10 @@ class HeteroCacheDecoder:
             return
         cum = [st.cumulative_bytes for st in self.states]
         done_of = order_fires(t, gathered, cum, cfg)
+        # the fire selection and gathers first (the GPU is waiting for them), the
+        # host bookkeeping after
+        if local:
+            issued = self._fire_batch(t, local, [done_of[(b, p)][0] for b, p, _, _, _ in local], sh)
         for b, _ in done_of:
             flags[b] = 1
         for st in self.states:  # landed transfers never count as in flight again
@@ -465,32 +468,23 @@ class HeteroCacheDecoder:
             self.states[b].ledger.append((done_of[(b, p)][0], n_))
         for b, st in enumerate(self.states):
             st.cumulative_bytes = cum[b]
-        fire_units, fire_done = [], []
-        for b, p, sats, ks, nbytes in local:
-            st = self.states[b]
-            done = done_of[(b, p)][0]
-            ev = _Event(trigger_step=t, pivot=p, completion_step=done, transfer_bytes=nbytes,
-                        sats=sats, ks=ks)
-            st.raw_events.append(ev)
-            fire_units.append(self.unit(b, p))
-            fire_done.append(done)
-            self._fire_events.append((st, ev))
-        if fire_units:
-            self._fire_batch(t, fire_units, fire_done, sh)
+        if local:
+            self._record_fires(t, local, done_of, *issued)
 
-    def _fire_batch(self, t: int, units, done, sh) -> None:
-        evs = self._fire_events
-        self._fire_events = []
-        total = sum(sum(ev.ks) for _, ev in evs)
+    def _fire_batch(self, t: int, local, done, sh):
+        """hc_engine_fire_batch for this boundary's local fires: selection, K_base
+        restamp, fetched-set copies into the pinned ring, gathers.  Returns the
+        transfer ids and the ring offset of the batch."""
+        total = sum(sum(ks) for _, _, _, ks, _ in local)
         self._reserve_pinned(total)
         base = self._pin_head
-        n_ids = sum(len(ev.sats) for _, ev in evs)
-        ids = np.zeros(n_ids, dtype=np.int32)
-        u = np.asarray(units, dtype=np.int32)
+        ids = np.zeros(sum(len(sats) for _, _, sats, _, _ in local), dtype=np.int32)
+        u = np.asarray([self.unit(b, p) for b, p, _, _, _ in local], dtype=np.int32)
         d = np.asarray(done, dtype=np.int32)
         _lib.check(self.lib.hc_engine_fire_batch(self.handle, len(u), u.ctypes.data, t,
                                                  d.ctypes.data, ids.ctypes.data,
                                                  self._pinned.data_ptr() + 4 * base, sh))
+        self._pin_head = base + total
         # the caller's stream waits for the fetched-set copies: an event on it from
         # here marks this batch's part of the ring readable
         import torch
@@ -498,24 +492,32 @@ class HeteroCacheDecoder:
         self._fetch_ev = torch.cuda.Event()
         self._fetch_ev.record(torch.cuda.default_stream() if not sh else
                               torch.cuda.ExternalStream(sh))
+        return ids, base
+
+    def _record_fires(self, t: int, local, done_of, ids, base) -> None:
+        """RetrievalRecords (engine.py:338-347) and pending landings of the fires
+        just issued, in firing order."""
         q = 0
         off = base
         unsorted = []
-        for st, ev in evs:
-            ev.tids = ids[q:q + len(ev.sats)].tolist()
+        for b, p, sats, ks, nbytes in local:
+            st = self.states[b]
+            ev = _Event(trigger_step=t, pivot=p, completion_step=done_of[(b, p)][0],
+                        transfer_bytes=nbytes, sats=sats, ks=ks)
+            st.raw_events.append(ev)
+            ev.tids = ids[q:q + len(sats)].tolist()
             ev.offsets = []
-            for k in ev.ks:
+            for k in ks:
                 ev.offsets.append((off, k))
                 off += k
-            q += len(ev.sats)
-            for s, k, tid in zip(ev.sats, ev.ks, ev.tids):
+            q += len(sats)
+            for s, k, tid in zip(sats, ks, ev.tids):
                 if st.pending and st.pending[-1][0] > ev.completion_step and \
                         all(x is not st for x in unsorted):
                     unsorted.append(st)
                 st.pending.append((ev.completion_step, st.order, s, tid, k, ev))
                 st.order += 1
             self._uncollected.append(ev)
-        self._pin_head = off
         # completion steps are nondecreasing in firing order (cumulative bytes only
         # grow), so appends keep the (completion, order) landing order of
         # engine.py:293-296; re-sort only if that ever does not hold
