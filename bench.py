@@ -75,6 +75,8 @@ def parse():
     ap.add_argument("--shard", choices=("sequences", "units"), default="sequences",
                     help="N>1: sequences = every rank its own batch (weak); units = one batch's "
                          "units bin-packed over the ranks (strong)")
+    ap.add_argument("--score-material", choices=("fp32", "fp16"), default="fp32",
+                    help="pivot score material between K4 and the GQA-mean rows")
     ap.add_argument("--link-mib-per-step", type=float, default=0.0,
                     help="EngineConfig.transfer_bandwidth in MiB per decode step (host link "
                          "model); 0: the workload's measured-link value")
@@ -174,7 +176,7 @@ def run_b200(args, rank, world):
     lib = _lib.load()
     obs = args.obs_window or max(1, min(32, 128 // m.group))  # w_obs = 32 (Llama)
     dkw = dict(batch=w.batch, group=m.group, max_decode=T, chunk=args.chunk, host_pool=True,
-               track_sets=False, obs_window=obs)
+               track_sets=False, obs_window=obs, score_material=args.score_material)
     units_mode = args.shard == "units" and world > 1
     owned_all = None
     if units_mode:

@@ -192,6 +192,10 @@ typedef struct hc_engine_desc {
   int32_t monitor;        /* drift monitoring on (variant != no_retrieval)           */
   int32_t host_pool;      /* 1: satellite prefill K/V in pinned host memory          */
   int32_t obs_window;     /* prefill observation window w (0/1: last prompt token)   */
+  int32_t score_material; /* pivot score material between K4 and the GQA-mean row:   */
+                          /* 0 = fp32 e = 2^(x - m) (default: rows within fp32       */
+                          /* rounding of the oracle's), 1 = fp16 (half the bytes,    */
+                          /* ~5e-4 relative row error)                               */
 } hc_engine_desc;
 
 /* CacheEngine.__init__ (engine.py:156-214): allocate and lay out the store.

@@ -38,7 +38,7 @@ class EngineDesc(C.Structure):
     _fields_ = [(n, C.c_int32) for n in (
         "batch", "num_layers", "kv_heads", "group", "head_dim", "prefill_len", "max_decode",
         "sink_count", "recency_window", "l_base_int", "chunk", "monitor", "host_pool",
-        "obs_window")]
+        "obs_window", "score_material")]
 
 
 class RecallHead(C.Structure):

@@ -100,9 +100,31 @@ __device__ __forceinline__ uint32_t swz(uint32_t base, int r, int J) {
   return base + (J >> 3) * kBoxBytes + r * 128 + (((J & 7) ^ (r & 7)) << 4);
 }
 
+// Pivot score material element: fp32 (default) or fp16 (compact).
+template <bool F16>
+struct Mat;
+template <>
+struct Mat<false> {
+  using T = float;
+  __device__ static void put2(float* dst, float a, float b) {
+    *reinterpret_cast<float2*>(dst) = make_float2(a, b);
+  }
+  __device__ static void put1(float* dst, float a) { *dst = a; }
+};
+template <>
+struct Mat<true> {
+  using T = __half;
+  __device__ static void put2(__half* dst, float a, float b) {
+    *reinterpret_cast<__half2*>(dst) = __floats2half2_rn(a, b);
+  }
+  __device__ static void put1(__half* dst, float a) { *dst = __float2half_rn(a); }
+};
+
+template <bool F16>
 __global__ void __launch_bounds__(kThreadsAttn, 2)
 attn_tiles_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                   const AttnParams p) {
+  using MT = typename Mat<F16>::T;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t sbase = (smem_u32(smem_raw) + 1023u) & ~1023u;
   uint8_t* sgen = smem_raw + (sbase - smem_u32(smem_raw));
@@ -180,14 +202,16 @@ attn_tiles_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant
   for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
   float m_run = -INFINITY, l_run = 0.f;
   const int tb = warp * 16;  // this warp's 16 rows of each sub-tile
-  // pivot score-row material: fp16 e = 2^(x - m) per token (m = this warp's
+  // pivot score-row material: e = 2^(x - m) per token (m = this warp's
   // running max after the 16-token group, one fp32 per group), finalised by
-  // score_rows_kernel once the global (M, L) are known
-  __half* lg = nullptr;
+  // score_rows_kernel once the global (M, L) are known.  fp32 keeps the row
+  // within fp32 rounding of the oracle's; fp16 halves these bytes at ~5e-4
+  // relative error
+  MT* lg = nullptr;
   float* mr = nullptr;
   if (unit.pivot_slot >= 0 && rg.pos >= 0 && row_ok) {
     const size_t hg = size_t(unit.pivot_slot) * G + g;
-    lg = reinterpret_cast<__half*>(p.logits) + hg * p.logit_stride + rg.pos;
+    lg = reinterpret_cast<MT*>(p.logits) + hg * p.logit_stride + rg.pos;
     mr = p.mref + hg * (p.logit_stride / 16) + rg.pos / 16;
   }
 
@@ -240,9 +264,9 @@ attn_tiles_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant
       for (int nt = 0; nt < 2; ++nt) {
         const int tok = base_tok + nt * 8 + 2 * c;
         if (tok + 1 < rg.n) {
-          *reinterpret_cast<__half2*>(lg + tok) = __floats2half2_rn(pr[nt][0], pr[nt][1]);
+          Mat<F16>::put2(lg + tok, pr[nt][0], pr[nt][1]);
         } else if (tok < rg.n) {
-          lg[tok] = __float2half_rn(pr[nt][0]);
+          Mat<F16>::put1(lg + tok, pr[nt][0]);
         }
       }
       if (c == 0 && base_tok < rg.n) mr[base_tok / 16] = mb;
@@ -387,9 +411,26 @@ __global__ void __launch_bounds__(128) combine_kernel(const AttnParams p) {
 constexpr int kRowsThreads = 256;
 constexpr int kRowsSpan = kRowsThreads * 8;  // positions per block
 
-template <int G>
+__device__ __forceinline__ void unpack8(const uint4 (&raw)[2], float (&f)[8], const float*) {
+  const float4 a = *reinterpret_cast<const float4*>(&raw[0]);
+  const float4 b = *reinterpret_cast<const float4*>(&raw[1]);
+  f[0] = a.x, f[1] = a.y, f[2] = a.z, f[3] = a.w, f[4] = b.x, f[5] = b.y, f[6] = b.z, f[7] = b.w;
+}
+__device__ __forceinline__ void unpack8(const uint4 (&raw)[1], float (&f)[8], const __half*) {
+  const uint32_t w[4] = {raw[0].x, raw[0].y, raw[0].z, raw[0].w};
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float2 v = __half22float2(*reinterpret_cast<const __half2*>(&w[q]));
+    f[2 * q] = v.x;
+    f[2 * q + 1] = v.y;
+  }
+}
+
+template <int G, bool F16>
 __global__ void __launch_bounds__(kRowsThreads) score_rows_kernel(const AttnParams p,
                                                                   const int32_t* __restrict__ pivot_units) {
+  using MT = typename Mat<F16>::T;
+  constexpr int kV = F16 ? 1 : 2;  // 16-B vectors per 8 positions
   __shared__ float s_m[G], s_inv[G];
   const UnitDesc u = p.units[pivot_units[blockIdx.y]];
   const int slot = u.pivot_slot;
@@ -402,13 +443,15 @@ __global__ void __launch_bounds__(kRowsThreads) score_rows_kernel(const AttnPara
   __syncthreads();
   const int pos = blockIdx.x * kRowsSpan + tid * 8;
   if (pos >= len) return;
-  const __half* lg = reinterpret_cast<const __half*>(p.logits) + size_t(slot) * G * p.logit_stride;
+  const MT* lg = reinterpret_cast<const MT*>(p.logits) + size_t(slot) * G * p.logit_stride;
   const float* mr = p.mref + size_t(slot) * G * (p.logit_stride / 16);
-  uint4 raw[G];
+  uint4 raw[G][kV];
   float mv[G];
 #pragma unroll
   for (int j = 0; j < G; ++j) {
-    raw[j] = __ldcs(reinterpret_cast<const uint4*>(lg + size_t(j) * p.logit_stride + pos));
+    const uint4* src = reinterpret_cast<const uint4*>(lg + size_t(j) * p.logit_stride + pos);
+#pragma unroll
+    for (int v = 0; v < kV; ++v) raw[j][v] = __ldcs(src + v);
     mv[j] = __ldg(mr + size_t(j) * (p.logit_stride / 16) + pos / 16);
   }
   float acc[8];
@@ -417,13 +460,10 @@ __global__ void __launch_bounds__(kRowsThreads) score_rows_kernel(const AttnPara
 #pragma unroll
   for (int j = 0; j < G; ++j) {
     const float cj = exp2f(mv[j] - s_m[j]) * s_inv[j];
-    const uint32_t w[4] = {raw[j].x, raw[j].y, raw[j].z, raw[j].w};
+    float f[8];
+    unpack8(raw[j], f, static_cast<const MT*>(nullptr));
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[q]));
-      acc[2 * q] += f.x * cj;
-      acc[2 * q + 1] += f.y * cj;
-    }
+    for (int e = 0; e < 8; ++e) acc[e] += f[e] * cj;
   }
   const float rg = float(G);
 #pragma unroll
@@ -491,7 +531,9 @@ int make_bf16_tensor_map(CUtensorMap* map, const void* base, int64_t rows, int64
 static int configure_attn() {
   static bool configured = false;
   if (!configured) {
-    HC_CUDA_TRY(cudaFuncSetAttribute(attn_tiles_kernel,
+    HC_CUDA_TRY(cudaFuncSetAttribute(attn_tiles_kernel<false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemAttn));
+    HC_CUDA_TRY(cudaFuncSetAttribute(attn_tiles_kernel<true>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemAttn));
     configured = true;
   }
@@ -517,7 +559,11 @@ int launch_score_rows(const AttnParams& p, const int32_t* pivot_units_dev, int n
     const int len = p.L + p.t;
     dim3 grid((len + kRowsSpan - 1) / kRowsSpan, n_pivots);
     switch (p.group) {
-#define HC_ROWS(GG) case GG: score_rows_kernel<GG><<<grid, kRowsThreads, 0, st>>>(p, pivot_units_dev); break;
+#define HC_ROWS(GG)                                                                     \
+  case GG:                                                                              \
+    if (p.mat_f16) score_rows_kernel<GG, true><<<grid, kRowsThreads, 0, st>>>(p, pivot_units_dev); \
+    else score_rows_kernel<GG, false><<<grid, kRowsThreads, 0, st>>>(p, pivot_units_dev);         \
+    break;
       HC_ROWS(1) HC_ROWS(2) HC_ROWS(3) HC_ROWS(4) HC_ROWS(5) HC_ROWS(6) HC_ROWS(7) HC_ROWS(8)
 #undef HC_ROWS
     }
@@ -531,7 +577,8 @@ int launch_attn_tiles(const CUtensorMap& tmK, const CUtensorMap& tmV, const Attn
                       int n_tiles, cudaStream_t st) {
   HC_TRY(configure_attn());
   if (n_tiles > 0) {
-    attn_tiles_kernel<<<n_tiles, kThreadsAttn, kSmemAttn, st>>>(tmK, tmV, p);
+    if (p.mat_f16) attn_tiles_kernel<true><<<n_tiles, kThreadsAttn, kSmemAttn, st>>>(tmK, tmV, p);
+    else attn_tiles_kernel<false><<<n_tiles, kThreadsAttn, kSmemAttn, st>>>(tmK, tmV, p);
     HC_CHECK_LAUNCH();
   }
   return HC_OK;

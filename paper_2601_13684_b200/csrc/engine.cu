@@ -170,7 +170,9 @@ struct EngineImpl {
   int n_piv = 0;
   int64_t row_len = 0;
   int words = 0;
-  void* logits = nullptr;  // fp16 per-token pivot material
+  void* logits = nullptr;  // per-token pivot material (fp32, or fp16 when mat_f16)
+  int mat_f16 = 0;
+  size_t mat_bytes = 4;    // bytes per material element
   float *mref = nullptr, *stats = nullptr, *rowbuf = nullptr;
   uint32_t *top_idx = nullptr, *top_cnt = nullptr, *kbase = nullptr;
   uint32_t* ovl_ring = nullptr;
@@ -501,7 +503,11 @@ int engine_create(EngineImpl& e, const hc_engine_desc& c, const int32_t* roles,
                            cudaMemcpyHostToDevice));
   // pivot score material and statistics, double-buffered by step parity: the
   // score rows of step t run beside step t+1's attention
-  HC_TRY(dalloc((void**)&e.logits, 2 * size_t(np) * e.G * e.row_len * 2, &e.dev_bytes));
+  e.mat_f16 = c.score_material == 1 ? 1 : 0;
+  HC_REQUIRE(c.score_material == 0 || c.score_material == 1, HC_EINVAL,
+             "score_material must be 0 (fp32) or 1 (fp16)");
+  e.mat_bytes = e.mat_f16 ? 2 : 4;
+  HC_TRY(dalloc((void**)&e.logits, 2 * size_t(np) * e.G * e.row_len * e.mat_bytes, &e.dev_bytes));
   HC_TRY(dalloc((void**)&e.mref, 2 * size_t(np) * e.G * (e.row_len / 16) * 4, &e.dev_bytes));
   HC_TRY(dalloc((void**)&e.stats, 2 * size_t(np) * e.G * 2 * 4, &e.dev_bytes));
   HC_TRY(dalloc((void**)&e.rowbuf, size_t(np) * e.row_len * 4, &e.dev_bytes));
@@ -590,7 +596,8 @@ AttnParams decode_params(EngineImpl& e, int t, const void* q, void* o) {
   p.out = o;
   p.partial = e.partial;
   const size_t np = size_t(std::max(1, e.n_piv));
-  p.logits = static_cast<char*>(e.logits) + size_t(t & 1) * np * e.G * e.row_len * 2;
+  p.logits = static_cast<char*>(e.logits) + size_t(t & 1) * np * e.G * e.row_len * e.mat_bytes;
+  p.mat_f16 = e.mat_f16;
   p.mref = e.mref + size_t(t & 1) * np * e.G * (e.row_len / 16);
   p.stats = e.stats + size_t(t & 1) * np * e.G * 2;
   p.rows = e.n_piv ? e.rowbuf : nullptr;

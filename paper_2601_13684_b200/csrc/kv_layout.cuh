@@ -124,7 +124,8 @@ struct AttnParams {
   const void* q;         // bf16 [q_rows][128]
   void* out;             // bf16 [q_rows][128] (combine)
   float* partial;        // [slots][G][kPartStride]
-  void* logits;          // [pivot slots][G][logit_stride] fp16 e = 2^(x - m_ref), x = log2 score
+  void* logits;          // [pivot slots][G][logit_stride] e = 2^(x - m_ref), x = log2 score
+                         // (fp32, or fp16 when mat_f16)
   float* mref;           // [pivot slots][G][logit_stride / 16] m_ref per 16-position group
   float* stats;          // [pivot slots][G][2]  (M, L) after combine
   float* rows;           // [pivot slots][row_stride]  GQA-mean probability rows
@@ -138,6 +139,8 @@ struct AttnParams {
   int32_t n_units;
   float scale_log2;      // log2(e) / sqrt(d)
   const uint8_t* skip;   // per unit: 1 = tiles deferred to a later launch (landing units), or null
+  int32_t mat_f16;       // pivot score material: 0 = fp32, 1 = fp16
+  int32_t pad_;
 };
 
 constexpr int kPartStride = 132;  // M, L, pad, pad, O[128]

@@ -111,11 +111,16 @@ class HeteroCacheDecoder:
                  group: int, max_decode: int, head_dim: int = 128, chunk: int = 1024,
                  host_pool: bool = True, bytes_per_kv_entry: int | None = None,
                  track_sets: bool = True, obs_window: int = 1, overlap_decisions: bool = True,
-                 recall_topk: int = 0, owned=None, exchange=None):
+                 recall_topk: int = 0, owned=None, exchange=None,
+                 score_material: str = "fp32"):
         """owned: optional [batch, layers, kv_heads] bool mask of the units this
         rank holds (parallel.assign_units; None = all).  exchange: the fire
         exchange of a unit-sharded run (parallel.FireExchange); every rank of
-        the run must step in lockstep, since boundary decisions all_gather."""
+        the run must step in lockstep, since boundary decisions all_gather.
+        score_material: "fp32" (default) or "fp16", the per-token pivot material
+        K4 hands to the GQA-mean row pass; fp16 halves those bytes but its
+        ~5e-4 relative row error moves near-tied positions across the top-k
+        boundary (profiles/r02_selection_precision.json)."""
         _lib.require_cuda()
         self.lib = _lib.load()
         self.taxonomy, self.plan, self.config = taxonomy, plan, config
@@ -148,7 +153,8 @@ class HeteroCacheDecoder:
                                head_dim=head_dim, prefill_len=self.L, max_decode=max_decode,
                                sink_count=config.sink_count, recency_window=config.recency_window,
                                l_base_int=self.l_base_int, chunk=chunk, monitor=int(self.monitor),
-                               host_pool=int(host_pool), obs_window=obs_window)
+                               host_pool=int(host_pool), obs_window=obs_window,
+                               score_material={"fp32": 0, "fp16": 1}[score_material])
         self.W = obs_window
         h = C.c_void_p()
         if owned is None:

@@ -1,0 +1,69 @@
+"""Parity at the benchmarked context lengths (128K cfg3-shaped, 224K cfg5-shaped).
+
+The bench's throughput claims are made at 128K-224K, where a full head spans
+128-224 split-K tiles of 1024 rows; the small-size decoder tests cover at most
+11.  Here the decoder runs at those lengths across a planted topic shift
+(fire at a window boundary, landing one step later) and every unit of every
+role is checked against the fp32 oracle (tests/scale_parity.py):
+
+  * O within |O - O_ref| <= 4e-3 + 1e-2 |O_ref| (bf16 K/V/Q, fp32 accumulate,
+    bf16 P in PV, bf16 out) at steps 1, 8, every landing step and T;
+  * pivot rows within 1e-9 + 2e-5 |row| of the GQA-mean oracle row;
+  * event log and dynamic sets == the oracle replay of the GPU rows;
+  * selection: top-k sets of the GPU rows == those of the oracle's fp32 and
+    fp64 rows at every step for l_base and every satellite's l_s (fp32 score
+    material; the fp16 material moves ~1-2 near-tied positions in 10-40% of
+    selections, profiles/r02_selection_precision.json).
+"""
+
+import pytest
+
+import scale_parity as SP
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("shape,layout", [("cfg3", dict(B=2, NL=2)), ("cfg5", dict(B=1, NL=1))])
+def test_outputs_rows_events_and_selection_at_scale(shape, layout):
+    import torch
+
+    ctx = SP.build(shape, T=24, shift=9, **layout)
+    try:
+        SP.run(ctx)
+        events = SP.check_events(ctx)
+        assert events, "the planted topic shift must fire a retrieval"
+        lands = sorted({e["completion_step"] for _, e in events if e["completion_step"] <= 24})
+        assert lands, "a fired transfer must land inside the run"
+        st = SP.check_outputs(ctx, sorted({1, 8, 24} | set(lands)))
+        assert not st["violations"], st["violations"][:5]
+        assert set(st["by_role"]) >= {"pivot", "satellite", "anchor"}
+        print(f"{shape}: max|O-O_ref| {st['max_abs']:.2e} over {st['units']} units, "
+              f"row max abs {st['row_max_abs']:.2e}")
+        sel = SP.selection_precision(ctx)
+        summ = SP.summarise(sel)
+        assert summ["fp32_vs_fp64"]["total"] == 0  # the oracle's own rounding floor here
+        assert summ["gpu_vs_fp32"]["total"] == 0, [x for x in sel if x["gpu_vs_fp32"]][:5]
+        assert summ["gpu_vs_fp64"]["total"] == 0
+    finally:
+        ctx["dec"].close()
+        torch.cuda.empty_cache()
+
+
+def test_fp16_material_keeps_outputs_and_event_replay():
+    """The compact fp16 score material still gives in-tolerance outputs and
+    events equal to the replay of its own rows (decisions bit-exact given the
+    rows); only near-tied selections may differ from the fp32 oracle's."""
+    import torch
+
+    ctx = SP.build("cfg3", B=1, NL=2, T=20, shift=9, score_material="fp16")
+    try:
+        SP.run(ctx)
+        events = SP.check_events(ctx)
+        assert events
+        st = SP.check_outputs(ctx, [1, 20])
+        assert not [v for v in st["violations"] if v[3] != "row"], st["violations"][:5]
+        sel = SP.summarise(SP.selection_precision(ctx, steps=[4, 12, 20]))
+        assert sel["gpu_vs_fp32"]["max"] <= 4
+    finally:
+        ctx["dec"].close()
+        torch.cuda.empty_cache()
