@@ -1,8 +1,9 @@
 """Synthetic decode workloads: model shapes, head roles,
 budgets and seeded bf16 K/V/Q with planted hot sets and topic shifts.
 
-Everything is generated on the device (torch RNG) so 128K-224K contexts never
-touch host memory.  Roles per layer follow the survey's synthetic mix:
+Noise is a counter-based generator (csrc/synth.cu on the GPU, so 128K-224K
+contexts never touch host memory; a bit-identical host twin for the CPU
+arms).  Roles per layer follow the survey's synthetic mix:
 Llama-shaped layers hold 1 pivot + 4 satellites + 2 anchors + 1 volatile
 head, Qwen-shaped layers 1 pivot + 2 satellites + 1 anchor.  "c% budget" is
 read as L_base = c*L, i.e. rho = (N_full + c*N_comp) / N (SURVEY.md section 7,
@@ -122,6 +123,44 @@ def plan_for(w: Workload, policy: str = "heterocache"):
     return tax, plan
 
 
+M64 = (1 << 64) - 1
+
+
+def _splitmix64(x: int) -> int:
+    x = (x + 0x9E3779B97F4A7C15) & M64
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & M64
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & M64
+    return x ^ (x >> 31)
+
+
+def stream_key(*parts: int) -> int:
+    """64-bit key of one generator stream (seed, tensor kind, indices...)."""
+    h = 0x6A09E667F3BCC908
+    for p in parts:
+        h = _splitmix64(h ^ (int(p) & M64))
+    return h
+
+
+class DeviceNormal:
+    """N(key, offset + i) on the GPU (csrc/synth.cu, hc_synth_normal)."""
+
+    device = "cuda"
+
+    def __call__(self, shape, key: int, offset: int = 0):
+        import torch
+
+        from . import _lib
+
+        out = torch.empty(shape, dtype=torch.float32, device="cuda")
+        _lib.check(_lib.load().hc_synth_normal(out.data_ptr(), out.numel(), key & M64, offset,
+                                               _lib.stream_handle()))
+        return out
+
+
+# generator stream kinds
+_K, _V, _Q, _QN, _KN, _VN = 1, 2, 3, 4, 5, 6
+
+
 class SyntheticKV:
     """Seeded K/V/Q with planted per-cluster hot sets and topic shifts.
 
@@ -131,45 +170,72 @@ class SyntheticKV:
     +alpha*u, queries are beta*u(t) + N(0, I) with the cluster topic switching
     from u0 to u1 at the shift step, so the pivot's top set moves and the drift
     monitor fires (engine.py:313-321).
+
+    Noise comes from a counter-based generator keyed by (seed, tensor, b, l,
+    h): `normal` is the GPU generator by default; the CPU arms of the bench
+    pass its bit-identical host twin (oracle/synth.py) and, with `seqs`,
+    generate any subset of the batch's sequences -- the same values the GPU
+    arm decodes.  Topic directions and hot sets come from a seeded CPU torch
+    generator (identical on every host).
     """
 
     def __init__(self, model: ModelShape, *, batch: int, prefill_len: int, num_layers: int,
-                 hot: int, seed: int, alpha: float = 9.0, beta: float = 9.0, device="cuda"):
+                 hot: int, seed: int, alpha: float = 9.0, beta: float = 9.0, device="cuda",
+                 normal=None, seqs=None):
         import torch
 
         self.torch = torch
         self.m, self.B, self.L, self.NL = model, batch, prefill_len, num_layers
         self.D, self.H, self.G = model.head_dim, model.kv_heads, model.group
-        self.hot, self.seed, self.alpha, self.beta, self.dev = hot, seed, alpha, beta, device
+        self.hot, self.seed, self.alpha, self.beta = hot, seed, alpha, beta
+        self.normal = normal or DeviceNormal()
+        self.dev = getattr(self.normal, "device", device)
+        self.seqs = list(range(batch)) if seqs is None else list(seqs)
         self.roles = model.layer_roles()
+        self.n_anchor = sum(r == "anchor" for r in self.roles)
+        nt = 2 + self.n_anchor
         g = torch.Generator(device="cpu").manual_seed(seed)
-        # per (b, l): topic directions [B, NL, 3 topics, D] (0/1: cluster, 2: anchor)
-        u = torch.randn(batch, num_layers, 3, self.D, generator=g)
-        self.u = (u / u.norm(dim=-1, keepdim=True)).to(device)
-        hot = min(hot, prefill_len // 4)
-        self.hot_sets = torch.stack([
-            torch.stack([torch.randperm(prefill_len, generator=g)[:3 * hot].view(3, hot)
-                         for _ in range(num_layers)]) for _ in range(batch)]).to(device)
+        # per (b, l): topic directions [B, NL, topics, D]: 0/1 the cluster's two
+        # topics, 2 + a the a-th anchor's own steady topic (distinct anchors are
+        # stable but not similar: profiling keeps them anchors, profiling.py:397-438)
+        u = torch.randn(batch, num_layers, nt, self.D, generator=g)
+        u = u / u.norm(dim=-1, keepdim=True)
+        hot = min(hot, prefill_len // nt)
+        hs = torch.stack([
+            torch.stack([torch.randperm(prefill_len, generator=g)[:nt * hot].view(nt, hot)
+                         for _ in range(num_layers)]) for _ in range(batch)])
+        sel = torch.as_tensor(self.seqs, dtype=torch.long)
+        self.u_all = u.to(self.dev)                 # every sequence (queries are batch-wide)
+        self.u = u[sel].to(self.dev)                # the generated sequences
+        self.hot_sets = hs[sel].to(self.dev)
 
     def _head_topic(self, h: int) -> int:
+        """0: cluster head (topic 0/1), 2 + a: the a-th anchor, -1: volatile."""
         r = self.roles[h]
-        return {"pivot": 0, "satellite": 0, "anchor": 2, "volatile": -1}[r]
+        if r == "anchor":
+            return 2 + sum(x == "anchor" for x in self.roles[:h])
+        return {"pivot": 0, "satellite": 0, "volatile": -1}[r]
 
     def layer_kv(self, layer: int, window: int = 1):
-        """K, V [B, H, L, D] bf16 and the prefill observation queries for one layer:
-        q_last [B, H*G, D] (window 1) or [B, window, H*G, D] (last `window` tokens)."""
+        """K, V [b, H, L, D] bf16 (b = the generated sequences) and the prefill
+        observation queries for one layer: q_last [b, H*G, D] (window 1) or
+        [b, window, H*G, D] (last `window` tokens)."""
         torch = self.torch
-        g = torch.Generator(device=self.dev).manual_seed(self.seed * 1000 + layer)
-        B, H, L, D = self.B, self.H, self.L, self.D
-        k = torch.randn(B, H, L, D, device=self.dev, generator=g, dtype=torch.float32)
-        v = torch.randn(B, H, L, D, device=self.dev, generator=g, dtype=torch.float32)
+        H, L, D = self.H, self.L, self.D
+        nb = len(self.seqs)
+        k = torch.empty(nb, H, L, D, device=self.dev, dtype=torch.float32)
+        v = torch.empty_like(k)
+        for i, b in enumerate(self.seqs):
+            for h in range(H):
+                k[i, h] = self.normal((L, D), stream_key(self.seed, _K, b, layer, h))
+                v[i, h] = self.normal((L, D), stream_key(self.seed, _V, b, layer, h))
         for h in range(H):
             tp = self._head_topic(h)
             if tp < 0:
                 continue
-            for topic in ((0, 1) if tp == 0 else (2,)):
-                idx = self.hot_sets[:, layer, topic]                      # [B, hot]
-                add = self.alpha * self.u[:, layer, topic]               # [B, D]
+            for topic in ((0, 1) if tp == 0 else (tp,)):
+                idx = self.hot_sets[:, layer, topic]                      # [b, hot]
+                add = self.alpha * self.u[:, layer, topic]               # [b, D]
                 k[:, h].scatter_add_(1, idx[:, :, None].expand(-1, -1, D),
                                      add[:, None, :].expand(-1, idx.shape[1], -1).contiguous())
         if window == 1:
@@ -179,13 +245,12 @@ class SyntheticKV:
         return k.to(torch.bfloat16).contiguous(), v.to(torch.bfloat16).contiguous(), q.contiguous()
 
     def queries(self, layer: int, step: int, shift_step=None):
-        """[B, H*G, D] bf16 queries of one layer at a decode step.  shift_step: the
+        """[b, H*G, D] bf16 queries of one layer at a decode step.  shift_step: the
         step of the planted topic shift, or a sequence of shift steps (the cluster
         topic toggles at each)."""
         torch = self.torch
-        g = torch.Generator(device=self.dev).manual_seed((self.seed * 7919 + layer) * 100003 + step)
         B, H, G, D = self.B, self.H, self.G, self.D
-        q = torch.randn(B, H, G, D, device=self.dev, generator=g)
+        q = self.normal((B, H, G, D), stream_key(self.seed, _Q, layer, step))
         for h in range(H):
             tp = self._head_topic(h)
             if tp < 0:
@@ -193,16 +258,20 @@ class SyntheticKV:
             if tp == 0 and shift_step is not None:
                 shifts = shift_step if isinstance(shift_step, (list, tuple)) else (shift_step,)
                 tp = sum(step >= x for x in shifts) % 2
-            q[:, h] += self.beta * self.u[:, layer, tp][:, None, :]
-        return q.view(B, H * G, D).to(torch.bfloat16).contiguous()
+            q[:, h] += self.beta * self.u_all[:, layer, tp][:, None, :]
+        q = q[torch.as_tensor(self.seqs, device=q.device)] if len(self.seqs) != B else q
+        return q.reshape(-1, H * G, D).to(torch.bfloat16).contiguous()
 
     def step_inputs(self, step: int, shift_step: int | None):
-        """q [B, NL, H*G, D], k_new/v_new [B, NL, H, D] (bf16, device)."""
+        """q [b, NL, H*G, D], k_new/v_new [b, NL, H, D] (bf16)."""
         torch = self.torch
         q = torch.stack([self.queries(l, step, shift_step) for l in range(self.NL)], dim=1)
-        g = torch.Generator(device=self.dev).manual_seed(self.seed * 31 + step)
-        kn = torch.randn(self.B, self.NL, self.H, self.D, device=self.dev, generator=g)
-        vn = torch.randn(self.B, self.NL, self.H, self.D, device=self.dev, generator=g)
+        shp = (self.B, self.NL, self.H, self.D)
+        kn = self.normal(shp, stream_key(self.seed, _KN, step))
+        vn = self.normal(shp, stream_key(self.seed, _VN, step))
+        sel = torch.as_tensor(self.seqs, device=kn.device)
+        if len(self.seqs) != self.B:
+            kn, vn = kn[sel], vn[sel]
         return (q.contiguous(), kn.to(torch.bfloat16).contiguous(),
                 vn.to(torch.bfloat16).contiguous())
 
@@ -230,31 +299,34 @@ def staggered_shifts(batch: int, num_layers: int, start: int, span: int, every: 
 
 
 def decode_queries(gen: "SyntheticKV", steps: int, shifts: dict, n_noise: int = 4):
-    """Queries for decode steps 1..steps: [steps + 1, B, NL, H*G, D] bf16 (device).
+    """Queries for decode steps 1..steps: [steps + 1, b, NL, H*G, D] bf16 (the
+    generator's device; b = its generated sequences).
 
     Cluster heads (pivot, satellites) of (b, l) follow topic u0 or u1, toggling at
     each of that cluster's shift steps; noise cycles through n_noise draws."""
     torch = gen.torch
     B, NL, H, G, D = gen.B, gen.NL, gen.H, gen.G, gen.D
-    noise = []
-    for i in range(n_noise):
-        g = torch.Generator(device=gen.dev).manual_seed(gen.seed * 131 + i)
-        noise.append(torch.randn(B, NL, H, G, D, device=gen.dev, generator=g))
+    sel = torch.as_tensor(gen.seqs, dtype=torch.long)
+    nb = len(gen.seqs)
+    noise = [gen.normal((B, NL, H, G, D), stream_key(gen.seed, _QN, i))[sel.to(gen.dev)]
+             for i in range(n_noise)]
     cluster = torch.tensor([gen._head_topic(h) == 0 for h in range(H)], device=gen.dev)
-    anchor = torch.tensor([gen._head_topic(h) == 2 for h in range(H)], device=gen.dev)
-    u = gen.u  # [B, NL, 3, D]
-    out = torch.empty(steps + 1, B, NL, H * G, D, device=gen.dev, dtype=torch.bfloat16)
-    topic = torch.zeros(steps + 1, B, NL, dtype=torch.long, device=gen.dev)
-    for (b, l), xs in shifts.items():
-        for x in xs:
-            if 0 <= x <= steps:
-                topic[x:, b, l] ^= 1
+    anchors = [(h, gen._head_topic(h)) for h in range(H) if gen._head_topic(h) >= 2]
+    u = gen.u  # [b, NL, 3, D]
+    out = torch.empty(steps + 1, nb, NL, H * G, D, device=gen.dev, dtype=torch.bfloat16)
+    topic = torch.zeros(steps + 1, nb, NL, dtype=torch.long, device=gen.dev)
+    for i, b in enumerate(gen.seqs):
+        for l in range(NL):
+            for x in shifts.get((b, l), ()):
+                if 0 <= x <= steps:
+                    topic[x:, i, l] ^= 1
     for t in range(steps + 1):
-        ut = torch.gather(u, 2, topic[t][:, :, None, None].expand(B, NL, 1, D))[:, :, 0]  # [B,NL,D]
+        ut = torch.gather(u, 2, topic[t][:, :, None, None].expand(nb, NL, 1, D))[:, :, 0]
         q = noise[t % n_noise].clone()
         q += gen.beta * (cluster[None, None, :, None, None] * ut[:, :, None, None, :])
-        q += gen.beta * (anchor[None, None, :, None, None] * u[:, :, 2][:, :, None, None, :])
-        out[t] = q.view(B, NL, H * G, D).to(torch.bfloat16)
+        for h, tp in anchors:
+            q[:, :, h] += gen.beta * u[:, :, tp][:, :, None, :]
+        out[t] = q.view(nb, NL, H * G, D).to(torch.bfloat16)
     return out
 
 

@@ -35,3 +35,6 @@ def pytest_sessionstart(session):
     from paper_2601_13684_b200 import build
 
     build.build()
+    from oracle import build_oracle
+
+    build_oracle.build()
