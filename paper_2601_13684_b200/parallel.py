@@ -19,8 +19,18 @@ Two partitionings, one process per GPU (torchrun):
   exactly the reference's.  ``merge_reports`` sums the per-rank partial
   StepRows and unions the events.
 
-NCCL carries the timing reduction and the optional output gather; the fire
-exchange is host data and goes over a gloo group.
+* **slabs** (``slab_units``, the bench's N>1 default): rank r owns the
+  contiguous range [r*S, (r+1)*S) of the batch's (sequence, layer) pairs,
+  S = B*NL / world -- the north star's (batch, KV-head) split of ONE batch
+  (strong scaling).  Clusters are layer-local, so no cluster splits; each
+  rank's query / output rows are one contiguous slab of O[B, NL, Hq, d], so
+  the per-step output all-gather lands straight in place
+  (``all_gather_into_tensor``, no index shuffle).  A sequence whose layers
+  straddle two ranks shares its byte counter through the fire exchange.
+
+``TensorFireExchange`` is the fire exchange as one fixed-size tensor
+all-gather (NCCL on a side stream, so it runs beside the step's attention;
+gloo on host tensors for the single-GPU functional tests).
 """
 
 from __future__ import annotations
@@ -93,6 +103,20 @@ def assign_units(taxonomy, plan, batch: int, world: int, max_decode: int, **kw) 
     return owned
 
 
+def slab_units(taxonomy, batch: int, world: int) -> np.ndarray:
+    """owned[rank][b, layer, head]: rank r owns (sequence, layer) pairs
+    [r*S, (r+1)*S) in (b, layer) order, S = batch*num_layers / world."""
+    NL, H = taxonomy.num_layers, taxonomy.heads_per_layer
+    n = batch * NL
+    if world < 1 or n % world:
+        raise ValueError(f"{batch} x {NL} (sequence, layer) pairs do not split over {world} ranks")
+    S = n // world
+    owned = np.zeros((world, n, H), dtype=bool)
+    for r in range(world):
+        owned[r, r * S:(r + 1) * S] = True
+    return owned.reshape(world, batch, NL, H)
+
+
 def order_fires(step: int, gathered, cumulative: list, cfg) -> dict:
     """Completion steps of one boundary's fires over all ranks.
 
@@ -141,6 +165,60 @@ class FireExchange:
 
         out = [None] * self.world
         dist.all_gather_object(out, obj, group=self.group)
+        return out
+
+
+class TensorFireExchange:
+    """The boundary fire exchange as ONE fixed-size all-gather of a tensor.
+
+    Each rank packs its fires (sequence, pivot layer, pivot head, bytes) into a
+    [capacity + 1, 4] int64 block (row 0: the count) and all-gathers the blocks
+    of every rank.  With NCCL the gather runs on a side stream, so it does not
+    wait for (and runs beside) the attention already queued on the decode
+    stream; the host then reads back only that side stream.  gloo (functional
+    tests on one GPU) gathers host tensors.
+    """
+
+    def __init__(self, capacity: int, group=None):
+        import torch
+        import torch.distributed as dist
+
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.cap = max(1, int(capacity))
+        self.nccl = dist.get_backend(group) == "nccl"
+        dev = "cuda" if self.nccl else "cpu"
+        self.send = torch.zeros(self.cap + 1, 4, dtype=torch.int64, device=dev)
+        self.recv = torch.zeros(self.world, self.cap + 1, 4, dtype=torch.int64, device=dev)
+        self.stage = torch.zeros(self.cap + 1, 4, dtype=torch.int64,
+                                 pin_memory=self.nccl)
+        self.stream = torch.cuda.Stream() if self.nccl else None
+
+    def all_gather(self, obj) -> list:
+        import torch
+        import torch.distributed as dist
+
+        if len(obj) > self.cap:
+            raise ValueError(f"{len(obj)} fires exceed the exchange capacity {self.cap}")
+        st = self.stage
+        st[0, 0] = len(obj)
+        for i, (b, p, n) in enumerate(obj):
+            st[i + 1, 0], st[i + 1, 1], st[i + 1, 2], st[i + 1, 3] = int(b), p[0], p[1], int(n)
+        if self.nccl:
+            with torch.cuda.stream(self.stream):
+                self.send.copy_(st, non_blocking=True)
+                dist.all_gather_into_tensor(self.recv.view(-1, 4), self.send, group=self.group)
+                host = self.recv.cpu()  # waits on this side stream only
+        else:
+            self.send.copy_(st)
+            dist.all_gather_into_tensor(self.recv.view(-1, 4), self.send, group=self.group)
+            host = self.recv
+        out = []
+        for r in range(self.world):
+            n = int(host[r, 0, 0])
+            out.append([(int(x[0]), (int(x[1]), int(x[2])), int(x[3]))
+                        for x in host[r, 1:n + 1].tolist()])
         return out
 
 

@@ -36,29 +36,37 @@ def _run(args, timeout=900, ranks=1, **env_kw):
 
 
 def test_reference_arm_runs_on_the_host():
-    d = _run(["--impl", "reference", "--workload", "cfg1", "--steps", "2", "--warmup", "3",
-              "--cpu-seconds", "0.5"])
+    d = _run(["--impl", "reference", "--workload", "cfg1", "--steps", "2", "--warmup", "3"])
     assert d["impl"] == "reference" and d["value"] > 0
     assert KEYS <= set(d) and d["cpu_baseline"]["kind"] == "port"
     assert d["e2e"]["h2d_bytes_per_step"] == 0
 
 
 @pytest.mark.gpu
-def test_b200_arm_full_line_with_cpu_baseline():
-    d = _run(["--workload", "cfg1", "--steps", "6", "--warmup", "3", "--cpu-seconds", "0.5"])
-    assert KEYS <= set(d) and {"roofline", "gpu_launches", "clocks"} <= set(d)
+def test_b200_arm_full_line_with_cpu_baseline_and_parity():
+    args = ["--workload", "cfg1", "--steps", "12", "--warmup", "3"]
+    d = _run(args + ["--secondary", "none"])
+    assert KEYS <= set(d) and {"roofline", "gpu_launches", "clocks", "parity"} <= set(d)
     assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
     assert d["cpu_baseline"]["value"] > 0 and d["roofline"]["bound"] == "hbm"
+    p = d["parity"]
+    assert p["within_tolerance"] and p["events_identical"] and p["step"] == 15
+    ref = _run(["--impl", "reference"] + args)
+    assert ref["config"] == d["config"]  # both arms run the same workload
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("shard", ["sequences", "units"])
-def test_two_rank_paths_run_end_to_end(shard):
+@pytest.mark.parametrize("shard,launch", [("sequences", "torchrun"), ("slabs", "torchrun"),
+                                          ("slabs", "self"), ("units", "torchrun")])
+def test_two_rank_paths_run_end_to_end(shard, launch):
     """Functional check of the N>1 bench paths on one GPU: two ranks over gloo
-    (HC_BENCH_BACKEND; the driver's runs use NCCL, one GPU per rank).  Units
-    mode exercises the fire exchange and the all-gather of O; the numbers of
-    such a run are not measurements."""
-    d = _run(["--gpus", "2", "--shard", shard, "--workload", "cfg1", "--steps", "16",
-              "--warmup", "3"], ranks=2, HC_BENCH_BACKEND="gloo")
+    (HC_BENCH_BACKEND; the driver's runs use NCCL, one GPU per rank).  Slab and
+    unit modes exercise the fire exchange and the all-gather of O; "self" is
+    `bench.py --gpus 2` re-launching itself under torchrun.  The numbers of such
+    a run are not measurements."""
+    d = _run(["--gpus", "2", "--shard", shard, "--workload", "cfg2", "--layers", "4",
+              "--steps", "16", "--warmup", "3", "--calib-samples", "2"],
+             ranks=2 if launch == "torchrun" else 1, HC_BENCH_BACKEND="gloo")
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0
-    assert d["scaling"] == ("strong" if shard == "units" else "weak")
+    assert d["scaling"] == ("weak" if shard == "sequences" else "strong")
+    assert d["config"]["parallelism"].startswith(shard)
