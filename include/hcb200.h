@@ -301,6 +301,11 @@ int hc_engine_fire_batch(hc_engine* eng, int32_t n, const int32_t* pivot_units, 
                          const int32_t* completion_steps, int32_t* transfer_ids,
                          uint32_t* fetched_host, void* stream);
 
+/* Block the calling host thread until the last fire batch's selection and
+ * fetched-set copies (fetched_host) are done -- only those, on the engine's
+ * side stream, not the work queued on the caller's stream since. */
+int hc_engine_wait_fetched(hc_engine* eng);
+
 /* Landing of a due transfer (engine.py:293-299): applied inside the next
  * decode step (or before the next call that reads engine state), where the
  * step's stream waits for the gather after attending every other unit; the
@@ -351,6 +356,16 @@ int hc_engine_prefill_stats(hc_engine* eng, double* out3);
 
 /* Number of attention tiles (CTAs) the step launches. */
 int hc_engine_active_tiles(const hc_engine* eng, int32_t step, int32_t* n_tiles);
+
+/* ---------------------------------------------------------------------------
+ * Synthetic workload generator (bench inputs; no reference counterpart).
+ *
+ * out_dev[i] = N(key, offset + i) as fp32: splitmix64 of the counter, an
+ * Irwin-Hall(4) normal from its four 16-bit fields, every step exact or one
+ * IEEE rounding -- bit-identical to the host twin oracle/synth.c, so the CPU
+ * arms of bench.py decode the same K/V/Q (workload.SyntheticKV).
+ * ------------------------------------------------------------------------- */
+int hc_synth_normal(float* out_dev, int64_t n, uint64_t key, int64_t offset, void* stream);
 
 #ifdef __cplusplus
 }

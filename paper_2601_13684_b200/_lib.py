@@ -77,6 +77,7 @@ def _declare(lib):
         "hc_engine_overlaps": (i32, [vp, i32, i32, vp, vp]),
         "hc_engine_fire": (i32, [vp, i32, i32, i32, vp, vp]),
         "hc_engine_land": (i32, [vp, i32, vp]),
+        "hc_engine_wait_fetched": (i32, [vp]),
         "hc_engine_fire_batch": (i32, [vp, i32, vp, i32, vp, vp, vp, vp]),
         "hc_engine_land_batch": (i32, [vp, i32, vp, vp]),
         "hc_engine_read_indices": (i32, [vp, i32, i32, vp, i32, vp, vp]),

@@ -226,6 +226,8 @@ struct EngineImpl {
   size_t stage_cap = 0, stage_head = 0;
   std::deque<std::tuple<size_t, size_t, cudaEvent_t>> stage_busy;  // (lo, hi, copy done)
   cudaStream_t retr = nullptr;
+  cudaMemPool_t mpool = nullptr;  // private stream-ordered pool (descriptors, transfer blocks)
+  cudaEvent_t last_selected = nullptr;  // side stream: the last fire batch's copies are done
   // per-step phase timeline (bench roofline): 7 events per step: start |
   // append | K4 | combine (step stream) | score rows | monitor (monitor
   // stream) | end (step stream)
@@ -317,6 +319,7 @@ int engine_destroy(EngineImpl& e) {
     if (e.pool_host) cudaFreeHost(e.pool);
     else cudaFree(e.pool);
   }
+  if (e.mpool) cudaMemPoolDestroy(e.mpool);  // every block above is freed by now
   if (e.retr) cudaStreamDestroy(e.retr);
   if (e.side) cudaStreamDestroy(e.side);
   if (e.mon) cudaStreamDestroy(e.mon);
@@ -546,11 +549,19 @@ int engine_create(EngineImpl& e, const hc_engine_desc& c, const int32_t* roles,
       HC_TRY(dalloc((void**)&e.pool, bytes, &e.dev_bytes));
     }
   }
-  {  // keep stream-ordered allocations (fire / land descriptors) cached in the pool
+  {  // a private stream-ordered pool for the engine's fire / land descriptors and
+     // transfer blocks: its settings must not leak into the process's default
+     // pool (torch's cudaMallocAsync backend, other libraries); destroyed with
+     // the engine
     int dev = 0;
-    cudaMemPool_t pool;
     HC_CUDA_TRY(cudaGetDevice(&dev));
-    HC_CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, dev));
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    HC_CUDA_TRY(cudaMemPoolCreate(&e.mpool, &props));
+    cudaMemPool_t pool = e.mpool;
+    // keep freed blocks cached in the pool (no release back to the driver)
     uint64_t keep = ~uint64_t(0);
     HC_CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
     // a block freed on one stream (a superseded transfer, on the caller's) must
@@ -568,7 +579,7 @@ int engine_create(EngineImpl& e, const hc_engine_desc& c, const int32_t* roles,
         if (e.sat_slot[u] >= 0) per += (2 * size_t(std::max(1, e.cap[u])) + 8) * 4;
       const size_t want = std::min<size_t>(per * 16, size_t(1) << 30);
       void* tmp = nullptr;
-      if (cudaMallocAsync(&tmp, want, 0) == cudaSuccess) {
+      if (cudaMallocFromPoolAsync(&tmp, want, pool, 0) == cudaSuccess) {
         HC_CUDA_TRY(cudaFreeAsync(tmp, 0));
         HC_CUDA_TRY(cudaStreamSynchronize(0));
       } else {
@@ -636,6 +647,7 @@ int gc_events(EngineImpl& e, int t) {
       live.push_back(e.xfers[id].selected);
       live.push_back(e.xfers[id].done);
     }
+  if (e.last_selected) live.push_back(e.last_selected);
   for (const auto& pr : e.gather_ev) live.push_back(pr.first), live.push_back(pr.second);
   for (const auto& pr : e.land_ev) live.push_back(pr.first), live.push_back(pr.second);
   std::sort(live.begin(), live.end());
@@ -824,7 +836,7 @@ int engine_decode_step(EngineImpl& e, int t, const void* q, const void* kn, cons
 }
 
 // Stream-ordered upload of a small host array: copy into the pinned staging
-// ring, cudaMallocAsync a device buffer on `st` and copy asynchronously.  The
+// ring, allocate a device buffer on `st` from the engine's pool and copy asynchronously.  The
 // caller frees *dev with cudaFreeAsync on the same stream.
 int upload(EngineImpl& e, const void* src, size_t bytes, cudaStream_t st, void** dev) {
   const size_t need = (bytes + 255) & ~size_t(255);
@@ -843,7 +855,7 @@ int upload(EngineImpl& e, const void* src, size_t bytes, cudaStream_t st, void**
     }
   }
   std::memcpy(e.stage + lo, src, bytes);
-  HC_CUDA_TRY(cudaMallocAsync(dev, need, st));
+  HC_CUDA_TRY(cudaMallocFromPoolAsync(dev, need, e.mpool, st));
   HC_CUDA_TRY(cudaMemcpyAsync(*dev, e.stage + lo, bytes, cudaMemcpyHostToDevice, st));
   cudaEvent_t ev;
   HC_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -1293,7 +1305,7 @@ int engine_fire_batch(EngineImpl& e, int n, const int32_t* pus, int t, const int
   uint32_t* blk = nullptr;
   const int block_id = e.next_block++;
   if (m) {
-    HC_CUDA_TRY(cudaMallocAsync((void**)&blk, words_total * 4, st));
+    HC_CUDA_TRY(cudaMallocFromPoolAsync((void**)&blk, words_total * 4, e.mpool, st));
     e.blocks[block_id] = EngineImpl::XferBlock{blk, int(m)};
   }
   size_t a_sel = 0, a_pos = o_pos;
@@ -1367,6 +1379,7 @@ int engine_fire_batch(EngineImpl& e, int n, const int32_t* pus, int t, const int
   cudaEvent_t selected;
   HC_TRY(new_event(e, &selected));
   HC_CUDA_TRY(cudaEventRecord(selected, st));
+  e.last_selected = selected;  // after the fetched-set D2H copies (hc_engine_wait_fetched)
   HC_CUDA_TRY(cudaStreamWaitEvent(caller, selected, 0));
   std::vector<int> now;
   for (int id : new_ids) {
@@ -1876,6 +1889,13 @@ extern "C" int hc_engine_fire_batch(hc_engine* eng, int32_t n, const int32_t* pi
   HC_TRY(hc::flush_deferred(eng->e));  // pending landings first
   return hc::engine_fire_batch(eng->e, n, pivot_units, step, completion_steps, transfer_ids,
                                fetched_host, (cudaStream_t)stream);
+}
+
+extern "C" int hc_engine_wait_fetched(hc_engine* eng) {
+  HC_REQUIRE(eng, HC_EINVAL, "null argument");
+  // only the side stream's selection and fetched-set copies, not the caller's queue
+  if (eng->e.last_selected) HC_CUDA_TRY(cudaEventSynchronize(eng->e.last_selected));
+  return HC_OK;
 }
 
 extern "C" int hc_engine_land(hc_engine* eng, int32_t transfer_id, void* stream) {

@@ -112,7 +112,7 @@ class HeteroCacheDecoder:
                  host_pool: bool = True, bytes_per_kv_entry: int | None = None,
                  track_sets: bool = True, obs_window: int = 1, overlap_decisions: bool = True,
                  recall_topk: int = 0, owned=None, exchange=None,
-                 score_material: str = "fp32"):
+                 score_material: str = "fp32", fetch_ring_entries: int | None = None):
         """owned: optional [batch, layers, kv_heads] bool mask of the units this
         rank holds (parallel.assign_units; None = all).  exchange: the fire
         exchange of a unit-sharded run (parallel.FireExchange); every rank of
@@ -120,7 +120,9 @@ class HeteroCacheDecoder:
         score_material: "fp32" (default) or "fp16", the per-token pivot material
         K4 hands to the GQA-mean row pass; fp16 halves those bytes but its
         ~5e-4 relative row error moves near-tied positions across the top-k
-        boundary (profiles/r02_selection_precision.json)."""
+        boundary (profiles/r02_selection_precision.json).
+        fetch_ring_entries: size of the pinned ring the fetched sets land in
+        (default: four full drift bursts, at least 64K entries)."""
         _lib.require_cuda()
         self.lib = _lib.load()
         self.taxonomy, self.plan, self.config = taxonomy, plan, config
@@ -198,7 +200,8 @@ class HeteroCacheDecoder:
                       else [] for b in range(self.B)]
         self._pinned = None
         self._pin_head = 0
-        self._fetch_ev = None
+        self._ring_entries = fetch_ring_entries
+        self._fetch_pending = False
         self._uncollected = []
         np.median(np.zeros((2, 2)), axis=0)  # first call imports numpy.ma (~30 ms): not mid-run
         self._prefilled = set()
@@ -287,8 +290,8 @@ class HeteroCacheDecoder:
 
             cap = sum(self.effective_length(s) for b in range(self.B) for p in self.piv_of[b]
                       for s in self.satellites_of[p])
-            self._pinned = torch.empty(max(4 * cap, 1 << 16), dtype=torch.int32,
-                                       pin_memory=True)  # four full drift bursts
+            n = self._ring_entries or max(4 * cap, 1 << 16)  # four full drift bursts
+            self._pinned = torch.empty(max(n, cap), dtype=torch.int32, pin_memory=True)
             self._pin_head = 0
 
     # ---- decode -------------------------------------------------------------------
@@ -491,13 +494,7 @@ class HeteroCacheDecoder:
                                                  d.ctypes.data, ids.ctypes.data,
                                                  self._pinned.data_ptr() + 4 * base, sh))
         self._pin_head = base + total
-        # the caller's stream waits for the fetched-set copies: an event on it from
-        # here marks this batch's part of the ring readable
-        import torch
-
-        self._fetch_ev = torch.cuda.Event()
-        self._fetch_ev.record(torch.cuda.default_stream() if not sh else
-                              torch.cuda.ExternalStream(sh))
+        self._fetch_pending = True  # hc_engine_wait_fetched marks the ring readable
         return ids, base
 
     def _record_fires(self, t: int, local, done_of, ids, base) -> None:
@@ -529,8 +526,8 @@ class HeteroCacheDecoder:
         # engine.py:293-296; re-sort only if that ever does not hold
         for st in unsorted:
             st.pending.sort(key=lambda x: (x[0], x[1]))
-        if self.track_sets:
-            self.sync()
+        if self.track_sets:  # the host mirror needs the sets: wait for their copies only
+            self._drain_fetched()
 
     def _reserve_pinned(self, total: int) -> None:
         """Fetched sets land in a pinned ring; collect lazily, only before reuse."""
@@ -545,10 +542,11 @@ class HeteroCacheDecoder:
             self._pin_head = 0
 
     def _drain_fetched(self) -> None:
-        """Wait for the copies into the ring (the last batch's event), not for the
-        whole GPU queue, then copy the ring out."""
-        if self._fetch_ev is not None:
-            self._fetch_ev.synchronize()
+        """Wait for the copies into the ring (the engine's side-stream event of the
+        last fire batch), not for the caller's queue, then copy the ring out."""
+        if self._fetch_pending:
+            _lib.check(self.lib.hc_engine_wait_fetched(self.handle))
+            self._fetch_pending = False
         self._collect_fetched()
 
     def _collect_fetched(self) -> None:

@@ -59,7 +59,7 @@ def topk_rows(idx, scores, k, base_bitmaps=None):
     """
     torch = _torch()
     _lib.require_cuda()
-    sc = torch.as_tensor(np.ascontiguousarray(scores, dtype=np.float32)).cuda()
+    sc = torch.from_numpy(np.array(scores, dtype=np.float32, order="C")).cuda()
     R, K = sc.shape
     ix = None
     if idx is not None:

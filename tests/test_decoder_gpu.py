@@ -35,7 +35,7 @@ ROW_RTOL = 2e-3
 def _build(variant="heterocache", delay=1, bandwidth=1 << 30, B=2, NL=2, L=700, T=40,
            chunk=256, host_pool=True, window=8, eval_every_step=False, shift=13, seed=3,
            obs_window=1, sinks=4, recency=8, overlap_decisions=True, recall_topk=0,
-           heads=(16, 4)):
+           heads=(16, 4), **dec_kw):
     import torch
 
     from paper_2601_13684_b200.decoder import HeteroCacheDecoder
@@ -53,7 +53,8 @@ def _build(variant="heterocache", delay=1, bandwidth=1 << 30, B=2, NL=2, L=700, 
                        recency_window=recency)
     dec = HeteroCacheDecoder(tax, plan, cfg, batch=B, group=model.group, max_decode=T,
                              chunk=chunk, host_pool=host_pool, obs_window=obs_window,
-                             overlap_decisions=overlap_decisions, recall_topk=recall_topk)
+                             overlap_decisions=overlap_decisions, recall_topk=recall_topk,
+                             **dec_kw)
     gen = SyntheticKV(model, batch=B, prefill_len=L, num_layers=NL, hot=plan.l_base_int,
                       seed=seed)
     dump = torch.zeros(NL, B * model.kv_heads, L, device="cuda")
@@ -391,3 +392,21 @@ def test_randomized_configs_match_oracle(seed):
     ctx = _build(**kw)
     rows, _, _, _ = _run(ctx)
     _check_events(ctx, rows)
+
+
+def test_fetched_ring_wraps_without_track_sets():
+    """track_sets=False (the bench's mode) collects fetched sets lazily from a
+    pinned ring; a ring a few transfers long must wrap (drain, then reuse) many
+    times and still yield the same events as the track_sets=True run."""
+    kw = dict(B=2, T=48, window=4, shift=(5, 9, 13, 17, 21, 25, 29, 33, 37, 41), L=600)
+    logs = []
+    for track, ring in ((True, None), (False, 200)):
+        ctx = _build(track_sets=track, fetch_ring_entries=ring, **kw)
+        rows, _, _, _ = _run(ctx)
+        ctx["dec"].sync()  # collect the last fetched sets from the ring
+        if track:
+            _check_events(ctx, rows)
+        logs.append([[(e.trigger_step, e.pivot, e.completion_step, e.transfer_bytes, e.fetches)
+                      for e in st.events] for st in ctx["dec"].states])
+        ctx["dec"].close()
+    assert logs[0] == logs[1] and sum(len(x) for x in logs[0]) >= 10
