@@ -102,6 +102,9 @@ def parse(argv=None):
                          "sequences = every rank its own batch (weak)")
     ap.add_argument("--score-material", choices=("fp32", "fp16"), default="fp32",
                     help="pivot score material between K4 and the GQA-mean rows")
+    ap.add_argument("--decisions", choices=("device", "host"), default="device",
+                    help="boundary decisions on the device (devdec.cu; default where supported) "
+                         "or on the host")
     ap.add_argument("--link-mib-per-step", type=float, default=0.0,
                     help="EngineConfig.transfer_bandwidth in MiB per decode step (host link "
                          "model); 0: the workload's measured-link value")
@@ -273,6 +276,7 @@ def make_config(args, w, cfg, rho, l_base_int, roles: dict, world: int, mode: st
         "split_k_chunk": args.chunk, "start_step": args.start_step,
         "transfer_bandwidth_bytes_per_step": cfg.transfer_bandwidth,
         "score_material": args.score_material,
+        "decisions": args.decisions,
         "l2": "inputs larger than L2 (resident K/V per step >> 126 MB)",
         "parallelism": par,
     }
@@ -322,7 +326,8 @@ def run_b200(args, rank, world):
     lib = _lib.load()
     obs = obs_of(args, w)
     dkw = dict(batch=w.batch, group=m.group, max_decode=T, chunk=args.chunk, host_pool=True,
-               track_sets=False, obs_window=obs, score_material=args.score_material)
+               track_sets=False, obs_window=obs, score_material=args.score_material,
+               device_decisions=None if args.decisions == "device" else False)
     mode = shard_mode(args, w, world)
     owned_all = None
     if mode in ("slabs", "units"):

@@ -196,6 +196,19 @@ typedef struct hc_engine_desc {
                           /* 0 = fp32 e = 2^(x - m) (default: rows within fp32       */
                           /* rounding of the oracle's), 1 = fp16 (half the bytes,    */
                           /* ~5e-4 relative row error)                               */
+  /* Device-resident boundary decisions (devdec): 1 = the window median test,
+   * byte / completion accounting, fetch selection, gathers and landings run on
+   * device streams (engine.py:293-357) and the host only mirrors them
+   * (hc_engine_poll_decisions); the step never waits for the host.  The
+   * EngineConfig knobs below are then required (engine.py:52-79). */
+  int32_t device_decisions;
+  int32_t window;             /* EngineConfig.window (<= 64)                      */
+  int32_t update_delay_steps; /* EngineConfig.update_delay_steps                  */
+  int32_t eval_every_step;    /* EngineConfig.eval_every_step (sliding window)    */
+  int32_t bytes_per_kv_entry; /* transfer bytes per fetched index                 */
+  int32_t pad_;
+  int64_t transfer_bandwidth; /* EngineConfig.transfer_bandwidth, bytes per step  */
+  double tau_drift;           /* EngineConfig.tau_drift                           */
 } hc_engine_desc;
 
 /* CacheEngine.__init__ (engine.py:156-214): allocate and lay out the store.
@@ -300,6 +313,33 @@ int hc_engine_fire(hc_engine* eng, int32_t pivot_unit, int32_t step, int32_t com
 int hc_engine_fire_batch(hc_engine* eng, int32_t n, const int32_t* pivot_units, int32_t step,
                          const int32_t* completion_steps, int32_t* transfer_ids,
                          uint32_t* fetched_host, void* stream);
+
+/* Device decisions: one fire of a boundary (engine.py:322-347), as decided on
+ * the device.  Fires are listed per sequence, in sorted pivot order. */
+typedef struct hc_fire_record {
+  int32_t trigger_step, pivot_unit, completion_step, n_satellites;
+  int64_t transfer_bytes, cumulative_bytes;
+  int32_t first_satellite;  /* index into hc_engine_devdec_satellites()            */
+  int32_t fetched_offset;   /* the satellites' fetched sets, concatenated, at this */
+                            /* offset of fetched_out (-1: not available)           */
+  int32_t fetched_counts[8];
+} hc_fire_record;
+
+/* Device decisions: the next boundary not yet read, in step order.  wait = 0:
+ * returns *step_out = -1 if its decision has not completed yet; wait = 1:
+ * blocks on it (and returns -1 only when no boundary is outstanding).  Fills
+ * fires[0 .. *n_fires_out) and the fetched sets (ascending positions) into
+ * fetched_out (capacity entries; HC_EINVAL with the needed size in
+ * *n_fires_out if too small).  Reports device-side faults (a satellite's
+ * transfer ring overflowing, a landing wait timing out) as HC_ESTATE. */
+int hc_engine_poll_decisions(hc_engine* eng, int32_t wait, int32_t* step_out,
+                             hc_fire_record* fires, int32_t fire_capacity, int32_t* n_fires_out,
+                             uint32_t* fetched_out, int64_t fetched_capacity);
+/* Device decisions: the unit of every satellite, in the order
+ * hc_fire_record.first_satellite indexes (pivot slots ascending, each pivot's
+ * satellites by head). */
+int hc_engine_devdec_satellites(hc_engine* eng, int32_t* units_out, int32_t capacity,
+                                int32_t* n_out);
 
 /* Block the calling host thread until the last fire batch's selection and
  * fetched-set copies (fetched_host) are done -- only those, on the engine's

@@ -38,7 +38,17 @@ class EngineDesc(C.Structure):
     _fields_ = [(n, C.c_int32) for n in (
         "batch", "num_layers", "kv_heads", "group", "head_dim", "prefill_len", "max_decode",
         "sink_count", "recency_window", "l_base_int", "chunk", "monitor", "host_pool",
-        "obs_window", "score_material")]
+        "obs_window", "score_material", "device_decisions", "window", "update_delay_steps",
+        "eval_every_step", "bytes_per_kv_entry", "pad_")] + [
+        ("transfer_bandwidth", C.c_int64), ("tau_drift", C.c_double)]
+
+
+class FireRecord(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in (
+        "trigger_step", "pivot_unit", "completion_step", "n_satellites")] + [
+        ("transfer_bytes", C.c_int64), ("cumulative_bytes", C.c_int64),
+        ("first_satellite", C.c_int32), ("fetched_offset", C.c_int32),
+        ("fetched_counts", C.c_int32 * 8)]
 
 
 class RecallHead(C.Structure):
@@ -78,6 +88,8 @@ def _declare(lib):
         "hc_engine_fire": (i32, [vp, i32, i32, i32, vp, vp]),
         "hc_engine_land": (i32, [vp, i32, vp]),
         "hc_engine_wait_fetched": (i32, [vp]),
+        "hc_engine_poll_decisions": (i32, [vp, i32, vp, vp, i32, vp, vp, C.c_int64]),
+        "hc_engine_devdec_satellites": (i32, [vp, vp, i32, vp]),
         "hc_engine_fire_batch": (i32, [vp, i32, vp, i32, vp, vp, vp, vp]),
         "hc_engine_land_batch": (i32, [vp, i32, vp, vp]),
         "hc_engine_read_indices": (i32, [vp, i32, i32, vp, i32, vp, vp]),

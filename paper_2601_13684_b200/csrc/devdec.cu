@@ -1,0 +1,396 @@
+// Device-resident boundary decisions: kernels (see devdec.cuh).
+//
+// Reference semantics (engine.py:293-357), restated on the device:
+//   * the window test fires iff median(overlap / l_base_int) < tau_drift --
+//     values and the mean of the middle pair in float64, exactly as
+//     statistics.median / np.median compute them (engine.py:247-250);
+//   * per sequence, fires are accounted in sorted pivot order (engine.py:313):
+//     bytes = sum over satellites of min(l_s, L + t) * bytes_per_kv_entry,
+//     cumulative += bytes, completion = max(t + delay, ceil(cumulative / bw))
+//     with a correctly rounded float64 division (engine.py:330-337);
+//   * every pending transfer with completion <= t lands at step t in
+//     (completion, order) order (engine.py:293-299); a transfer followed by
+//     one of the same satellite with the same completion is overwritten in
+//     the same step and never served, so it is never gathered.
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "devdec.cuh"
+#include "retrieval.cuh"
+
+namespace hc {
+namespace {
+
+__device__ __forceinline__ DevXfer& xf(const DevDec& d, int sat, int64_t ring_idx) {
+  return d.xfers[size_t(sat) * kQ + size_t(ring_idx % kQ)];
+}
+
+__device__ __forceinline__ int32_t vload(const int32_t* p) {
+  return *reinterpret_cast<const volatile int32_t*>(p);
+}
+
+// median of n float64 values (insertion sort; n <= 64)
+__device__ double median_of(double* v, int n) {
+  for (int i = 1; i < n; ++i) {
+    const double x = v[i];
+    int j = i - 1;
+    while (j >= 0 && v[j] > x) {
+      v[j + 1] = v[j];
+      --j;
+    }
+    v[j + 1] = x;
+  }
+  return (n & 1) ? v[n / 2] : (v[n / 2 - 1] + v[n / 2]) / 2.0;
+}
+
+constexpr int kMaxPiv = 8192;
+
+// One CTA.  Boundary mode: the window's values are overlap ring rows first ..
+// first + nvals - 1.  Sliding mode (eval_every_step): this step's value joins
+// the pivot's buffer; the test runs once it holds >= window values and clears
+// it on a fire (engine.py:313-321, 358-360).  Then, per sequence in order and
+// per pivot in sorted order (engine.py:313), the fires' accounting.
+__global__ void __launch_bounds__(1024) decide_kernel(DevDec d, int t, int first, int nvals,
+                                                      int bidx, const uint32_t* __restrict__ ovl,
+                                                      int ring) {
+  __shared__ uint8_t fired[kMaxPiv];
+  const double lb = double(d.lbase);
+  for (int s = threadIdx.x; s < d.n_piv; s += blockDim.x) {
+    double v[64];
+    bool f = false;
+    if (!d.sliding) {
+      for (int j = 0; j < nvals; ++j) v[j] = double(ovl[size_t((first + j) % ring) * d.n_piv + s]) / lb;
+      f = nvals > 0 && median_of(v, nvals) < d.tau;
+    } else {
+      int c = d.scnt[s];
+      d.svals[size_t(s) * 64 + (c % 64)] = double(ovl[size_t(t % ring) * d.n_piv + s]) / lb;
+      ++c;
+      if (c >= d.window) {
+        for (int j = 0; j < d.window; ++j) v[j] = d.svals[size_t(s) * 64 + ((c - d.window + j) % 64)];
+        f = median_of(v, d.window) < d.tau;
+        if (f) c = 0;  // the buffer is cleared on a fire
+      }
+      d.scnt[s] = c;
+    }
+    fired[s] = f ? 1 : 0;
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  BoundaryHdr* hdr = d.hdr + (bidx % kLogRing);
+  FireLog* log = d.log + size_t(bidx % kLogRing) * d.n_piv;
+  const uint32_t* hist = d.ghist + size_t(t & 1) * d.n_piv * 8192;
+  int n_fires = 0;
+  uint32_t n_jobs = 0, n_rest = 0;
+  for (int b = 0; b < d.B; ++b) {
+    int64_t cum = d.cum[b];
+    int32_t ord = d.order[b];
+    for (int s = d.seq_piv[b]; s < d.seq_piv[b + 1]; ++s) {
+      if (!fired[s]) continue;
+      const int a0 = d.piv_sat_begin[s], a1 = d.piv_sat_begin[s + 1];
+      const int ns = a1 - a0;
+      int32_t ks[8];
+      int64_t n_ent = 0;
+      for (int i = 0; i < ns && i < 8; ++i) {
+        const int k = min(d.sats[a0 + i].k, d.L + t);
+        ks[i] = k;
+        n_ent += k;
+      }
+      if (ns > 8) atomicExch(d.error, int(kDDTooManySats));
+      const int64_t nbytes = n_ent * d.bpe;
+      cum += nbytes;
+      const int32_t completion = max(t + d.delay, int32_t(ceil(double(cum) / double(d.bw))));
+      // fetched sets for the host mirror: one contiguous span of the mapped ring
+      int64_t head = *d.fetched_head;
+      int64_t phys = head % d.fetched_cap;
+      if (phys + n_ent > d.fetched_cap) {  // no wrap inside a span: skip to the ring start
+        head += d.fetched_cap - phys;
+        phys = 0;
+      }
+      int32_t host_off = int32_t(phys);
+      if (head + n_ent - *d.fetched_tail > d.fetched_cap || n_ent > d.fetched_cap) {
+        atomicExch(d.error, int(kDDHostRingFull));
+        host_off = -1;
+      } else {
+        *d.fetched_head = head + n_ent;
+      }
+      int64_t hoff = host_off;
+      for (int i = 0; i < ns && i < 8; ++i) {
+        DevSat& sat = d.sats[a0 + i];
+        const int64_t idx = sat.tail;
+        if (idx - sat.head >= kQ) {
+          atomicExch(d.error, int(kDDRingFull));
+          continue;
+        }
+        DevXfer& x = xf(d, a0 + i, idx);
+        const int slot = int(idx % kQ);
+        x.completion = completion;
+        x.order = ord++;
+        x.trigger = t;
+        x.k = ks[i];
+        x.buf = -1;
+        x.host_off = host_off < 0 ? -1 : int32_t(hoff);
+        x.cnt = 0;
+        x.done_ctas = 0;
+        x.state = kXAlloc;
+        FireJob& jb = d.jobs[n_jobs++];
+        jb.row = d.rowbuf + size_t(s) * d.row_len;
+        jb.hist = hist + size_t(s) * 8192;
+        jb.n = uint32_t(d.L + t);
+        jb.k = uint32_t(ks[i]);
+        jb.out_idx = sat.sel + size_t(slot) * sat.k;
+        jb.out_count = &x.cnt;
+        jb.host_out = host_off < 0 ? nullptr : d.fetched + hoff;
+        jb.state_out = &x.state;
+        hoff += ks[i];
+        __threadfence();
+        sat.tail = idx + 1;
+      }
+      d.restamp_slots[n_rest++] = s;
+      FireLog& lg = log[n_fires++];
+      lg.trigger = t;
+      lg.pivot_unit = d.piv_unit[s];
+      lg.completion = completion;
+      lg.n_sats = ns;
+      lg.bytes = nbytes;
+      lg.cum_after = cum;
+      lg.first_sat = a0;
+      lg.host_off = host_off;
+      for (int i = 0; i < 8; ++i) lg.ks[i] = i < ns ? ks[i] : 0;
+    }
+    d.cum[b] = cum;
+    d.order[b] = ord;
+  }
+  *d.n_jobs = n_jobs;
+  *d.n_restamp = n_rest;
+  hdr->t = t;
+  hdr->n_fires = n_fires;
+  hdr->head_after = *d.fetched_head;
+  __threadfence_system();
+  hdr->pad = 1;  // written: the host reads this boundary once its event completed
+}
+
+constexpr int kSchedMax = 2048;  // one item per satellite per pass (n_sat beyond: next pass)
+
+// Which selected transfers can be gathered now, in (completion, sequence,
+// order) order.  One CTA; every satellite is visited by one thread.
+__global__ void __launch_bounds__(1024) schedule_kernel(DevDec d) {
+  __shared__ GatherItem items[kSchedMax];
+  __shared__ uint32_t n_items;
+  if (threadIdx.x == 0) n_items = 0;
+  __syncthreads();
+  for (int si = threadIdx.x; si < d.n_sat; si += blockDim.x) {
+    DevSat& sat = d.sats[si];
+    const int64_t tail = *reinterpret_cast<volatile int64_t*>(&sat.tail);
+    for (int64_t i = sat.head; i < tail; ++i) {
+      DevXfer& x = xf(d, si, i);
+      const int32_t st = vload(&x.state);
+      if (st == kXAlloc) break;  // selection still pending (ring order)
+      if (st != kXSelected) continue;  // scheduled / gathered / superseded
+      if (i + 1 < tail && xf(d, si, i + 1).completion == x.completion) {
+        x.state = kXSuperseded;  // overwritten in its landing step: never read
+        continue;
+      }
+      int target;
+      if (sat.staging_owner < 0) {
+        target = 1 - sat.active;
+      } else {
+        DevXfer& z = xf(d, si, sat.staging_owner);
+        if (vload(&z.state) == kXGathered && z.completion == x.completion) {
+          target = z.buf;  // z lands in the same step and is overwritten at once
+          z.state = kXSuperseded;
+        } else {
+          break;  // staging busy until an earlier transfer lands
+        }
+      }
+      x.buf = target;
+      x.state = kXScheduled;
+      sat.staging_owner = int32_t(i);
+      const uint32_t at = atomicAdd(&n_items, 1u);
+      if (at < kSchedMax) items[at] = GatherItem{si, int32_t(i % kQ), x.completion, x.order};
+      break;
+    }
+  }
+  __syncthreads();
+  const uint32_t n = min(n_items, uint32_t(kSchedMax));
+  // rank sort by (completion, sequence, order): earliest deadline first
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const GatherItem a = items[i];
+    const int sa = d.sats[a.sat].seq;
+    uint32_t r = 0;
+    for (uint32_t j = 0; j < n; ++j) {
+      const GatherItem c = items[j];
+      const int sc = d.sats[c.sat].seq;
+      const bool less = c.completion < a.completion ||
+                        (c.completion == a.completion &&
+                         (sc < sa || (sc == sa && (c.order < a.order ||
+                                                   (c.order == a.order && j < i)))));
+      r += less ? 1u : 0u;
+    }
+    d.glist[r] = a;
+  }
+  if (threadIdx.x == 0) *d.n_glist = n;
+}
+
+__global__ void __launch_bounds__(256) build_dev_kernel(DevDec d) {
+  if (blockIdx.x >= *d.n_glist) return;
+  const GatherItem it = d.glist[blockIdx.x];
+  const DevSat& sat = d.sats[it.sat];
+  DevXfer& x = d.xfers[size_t(it.sat) * kQ + it.slot];
+  build_positions_block(sat.sel + size_t(it.slot) * sat.k, int(x.cnt),
+                        sat.pos + size_t(it.slot) * sat.cap, x.meta, d.L, d.S, d.R,
+                        x.completion);
+}
+
+// 40 CTAs stream the scheduled transfers' rows from the pinned host pool
+// (zero-copy, as gather_host_rows_kernel); the last CTA through a transfer
+// flags it GATHERED.
+__global__ void __launch_bounds__(256) gather_dev_kernel(DevDec d, uint4* __restrict__ K,
+                                                         uint4* __restrict__ V) {
+  const uint32_t n = *d.n_glist;
+  const int nw = gridDim.x * (blockDim.x >> 5);
+  const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  for (uint32_t i = 0; i < n; ++i) {
+    const GatherItem it = d.glist[i];
+    const DevSat& sat = d.sats[it.sat];
+    DevXfer& x = d.xfers[size_t(it.sat) * kQ + it.slot];
+    gather_rows(sat.pos + size_t(it.slot) * sat.cap, x.meta[0], sat.srcK, sat.srcV, K, V,
+                sat.row0[x.buf], gw, nw);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(&x.done_ctas, 1u) == gridDim.x - 1) {
+        __threadfence();
+        atomicExch(&x.state, int(kXGathered));
+      }
+    }
+  }
+}
+
+__device__ void land_one(const DevDec& d, DevSat& sat, DevXfer& x, int64_t idx, UnitDesc* units) {
+  UnitDesc& u = units[sat.unit];
+  u.row0 = sat.row0[x.buf];
+  u.n_prefix = x.meta[0];
+  u.tail_mask = uint32_t(x.meta[1]);
+  u.pad_ = x.meta[2];
+  sat.active = x.buf;
+  sat.cur_slot = int32_t(idx % kQ);
+  if (sat.staging_owner == int32_t(idx)) sat.staging_owner = -1;
+  sat.head = idx + 1;
+}
+
+// Landing point of step t (engine.py:293-299).  One CTA; thread per satellite.
+__global__ void __launch_bounds__(1024) land_kernel(DevDec d, int t, UnitDesc* units,
+                                                    uint4* __restrict__ K,
+                                                    uint4* __restrict__ V) {
+  __shared__ int32_t inl_sat[2048];
+  __shared__ int64_t inl_idx[2048];
+  __shared__ uint32_t n_inl;
+  for (int round = 0; round < 4; ++round) {
+    if (threadIdx.x == 0) n_inl = 0;
+    __syncthreads();
+    for (int si = threadIdx.x; si < d.n_sat; si += blockDim.x) {
+      DevSat& sat = d.sats[si];
+      while (sat.head < sat.tail) {
+        const int64_t i = sat.head;
+        DevXfer& x = xf(d, si, i);
+        if (x.completion > t) break;
+        int32_t st = vload(&x.state);
+        if (st == kXSuperseded) {
+          if (sat.staging_owner == int32_t(i)) sat.staging_owner = -1;
+          sat.head = i + 1;
+          continue;
+        }
+        if (st == kXSelected && i + 1 < sat.tail && xf(d, si, i + 1).completion == x.completion) {
+          x.state = kXSuperseded;
+          sat.head = i + 1;
+          continue;
+        }
+        if (st == kXScheduled) {  // in flight on the retrieval stream: wait (bounded)
+          const long long t0 = clock64();
+          while ((st = vload(&x.state)) == kXScheduled) {
+            __nanosleep(2000);
+            if (clock64() - t0 > (long long)8e9) {  // ~4 s
+              atomicExch(d.error, int(kDDSpinTimeout));
+              break;
+            }
+          }
+          if (st != kXGathered) break;
+        }
+        if (st == kXGathered) {
+          __threadfence();
+          land_one(d, sat, x, i, units);
+          continue;
+        }
+        // selected but never scheduled: its staging buffer was busy until a
+        // landing of this very pass -- gather it inline below
+        if (st == kXSelected) {
+          x.buf = 1 - sat.active;
+          x.state = kXScheduled;
+          sat.staging_owner = int32_t(i);
+          const uint32_t at = atomicAdd(&n_inl, 1u);
+          if (at < 2048) {
+            inl_sat[at] = si;
+            inl_idx[at] = i;
+          }
+        }
+        break;
+      }
+    }
+    __syncthreads();
+    const uint32_t n = min(n_inl, 2048u);
+    if (n == 0) break;
+    for (uint32_t q = 0; q < n; ++q) {  // the whole CTA gathers each inline transfer
+      const int si = inl_sat[q];
+      DevSat& sat = d.sats[si];
+      DevXfer& x = xf(d, si, inl_idx[q]);
+      const int slot = int(inl_idx[q] % kQ);
+      build_positions_block(sat.sel + size_t(slot) * sat.k, int(x.cnt),
+                            sat.pos + size_t(slot) * sat.cap, x.meta, d.L, d.S, d.R,
+                            x.completion);
+      gather_rows(sat.pos + size_t(slot) * sat.cap, x.meta[0], sat.srcK, sat.srcV, K, V,
+                  sat.row0[x.buf], threadIdx.x >> 5, blockDim.x >> 5);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        x.state = kXGathered;
+      }
+      __syncthreads();
+    }
+    // next round lands them (and anything due behind them)
+  }
+}
+
+}  // namespace
+
+int launch_decide(const DevDec& d, int t, int first, int nvals, int bidx, const uint32_t* ovl_ring,
+                  int ring, cudaStream_t st) {
+  HC_REQUIRE(nvals <= 64 && d.window <= 64, HC_EINVAL, "decision window > 64");
+  HC_REQUIRE(d.n_piv <= kMaxPiv, HC_EINVAL, "more than %d monitored pivots", kMaxPiv);
+  decide_kernel<<<1, 1024, 0, st>>>(d, t, first, nvals, bidx, ovl_ring, ring);
+  HC_CHECK_LAUNCH();
+  return HC_OK;
+}
+
+int launch_schedule(const DevDec& d, cudaStream_t st) {
+  schedule_kernel<<<1, 1024, 0, st>>>(d);
+  HC_CHECK_LAUNCH();
+  return HC_OK;
+}
+
+int launch_dev_gathers(const DevDec& d, uint4* K, uint4* V, cudaStream_t st) {
+  build_dev_kernel<<<std::max(1, d.n_sat), 256, 0, st>>>(d);
+  HC_CHECK_LAUNCH();
+  gather_dev_kernel<<<40, 256, 0, st>>>(d, K, V);
+  HC_CHECK_LAUNCH();
+  return HC_OK;
+}
+
+int launch_land(const DevDec& d, int t, UnitDesc* units, uint4* K, uint4* V, cudaStream_t st) {
+  land_kernel<<<1, 1024, 0, st>>>(d, t, units, K, V);
+  HC_CHECK_LAUNCH();
+  return HC_OK;
+}
+
+}  // namespace hc

@@ -32,6 +32,8 @@
 
 #include "hc_common.cuh"
 #include "kv_layout.cuh"
+#include "retrieval.cuh"
+#include "devdec.cuh"
 
 namespace hc {
 
@@ -48,12 +50,13 @@ int launch_obs_scores(const void* k, const void* q_obs, int B, int H, int G, int
 int launch_monitor(const float* rows, int64_t row_stride, const int32_t* slots, int n_rows,
                    uint32_t n, uint32_t k, const uint32_t* kbase, int words, uint64_t* thr,
                    uint32_t* ovl, cudaStream_t st, uint32_t* hist_out = nullptr);
-int launch_fire_select(const FireJob* jobs_dev, int n_jobs, cudaStream_t st);
+int launch_fire_select(const FireJob* jobs_dev, int n_jobs, cudaStream_t st,
+                       const uint32_t* n_jobs_dev = nullptr);
 int segmented_sort_desc_u64(void* temp, size_t* temp_bytes, const uint64_t* in, uint64_t* out,
                             int n_items, int n_segments, const int* offsets, cudaStream_t st);
 int launch_restamp_threshold(const float* rows, int64_t row_stride, const int32_t* slots,
                              int n_rows, uint32_t n, const uint64_t* thr, uint32_t* kbase,
-                             int words, cudaStream_t st);
+                             int words, cudaStream_t st, const uint32_t* n_rows_dev = nullptr);
 
 namespace {
 
@@ -272,6 +275,24 @@ struct EngineImpl {
   size_t mscratch_bytes = 0;
   int measured_t = -1;
 
+  // device-resident boundary decisions (devdec.cuh)
+  bool devdec = false;
+  DevDec dd{};
+  cudaStream_t sched = nullptr;         // schedule passes (tiny, never behind a gather)
+  cudaEvent_t ev_land = nullptr, ev_sched = nullptr, ev_sel = nullptr, ev_dec = nullptr;
+  bool sched_valid = false, sel_valid = false;
+  cudaEvent_t ev_log[kLogRing] = {};    // side stream: boundary decided and selected
+  int64_t n_bound = 0, n_read = 0;      // boundaries issued / read by the host
+  std::vector<int32_t> dd_sat_units;
+  std::vector<int32_t> dd_sat_of_unit;  // unit -> DevSat index or -1
+  std::vector<void*> dd_dev;            // device allocations of the devdec state
+  std::vector<void*> dd_host;           // mapped pinned allocations
+  BoundaryHdr* hdr_h = nullptr;
+  FireLog* log_h = nullptr;
+  uint32_t* fetched_h = nullptr;
+  int64_t* fetched_tail_h = nullptr;
+  int32_t* error_h = nullptr;
+
   int lh(int u) const { return u % (NL * H); }
   int mu_of(int u) const { const int b = u / (NL * H), l = (u / H) % NL, h = u % H;
                            return (l * B + b) * H + h; }
@@ -319,6 +340,13 @@ int engine_destroy(EngineImpl& e) {
     if (e.pool_host) cudaFreeHost(e.pool);
     else cudaFree(e.pool);
   }
+  for (void* p : e.dd_dev) cudaFree(p);
+  for (void* p : e.dd_host) cudaFreeHost(p);
+  for (cudaEvent_t x : {e.ev_land, e.ev_sched, e.ev_sel, e.ev_dec})
+    if (x) cudaEventDestroy(x);
+  for (cudaEvent_t x : e.ev_log)
+    if (x) cudaEventDestroy(x);
+  if (e.sched) cudaStreamDestroy(e.sched);
   if (e.mpool) cudaMemPoolDestroy(e.mpool);  // every block above is freed by now
   if (e.retr) cudaStreamDestroy(e.retr);
   if (e.side) cudaStreamDestroy(e.side);
@@ -326,6 +354,144 @@ int engine_destroy(EngineImpl& e) {
   if (e.pf_ev0) cudaEventDestroy(e.pf_ev0);
   if (e.pf_ev1) cudaEventDestroy(e.pf_ev1);
   for (auto x : e.tev) cudaEventDestroy(x);
+  return HC_OK;
+}
+
+// Device decisions: satellites in pivot-slot order, rings, mapped host log.
+int devdec_create(EngineImpl& e, const hc_engine_desc& c) {
+  HC_REQUIRE(c.monitor && e.n_piv > 0, HC_EINVAL, "device decisions need monitored pivots");
+  HC_REQUIRE(e.n_absent == 0, HC_EINVAL, "device decisions need an unsharded engine");
+  HC_REQUIRE(c.window >= 1 && c.window <= 64, HC_EINVAL, "window must be 1..64");
+  HC_REQUIRE(c.transfer_bandwidth >= 1 && c.update_delay_steps >= 0 && c.bytes_per_kv_entry >= 1,
+             HC_EINVAL, "bad device-decision parameters");
+  DevDec& d = e.dd;
+  d.n_piv = e.n_piv;
+  d.B = e.B;
+  d.L = e.L;
+  d.S = e.S;
+  d.R = e.R;
+  d.lbase = e.lbase;
+  d.window = c.window;
+  d.sliding = c.eval_every_step ? 1 : 0;
+  d.delay = c.update_delay_steps;
+  d.tau = c.tau_drift;
+  d.bw = c.transfer_bandwidth;
+  d.bpe = c.bytes_per_kv_entry;
+  d.rowbuf = e.rowbuf;
+  d.row_len = e.row_len;
+  d.ghist = e.ghist;
+  const int LH = e.NL * e.H;
+  std::vector<int32_t> seq_piv(e.B + 1, 0), psb{0}, punit(e.n_piv);
+  std::vector<DevSat> sats;
+  e.dd_sat_of_unit.assign(e.n_units, -1);
+  auto dev = [&](size_t bytes) -> void* {
+    void* p = nullptr;
+    if (dalloc(&p, bytes, &e.dev_bytes) != HC_OK) return nullptr;
+    e.dd_dev.push_back(p);
+    return p;
+  };
+  for (int s = 0; s < e.n_piv; ++s) {
+    const int pu = e.piv_units[s];
+    punit[s] = pu;
+    const int b = pu / LH, i = e.lh(pu), l = i / e.H, ph = i % e.H;
+    seq_piv[b + 1]++;
+    for (int h = 0; h < e.H; ++h) {
+      const int j = l * e.H + h;
+      if (e.role[j] != HC_ROLE_SATELLITE || e.cpivot[j] != ph) continue;
+      const int u = (b * e.NL + l) * e.H + h;
+      DevSat x{};
+      x.unit = u;
+      x.pivot_slot = s;
+      x.k = e.length[j];
+      x.cap = e.cap[u];
+      x.active = 0;
+      x.staging_owner = -1;
+      x.cur_slot = -1;
+      x.seq = b;
+      x.row0[0] = e.buf_row0[u];
+      x.row0[1] = e.buf_row1[u];
+      x.sel = static_cast<uint32_t*>(dev(size_t(kQ) * std::max(1, x.k) * 4));
+      x.pos = static_cast<uint32_t*>(dev(size_t(kQ) * std::max(1, x.cap) * 4));
+      HC_REQUIRE(x.sel && x.pos, HC_ENOMEM, "device decisions: transfer rings");
+      const __nv_bfloat16* sk = e.pool + size_t(e.sat_slot[u]) * 2 * e.L * kHeadDim;
+      x.srcK = reinterpret_cast<const uint4*>(sk);
+      x.srcV = reinterpret_cast<const uint4*>(sk + size_t(e.L) * kHeadDim);
+      e.dd_sat_of_unit[u] = int32_t(sats.size());
+      sats.push_back(x);
+      e.dd_sat_units.push_back(u);
+    }
+    psb.push_back(int32_t(sats.size()));
+  }
+  for (int b = 0; b < e.B; ++b) seq_piv[b + 1] += seq_piv[b];
+  d.n_sat = int32_t(sats.size());
+  const size_t ns = std::max<size_t>(1, sats.size());
+  auto up = [&](const void* src, size_t bytes) -> void* {
+    void* p = dev(bytes);
+    if (p && bytes) cudaMemcpy(p, src, bytes, cudaMemcpyHostToDevice);
+    return p;
+  };
+  d.seq_piv = static_cast<int32_t*>(up(seq_piv.data(), seq_piv.size() * 4));
+  d.piv_sat_begin = static_cast<int32_t*>(up(psb.data(), psb.size() * 4));
+  d.piv_unit = static_cast<int32_t*>(up(punit.data(), punit.size() * 4));
+  d.sats = static_cast<DevSat*>(up(sats.data(), sats.size() * sizeof(DevSat)));
+  d.xfers = static_cast<DevXfer*>(dev(ns * kQ * sizeof(DevXfer)));
+  d.cum = static_cast<int64_t*>(dev(size_t(e.B) * 8));
+  d.order = static_cast<int32_t*>(dev(size_t(e.B) * 4));
+  d.svals = static_cast<double*>(dev(size_t(e.n_piv) * 64 * 8));
+  d.scnt = static_cast<int32_t*>(dev(size_t(e.n_piv) * 4));
+  d.jobs = static_cast<FireJob*>(dev(ns * sizeof(FireJob)));
+  d.n_jobs = static_cast<uint32_t*>(dev(4));
+  d.restamp_slots = static_cast<int32_t*>(dev(size_t(e.n_piv) * 4));
+  d.n_restamp = static_cast<uint32_t*>(dev(4));
+  d.glist = static_cast<GatherItem*>(dev(ns * sizeof(GatherItem)));
+  d.n_glist = static_cast<uint32_t*>(dev(4));
+  HC_CUDA_TRY(cudaGetLastError());
+  HC_REQUIRE(d.seq_piv && d.piv_sat_begin && d.piv_unit && d.sats && d.xfers && d.cum &&
+                 d.order && d.svals && d.scnt && d.jobs && d.n_jobs && d.restamp_slots &&
+                 d.n_restamp && d.glist && d.n_glist,
+             HC_ENOMEM, "device decisions: state");
+  // mapped host memory: the decision log and the fetched sets the host mirrors
+  int64_t ksum = 0;
+  for (const DevSat& x : sats) ksum += x.k;
+  d.fetched_cap = std::max<int64_t>(4 * ksum + 64, int64_t(1) << 20);
+  auto mapped = [&](void** h, size_t bytes) -> int {
+    HC_CUDA_TRY(cudaHostAlloc(h, bytes, cudaHostAllocMapped));
+    std::memset(*h, 0, bytes);
+    e.dd_host.push_back(*h);
+    e.host_bytes += int64_t(bytes);
+    return HC_OK;
+  };
+  void* p = nullptr;
+  HC_TRY(mapped(&p, sizeof(BoundaryHdr) * kLogRing));
+  e.hdr_h = static_cast<BoundaryHdr*>(p);
+  HC_TRY(mapped(&p, sizeof(FireLog) * kLogRing * std::max(1, e.n_piv)));
+  e.log_h = static_cast<FireLog*>(p);
+  HC_TRY(mapped(&p, size_t(d.fetched_cap) * 4));
+  e.fetched_h = static_cast<uint32_t*>(p);
+  HC_TRY(mapped(&p, 64));
+  int64_t* ctr = static_cast<int64_t*>(p);  // [0] head (device), [1] tail (host)
+  e.fetched_tail_h = ctr + 1;
+  HC_TRY(mapped(&p, 64));
+  e.error_h = static_cast<int32_t*>(p);
+  void* dp = nullptr;
+  HC_CUDA_TRY(cudaHostGetDevicePointer(&dp, e.hdr_h, 0));
+  d.hdr = static_cast<BoundaryHdr*>(dp);
+  HC_CUDA_TRY(cudaHostGetDevicePointer(&dp, e.log_h, 0));
+  d.log = static_cast<FireLog*>(dp);
+  HC_CUDA_TRY(cudaHostGetDevicePointer(&dp, e.fetched_h, 0));
+  d.fetched = static_cast<uint32_t*>(dp);
+  HC_CUDA_TRY(cudaHostGetDevicePointer(&dp, ctr, 0));
+  d.fetched_head = static_cast<int64_t*>(dp);
+  d.fetched_tail = static_cast<int64_t*>(dp) + 1;
+  HC_CUDA_TRY(cudaHostGetDevicePointer(&dp, e.error_h, 0));
+  d.error = static_cast<int32_t*>(dp);
+  int lo_prio = 0, hi_prio = 0;
+  HC_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+  HC_CUDA_TRY(cudaStreamCreateWithPriority(&e.sched, cudaStreamNonBlocking, hi_prio));
+  for (cudaEvent_t* x : {&e.ev_land, &e.ev_sched, &e.ev_sel, &e.ev_dec})
+    HC_CUDA_TRY(cudaEventCreateWithFlags(x, cudaEventDisableTiming));
+  for (auto& x : e.ev_log) HC_CUDA_TRY(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+  e.devdec = true;
   return HC_OK;
 }
 
@@ -596,6 +762,7 @@ int engine_create(EngineImpl& e, const hc_engine_desc& c, const int32_t* roles,
   HC_CUDA_TRY(cudaStreamCreateWithPriority(&e.retr, cudaStreamNonBlocking, hi_prio));
   HC_CUDA_TRY(cudaStreamCreateWithPriority(&e.side, cudaStreamNonBlocking, hi_prio));
   HC_CUDA_TRY(cudaStreamCreateWithPriority(&e.mon, cudaStreamNonBlocking, hi_prio));
+  if (c.device_decisions) HC_TRY(devdec_create(e, c));
   return HC_OK;
 }
 
@@ -680,6 +847,73 @@ __global__ void set_flags_kernel(uint8_t* flags, const int32_t* __restrict__ idx
   if (i < n) flags[idx[i]] = v;
 }
 
+// Device decisions: landing point of step t on the step's stream, then a
+// schedule pass and the gathers it frees (retrieval stream).
+int devdec_land(EngineImpl& e, int t, cudaStream_t st) {
+  if (e.sched_valid) HC_CUDA_TRY(cudaStreamWaitEvent(st, e.ev_sched, 0));
+  cudaEvent_t w0 = nullptr, w1 = nullptr;
+  if (e.timing) {
+    HC_TRY(new_event(e, &w0, true));
+    HC_TRY(new_event(e, &w1, true));
+    HC_CUDA_TRY(cudaEventRecord(w0, st));
+  }
+  HC_TRY(launch_land(e.dd, t, e.d_units, reinterpret_cast<uint4*>(e.K),
+                     reinterpret_cast<uint4*>(e.V), st));
+  if (e.timing) {
+    HC_CUDA_TRY(cudaEventRecord(w1, st));
+    e.land_ev.emplace_back(w0, w1);
+  }
+  HC_CUDA_TRY(cudaEventRecord(e.ev_land, st));
+  HC_CUDA_TRY(cudaStreamWaitEvent(e.sched, e.ev_land, 0));
+  return HC_OK;
+}
+
+// A schedule pass on the schedule stream and the gathers it lists.
+int devdec_schedule_and_gather(EngineImpl& e) {
+  HC_TRY(launch_schedule(e.dd, e.sched));
+  HC_CUDA_TRY(cudaEventRecord(e.ev_sched, e.sched));
+  e.sched_valid = true;
+  HC_CUDA_TRY(cudaStreamWaitEvent(e.retr, e.ev_sched, 0));
+  cudaEvent_t g0 = nullptr, g1 = nullptr;
+  if (e.timing) {
+    HC_TRY(new_event(e, &g0, true));
+    HC_TRY(new_event(e, &g1, true));
+    HC_CUDA_TRY(cudaEventRecord(g0, e.retr));
+  }
+  HC_TRY(launch_dev_gathers(e.dd, reinterpret_cast<uint4*>(e.K), reinterpret_cast<uint4*>(e.V),
+                            e.retr));
+  if (e.timing) {
+    HC_CUDA_TRY(cudaEventRecord(g1, e.retr));
+    e.gather_ev.emplace_back(g0, g1);
+  }
+  return HC_OK;
+}
+
+// The decision of boundary t on the monitor stream (after its monitor), the
+// K_base restamp, the fetch selection (side stream), a schedule pass and the
+// gathers.
+int devdec_decide(EngineImpl& e, int t) {
+  const bool boundary = e.dd.sliding || t % e.dd.window == 0;
+  if (!boundary) return HC_OK;
+  const int first = e.dd.sliding ? t : std::max(1, t - e.dd.window + 1);
+  const int nvals = t - first + 1;
+  const int64_t bidx = e.n_bound++;
+  HC_REQUIRE(e.n_bound - e.n_read <= kLogRing, HC_ESTATE,
+             "device decisions: %d boundaries unread (poll the decisions)", kLogRing);
+  HC_TRY(launch_decide(e.dd, t, first, nvals, int(bidx), e.ovl_ring, kRing, e.mon));
+  HC_TRY(launch_restamp_threshold(e.rowbuf, e.row_len, e.dd.restamp_slots, e.n_piv,
+                                  uint32_t(e.L + t), e.thr, e.kbase, e.words, e.mon,
+                                  e.dd.n_restamp));
+  HC_CUDA_TRY(cudaEventRecord(e.ev_dec, e.mon));
+  HC_CUDA_TRY(cudaStreamWaitEvent(e.side, e.ev_dec, 0));
+  HC_TRY(launch_fire_select(e.dd.jobs, std::max(1, e.dd.n_sat), e.side, e.dd.n_jobs));
+  HC_CUDA_TRY(cudaEventRecord(e.ev_sel, e.side));
+  HC_CUDA_TRY(cudaEventRecord(e.ev_log[bidx % kLogRing], e.side));
+  e.sel_valid = true;
+  HC_CUDA_TRY(cudaStreamWaitEvent(e.sched, e.ev_sel, 0));
+  return devdec_schedule_and_gather(e);
+}
+
 // Decode step t, in two halves so a host decision can overlap the attention:
 //
 //   decode_begin  append the token; K4 over every unit except those that may
@@ -697,6 +931,10 @@ int engine_decode_begin(EngineImpl& e, int t, const void* q, const void* kn, con
                         void* o, bool hold, cudaStream_t st) {
   HC_REQUIRE(t >= 1 && t <= e.T, HC_EINVAL, "step %d outside 1..%d", t, e.T);
   HC_REQUIRE(e.in_step == 0, HC_ESTATE, "decode_begin(%d) while step %d is open", t, e.in_step);
+  if (e.devdec) {  // landings are decided on the device: satellites always run after them
+    HC_REQUIRE(e.deferred.empty(), HC_ESTATE, "host landings with device decisions");
+    hold = true;
+  }
   if (!e.deferred.empty() && e.deferred_st != st) {  // landings requested on another stream
     std::vector<int> ids;
     ids.swap(e.deferred);
@@ -771,7 +1009,14 @@ int engine_decode_end(EngineImpl& e, int t, cudaStream_t st) {
   e.in_step = 0;  // landings below are applied for real
   AttnParams pl = e.cur_p;
   pl.skip = nullptr;
-  if (e.cur_hold) {
+  if (e.cur_hold && e.devdec) {
+    HC_TRY(devdec_land(e, t, st));
+    HC_TRY(devdec_schedule_and_gather(e));
+    const int n = int(std::upper_bound(e.sat_t_act.begin(), e.sat_t_act.end(), uint32_t(t)) -
+                      e.sat_t_act.begin());
+    pl.tiles = e.d_sat_tiles;
+    HC_TRY(launch_attn_tiles(e.tmK, e.tmV, pl, n, st));
+  } else if (e.cur_hold) {
     std::vector<int> land;
     land.swap(e.deferred);
     if (!land.empty()) HC_TRY(apply_landings(e, land, st));
@@ -808,6 +1053,8 @@ int engine_decode_end(EngineImpl& e, int t, cudaStream_t st) {
       HC_CUDA_TRY(cudaEventCreateWithFlags(&e.rows_done, cudaEventDisableTiming));
     HC_CUDA_TRY(cudaEventRecord(e.rows_done, st));
     HC_CUDA_TRY(cudaStreamWaitEvent(e.mon, e.rows_done, 0));
+    // the previous boundary's fetch selection still reads the rows and histograms
+    if (e.sel_valid) HC_CUDA_TRY(cudaStreamWaitEvent(e.mon, e.ev_sel, 0));
     HC_TRY(launch_score_rows(e.cur_p, e.d_piv_units, e.n_piv, e.mon));
     cudaEvent_t& re = e.rows_ev[t & 1];
     if (!re) HC_CUDA_TRY(cudaEventCreateWithFlags(&re, cudaEventDisableTiming));
@@ -817,6 +1064,7 @@ int engine_decode_end(EngineImpl& e, int t, cudaStream_t st) {
                           uint32_t(e.lbase), e.kbase, e.words, e.thr,
                           e.ovl_ring + size_t(t % kRing) * e.n_piv, e.mon,
                           e.ghist + size_t(t & 1) * e.n_piv * 8192));
+    if (e.devdec) HC_TRY(devdec_decide(e, t));
   } else if (ev) {
     HC_CUDA_TRY(cudaEventRecord(ev[4], st));
   }
@@ -881,75 +1129,14 @@ struct XferDev {
 
 __global__ void build_positions_batch_kernel(const XferDev* __restrict__ xs, int L, int S, int R) {
   const XferDev x = xs[blockIdx.x];
-  __shared__ int s_lo, s_hi, s_ntail;
-  __shared__ uint32_t s_mask;
-  const uint32_t* sel = x.sel;
-  const int k = int(*x.cnt);
-  const int sinks = S < L ? S : L;
-  if (threadIdx.x == 0) {
-    int a = 0, b = k;
-    while (a < b) { const int m = (a + b) >> 1; if (int(sel[m]) < sinks) a = m + 1; else b = m; }
-    const int lo = a;
-    b = k;
-    while (a < b) { const int m = (a + b) >> 1; if (int(sel[m]) < L) a = m + 1; else b = m; }
-    const int hi = a;
-    int nt = 0;
-    uint32_t mask = 0;
-    int first = L + x.t_c - R;
-    if (first < sinks) first = sinks;
-    for (int p = first; p < L; ++p) {
-      int u = lo, v = hi;
-      while (u < v) { const int m = (u + v) >> 1; if (int(sel[m]) < p) u = m + 1; else v = m; }
-      if (!(u < hi && int(sel[u]) == p)) {
-        x.pos[nt++] = uint32_t(p);
-        if (R <= 32) mask |= 1u << (p - (L - R));
-      }
-    }
-    if (R > 32) mask = uint32_t(nt);  // contiguous tail block [L - nt, L) (no dynamic set)
-    s_lo = lo;
-    s_hi = hi;
-    s_ntail = nt;
-    s_mask = mask;
-  }
-  __syncthreads();
-  const int nt = s_ntail, lo = s_lo, hi = s_hi;
-  for (int i = threadIdx.x; i < sinks; i += blockDim.x) x.pos[nt + i] = uint32_t(i);
-  for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) x.pos[nt + sinks + (i - lo)] = sel[i];
-  if (threadIdx.x == 0) {
-    x.meta[0] = nt + sinks + (hi - lo);
-    x.meta[1] = int32_t(s_mask);
-    x.meta[2] = k - hi;
-  }
+  build_positions_block(x.sel, int(*x.cnt), x.pos, x.meta, L, S, R, x.t_c);
 }
 
 __global__ void gather_rows_batch_kernel(const XferDev* __restrict__ xs, uint4* __restrict__ K,
                                          uint4* __restrict__ V) {
   const XferDev x = xs[blockIdx.y];
-  const int n = x.meta[0];
-  const int lane = threadIdx.x & 31;
-  const int warps = gridDim.x * (blockDim.x >> 5);
-  constexpr int kUnroll = 4;
-  for (int j0 = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * kUnroll; j0 < n;
-       j0 += warps * kUnroll) {
-    uint4 v[kUnroll];
-#pragma unroll
-    for (int q = 0; q < kUnroll; ++q) {
-      const int j = j0 + q;
-      if (j < n) {
-        const size_t p = x.pos[j];
-        v[q] = lane < 16 ? x.srcK[p * 16 + lane] : x.srcV[p * 16 + lane - 16];
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < kUnroll; ++q) {
-      const int j = j0 + q;
-      if (j < n) {
-        const int64_t r = x.dst_row + j;
-        if (lane < 16) K[r * 16 + lane] = v[q];
-        else V[r * 16 + lane - 16] = v[q];
-      }
-    }
-  }
+  gather_rows(x.pos, x.meta[0], x.srcK, x.srcV, K, V, x.dst_row,
+              blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), gridDim.x * (blockDim.x >> 5));
 }
 
 // Retrieval gather from the pinned host pool (zero-copy over the host link).
@@ -965,33 +1152,11 @@ constexpr int kGatherCtas = 40;
 __global__ void __launch_bounds__(256) gather_host_rows_kernel(const XferDev* __restrict__ xs,
                                                                int n_x, uint4* __restrict__ K,
                                                                uint4* __restrict__ V) {
-  const int lane = threadIdx.x & 31;
   const int nw = gridDim.x * (blockDim.x >> 5);
   const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  constexpr int kUnroll = 4;
   for (int xi = 0; xi < n_x; ++xi) {
     const XferDev x = xs[xi];
-    const int n = x.meta[0];
-    for (int j0 = gw * kUnroll; j0 < n; j0 += nw * kUnroll) {
-      uint4 v[kUnroll];
-#pragma unroll
-      for (int q = 0; q < kUnroll; ++q) {
-        const int j = j0 + q;
-        if (j < n) {
-          const size_t p = x.pos[j];
-          v[q] = lane < 16 ? x.srcK[p * 16 + lane] : x.srcV[p * 16 + lane - 16];
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < kUnroll; ++q) {
-        const int j = j0 + q;
-        if (j < n) {
-          const int64_t r = x.dst_row + j;
-          if (lane < 16) K[r * 16 + lane] = v[q];
-          else V[r * 16 + lane - 16] = v[q];
-        }
-      }
-    }
+    gather_rows(x.pos, x.meta[0], x.srcK, x.srcV, K, V, x.dst_row, gw, nw);
   }
 }
 
@@ -1808,6 +1973,7 @@ extern "C" int hc_engine_decode_end(hc_engine* eng, int32_t step, void* stream) 
 
 extern "C" int hc_engine_enable_measure(hc_engine* eng, int32_t recall_topk) {
   HC_REQUIRE(eng, HC_EINVAL, "null argument");
+  HC_REQUIRE(!eng->e.devdec, HC_ESTATE, "measure mode needs host decisions");
   return hc::engine_enable_measure(eng->e, recall_topk);
 }
 
@@ -1845,6 +2011,7 @@ extern "C" int hc_engine_join(hc_engine* eng, void* stream) {
 extern "C" int hc_engine_overlaps(hc_engine* eng, int32_t first, int32_t last, int32_t* out,
                                   void* stream) {
   HC_REQUIRE(eng && out, HC_EINVAL, "null argument");
+  HC_REQUIRE(!eng->e.devdec, HC_ESTATE, "overlap readback: decisions are on the device");
   HC_TRY(hc::flush_deferred(eng->e));  // pending landings first
   auto& e = eng->e;
   HC_REQUIRE(last >= first && last - first < hc::kRing, HC_EINVAL, "overlap window too long");
@@ -1876,6 +2043,7 @@ extern "C" int hc_engine_overlaps(hc_engine* eng, int32_t first, int32_t last, i
 extern "C" int hc_engine_fire(hc_engine* eng, int32_t pivot_unit, int32_t step,
                               int32_t completion_step, int32_t* transfer_ids, void* stream) {
   HC_REQUIRE(eng && transfer_ids, HC_EINVAL, "null argument");
+  HC_REQUIRE(!eng->e.devdec, HC_ESTATE, "host fires: decisions are on the device");
   HC_TRY(hc::flush_deferred(eng->e));  // pending landings first
   return hc::engine_fire_batch(eng->e, 1, &pivot_unit, step, &completion_step, transfer_ids,
                                nullptr, (cudaStream_t)stream);
@@ -1886,6 +2054,7 @@ extern "C" int hc_engine_fire_batch(hc_engine* eng, int32_t n, const int32_t* pi
                                     int32_t* transfer_ids, uint32_t* fetched_host, void* stream) {
   HC_REQUIRE(eng && (n == 0 || (pivot_units && completion_steps && transfer_ids)), HC_EINVAL,
              "null argument");
+  HC_REQUIRE(!eng->e.devdec, HC_ESTATE, "host fires: decisions are on the device");
   HC_TRY(hc::flush_deferred(eng->e));  // pending landings first
   return hc::engine_fire_batch(eng->e, n, pivot_units, step, completion_steps, transfer_ids,
                                fetched_host, (cudaStream_t)stream);
@@ -1900,12 +2069,14 @@ extern "C" int hc_engine_wait_fetched(hc_engine* eng) {
 
 extern "C" int hc_engine_land(hc_engine* eng, int32_t transfer_id, void* stream) {
   HC_REQUIRE(eng, HC_EINVAL, "null argument");
+  HC_REQUIRE(!eng->e.devdec, HC_ESTATE, "host landings: decisions are on the device");
   return hc::engine_land_batch(eng->e, 1, &transfer_id, (cudaStream_t)stream);
 }
 
 extern "C" int hc_engine_land_batch(hc_engine* eng, int32_t n, const int32_t* transfer_ids,
                                     void* stream) {
   HC_REQUIRE(eng && (n == 0 || transfer_ids), HC_EINVAL, "null argument");
+  HC_REQUIRE(!eng->e.devdec || n == 0, HC_ESTATE, "host landings: decisions are on the device");
   return hc::engine_land_batch(eng->e, n, transfer_ids, (cudaStream_t)stream);
 }
 
@@ -1925,7 +2096,23 @@ extern "C" int hc_engine_read_indices(hc_engine* eng, int32_t kind, int32_t id, 
   } else if (kind == 1 || kind == 3) {
     HC_REQUIRE(id >= 0 && id < e.n_units && e.units[id].kind == hc::kUnitComp, HC_EINVAL,
                "unit %d is not compressed", id);
-    if (kind == 1) {
+    hc::DevSat ds{};
+    int si = e.devdec ? e.dd_sat_of_unit[id] : -1;
+    if (si >= 0) {  // device decisions: the satellite's landed transfer, if any
+      HC_CUDA_TRY(cudaStreamSynchronize(st));
+      HC_CUDA_TRY(cudaMemcpy(&ds, e.dd.sats + si, sizeof(ds), cudaMemcpyDeviceToHost));
+      if (ds.cur_slot < 0) si = -1;
+    }
+    if (si >= 0) {
+      hc::DevXfer* x = e.dd.xfers + size_t(si) * hc::kQ + ds.cur_slot;
+      if (kind == 1) {
+        list = ds.sel + size_t(ds.cur_slot) * ds.k;
+        cnt = &x->cnt;
+      } else {
+        list = ds.pos + size_t(ds.cur_slot) * ds.cap;
+        meta = x->meta;
+      }
+    } else if (kind == 1) {
       list = hc::dyn_list(e, id, &cnt);
     } else {
       const int ow = e.dyn_owner[id];
@@ -2094,5 +2281,90 @@ extern "C" int hc_engine_prefill_stats(hc_engine* eng, double* out3) {
   out3[0] = e.pf_score_ms;
   out3[1] = e.pf_layers;
   out3[2] = e.W;
+  return HC_OK;
+}
+
+extern "C" int hc_engine_poll_decisions(hc_engine* eng, int32_t wait, int32_t* step_out,
+                                        hc_fire_record* fires, int32_t fire_capacity,
+                                        int32_t* n_fires_out, uint32_t* fetched_out,
+                                        int64_t fetched_capacity) {
+  HC_REQUIRE(eng && step_out && n_fires_out, HC_EINVAL, "null argument");
+  auto& e = eng->e;
+  HC_REQUIRE(e.devdec, HC_ESTATE, "the engine takes its decisions on the host");
+  *step_out = -1;
+  *n_fires_out = 0;
+  static const char* kWhy[] = {"", "a satellite's transfer ring overflowed (more than 8 pending)",
+                               "the host did not consume the fetched-set ring",
+                               "a due gather did not complete (landing wait timed out)",
+                               "a cluster has more than 8 satellites"};
+  auto fault = [&]() -> int {
+    const int code = *reinterpret_cast<volatile int32_t*>(e.error_h);
+    HC_REQUIRE(code == 0, HC_ESTATE, "device decisions: %s",
+               kWhy[code > 0 && code < 5 ? code : 0]);
+    return HC_OK;
+  };
+  HC_TRY(fault());
+  if (e.n_read >= e.n_bound) return HC_OK;
+  cudaEvent_t ev = e.ev_log[e.n_read % hc::kLogRing];
+  if (wait) {
+    HC_CUDA_TRY(cudaEventSynchronize(ev));
+  } else {
+    const cudaError_t q = cudaEventQuery(ev);
+    if (q == cudaErrorNotReady) return HC_OK;
+    HC_CUDA_TRY(q);
+  }
+  HC_TRY(fault());
+  const volatile hc::BoundaryHdr* hp = e.hdr_h + (e.n_read % hc::kLogRing);
+  const int n = hp->n_fires;
+  const int64_t head_after = hp->head_after;
+  const hc::FireLog* lg = e.log_h + size_t(e.n_read % hc::kLogRing) * std::max(1, e.n_piv);
+  int64_t need = 0;
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < lg[i].n_sats && j < 8; ++j) need += lg[i].ks[j];
+  if (n > fire_capacity || need > fetched_capacity) {
+    *n_fires_out = n;
+    HC_REQUIRE(false, HC_EINVAL, "poll_decisions: needs %d fire records and %lld fetched entries",
+               n, (long long)need);
+  }
+  int64_t off = 0;
+  for (int i = 0; i < n; ++i) {
+    const hc::FireLog& f = lg[i];
+    hc_fire_record& r = fires[i];
+    r.trigger_step = f.trigger;
+    r.pivot_unit = f.pivot_unit;
+    r.completion_step = f.completion;
+    r.n_satellites = f.n_sats;
+    r.transfer_bytes = f.bytes;
+    r.cumulative_bytes = f.cum_after;
+    r.first_satellite = f.first_sat;
+    int64_t cnt = 0;
+    for (int j = 0; j < 8; ++j) {
+      r.fetched_counts[j] = f.ks[j];
+      cnt += f.ks[j];
+    }
+    r.fetched_offset = f.host_off < 0 ? -1 : int32_t(off);
+    if (f.host_off >= 0 && cnt) {
+      std::memcpy(fetched_out + off, e.fetched_h + f.host_off, size_t(cnt) * 4);
+      if (e.timing)
+        for (int j = 0; j < f.n_sats && j < 8; ++j)
+          e.gather_rows_issued += f.ks[j] + std::min(e.S, e.L) + e.R;
+    }
+    off += cnt;
+  }
+  *reinterpret_cast<volatile int64_t*>(e.fetched_tail_h) = head_after;  // ring space released
+  *step_out = hp->t;
+  *n_fires_out = n;
+  ++e.n_read;
+  return HC_OK;
+}
+
+extern "C" int hc_engine_devdec_satellites(hc_engine* eng, int32_t* units_out, int32_t capacity,
+                                           int32_t* n_out) {
+  HC_REQUIRE(eng && n_out, HC_EINVAL, "null argument");
+  auto& e = eng->e;
+  *n_out = int32_t(e.dd_sat_units.size());
+  HC_REQUIRE(int(e.dd_sat_units.size()) <= capacity || !units_out, HC_EINVAL, "capacity");
+  if (units_out)
+    std::memcpy(units_out, e.dd_sat_units.data(), e.dd_sat_units.size() * 4);
   return HC_OK;
 }

@@ -529,7 +529,8 @@ monitor_kernel(const float* __restrict__ rows, int64_t row_stride, const int32_t
 __global__ void restamp_threshold_kernel(const float* __restrict__ rows, int64_t row_stride,
                                          const int32_t* __restrict__ slots, uint32_t n,
                                          const uint64_t* __restrict__ thr, uint32_t* kbase,
-                                         int words) {
+                                         int words, const uint32_t* n_rows_dev) {
+  if (n_rows_dev && blockIdx.y >= *n_rows_dev) return;  // device-written slot list
   const int s = slots[blockIdx.y];
   const float* row = rows + size_t(s) * row_stride;
   const uint64_t T = thr[s];
@@ -556,7 +557,9 @@ __global__ void restamp_threshold_kernel(const float* __restrict__ rows, int64_t
 constexpr int kFireCand = 12288;
 constexpr int kFireSmem = kFireCand * 8 + kSelThreads * 4 + 96 * 4;
 
-__global__ void __launch_bounds__(kSelThreads, 2) fire_select_kernel(const FireJob* __restrict__ jobs) {
+__global__ void __launch_bounds__(kSelThreads, 2) fire_select_kernel(const FireJob* __restrict__ jobs,
+                                                                      const uint32_t* n_jobs_dev) {
+  if (n_jobs_dev && blockIdx.x >= *n_jobs_dev) return;  // device-written job list
   extern __shared__ __align__(16) uint8_t fs_smem[];
   uint64_t* cand = reinterpret_cast<uint64_t*>(fs_smem);
   uint32_t* hist = reinterpret_cast<uint32_t*>(fs_smem + kFireCand * 8);  // radix scratch
@@ -568,8 +571,18 @@ __global__ void __launch_bounds__(kSelThreads, 2) fire_select_kernel(const FireJ
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (k >= n || k == 0) {  // everything / nothing
     const uint32_t c = k >= n ? n : 0u;
-    for (uint32_t i = tid; i < c; i += kSelThreads) job.out_idx[i] = i;
-    if (tid == 0) *job.out_count = c;
+    for (uint32_t i = tid; i < c; i += kSelThreads) {
+      job.out_idx[i] = i;
+      if (job.host_out) job.host_out[i] = i;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      *job.out_count = c;
+      if (job.state_out) {
+        __threadfence_system();
+        atomicExch(job.state_out, 2);
+      }
+    }
     return;
   }
   block_find_bucket<kMonBins, kSelThreads>(job.hist, k, sh, warp_tot);
@@ -681,16 +694,27 @@ __global__ void __launch_bounds__(kSelThreads, 2) fire_select_kernel(const FireJ
       uint32_t p = off + incl - c;
 #pragma unroll
       for (int e = 0; e < 4; ++e)
-        if (selm & (1u << e)) job.out_idx[p++] = 4 * v + e;
+        if (selm & (1u << e)) {
+          if (job.host_out) job.host_out[p] = 4 * v + e;
+          job.out_idx[p++] = 4 * v + e;
+        }
       off += __shfl_sync(0xffffffffu, incl, 31);
     }
   }
-  if (tid == 0) *job.out_count = k;
+  __syncthreads();
+  if (tid == 0) {
+    *job.out_count = k;
+    if (job.state_out) {  // device decisions: the transfer's set is complete
+      __threadfence_system();
+      atomicExch(job.state_out, 2);
+    }
+  }
 }
 
 }  // namespace
 
-int launch_fire_select(const FireJob* jobs_dev, int n_jobs, cudaStream_t st) {
+int launch_fire_select(const FireJob* jobs_dev, int n_jobs, cudaStream_t st,
+                       const uint32_t* n_jobs_dev) {
   static bool configured = false;
   if (!configured) {
     HC_CUDA_TRY(cudaFuncSetAttribute(fire_select_kernel,
@@ -698,7 +722,7 @@ int launch_fire_select(const FireJob* jobs_dev, int n_jobs, cudaStream_t st) {
     configured = true;
   }
   if (n_jobs <= 0) return HC_OK;
-  fire_select_kernel<<<n_jobs, kSelThreads, kFireSmem, st>>>(jobs_dev);
+  fire_select_kernel<<<n_jobs, kSelThreads, kFireSmem, st>>>(jobs_dev, n_jobs_dev);
   HC_CHECK_LAUNCH();
   return HC_OK;
 }
@@ -721,11 +745,11 @@ int launch_monitor(const float* rows, int64_t row_stride, const int32_t* slots, 
 
 int launch_restamp_threshold(const float* rows, int64_t row_stride, const int32_t* slots,
                              int n_rows, uint32_t n, const uint64_t* thr, uint32_t* kbase,
-                             int words, cudaStream_t st) {
+                             int words, cudaStream_t st, const uint32_t* n_rows_dev) {
   if (n_rows <= 0) return HC_OK;
   const int blocks = std::min(64, (words + 7) / 8);
   restamp_threshold_kernel<<<dim3(std::max(1, blocks), n_rows), 256, 0, st>>>(
-      rows, row_stride, slots, n, thr, kbase, words);
+      rows, row_stride, slots, n, thr, kbase, words, n_rows_dev);
   HC_CHECK_LAUNCH();
   return HC_OK;
 }

@@ -112,7 +112,8 @@ class HeteroCacheDecoder:
                  host_pool: bool = True, bytes_per_kv_entry: int | None = None,
                  track_sets: bool = True, obs_window: int = 1, overlap_decisions: bool = True,
                  recall_topk: int = 0, owned=None, exchange=None,
-                 score_material: str = "fp32", fetch_ring_entries: int | None = None):
+                 score_material: str = "fp32", fetch_ring_entries: int | None = None,
+                 device_decisions: bool | None = None):
         """owned: optional [batch, layers, kv_heads] bool mask of the units this
         rank holds (parallel.assign_units; None = all).  exchange: the fire
         exchange of a unit-sharded run (parallel.FireExchange); every rank of
@@ -122,7 +123,12 @@ class HeteroCacheDecoder:
         ~5e-4 relative row error moves near-tied positions across the top-k
         boundary (profiles/r02_selection_precision.json).
         fetch_ring_entries: size of the pinned ring the fetched sets land in
-        (default: four full drift bursts, at least 64K entries)."""
+        (default: four full drift bursts, at least 64K entries).
+        device_decisions: take the boundary decisions on the device (devdec.cu:
+        window median, accounting, fetch selection, gathers, landings in device
+        streams; this mirror reads them from a mapped log without ever blocking
+        the step).  None (default) = on whenever supported: monitored pivots, an
+        unsharded engine, no measure mode, window <= 64."""
         _lib.require_cuda()
         self.lib = _lib.load()
         self.taxonomy, self.plan, self.config = taxonomy, plan, config
@@ -151,12 +157,24 @@ class HeteroCacheDecoder:
         for p, sats in self.satellites_of.items():
             for s in sats:
                 cpiv[s[0] * self.H + s[1]] = p[1]
+        ok_dev = (self.monitor and owned is None and not recall_topk and config.window <= 64
+                  and len(plan.lengths) > 0)
+        if device_decisions and not ok_dev:
+            raise EngineError("device decisions need monitored pivots, an unsharded engine, "
+                              "no measure mode and window <= 64")
+        self.devdec = ok_dev if device_decisions is None else bool(device_decisions)
         desc = _lib.EngineDesc(batch=batch, num_layers=self.NL, kv_heads=self.H, group=group,
                                head_dim=head_dim, prefill_len=self.L, max_decode=max_decode,
                                sink_count=config.sink_count, recency_window=config.recency_window,
                                l_base_int=self.l_base_int, chunk=chunk, monitor=int(self.monitor),
                                host_pool=int(host_pool), obs_window=obs_window,
-                               score_material={"fp32": 0, "fp16": 1}[score_material])
+                               score_material={"fp32": 0, "fp16": 1}[score_material],
+                               device_decisions=int(self.devdec), window=config.window,
+                               update_delay_steps=config.update_delay_steps,
+                               eval_every_step=int(config.eval_every_step),
+                               bytes_per_kv_entry=self.bytes_per_entry,
+                               transfer_bandwidth=int(config.transfer_bandwidth),
+                               tau_drift=float(config.tau_drift))
         self.W = obs_window
         h = C.c_void_p()
         if owned is None:
@@ -209,6 +227,23 @@ class HeteroCacheDecoder:
         # decode_step); (step, first, per-sequence (charged, extra)) or None
         self.overlap_decisions = overlap_decisions
         self._open = None
+        # device decisions: steps not yet turned into StepRows, boundaries not yet read
+        self._dd_steps = []       # (t, boundary, rows)
+        self._dd_unread = []      # boundary steps issued, decision not read yet
+        self._dd_fired = {}       # boundary step -> sequences that fired
+        if self.devdec:
+            n = C.c_int32()
+            _lib.check(self.lib.hc_engine_devdec_satellites(self.handle, None, 0, C.byref(n)))
+            su = np.zeros(max(1, n.value), dtype=np.int32)
+            _lib.check(self.lib.hc_engine_devdec_satellites(self.handle, su.ctypes.data,
+                                                            su.size, C.byref(n)))
+            LHn = self.NL * self.H
+            self._dd_sat_head = [((int(u) % LHn) // self.H, int(u) % self.H)
+                                 for u in su[:n.value]]
+            self._dd_recs = (_lib.FireRecord * max(1, self.n_pivot_units))()
+            cap = sum(self.effective_length(s) for b in range(self.B) for p in self.piv_of[b]
+                      for s in self.satellites_of[p])
+            self._dd_fetched = np.empty(max(1, cap), dtype=np.uint32)
 
     # ---- helpers -------------------------------------------------------------
 
@@ -383,6 +418,17 @@ class HeteroCacheDecoder:
         """
         cfg = self.config
         sh = _lib.stream_handle(stream)
+        if self.devdec:
+            _lib.check(self.lib.hc_engine_decode_step(self.handle, t, _lib.ptr(q), _lib.ptr(k_new),
+                                                      _lib.ptr(v_new), _lib.ptr(out), sh))
+            boundary = cfg.eval_every_step or t % cfg.window == 0
+            self._dd_steps.append((t, boundary, rows))
+            if boundary:
+                self._dd_unread.append(t)
+            # read whatever the device has decided by now; block only if the
+            # mapped log (256 boundaries) is about to wrap
+            self._dd_poll(wait=len(self._dd_unread) > 192)
+            return
         hold = self._open is not None
         self._land_due(t, sh)
         if hold:
@@ -407,6 +453,78 @@ class HeteroCacheDecoder:
             for b, st in enumerate(self.states):
                 st.rows.append(self._row(st, t, 0, self._row_sizes(b, t, rec[b])))
 
+    # ---- device decisions: the host mirror ----------------------------------------
+
+    def _dd_poll(self, wait: bool) -> None:
+        """Read device decisions in boundary order (all of them with wait) and turn
+        the steps they complete into StepRows."""
+        step = C.c_int32()
+        nf = C.c_int32()
+        while self._dd_unread:
+            _lib.check(self.lib.hc_engine_poll_decisions(
+                self.handle, int(wait), C.byref(step), self._dd_recs, len(self._dd_recs),
+                C.byref(nf), self._dd_fetched.ctypes.data, self._dd_fetched.size))
+            if step.value < 0:
+                break
+            t = step.value
+            if t != self._dd_unread[0]:
+                raise EngineError(f"device decision for step {t}, expected {self._dd_unread[0]}")
+            self._dd_unread.pop(0)
+            self._dd_record(t, nf.value)
+        self._dd_materialise()
+
+    def _dd_record(self, t: int, n: int) -> None:
+        """RetrievalRecords and pending landings of boundary t's fires (device order:
+        per sequence, sorted pivots -- engine.py:313)."""
+        LHn = self.NL * self.H
+        fired = set()
+        for i in range(n):
+            r = self._dd_recs[i]
+            b = r.pivot_unit // LHn
+            p = ((r.pivot_unit % LHn) // self.H, r.pivot_unit % self.H)
+            sats = tuple(self._dd_sat_head[r.first_satellite + j] for j in range(r.n_satellites))
+            ks = [int(r.fetched_counts[j]) for j in range(r.n_satellites)]
+            if r.fetched_offset < 0:
+                raise EngineError("device decisions: fetched sets unavailable")
+            fetched, o = [], r.fetched_offset
+            for k in ks:
+                fetched.append(self._dd_fetched[o:o + k].copy())
+                o += k
+            st = self.states[b]
+            ev = _Event(trigger_step=t, pivot=p, completion_step=r.completion_step,
+                        transfer_bytes=int(r.transfer_bytes), sats=sats, ks=ks, fetched=fetched)
+            st.raw_events.append(ev)
+            for s, k, f in zip(sats, ks, fetched):
+                st.pending.append((r.completion_step, st.order, s, -1, k, ev))
+                st.order += 1
+            st.cumulative_bytes = int(r.cumulative_bytes)
+            st.ledger = [(c, n_) for c, n_ in st.ledger if c > t - 1]
+            st.ledger.append((r.completion_step, int(r.transfer_bytes)))
+            fired.add(b)
+        self._dd_fired[t] = fired
+
+    def _dd_materialise(self) -> None:
+        """StepRows of every step whose decisions (and all earlier ones) are read."""
+        first_unread = self._dd_unread[0] if self._dd_unread else None
+        while self._dd_steps and (first_unread is None or self._dd_steps[0][0] < first_unread):
+            t, boundary, rows = self._dd_steps.pop(0)
+            for st in self.states:  # landings due at t (engine.py:293-299), before t's
+                # own decision: a transfer fired at t lands at t + 1 at the earliest
+                due = [x for x in st.pending if x[0] <= t and x[5].trigger_step < t]
+                if due:
+                    due.sort(key=lambda x: (x[0], x[1]))
+                    for _, _, s, _, n_, ev in due:
+                        st.dyn_count[s] = n_
+                        if self.track_sets:
+                            st.dyn_sets[s] = ev.fetched[ev.sats.index(s)]
+                    st.pending = [x for x in st.pending if not (x[0] <= t and
+                                                                x[5].trigger_step < t)]
+                st.step = t
+            fired = self._dd_fired.pop(t, set()) if boundary else set()
+            if rows:
+                for b, st in enumerate(self.states):
+                    st.rows.append(self._row(st, t, int(b in fired), self._row_sizes(b, t)))
+
     def _close_decision(self, sh) -> None:
         t, first, sizes = self._open
         self._open = None
@@ -417,7 +535,11 @@ class HeteroCacheDecoder:
                 st.rows.append(self._row(st, t, flags[b], sizes[b]))
 
     def finish(self, stream=None) -> None:
-        """Take a still-open boundary decision (the last decoded step's)."""
+        """Take a still-open boundary decision (the last decoded step's); with
+        device decisions, read all of them."""
+        if self.devdec:
+            self._dd_poll(wait=True)
+            return
         if self._open is not None:
             self._close_decision(_lib.stream_handle(stream))
 

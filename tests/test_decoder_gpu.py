@@ -233,8 +233,11 @@ def test_prefill_rows_match_oracle():
     dict(heads=(32, 8), B=1, shift=11, T=30),
     dict(heads=(32, 4), B=1, shift=9, T=24, window=4),
 ])
-def test_decoder_variants_match_oracle(kw):
-    ctx = _build(**kw)
+@pytest.mark.parametrize("dd", [None, False], ids=["auto", "host"])
+def test_decoder_variants_match_oracle(kw, dd):
+    """auto: device decisions wherever the configuration supports them
+    (devdec.cu); host: the host-side decision path."""
+    ctx = _build(device_decisions=dd, **kw)
     rows, _, _, _ = _run(ctx)
     _check_events(ctx, rows)
 
@@ -343,7 +346,7 @@ def test_single_call_fire_and_land_abi():
 
     from paper_2601_13684_b200 import _lib
 
-    ctx = _build(T=12, B=1)
+    ctx = _build(T=12, B=1, device_decisions=False)  # host-driven fires / landings
     dec, gen = ctx["dec"], ctx["gen"]
     lib, h, sh = dec.lib, dec.handle, _lib.stream_handle()
     p = dec.pivots[0]
@@ -372,8 +375,9 @@ def test_single_call_fire_and_land_abi():
     assert want <= pre
 
 
+@pytest.mark.parametrize("dd", [None, False], ids=["auto", "host"])
 @pytest.mark.parametrize("seed", range(N_RANDOM_CONFIGS))
-def test_randomized_configs_match_oracle(seed):
+def test_randomized_configs_match_oracle(seed, dd):
     """Seeded random engine configurations (window, delay, host-link model, sinks /
     recency, chunk, batch, prompt length, shift schedule, decision order): events,
     StepRows and dynamic sets must equal the oracle's replay of the GPU rows."""
@@ -389,7 +393,7 @@ def test_randomized_configs_match_oracle(seed):
         shift=tuple(sorted(int(x) for x in rng.choice(np.arange(3, T - 2), n_shift,
                                                          replace=False))),
         seed=int(rng.integers(0, 1000)))
-    ctx = _build(**kw)
+    ctx = _build(device_decisions=dd, **kw)
     rows, _, _, _ = _run(ctx)
     _check_events(ctx, rows)
 
