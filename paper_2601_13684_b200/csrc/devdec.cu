@@ -24,7 +24,7 @@ namespace hc {
 namespace {
 
 __device__ __forceinline__ DevXfer& xf(const DevDec& d, int sat, int64_t ring_idx) {
-  return d.xfers[size_t(sat) * kQ + size_t(ring_idx % kQ)];
+  return d.xfers[size_t(sat) * d.nq + size_t(ring_idx % d.nq)];
 }
 
 __device__ __forceinline__ int32_t vload(const int32_t* p) {
@@ -119,12 +119,12 @@ __global__ void __launch_bounds__(1024) decide_kernel(DevDec d, int t, int first
       for (int i = 0; i < ns && i < 8; ++i) {
         DevSat& sat = d.sats[a0 + i];
         const int64_t idx = sat.tail;
-        if (idx - sat.head >= kQ) {
+        if (idx - sat.head >= d.nq) {
           atomicExch(d.error, int(kDDRingFull));
           continue;
         }
         DevXfer& x = xf(d, a0 + i, idx);
-        const int slot = int(idx % kQ);
+        const int slot = int(idx % d.nq);
         x.completion = completion;
         x.order = ord++;
         x.trigger = t;
@@ -171,15 +171,12 @@ __global__ void __launch_bounds__(1024) decide_kernel(DevDec d, int t, int first
   hdr->pad = 1;  // written: the host reads this boundary once its event completed
 }
 
-constexpr int kSchedMax = 2048;  // one item per satellite per pass (n_sat beyond: next pass)
-
-// Which selected transfers can be gathered now, in (completion, sequence,
-// order) order.  One CTA; every satellite is visited by one thread.
+// Which selected transfers can be gathered now: the satellite's staging
+// buffer is free, or the transfer holding it is superseded at the same
+// completion step.  Marks them SCHEDULED (target buffer chosen); the
+// retrieval stream's next build pass picks them up.  One CTA, a thread per
+// satellite.
 __global__ void __launch_bounds__(1024) schedule_kernel(DevDec d) {
-  __shared__ GatherItem items[kSchedMax];
-  __shared__ uint32_t n_items;
-  if (threadIdx.x == 0) n_items = 0;
-  __syncthreads();
   for (int si = threadIdx.x; si < d.n_sat; si += blockDim.x) {
     DevSat& sat = d.sats[si];
     const int64_t tail = *reinterpret_cast<volatile int64_t*>(&sat.tail);
@@ -205,22 +202,56 @@ __global__ void __launch_bounds__(1024) schedule_kernel(DevDec d) {
         }
       }
       x.buf = target;
-      x.state = kXScheduled;
+      x.pad0 = 0;  // not yet built by the retrieval stream
+      __threadfence();
       sat.staging_owner = int32_t(i);
-      const uint32_t at = atomicAdd(&n_items, 1u);
-      if (at < kSchedMax) items[at] = GatherItem{si, int32_t(i % kQ), x.completion, x.order};
+      atomicExch(&x.state, int(kXScheduled));
       break;
     }
   }
+}
+
+// Retrieval stream, one CTA per satellite: the scheduled transfer not yet
+// taken by a gather pass gets its prefix position list and joins this pass's
+// list (the list belongs to the retrieval stream: passes never overlap).
+__global__ void __launch_bounds__(256) build_dev_kernel(DevDec d, int t_max) {
+  const int si = blockIdx.x;
+  DevSat& sat = d.sats[si];
+  __shared__ int64_t s_i;
+  if (threadIdx.x == 0) {
+    s_i = -1;
+    const int64_t tail = *reinterpret_cast<volatile int64_t*>(&sat.tail);
+    for (int64_t i = sat.head; i < tail; ++i) {
+      DevXfer& x = xf(d, si, i);
+      if (vload(&x.state) == kXScheduled && x.pad0 == 0) {
+        if (x.completion <= t_max) s_i = i;  // later passes take the later deadlines
+        break;
+      }
+    }
+  }
   __syncthreads();
-  const uint32_t n = min(n_items, uint32_t(kSchedMax));
-  // rank sort by (completion, sequence, order): earliest deadline first
+  if (s_i < 0) return;
+  DevXfer& x = xf(d, si, s_i);
+  const int slot = int(s_i % d.nq);
+  build_positions_block(sat.sel + size_t(slot) * sat.k, int(x.cnt),
+                        sat.pos + size_t(x.buf) * sat.cap, x.meta, d.L, d.S, d.R, x.completion);
+  if (threadIdx.x == 0) {
+    x.pad0 = 1;
+    const uint32_t at = atomicAdd(d.n_glist, 1u);
+    d.glist[at] = GatherItem{si, slot, x.completion, x.order};
+  }
+}
+
+// Earliest deadline first: rank sort of the pass's list by (completion,
+// sequence, order) into glist2.
+__global__ void __launch_bounds__(1024) order_kernel(DevDec d) {
+  const uint32_t n = *d.n_glist;
   for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-    const GatherItem a = items[i];
+    const GatherItem a = d.glist[i];
     const int sa = d.sats[a.sat].seq;
     uint32_t r = 0;
     for (uint32_t j = 0; j < n; ++j) {
-      const GatherItem c = items[j];
+      const GatherItem c = d.glist[j];
       const int sc = d.sats[c.sat].seq;
       const bool less = c.completion < a.completion ||
                         (c.completion == a.completion &&
@@ -228,34 +259,20 @@ __global__ void __launch_bounds__(1024) schedule_kernel(DevDec d) {
                                                    (c.order == a.order && j < i)))));
       r += less ? 1u : 0u;
     }
-    d.glist[r] = a;
+    d.glist2[r] = a;
   }
-  if (threadIdx.x == 0) *d.n_glist = n;
 }
 
-__global__ void __launch_bounds__(256) build_dev_kernel(DevDec d) {
-  if (blockIdx.x >= *d.n_glist) return;
-  const GatherItem it = d.glist[blockIdx.x];
-  const DevSat& sat = d.sats[it.sat];
-  DevXfer& x = d.xfers[size_t(it.sat) * kQ + it.slot];
-  build_positions_block(sat.sel + size_t(it.slot) * sat.k, int(x.cnt),
-                        sat.pos + size_t(it.slot) * sat.cap, x.meta, d.L, d.S, d.R,
-                        x.completion);
-}
-
-// 40 CTAs stream the scheduled transfers' rows from the pinned host pool
-// (zero-copy, as gather_host_rows_kernel); the last CTA through a transfer
-// flags it GATHERED.
 __global__ void __launch_bounds__(256) gather_dev_kernel(DevDec d, uint4* __restrict__ K,
                                                          uint4* __restrict__ V) {
   const uint32_t n = *d.n_glist;
   const int nw = gridDim.x * (blockDim.x >> 5);
   const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   for (uint32_t i = 0; i < n; ++i) {
-    const GatherItem it = d.glist[i];
+    const GatherItem it = d.glist2[i];
     const DevSat& sat = d.sats[it.sat];
-    DevXfer& x = d.xfers[size_t(it.sat) * kQ + it.slot];
-    gather_rows(sat.pos + size_t(it.slot) * sat.cap, x.meta[0], sat.srcK, sat.srcV, K, V,
+    DevXfer& x = d.xfers[size_t(it.sat) * d.nq + it.slot];
+    gather_rows(sat.pos + size_t(x.buf) * sat.cap, x.meta[0], sat.srcK, sat.srcV, K, V,
                 sat.row0[x.buf], gw, nw);
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -275,13 +292,14 @@ __device__ void land_one(const DevDec& d, DevSat& sat, DevXfer& x, int64_t idx, 
   u.tail_mask = uint32_t(x.meta[1]);
   u.pad_ = x.meta[2];
   sat.active = x.buf;
-  sat.cur_slot = int32_t(idx % kQ);
+  sat.cur_slot = int32_t(idx % d.nq);
   if (sat.staging_owner == int32_t(idx)) sat.staging_owner = -1;
   sat.head = idx + 1;
 }
 
-// Landing point of step t (engine.py:293-299).  One CTA; thread per satellite.
-__global__ void __launch_bounds__(1024) land_kernel(DevDec d, int t, UnitDesc* units,
+// Landing point of step t (engine.py:293-299).  One small CTA (it runs beside
+// the step's main attention), a thread per satellite.
+__global__ void __launch_bounds__(256) land_kernel(DevDec d, int t, UnitDesc* units,
                                                     uint4* __restrict__ K,
                                                     uint4* __restrict__ V) {
   __shared__ int32_t inl_sat[2048];
@@ -327,6 +345,8 @@ __global__ void __launch_bounds__(1024) land_kernel(DevDec d, int t, UnitDesc* u
         // landing of this very pass -- gather it inline below
         if (st == kXSelected) {
           x.buf = 1 - sat.active;
+          x.pad0 = 1;  // gathered here, never by a retrieval pass
+          __threadfence();
           x.state = kXScheduled;
           sat.staging_owner = int32_t(i);
           const uint32_t at = atomicAdd(&n_inl, 1u);
@@ -345,11 +365,11 @@ __global__ void __launch_bounds__(1024) land_kernel(DevDec d, int t, UnitDesc* u
       const int si = inl_sat[q];
       DevSat& sat = d.sats[si];
       DevXfer& x = xf(d, si, inl_idx[q]);
-      const int slot = int(inl_idx[q] % kQ);
+      const int slot = int(inl_idx[q] % d.nq);
       build_positions_block(sat.sel + size_t(slot) * sat.k, int(x.cnt),
-                            sat.pos + size_t(slot) * sat.cap, x.meta, d.L, d.S, d.R,
+                            sat.pos + size_t(x.buf) * sat.cap, x.meta, d.L, d.S, d.R,
                             x.completion);
-      gather_rows(sat.pos + size_t(slot) * sat.cap, x.meta[0], sat.srcK, sat.srcV, K, V,
+      gather_rows(sat.pos + size_t(x.buf) * sat.cap, x.meta[0], sat.srcK, sat.srcV, K, V,
                   sat.row0[x.buf], threadIdx.x >> 5, blockDim.x >> 5);
       __syncthreads();
       if (threadIdx.x == 0) {
@@ -379,16 +399,22 @@ int launch_schedule(const DevDec& d, cudaStream_t st) {
   return HC_OK;
 }
 
-int launch_dev_gathers(const DevDec& d, uint4* K, uint4* V, cudaStream_t st) {
-  build_dev_kernel<<<std::max(1, d.n_sat), 256, 0, st>>>(d);
+int launch_dev_gathers(const DevDec& d, uint4* K, uint4* V, cudaStream_t st, int t_max,
+                       cudaEvent_t g0, cudaEvent_t g1) {
+  HC_CUDA_TRY(cudaMemsetAsync(d.n_glist, 0, 4, st));
+  build_dev_kernel<<<std::max(1, d.n_sat), 256, 0, st>>>(d, t_max);
   HC_CHECK_LAUNCH();
+  order_kernel<<<1, 1024, 0, st>>>(d);
+  HC_CHECK_LAUNCH();
+  if (g0) HC_CUDA_TRY(cudaEventRecord(g0, st));
   gather_dev_kernel<<<40, 256, 0, st>>>(d, K, V);
+  if (g1) HC_CUDA_TRY(cudaEventRecord(g1, st));
   HC_CHECK_LAUNCH();
   return HC_OK;
 }
 
 int launch_land(const DevDec& d, int t, UnitDesc* units, uint4* K, uint4* V, cudaStream_t st) {
-  land_kernel<<<1, 1024, 0, st>>>(d, t, units, K, V);
+  land_kernel<<<1, 256, 0, st>>>(d, t, units, K, V);
   HC_CHECK_LAUNCH();
   return HC_OK;
 }

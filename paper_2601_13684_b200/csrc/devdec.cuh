@@ -35,7 +35,6 @@
 
 namespace hc {
 
-constexpr int kQ = 8;         // transfer slots per satellite ring
 constexpr int kLogRing = 256;  // boundaries the mapped host log holds
 
 enum XState : int32_t {
@@ -49,7 +48,7 @@ enum XState : int32_t {
 
 struct DevXfer {
   int32_t completion, order, trigger, k;
-  int32_t state, buf, host_off, pad0;
+  int32_t state, buf, host_off, pad0;  // pad0: taken by a gather pass
   int32_t meta[4];  // prefix rows, tail mask, positions >= L (build_positions)
   uint32_t cnt, done_ctas;
 };
@@ -59,8 +58,8 @@ struct DevSat {
   int32_t active, staging_owner, cur_slot, seq;
   int64_t head, tail;                // ring counters (slot = counter % kQ)
   int64_t row0[2];                   // the two prefix buffers' first arena rows
-  uint32_t* sel;                     // [kQ][k]
-  uint32_t* pos;                     // [kQ][cap]
+  uint32_t* sel;                     // [nq][k] fetched sets of the ring's transfers
+  uint32_t* pos;                     // [2][cap] prefix position lists of the two buffers
   const uint4* srcK;                 // host pool (mapped pinned) prefill K / V of the satellite
   const uint4* srcV;
 };
@@ -86,6 +85,7 @@ struct GatherItem {
 struct DevDec {
   // static geometry
   int32_t n_sat, n_piv, B, L, S, R, lbase, window, sliding, delay;
+  int32_t nq, pad_;        // transfer slots per satellite ring
   double tau;
   int64_t bw, bpe;
   int32_t* seq_piv;        // [B + 1] pivot slot ranges per sequence
@@ -95,7 +95,7 @@ struct DevDec {
   int64_t row_len;
   const uint32_t* ghist;   // [2][n_piv][8192] the monitor's key histograms (step parity)
   DevSat* sats;            // [n_sat]
-  DevXfer* xfers;          // [n_sat][kQ]
+  DevXfer* xfers;          // [n_sat][nq]
   // per-sequence accounting
   int64_t* cum;            // [B]
   int32_t* order;          // [B]
@@ -107,7 +107,8 @@ struct DevDec {
   uint32_t* n_jobs;
   int32_t* restamp_slots;  // [n_piv]
   uint32_t* n_restamp;
-  GatherItem* glist;       // [n_sat]
+  GatherItem* glist;       // [n_sat] this gather pass (retrieval stream)
+  GatherItem* glist2;      // [n_sat] the same, earliest deadline first
   uint32_t* n_glist;
   // host-mapped log and fetched-set ring
   BoundaryHdr* hdr;        // [kLogRing]
@@ -121,7 +122,7 @@ struct DevDec {
 
 enum DevDecError : int32_t {
   kDDOk = 0,
-  kDDRingFull = 1,     // more than kQ transfers pending for one satellite
+  kDDRingFull = 1,     // more than nq transfers pending for one satellite
   kDDHostRingFull = 2, // the host has not consumed the fetched-set ring
   kDDSpinTimeout = 3,  // a due gather never completed
   kDDTooManySats = 4,
@@ -130,7 +131,8 @@ enum DevDecError : int32_t {
 int launch_decide(const DevDec& d, int t, int first, int nvals, int bidx, const uint32_t* ovl_ring,
                   int ring, cudaStream_t st);
 int launch_schedule(const DevDec& d, cudaStream_t st);
-int launch_dev_gathers(const DevDec& d, uint4* K, uint4* V, cudaStream_t st);
+int launch_dev_gathers(const DevDec& d, uint4* K, uint4* V, cudaStream_t st, int t_max,
+                       cudaEvent_t g0 = nullptr, cudaEvent_t g1 = nullptr);
 int launch_land(const DevDec& d, int t, UnitDesc* units, uint4* K, uint4* V, cudaStream_t st);
 
 }  // namespace hc

@@ -23,6 +23,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <new>
@@ -279,8 +280,14 @@ struct EngineImpl {
   bool devdec = false;
   DevDec dd{};
   cudaStream_t sched = nullptr;         // schedule passes (tiny, never behind a gather)
+  cudaStream_t lnd = nullptr;           // landing + satellites' K4, beside the main K4
   cudaEvent_t ev_land = nullptr, ev_sched = nullptr, ev_sel = nullptr, ev_dec = nullptr;
+  cudaEvent_t ev_app = nullptr, ev_sats = nullptr;
   bool sched_valid = false, sel_valid = false;
+  // a gather pass takes only transfers due within this many steps (0: all of
+  // them, the default -- keeping the host link busy as early as possible beat
+  // every horizon of 1-8 steps at cfg4; HC_DEVDEC_HORIZON overrides)
+  int dd_horizon = 0;
   cudaEvent_t ev_log[kLogRing] = {};    // side stream: boundary decided and selected
   int64_t n_bound = 0, n_read = 0;      // boundaries issued / read by the host
   std::vector<int32_t> dd_sat_units;
@@ -342,8 +349,9 @@ int engine_destroy(EngineImpl& e) {
   }
   for (void* p : e.dd_dev) cudaFree(p);
   for (void* p : e.dd_host) cudaFreeHost(p);
-  for (cudaEvent_t x : {e.ev_land, e.ev_sched, e.ev_sel, e.ev_dec})
+  for (cudaEvent_t x : {e.ev_land, e.ev_sched, e.ev_sel, e.ev_dec, e.ev_app, e.ev_sats})
     if (x) cudaEventDestroy(x);
+  if (e.lnd) cudaStreamDestroy(e.lnd);
   for (cudaEvent_t x : e.ev_log)
     if (x) cudaEventDestroy(x);
   if (e.sched) cudaStreamDestroy(e.sched);
@@ -410,9 +418,8 @@ int devdec_create(EngineImpl& e, const hc_engine_desc& c) {
       x.seq = b;
       x.row0[0] = e.buf_row0[u];
       x.row0[1] = e.buf_row1[u];
-      x.sel = static_cast<uint32_t*>(dev(size_t(kQ) * std::max(1, x.k) * 4));
-      x.pos = static_cast<uint32_t*>(dev(size_t(kQ) * std::max(1, x.cap) * 4));
-      HC_REQUIRE(x.sel && x.pos, HC_ENOMEM, "device decisions: transfer rings");
+      x.pos = static_cast<uint32_t*>(dev(2 * size_t(std::max(1, x.cap)) * 4));
+      HC_REQUIRE(x.pos, HC_ENOMEM, "device decisions: position lists");
       const __nv_bfloat16* sk = e.pool + size_t(e.sat_slot[u]) * 2 * e.L * kHeadDim;
       x.srcK = reinterpret_cast<const uint4*>(sk);
       x.srcV = reinterpret_cast<const uint4*>(sk + size_t(e.L) * kHeadDim);
@@ -424,6 +431,18 @@ int devdec_create(EngineImpl& e, const hc_engine_desc& c) {
   }
   for (int b = 0; b < e.B; ++b) seq_piv[b + 1] += seq_piv[b];
   d.n_sat = int32_t(sats.size());
+  // transfer slots per satellite: as many as ~2 GB of fetched-set storage holds
+  // (8..512); a satellite with more transfers pending at once faults loudly
+  {
+    int64_t per_slot = 0;
+    for (const DevSat& x : sats) per_slot += int64_t(std::max(1, x.k)) * 4;
+    d.nq = int32_t(std::max<int64_t>(8, std::min<int64_t>(512, (int64_t(2) << 30) /
+                                                                   std::max<int64_t>(1, per_slot))));
+    for (DevSat& x : sats) {
+      x.sel = static_cast<uint32_t*>(dev(size_t(d.nq) * std::max(1, x.k) * 4));
+      HC_REQUIRE(x.sel, HC_ENOMEM, "device decisions: transfer rings");
+    }
+  }
   const size_t ns = std::max<size_t>(1, sats.size());
   auto up = [&](const void* src, size_t bytes) -> void* {
     void* p = dev(bytes);
@@ -434,7 +453,7 @@ int devdec_create(EngineImpl& e, const hc_engine_desc& c) {
   d.piv_sat_begin = static_cast<int32_t*>(up(psb.data(), psb.size() * 4));
   d.piv_unit = static_cast<int32_t*>(up(punit.data(), punit.size() * 4));
   d.sats = static_cast<DevSat*>(up(sats.data(), sats.size() * sizeof(DevSat)));
-  d.xfers = static_cast<DevXfer*>(dev(ns * kQ * sizeof(DevXfer)));
+  d.xfers = static_cast<DevXfer*>(dev(ns * d.nq * sizeof(DevXfer)));
   d.cum = static_cast<int64_t*>(dev(size_t(e.B) * 8));
   d.order = static_cast<int32_t*>(dev(size_t(e.B) * 4));
   d.svals = static_cast<double*>(dev(size_t(e.n_piv) * 64 * 8));
@@ -444,16 +463,19 @@ int devdec_create(EngineImpl& e, const hc_engine_desc& c) {
   d.restamp_slots = static_cast<int32_t*>(dev(size_t(e.n_piv) * 4));
   d.n_restamp = static_cast<uint32_t*>(dev(4));
   d.glist = static_cast<GatherItem*>(dev(ns * sizeof(GatherItem)));
+  d.glist2 = static_cast<GatherItem*>(dev(ns * sizeof(GatherItem)));
   d.n_glist = static_cast<uint32_t*>(dev(4));
   HC_CUDA_TRY(cudaGetLastError());
   HC_REQUIRE(d.seq_piv && d.piv_sat_begin && d.piv_unit && d.sats && d.xfers && d.cum &&
                  d.order && d.svals && d.scnt && d.jobs && d.n_jobs && d.restamp_slots &&
-                 d.n_restamp && d.glist && d.n_glist,
+                 d.n_restamp && d.glist && d.glist2 && d.n_glist,
              HC_ENOMEM, "device decisions: state");
   // mapped host memory: the decision log and the fetched sets the host mirrors
   int64_t ksum = 0;
   for (const DevSat& x : sats) ksum += x.k;
-  d.fetched_cap = std::max<int64_t>(4 * ksum + 64, int64_t(1) << 20);
+  // the host reads boundaries within a few of their decision (decoder.py blocks
+  // beyond 4 unread): 6 boundaries of every satellite firing fit
+  d.fetched_cap = std::max<int64_t>(6 * ksum + 64, int64_t(1) << 20);
   auto mapped = [&](void** h, size_t bytes) -> int {
     HC_CUDA_TRY(cudaHostAlloc(h, bytes, cudaHostAllocMapped));
     std::memset(*h, 0, bytes);
@@ -488,9 +510,12 @@ int devdec_create(EngineImpl& e, const hc_engine_desc& c) {
   int lo_prio = 0, hi_prio = 0;
   HC_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
   HC_CUDA_TRY(cudaStreamCreateWithPriority(&e.sched, cudaStreamNonBlocking, hi_prio));
-  for (cudaEvent_t* x : {&e.ev_land, &e.ev_sched, &e.ev_sel, &e.ev_dec})
+  HC_CUDA_TRY(cudaStreamCreateWithPriority(&e.lnd, cudaStreamNonBlocking, hi_prio));
+  for (cudaEvent_t* x : {&e.ev_land, &e.ev_sched, &e.ev_sel, &e.ev_dec, &e.ev_app, &e.ev_sats})
     HC_CUDA_TRY(cudaEventCreateWithFlags(x, cudaEventDisableTiming));
   for (auto& x : e.ev_log) HC_CUDA_TRY(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+  if (const char* h = getenv("HC_DEVDEC_HORIZON")) e.dd_horizon = atoi(h);
+  if (e.dd_horizon <= 0) e.dd_horizon = 1 << 29;
   e.devdec = true;
   return HC_OK;
 }
@@ -851,25 +876,15 @@ __global__ void set_flags_kernel(uint8_t* flags, const int32_t* __restrict__ idx
 // schedule pass and the gathers it frees (retrieval stream).
 int devdec_land(EngineImpl& e, int t, cudaStream_t st) {
   if (e.sched_valid) HC_CUDA_TRY(cudaStreamWaitEvent(st, e.ev_sched, 0));
-  cudaEvent_t w0 = nullptr, w1 = nullptr;
-  if (e.timing) {
-    HC_TRY(new_event(e, &w0, true));
-    HC_TRY(new_event(e, &w1, true));
-    HC_CUDA_TRY(cudaEventRecord(w0, st));
-  }
   HC_TRY(launch_land(e.dd, t, e.d_units, reinterpret_cast<uint4*>(e.K),
                      reinterpret_cast<uint4*>(e.V), st));
-  if (e.timing) {
-    HC_CUDA_TRY(cudaEventRecord(w1, st));
-    e.land_ev.emplace_back(w0, w1);
-  }
   HC_CUDA_TRY(cudaEventRecord(e.ev_land, st));
   HC_CUDA_TRY(cudaStreamWaitEvent(e.sched, e.ev_land, 0));
   return HC_OK;
 }
 
 // A schedule pass on the schedule stream and the gathers it lists.
-int devdec_schedule_and_gather(EngineImpl& e) {
+int devdec_schedule_and_gather(EngineImpl& e, int t_max) {
   HC_TRY(launch_schedule(e.dd, e.sched));
   HC_CUDA_TRY(cudaEventRecord(e.ev_sched, e.sched));
   e.sched_valid = true;
@@ -878,14 +893,10 @@ int devdec_schedule_and_gather(EngineImpl& e) {
   if (e.timing) {
     HC_TRY(new_event(e, &g0, true));
     HC_TRY(new_event(e, &g1, true));
-    HC_CUDA_TRY(cudaEventRecord(g0, e.retr));
   }
   HC_TRY(launch_dev_gathers(e.dd, reinterpret_cast<uint4*>(e.K), reinterpret_cast<uint4*>(e.V),
-                            e.retr));
-  if (e.timing) {
-    HC_CUDA_TRY(cudaEventRecord(g1, e.retr));
-    e.gather_ev.emplace_back(g0, g1);
-  }
+                            e.retr, t_max, g0, g1));
+  if (e.timing) e.gather_ev.emplace_back(g0, g1);
   return HC_OK;
 }
 
@@ -911,7 +922,7 @@ int devdec_decide(EngineImpl& e, int t) {
   HC_CUDA_TRY(cudaEventRecord(e.ev_log[bidx % kLogRing], e.side));
   e.sel_valid = true;
   HC_CUDA_TRY(cudaStreamWaitEvent(e.sched, e.ev_sel, 0));
-  return devdec_schedule_and_gather(e);
+  return devdec_schedule_and_gather(e, t + e.dd_horizon);
 }
 
 // Decode step t, in two halves so a host decision can overlap the attention:
@@ -989,11 +1000,35 @@ int engine_decode_begin(EngineImpl& e, int t, const void* q, const void* kn, con
       int64_t(e.L) + e.T);
   HC_CHECK_LAUNCH();
   if (ev) HC_CUDA_TRY(cudaEventRecord(ev[1], st));
+  if (e.devdec) HC_CUDA_TRY(cudaEventRecord(e.ev_app, st));  // the token is appended
   AttnParams p = decode_params(e, t, q, o);
   // K4 overwrites the score material of parity t&1: step t-2's rows must be done
   if (e.rows_ev[t & 1]) HC_CUDA_TRY(cudaStreamWaitEvent(st, e.rows_ev[t & 1], 0));
   p.skip = hold ? e.d_sat_flags : (land.empty() ? nullptr : e.d_skip);
   HC_TRY(launch_attn_tiles(e.tmK, e.tmV, p, active_tiles(e, t), st));
+  if (e.devdec) {
+    // landing point (device-decided transfers due at t), then the satellites'
+    // K4, on their own stream beside the main K4: the landing's wait for a late
+    // gather no longer serialises the step
+    HC_CUDA_TRY(cudaStreamWaitEvent(e.lnd, e.ev_app, 0));
+    HC_TRY(devdec_land(e, t, e.lnd));
+    HC_TRY(devdec_schedule_and_gather(e, t + e.dd_horizon));
+    AttnParams ps = p;
+    ps.skip = nullptr;
+    ps.tiles = e.d_sat_tiles;
+    const int n = int(std::upper_bound(e.sat_t_act.begin(), e.sat_t_act.end(), uint32_t(t)) -
+                      e.sat_t_act.begin());
+    HC_TRY(launch_attn_tiles(e.tmK, e.tmV, ps, n, e.lnd));
+    HC_CUDA_TRY(cudaEventRecord(e.ev_sats, e.lnd));
+    if (e.timing) {  // landing stall = how far the satellites' path ends after the main K4
+      cudaEvent_t w0 = nullptr, w1 = nullptr;
+      HC_TRY(new_event(e, &w0, true));
+      HC_TRY(new_event(e, &w1, true));
+      HC_CUDA_TRY(cudaEventRecord(w0, st));
+      HC_CUDA_TRY(cudaEventRecord(w1, e.lnd));
+      e.land_ev.emplace_back(w0, w1);
+    }
+  }
   e.in_step = t;
   e.cur_hold = hold;
   e.cur_st = st;
@@ -1009,13 +1044,8 @@ int engine_decode_end(EngineImpl& e, int t, cudaStream_t st) {
   e.in_step = 0;  // landings below are applied for real
   AttnParams pl = e.cur_p;
   pl.skip = nullptr;
-  if (e.cur_hold && e.devdec) {
-    HC_TRY(devdec_land(e, t, st));
-    HC_TRY(devdec_schedule_and_gather(e));
-    const int n = int(std::upper_bound(e.sat_t_act.begin(), e.sat_t_act.end(), uint32_t(t)) -
-                      e.sat_t_act.begin());
-    pl.tiles = e.d_sat_tiles;
-    HC_TRY(launch_attn_tiles(e.tmK, e.tmV, pl, n, st));
+  if (e.devdec) {
+    HC_CUDA_TRY(cudaStreamWaitEvent(st, e.ev_sats, 0));  // satellites attended
   } else if (e.cur_hold) {
     std::vector<int> land;
     land.swap(e.deferred);
@@ -2104,12 +2134,12 @@ extern "C" int hc_engine_read_indices(hc_engine* eng, int32_t kind, int32_t id, 
       if (ds.cur_slot < 0) si = -1;
     }
     if (si >= 0) {
-      hc::DevXfer* x = e.dd.xfers + size_t(si) * hc::kQ + ds.cur_slot;
+      hc::DevXfer* x = e.dd.xfers + size_t(si) * e.dd.nq + ds.cur_slot;
       if (kind == 1) {
         list = ds.sel + size_t(ds.cur_slot) * ds.k;
         cnt = &x->cnt;
       } else {
-        list = ds.pos + size_t(ds.cur_slot) * ds.cap;
+        list = ds.pos + size_t(ds.active) * ds.cap;
         meta = x->meta;
       }
     } else if (kind == 1) {
@@ -2245,9 +2275,10 @@ extern "C" int hc_engine_retrieval_stats(hc_engine* eng, double* out4) {
   }
   for (auto& pr : e.land_ev) {
     HC_CUDA_TRY(cudaEventSynchronize(pr.second));
+    HC_CUDA_TRY(cudaEventSynchronize(pr.first));
     float ms = 0;
     HC_CUDA_TRY(cudaEventElapsedTime(&ms, pr.first, pr.second));
-    w += ms;
+    w += ms > 0 ? ms : 0;  // device decisions: the pair may end in either order
   }
   out4[0] = double(e.gather_rows_issued) * 2 * hc::kHeadDim * 2;  // bytes (upper bound)
   out4[1] = g;                                                     // gather kernel ms

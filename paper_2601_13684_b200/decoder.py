@@ -37,6 +37,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+from collections import deque
 from dataclasses import dataclass, field
 from math import ceil
 
@@ -214,6 +215,9 @@ class HeteroCacheDecoder:
         self.pivot_units.sort()
         self.pivot_slot = {u: i for i, u in enumerate(self.pivot_units)}
         self.states = [SequenceState() for _ in range(self.B)]
+        if self.devdec:  # the device mirror pops landings / landed ledger entries in order
+            for st in self.states:
+                st.pending, st.ledger = deque(), deque()
         self._cols = [[self.pivot_slot[self.unit(b, p)] for p in self.piv_of[b]] if self.monitor
                       else [] for b in range(self.B)]
         self._pinned = None
@@ -228,7 +232,7 @@ class HeteroCacheDecoder:
         self.overlap_decisions = overlap_decisions
         self._open = None
         # device decisions: steps not yet turned into StepRows, boundaries not yet read
-        self._dd_steps = []       # (t, boundary, rows)
+        self._dd_steps = deque()  # (t, boundary, rows)
         self._dd_unread = []      # boundary steps issued, decision not read yet
         self._dd_fired = {}       # boundary step -> sequences that fired
         if self.devdec:
@@ -425,9 +429,11 @@ class HeteroCacheDecoder:
             self._dd_steps.append((t, boundary, rows))
             if boundary:
                 self._dd_unread.append(t)
-            # read whatever the device has decided by now; block only if the
-            # mapped log (256 boundaries) is about to wrap
-            self._dd_poll(wait=len(self._dd_unread) > 192)
+            # read whatever the device has decided by now; block (on a decision
+            # several boundaries old -- the GPU still has those steps queued)
+            # only when more than 4 are unread: the mapped fetched-set ring
+            # holds 6 boundaries of every satellite firing
+            self._dd_poll(keep=4)
             return
         hold = self._open is not None
         self._land_due(t, sh)
@@ -455,12 +461,14 @@ class HeteroCacheDecoder:
 
     # ---- device decisions: the host mirror ----------------------------------------
 
-    def _dd_poll(self, wait: bool) -> None:
-        """Read device decisions in boundary order (all of them with wait) and turn
-        the steps they complete into StepRows."""
+    def _dd_poll(self, keep: int = 0) -> None:
+        """Read device decisions in boundary order -- those already done, and
+        blocking on the oldest while more than `keep` are unread -- and turn the
+        steps they complete into StepRows."""
         step = C.c_int32()
         nf = C.c_int32()
         while self._dd_unread:
+            wait = len(self._dd_unread) > keep
             _lib.check(self.lib.hc_engine_poll_decisions(
                 self.handle, int(wait), C.byref(step), self._dd_recs, len(self._dd_recs),
                 C.byref(nf), self._dd_fetched.ctypes.data, self._dd_fetched.size))
@@ -469,6 +477,7 @@ class HeteroCacheDecoder:
             t = step.value
             if t != self._dd_unread[0]:
                 raise EngineError(f"device decision for step {t}, expected {self._dd_unread[0]}")
+            self._dd_materialise(upto=t - 1)  # rows before t must not see t's fires
             self._dd_unread.pop(0)
             self._dd_record(t, nf.value)
         self._dd_materialise()
@@ -494,31 +503,32 @@ class HeteroCacheDecoder:
             ev = _Event(trigger_step=t, pivot=p, completion_step=r.completion_step,
                         transfer_bytes=int(r.transfer_bytes), sats=sats, ks=ks, fetched=fetched)
             st.raw_events.append(ev)
+            # completion steps never decrease in firing order (cumulative bytes
+            # only grow): the pending deque stays in (completion, order) order
             for s, k, f in zip(sats, ks, fetched):
                 st.pending.append((r.completion_step, st.order, s, -1, k, ev))
                 st.order += 1
             st.cumulative_bytes = int(r.cumulative_bytes)
-            st.ledger = [(c, n_) for c, n_ in st.ledger if c > t - 1]
+            while st.ledger and st.ledger[0][0] <= t - 1:  # landed: never in flight again
+                st.ledger.popleft()
             st.ledger.append((r.completion_step, int(r.transfer_bytes)))
             fired.add(b)
         self._dd_fired[t] = fired
 
-    def _dd_materialise(self) -> None:
-        """StepRows of every step whose decisions (and all earlier ones) are read."""
+    def _dd_materialise(self, upto: int | None = None) -> None:
+        """StepRows of every step whose decisions (and all earlier ones) are read
+        (and, with upto, of steps <= upto only)."""
         first_unread = self._dd_unread[0] if self._dd_unread else None
-        while self._dd_steps and (first_unread is None or self._dd_steps[0][0] < first_unread):
-            t, boundary, rows = self._dd_steps.pop(0)
+        while self._dd_steps and (first_unread is None or self._dd_steps[0][0] < first_unread) \
+                and (upto is None or self._dd_steps[0][0] <= upto):
+            t, boundary, rows = self._dd_steps.popleft()
             for st in self.states:  # landings due at t (engine.py:293-299), before t's
                 # own decision: a transfer fired at t lands at t + 1 at the earliest
-                due = [x for x in st.pending if x[0] <= t and x[5].trigger_step < t]
-                if due:
-                    due.sort(key=lambda x: (x[0], x[1]))
-                    for _, _, s, _, n_, ev in due:
-                        st.dyn_count[s] = n_
-                        if self.track_sets:
-                            st.dyn_sets[s] = ev.fetched[ev.sats.index(s)]
-                    st.pending = [x for x in st.pending if not (x[0] <= t and
-                                                                x[5].trigger_step < t)]
+                while st.pending and st.pending[0][0] <= t and st.pending[0][5].trigger_step < t:
+                    _, _, s, _, n_, ev = st.pending.popleft()
+                    st.dyn_count[s] = n_
+                    if self.track_sets:
+                        st.dyn_sets[s] = ev.fetched[ev.sats.index(s)]
                 st.step = t
             fired = self._dd_fired.pop(t, set()) if boundary else set()
             if rows:
@@ -538,7 +548,7 @@ class HeteroCacheDecoder:
         """Take a still-open boundary decision (the last decoded step's); with
         device decisions, read all of them."""
         if self.devdec:
-            self._dd_poll(wait=True)
+            self._dd_poll(keep=0)
             return
         if self._open is not None:
             self._close_decision(_lib.stream_handle(stream))
