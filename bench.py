@@ -77,6 +77,8 @@ def parse(argv=None):
     ap.add_argument("--secondary", default="cfg3",
                     help="N=1: a second workload measured in a child process ('none': skip)")
     ap.add_argument("--layers", type=int, default=0, help="override layer count (debug)")
+    ap.add_argument("--batch", type=int, default=0,
+                    help="override the batch (e.g. one rank's share of a batch-sharded run)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seqs", type=int, default=1,
                     help="sequences the CPU decoder samples (cpu_baseline, parity, reference)")
@@ -96,9 +98,11 @@ def parse(argv=None):
     ap.add_argument("--calib-steps", type=int, default=16)
     ap.add_argument("--obs-window", type=int, default=0,
                     help="prefill observation window (0: min(32, 128 // G))")
-    ap.add_argument("--shard", choices=("auto", "slabs", "units", "sequences"), default="auto",
-                    help="N>1: slabs (default) = one batch's (sequence, layer) pairs in contiguous "
-                         "ranges per rank; units = bin-packed (sequence, layer, cluster) units; "
+    ap.add_argument("--shard", choices=("auto", "batch", "slabs", "units", "sequences"),
+                    default="auto",
+                    help="N>1, one batch split over the ranks (strong): batch = whole sequences "
+                         "per rank (auto when the batch divides), slabs = contiguous (sequence, "
+                         "layer) ranges, units = bin-packed (sequence, layer, cluster) units; "
                          "sequences = every rank its own batch (weak)")
     ap.add_argument("--score-material", choices=("fp32", "fp16"), default="fp32",
                     help="pivot score material between K4 and the GQA-mean rows")
@@ -188,6 +192,8 @@ def workload_of(args):
     w = CONFIGS[args.workload]
     if args.layers:
         w = replace(w, layers=args.layers)
+    if args.batch:
+        w = replace(w, batch=args.batch)
     return w
 
 
@@ -229,7 +235,11 @@ def shard_mode(args, w, world: int) -> str:
     """replicas (N=1), sequences (weak), slabs or units (strong) -- both arms."""
     if world == 1:
         return "replicas"
-    mode = args.shard if args.shard != "auto" else "slabs"
+    mode = args.shard
+    if mode == "auto":  # whole sequences of the batch per rank when they split evenly
+        mode = "batch" if w.batch % world == 0 else "slabs"
+    if mode == "batch" and w.batch % world:
+        mode = "slabs"
     if mode == "slabs" and (w.batch * w.num_layers) % world:
         mode = "units"  # (sequence, layer) pairs do not split evenly: bin-pack clusters
     return mode
@@ -257,6 +267,8 @@ def make_config(args, w, cfg, rho, l_base_int, roles: dict, world: int, mode: st
     m = w.model
     par = {"replicas": f"replicas x{world} (weak: each GPU decodes its own batch)",
            "sequences": f"sequences x{world} (weak: each GPU decodes its own batch)",
+           "batch": f"batch x{world} (strong: rank r decodes sequences [r*B/N, (r+1)*B/N) of "
+                    f"one batch, decisions on its device, no exchange; O all-gathered in place)",
            "slabs": f"slabs x{world} (strong: rank r owns (sequence, layer) pairs "
                     f"[r*S, (r+1)*S) of one batch; NCCL fire exchange at boundaries, "
                     f"O all-gathered in place)",
@@ -330,6 +342,11 @@ def run_b200(args, rank, world):
                device_decisions=None if args.decisions == "device" else False)
     mode = shard_mode(args, w, world)
     owned_all = None
+    Bl, seqs = w.batch, None  # sequences this rank decodes
+    if mode == "batch":
+        Bl = w.batch // world
+        seqs = list(range(rank * Bl, (rank + 1) * Bl))
+        dkw.update(batch=Bl)
     if mode in ("slabs", "units"):
         import torch.distributed as dist
 
@@ -352,7 +369,7 @@ def run_b200(args, rank, world):
         dec = HeteroCacheDecoder(tax, plan, cfg, **dkw)
     seed = seed_of(args) + (rank if mode == "sequences" else 0)
     gen = SyntheticKV(m, batch=w.batch, prefill_len=w.prefill_len, num_layers=w.num_layers,
-                      hot=hot_of(w), seed=seed)
+                      hot=hot_of(w), seed=seed, seqs=seqs)
     t0 = time.time()
     for l in range(w.num_layers):
         k, v, q = gen.layer_kv(l, obs)
@@ -425,21 +442,31 @@ def run_b200(args, rank, world):
     # the all-gather of O) overlap the decode of step t.
     hq_all = qs[t + 1:t + K + 1].cpu().pin_memory()
     hkv = [[x.cpu().pin_memory() for x in kv] for kv in kv_pool]
-    hout = [torch.empty(out.shape, dtype=out.dtype, pin_memory=True) for _ in range(2)]
+    hout = [torch.empty((w.batch,) + tuple(out.shape[1:]), dtype=out.dtype, pin_memory=True)
+            for _ in range(2)]
     dbuf = [tuple(torch.empty_like(x) for x in inputs(1)) for _ in range(2)]
     t_e2e0 = t
-    obuf = [torch.empty_like(out) for _ in range(2)]
+    # the job's result: O of the whole batch (batch mode: this rank's sequences
+    # are one contiguous slab of it, gathered in place)
+    obuf = [torch.empty((w.batch,) + tuple(out.shape[1:]), dtype=out.dtype, device=out.device)
+            for _ in range(2)]
+    oview = [o[seqs[0]:seqs[-1] + 1] if seqs else o for o in obuf]
     copy = torch.cuda.Stream()
     mk = lambda: torch.cuda.Event(enable_timing=False)  # noqa: E731
     ev_in, ev_used, ev_out = [mk(), mk()], [mk(), mk()], [mk(), mk()]
     gather_o = None
-    if mode in ("slabs", "units"):
+    if mode in ("batch", "slabs", "units"):
         import torch.distributed as dist
 
-        if mode == "slabs" and BACKEND == "nccl":
+        if mode in ("batch", "slabs") and BACKEND == "nccl":
             def gather_o(o):  # rank r's rows are slab r of O: gather in place
                 flat = o.view(world, -1)
                 dist.all_gather_into_tensor(o.view(-1), flat[rank])
+        elif mode == "batch":
+            def gather_o(o):  # gloo (functional tests): host staging, rank-major slabs
+                parts = list(o.cpu().view(world, -1).unbind(0))
+                dist.all_gather(parts, parts[rank].clone())
+                o.copy_(torch.stack(parts).view(o.shape))
         else:
             from paper_2601_13684_b200.parallel import combine_unit_outputs
 
@@ -472,7 +499,7 @@ def run_b200(args, rank, world):
             upload(t + 1, 1 - slot)
         stream.wait_event(ev_in[slot])
         stream.wait_event(ev_out[slot])  # previous download of this output slot finished
-        dec.decode_step(t, *dbuf[slot], obuf[slot], rows=False)
+        dec.decode_step(t, *dbuf[slot], oview[slot], rows=False)
         ev_used[slot].record(stream)
         with torch.cuda.stream(copy):
             copy.wait_event(ev_used[slot])
@@ -504,7 +531,7 @@ def run_b200(args, rank, world):
         ms, ms_e2e = max_over_ranks([ms, ms_e2e], device=COLL_DEV)
     jobs = world if mode == "sequences" else 1  # batches decoded per step by the whole job
     own_rows = (rows_first + rows_last) / 2.0  # this rank's (K4 bytes per launch)
-    if mode in ("slabs", "units"):  # one batch over all ranks: rows and fires are the ranks' sum
+    if mode in ("batch", "slabs", "units"):  # one batch over all ranks: the ranks' sum
         import torch.distributed as dist
 
         tot = torch.tensor([rows_first, rows_last, events, exposed, ref_bytes],
@@ -544,7 +571,9 @@ def run_b200(args, rank, world):
         "hbm_gbs_step": jobs * step_bytes / (ms / K * 1e-3) / 1e9,
         "algorithmic_bytes_per_step": int(step_bytes),
         "e2e": {"value": jobs * K / (ms_e2e * 1e-3), "unit": "steps/s",
-                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+                # batch mode: every rank uploads its own sequences' inputs
+                "h2d_bytes_per_step": int(h2d * (world if mode == "batch" else 1)),
+                "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "kernel": "attn_tiles_kernel (K4)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s",

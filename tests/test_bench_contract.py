@@ -57,15 +57,18 @@ def test_b200_arm_full_line_with_cpu_baseline_and_parity():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("shard,launch", [("sequences", "torchrun"), ("slabs", "torchrun"),
-                                          ("slabs", "self"), ("units", "torchrun")])
+                                          ("slabs", "self"), ("units", "torchrun"),
+                                          ("batch", "torchrun")])
 def test_two_rank_paths_run_end_to_end(shard, launch):
     """Functional check of the N>1 bench paths on one GPU: two ranks over gloo
     (HC_BENCH_BACKEND; the driver's runs use NCCL, one GPU per rank).  Slab and
     unit modes exercise the fire exchange and the all-gather of O; "self" is
     `bench.py --gpus 2` re-launching itself under torchrun.  The numbers of such
     a run are not measurements."""
-    d = _run(["--gpus", "2", "--shard", shard, "--workload", "cfg2", "--layers", "4",
-              "--steps", "16", "--warmup", "3", "--calib-samples", "2"],
+    wl = ["--workload", "cfg3", "--layers", "2"] if shard == "batch" else \
+        ["--workload", "cfg2", "--layers", "4"]
+    d = _run(["--gpus", "2", "--shard", shard, *wl, "--steps", "16", "--warmup", "3",
+              "--calib-samples", "2"],
              ranks=2 if launch == "torchrun" else 1, HC_BENCH_BACKEND="gloo")
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0
     assert d["scaling"] == ("weak" if shard == "sequences" else "strong")
