@@ -491,11 +491,20 @@ def run_b200(args, rank, world):
     barrier()
     torch.cuda.synchronize()
     ev0.record(stream)
-    upload(t + 1, 0)
-    for i in range(K):
+    if world == 1 and dec.devdec:
+        # the C-ABI per-step call with HOST buffers (hc_engine_decode_step_host):
+        # inputs H2D and O D2H on the engine's copy stream, one call per step
+        for i in range(K):
+            t += 1
+            dec.decode_step_host(t, hq_all[i], *hkv[t % 4], hout[i % 2], rows=False)
+        K_left = 0
+    else:
+        K_left = K
+        upload(t + 1, 0)
+    for i in range(K_left):
         t += 1
         slot = i % 2
-        if i + 1 < K:
+        if i + 1 < K_left:
             upload(t + 1, 1 - slot)
         stream.wait_event(ev_in[slot])
         stream.wait_event(ev_out[slot])  # previous download of this output slot finished

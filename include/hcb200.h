@@ -249,6 +249,16 @@ int hc_engine_prefill_layer(hc_engine* eng, int32_t layer, const void* k_dev, co
 int hc_engine_decode_step(hc_engine* eng, int32_t step, const void* q_dev, const void* k_new_dev,
                           const void* v_new_dev, void* o_dev, void* stream);
 
+/* decode_step from pinned HOST buffers (a serving runtime's per-step call):
+ * q_host / o_host [B, NL, H*G, 128] and k_new_host / v_new_host [B, NL, H, 128]
+ * bf16.  The inputs cross H2D and the output D2H on an engine-owned copy
+ * stream, double-buffered by step parity so they overlap the neighbouring
+ * steps' decode; o_host holds the step's output once `stream` has passed
+ * hc_engine_join. */
+int hc_engine_decode_step_host(hc_engine* eng, int32_t step, const void* q_host,
+                               const void* k_new_host, const void* v_new_host, void* o_host,
+                               void* stream);
+
 /* decode_step in two halves (decode_step = begin(hold 0) + end), so that the
  * host's window decision of step-1 (engine.py:313-360, read with
  * hc_engine_overlaps, acted on with hc_engine_fire_batch / land_batch) runs

@@ -79,6 +79,7 @@ def _declare(lib):
         "hc_engine_decode_step": (i32, [vp, i32, vp, vp, vp, vp, vp]),
         "hc_engine_decode_begin": (i32, [vp, i32, vp, vp, vp, vp, i32, vp]),
         "hc_engine_decode_end": (i32, [vp, i32, vp]),
+        "hc_engine_decode_step_host": (i32, [vp, i32, vp, vp, vp, vp, vp]),
         "hc_engine_join": (i32, [vp, vp]),
         "hc_pooled_topk": (i32, [vp, u32, u32, u32, vp, vp]),
         "hc_engine_enable_measure": (i32, [vp, i32]),

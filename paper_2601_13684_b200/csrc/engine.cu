@@ -231,6 +231,11 @@ struct EngineImpl {
   std::deque<std::tuple<size_t, size_t, cudaEvent_t>> stage_busy;  // (lo, hi, copy done)
   cudaStream_t retr = nullptr;
   cudaMemPool_t mpool = nullptr;  // private stream-ordered pool (descriptors, transfer blocks)
+  // decode_step_host: copy stream, double-buffered device staging, ordering events
+  cudaStream_t hcopy = nullptr, hdown = nullptr;  // uploads / downloads
+  void* hbuf[2] = {nullptr, nullptr};
+  cudaEvent_t h_in[2] = {}, h_used[2] = {}, h_out[2] = {};
+  int h_last = -1;
   cudaEvent_t last_selected = nullptr;  // side stream: the last fire batch's copies are done
   // per-step phase timeline (bench roofline): 7 events per step: start |
   // append | K4 | combine (step stream) | score rows | monitor (monitor
@@ -355,6 +360,13 @@ int engine_destroy(EngineImpl& e) {
   for (cudaEvent_t x : e.ev_log)
     if (x) cudaEventDestroy(x);
   if (e.sched) cudaStreamDestroy(e.sched);
+  for (int i = 0; i < 2; ++i) {
+    if (e.hbuf[i]) cudaFree(e.hbuf[i]);
+    for (cudaEvent_t x : {e.h_in[i], e.h_used[i], e.h_out[i]})
+      if (x) cudaEventDestroy(x);
+  }
+  if (e.hcopy) cudaStreamDestroy(e.hcopy);
+  if (e.hdown) cudaStreamDestroy(e.hdown);
   if (e.mpool) cudaMemPoolDestroy(e.mpool);  // every block above is freed by now
   if (e.retr) cudaStreamDestroy(e.retr);
   if (e.side) cudaStreamDestroy(e.side);
@@ -1111,6 +1123,46 @@ int engine_decode_step(EngineImpl& e, int t, const void* q, const void* kn, cons
                        void* o, cudaStream_t st) {
   HC_TRY(engine_decode_begin(e, t, q, kn, vn, o, false, st));
   return engine_decode_end(e, t, st);
+}
+
+// decode_step from pinned HOST buffers: the step's inputs cross H2D and its
+// output D2H on engine-owned copy streams, double-buffered so step t's
+// download and step t+1's upload overlap the decode (the e2e path of a
+// serving runtime: one call per step, no framework on the host).
+int engine_decode_step_host(EngineImpl& e, int t, const void* q_h, const void* kn_h,
+                            const void* vn_h, void* o_h, cudaStream_t st) {
+  const size_t qb = size_t(e.B) * e.NL * e.Hq * kHeadDim * 2;
+  const size_t kb = size_t(e.B) * e.NL * e.H * kHeadDim * 2;
+  if (!e.hcopy) {
+    HC_CUDA_TRY(cudaStreamCreateWithFlags(&e.hcopy, cudaStreamNonBlocking));
+    HC_CUDA_TRY(cudaStreamCreateWithFlags(&e.hdown, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      HC_TRY(dalloc(&e.hbuf[i], 2 * qb + 2 * kb, &e.dev_bytes));
+      for (cudaEvent_t* x : {&e.h_in[i], &e.h_used[i], &e.h_out[i]}) {
+        HC_CUDA_TRY(cudaEventCreateWithFlags(x, cudaEventDisableTiming));
+        HC_CUDA_TRY(cudaEventRecord(*x, st));
+      }
+    }
+  }
+  const int s = t & 1;
+  char* d = static_cast<char*>(e.hbuf[s]);
+  void *dq = d, *dkn = d + qb, *dvn = d + qb + kb, *dout = d + qb + 2 * kb;
+  HC_CUDA_TRY(cudaStreamWaitEvent(e.hcopy, e.h_used[s], 0));  // the decode that read this slot
+  HC_CUDA_TRY(cudaMemcpyAsync(dq, q_h, qb, cudaMemcpyHostToDevice, e.hcopy));
+  HC_CUDA_TRY(cudaMemcpyAsync(dkn, kn_h, kb, cudaMemcpyHostToDevice, e.hcopy));
+  HC_CUDA_TRY(cudaMemcpyAsync(dvn, vn_h, kb, cudaMemcpyHostToDevice, e.hcopy));
+  HC_CUDA_TRY(cudaEventRecord(e.h_in[s], e.hcopy));
+  HC_CUDA_TRY(cudaStreamWaitEvent(st, e.h_in[s], 0));
+  HC_CUDA_TRY(cudaStreamWaitEvent(st, e.h_out[s], 0));  // the previous download of this slot
+  HC_TRY(engine_decode_step(e, t, dq, dkn, dvn, dout, st));
+  HC_CUDA_TRY(cudaEventRecord(e.h_used[s], st));
+  // the download runs on its own stream: the next step's upload must not
+  // queue behind it (it waits for this decode to finish)
+  HC_CUDA_TRY(cudaStreamWaitEvent(e.hdown, e.h_used[s], 0));
+  HC_CUDA_TRY(cudaMemcpyAsync(o_h, dout, qb, cudaMemcpyDeviceToHost, e.hdown));
+  HC_CUDA_TRY(cudaEventRecord(e.h_out[s], e.hdown));
+  e.h_last = s;
+  return HC_OK;
 }
 
 // Stream-ordered upload of a small host array: copy into the pinned staging
@@ -2035,7 +2087,17 @@ extern "C" int hc_engine_join(hc_engine* eng, void* stream) {
   HC_REQUIRE(eng, HC_EINVAL, "null argument");
   if (eng->e.step_end)
     HC_CUDA_TRY(cudaStreamWaitEvent((cudaStream_t)stream, eng->e.step_end, 0));
+  if (eng->e.h_last >= 0)  // the last decode_step_host download
+    HC_CUDA_TRY(cudaStreamWaitEvent((cudaStream_t)stream, eng->e.h_out[eng->e.h_last], 0));
   return HC_OK;
+}
+
+extern "C" int hc_engine_decode_step_host(hc_engine* eng, int32_t step, const void* q_host,
+                                          const void* k_new_host, const void* v_new_host,
+                                          void* o_host, void* stream) {
+  HC_REQUIRE(eng && q_host && k_new_host && v_new_host && o_host, HC_EINVAL, "null argument");
+  return hc::engine_decode_step_host(eng->e, step, q_host, k_new_host, v_new_host, o_host,
+                                     (cudaStream_t)stream);
 }
 
 extern "C" int hc_engine_overlaps(hc_engine* eng, int32_t first, int32_t last, int32_t* out,

@@ -425,15 +425,7 @@ class HeteroCacheDecoder:
         if self.devdec:
             _lib.check(self.lib.hc_engine_decode_step(self.handle, t, _lib.ptr(q), _lib.ptr(k_new),
                                                       _lib.ptr(v_new), _lib.ptr(out), sh))
-            boundary = cfg.eval_every_step or t % cfg.window == 0
-            self._dd_steps.append((t, boundary, rows))
-            if boundary:
-                self._dd_unread.append(t)
-            # read whatever the device has decided by now; block (on a decision
-            # several boundaries old -- the GPU still has those steps queued)
-            # only when more than 4 are unread: the mapped fetched-set ring
-            # holds 6 boundaries of every satellite firing
-            self._dd_poll(keep=4)
+            self._dd_after_step(t, rows)
             return
         hold = self._open is not None
         self._land_due(t, sh)
@@ -459,7 +451,34 @@ class HeteroCacheDecoder:
             for b, st in enumerate(self.states):
                 st.rows.append(self._row(st, t, 0, self._row_sizes(b, t, rec[b])))
 
+    def decode_step_host(self, t: int, q, k_new, v_new, out, stream=None, *, rows: bool = True):
+        """decode_step from pinned host tensors (a serving runtime's per-step call,
+        hc_engine_decode_step_host): the inputs cross H2D and the output D2H on
+        the engine's copy stream; `out` holds step t once `stream` has passed
+        join().  Needs device decisions."""
+        if not self.devdec:
+            raise EngineError("decode_step_host needs device decisions")
+        for x in (q, k_new, v_new, out):
+            if x.is_cuda or not x.is_pinned() or not x.is_contiguous():
+                raise EngineError("decode_step_host takes contiguous pinned host tensors")
+        _lib.check(self.lib.hc_engine_decode_step_host(
+            self.handle, t, _lib.ptr(q), _lib.ptr(k_new), _lib.ptr(v_new), _lib.ptr(out),
+            _lib.stream_handle(stream)))
+        self._dd_after_step(t, rows)
+
     # ---- device decisions: the host mirror ----------------------------------------
+
+    def _dd_after_step(self, t: int, rows: bool) -> None:
+        cfg = self.config
+        boundary = cfg.eval_every_step or t % cfg.window == 0
+        self._dd_steps.append((t, boundary, rows))
+        if boundary:
+            self._dd_unread.append(t)
+        # read whatever the device has decided by now; block (on a decision
+        # several boundaries old -- the GPU still has those steps queued) only
+        # when more than 4 are unread: the mapped fetched-set ring holds 6
+        # boundaries of every satellite firing
+        self._dd_poll(keep=4)
 
     def _dd_poll(self, keep: int = 0) -> None:
         """Read device decisions in boundary order -- those already done, and

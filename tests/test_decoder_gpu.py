@@ -414,3 +414,36 @@ def test_fetched_ring_wraps_without_track_sets():
                       for e in st.events] for st in ctx["dec"].states])
         ctx["dec"].close()
     assert logs[0] == logs[1] and sum(len(x) for x in logs[0]) >= 10
+
+
+def test_decode_step_host_matches_device_inputs():
+    """hc_engine_decode_step_host (pinned host in / out, the engine's copy stream)
+    gives bit-identical outputs and events to decode_step on device tensors."""
+    import torch
+
+    outs, evs = [], []
+    for host in (False, True):
+        ctx = _build(B=2, T=24, window=4, shift=(5, 13))
+        dec, gen = ctx["dec"], ctx["gen"]
+        seq = []
+        for t in range(1, 25):
+            q, kn, vn = gen.step_inputs(t, ctx["shift"])
+            if host:
+                hq, hk, hv = (x.cpu().pin_memory() for x in (q, kn, vn))
+                ho = torch.empty(q.shape, dtype=q.dtype, pin_memory=True)
+                dec.decode_step_host(t, hq, hk, hv, ho)
+                dec.join()
+                torch.cuda.synchronize()
+                seq.append(ho.clone())
+            else:
+                o = torch.empty_like(q)
+                dec.decode_step(t, q, kn, vn, o)
+                seq.append(o.cpu())
+        dec.sync()
+        outs.append(seq)
+        evs.append([[(e.trigger_step, e.pivot, e.completion_step, e.fetches) for e in st.events]
+                    for st in dec.states])
+        dec.close()
+    assert evs[0] == evs[1] and any(evs[0])
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
