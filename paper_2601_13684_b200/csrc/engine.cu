@@ -377,6 +377,8 @@ int engine_destroy(EngineImpl& e) {
   return HC_OK;
 }
 
+int host_io_init(EngineImpl& e);
+
 // Device decisions: satellites in pivot-slot order, rings, mapped host log.
 int devdec_create(EngineImpl& e, const hc_engine_desc& c) {
   HC_REQUIRE(c.monitor && e.n_piv > 0, HC_EINVAL, "device decisions need monitored pivots");
@@ -800,7 +802,7 @@ int engine_create(EngineImpl& e, const hc_engine_desc& c, const int32_t* roles,
   HC_CUDA_TRY(cudaStreamCreateWithPriority(&e.side, cudaStreamNonBlocking, hi_prio));
   HC_CUDA_TRY(cudaStreamCreateWithPriority(&e.mon, cudaStreamNonBlocking, hi_prio));
   if (c.device_decisions) HC_TRY(devdec_create(e, c));
-  return HC_OK;
+  return host_io_init(e);  // decode_step_host staging, outside any timed step
 }
 
 AttnParams decode_params(EngineImpl& e, int t, const void* q, void* o) {
@@ -1129,21 +1131,27 @@ int engine_decode_step(EngineImpl& e, int t, const void* q, const void* kn, cons
 // output D2H on engine-owned copy streams, double-buffered so step t's
 // download and step t+1's upload overlap the decode (the e2e path of a
 // serving runtime: one call per step, no framework on the host).
+// Staging of decode_step_host, set up with the engine (not inside a timed step).
+int host_io_init(EngineImpl& e) {
+  const size_t qb = size_t(e.B) * e.NL * e.Hq * kHeadDim * 2;
+  const size_t kb = size_t(e.B) * e.NL * e.H * kHeadDim * 2;
+  HC_CUDA_TRY(cudaStreamCreateWithFlags(&e.hcopy, cudaStreamNonBlocking));
+  HC_CUDA_TRY(cudaStreamCreateWithFlags(&e.hdown, cudaStreamNonBlocking));
+  for (int i = 0; i < 2; ++i) {
+    HC_TRY(dalloc(&e.hbuf[i], 2 * qb + 2 * kb, &e.dev_bytes));
+    for (cudaEvent_t* x : {&e.h_in[i], &e.h_used[i], &e.h_out[i]}) {
+      HC_CUDA_TRY(cudaEventCreateWithFlags(x, cudaEventDisableTiming));
+      HC_CUDA_TRY(cudaEventRecord(*x, 0));
+    }
+  }
+  return HC_OK;
+}
+
 int engine_decode_step_host(EngineImpl& e, int t, const void* q_h, const void* kn_h,
                             const void* vn_h, void* o_h, cudaStream_t st) {
   const size_t qb = size_t(e.B) * e.NL * e.Hq * kHeadDim * 2;
   const size_t kb = size_t(e.B) * e.NL * e.H * kHeadDim * 2;
-  if (!e.hcopy) {
-    HC_CUDA_TRY(cudaStreamCreateWithFlags(&e.hcopy, cudaStreamNonBlocking));
-    HC_CUDA_TRY(cudaStreamCreateWithFlags(&e.hdown, cudaStreamNonBlocking));
-    for (int i = 0; i < 2; ++i) {
-      HC_TRY(dalloc(&e.hbuf[i], 2 * qb + 2 * kb, &e.dev_bytes));
-      for (cudaEvent_t* x : {&e.h_in[i], &e.h_used[i], &e.h_out[i]}) {
-        HC_CUDA_TRY(cudaEventCreateWithFlags(x, cudaEventDisableTiming));
-        HC_CUDA_TRY(cudaEventRecord(*x, st));
-      }
-    }
-  }
+  if (!e.hcopy) HC_TRY(host_io_init(e));
   const int s = t & 1;
   char* d = static_cast<char*>(e.hbuf[s]);
   void *dq = d, *dkn = d + qb, *dvn = d + qb + kb, *dout = d + qb + 2 * kb;
