@@ -16,9 +16,10 @@
 //     hands accumulators to the epilogue;
 //   * warps 2-5: epilogue, one thread per query row, tcgen05.ld 32x32b.x32.
 // Pass 1 keeps per-row online softmax statistics (max, sum) per key chunk;
-// obs_merge combines chunks; pass 2 recomputes the tiles and turns them into
-// probabilities, reduced over the rows with a warp transpose-reduction (31
-// shuffles per 32 columns) and across warps through shared memory.  Each key
+// obs_merge combines chunks; pass 2 recomputes the tiles TRANSPOSED (S^T =
+// K Q^T: TMEM lane = key, column = query row), so each epilogue thread turns
+// its key's 64 query-row scores into probabilities and sums them in
+// registers; the two row halves meet in shared memory.  Each key
 // tile's score column is owned by exactly one CTA: no atomics, deterministic.
 
 #include <cuda.h>
@@ -137,30 +138,6 @@ __device__ __forceinline__ float fast_exp2(float x) {
   return y;
 }
 
-// Sum 32 column values over the 32 lanes (rows) of a warp -- afterwards lane c
-// holds the total of column c (halving butterfly, 31 shuffles) -- for two
-// independent 32x32 blocks, stage-interleaved so every
-// shuffle stage has twice the independent work (the chains are latency-bound).
-__device__ __forceinline__ void transpose_reduce32x2(float (&a)[32], float (&b)[32], float& ca,
-                                                     float& cb) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int off = 16; off >= 1; off >>= 1) {
-    const bool upper = (lane & off) != 0;
-#pragma unroll
-    for (int j = 0; j < off; ++j) {
-      const float ka = upper ? a[j + off] : a[j], sa = upper ? a[j] : a[j + off];
-      const float kb = upper ? b[j + off] : b[j], sb = upper ? b[j] : b[j + off];
-      const float ra = __shfl_xor_sync(0xffffffffu, sa, off);
-      const float rb = __shfl_xor_sync(0xffffffffu, sb, off);
-      a[j] = ka + ra;
-      b[j] = kb + rb;
-    }
-  }
-  ca = a[0];
-  cb = b[0];
-}
-
 __global__ void __launch_bounds__(kObsThreads, 2)
 obs_score_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmQ,
                  const ObsParams p) {
@@ -229,10 +206,15 @@ obs_score_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant_
         mb_wait(full + 8 * s, (i / kStagesObs) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d = tmem + a * kN;
+        // pass 1: S = Q K^T (TMEM lane = query row, column = key); pass 2: S^T =
+        // K Q^T (lane = key, column = query row), so each thread's column sum
+        // of probabilities is a plain sum over its registers -- no shuffles
+        const bool tr = p.pass == 2;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint32_t off = (kk >> 2) * kBox + (kk & 3) * 32;
-          umma(d, sdesc(sQ + off), sdesc(sK + s * kTile + off), kk > 0 ? 1u : 0u);
+          const uint64_t qd = sdesc(sQ + off), kd = sdesc(sK + s * kTile + off);
+          umma(d, tr ? kd : qd, tr ? qd : kd, kk > 0 ? 1u : 0u);
         }
         umma_commit(empty + 8 * s);  // ring slot reusable once these MMAs finish
         umma_commit(tfull + 8 * a);  // accumulator ready for the epilogue
@@ -246,13 +228,24 @@ obs_score_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant_
     const int r = q4 * 32 + lane;            // query row
     const bool row_ok = r < p.rows;
     const int qpos = p.L - p.w + (row_ok ? r / p.G : 0);  // causal limit of this row
-    float m = -INFINITY, l = 0.f, Mr = 0.f, log2L = 0.f;
-    if (p.pass == 2 && row_ok) {
-      Mr = p.stats[(size_t(unit) * kM + r) * 2 + 0];
-      const float Lr = p.stats[(size_t(unit) * kM + r) * 2 + 1];
-      log2L = Lr > 0.f ? log2f(Lr) : INFINITY;  // empty row: every probability is 0
-    }
+    float m = -INFINITY, l = 0.f;
     const float inv_rows = 1.f / float(p.rows);
+    // pass 2: per query row, exp2(x*scale - M - log2 L) = its probability;
+    // rows beyond w*G or with an empty softmax get +inf (probability 0)
+    float* s_off = colsum + 4 * 2 * kN;  // [128]
+    if (p.pass == 2) {
+      const int t = threadIdx.x - 64;  // 0..255
+      if (t < kM) {
+        float o = INFINITY;
+        if (t < p.rows) {
+          const float Mt = p.stats[(size_t(unit) * kM + t) * 2 + 0];
+          const float Lt = p.stats[(size_t(unit) * kM + t) * 2 + 1];
+          if (Lt > 0.f) o = Mt + log2f(Lt);
+        }
+        s_off[t] = o;
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+    }
     for (int i = 0; i < n_tiles; ++i) {
       const int a = i & 1;
       mb_wait(tfull + 8 * a, (i >> 1) & 1);
@@ -275,6 +268,20 @@ obs_score_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant_
         const int first = key0 + c * 32;
         const bool unmasked = row_ok && first + 31 <= qpos;  // common case: no causal cut
         if (p.pass == 1) {
+          // common case: the row's running reference m stays (softmax is shift
+          // invariant; m need not be the max, only keep exp2 finite), so no
+          // per-element max -- one FFMA + EX2 + FADD; a chunk whose sum would
+          // get large falls back to the exact max below
+          if (!row_ok) continue;  // padding rows: no statistics
+          if (unmasked && m != -INFINITY) {
+            float s = 0.f;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) s += fast_exp2(fmaf(v[j], p.scale_log2, -m));
+            if (s <= 0x1p64f) {
+              l += s;
+              continue;
+            }
+          }
           // max on raw scores (scale > 0), then exp2(v*scale - m) as one FFMA + EX2
           float tmax = -INFINITY;
           if (unmasked) {
@@ -294,37 +301,51 @@ obs_score_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant_
           for (int j = 0; j < 32; ++j) s += fast_exp2(fmaf(v[j], p.scale_log2, -mb));
           l = l * exp2f(m - mb) + s;
           m = mn;
-        } else {
-          // exp2(v*scale - M) / L  ==  exp2(v*scale - (M + log2 L)): one FFMA + EX2
-          const float off = -(Mr + log2L);
-          if (unmasked) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = fast_exp2(fmaf(v[j], p.scale_log2, off));
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              v[j] = (row_ok && first + j <= qpos) ? fast_exp2(fmaf(v[j], p.scale_log2, off)) : 0.f;
-          }
         }
       }
-      if (p.pass == 2) {  // column sums of both 32-column chunks (lane = column)
-        float ca, cb;
-        transpose_reduce32x2(v2[0], v2[1], ca, cb);
-        colsum[((i & 3) * 4 + q4) * kN + c0 * 32 + lane] = ca;
-        colsum[((i & 3) * 4 + q4) * kN + (c0 + 1) * 32 + lane] = cb;
+      if (p.pass == 2) {
+        // transposed accumulator: this thread is key `key`, its 64 columns the
+        // query rows [64*half, 64*half + 64); p = exp2(x*scale - off_row)
+        const int key = key0 + q4 * 32 + lane;
+        const int rb = half * 64;
+        float acc = 0.f;
+        if (key0 + kN - 1 <= p.L - p.w) {  // the whole tile precedes every query
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              const float4 o = *reinterpret_cast<const float4*>(s_off + rb + h * 32 + j);
+              acc += fast_exp2(fmaf(v2[h][j + 0], p.scale_log2, -o.x));
+              acc += fast_exp2(fmaf(v2[h][j + 1], p.scale_log2, -o.y));
+              acc += fast_exp2(fmaf(v2[h][j + 2], p.scale_log2, -o.z));
+              acc += fast_exp2(fmaf(v2[h][j + 3], p.scale_log2, -o.w));
+            }
+          }
+        } else {  // causal cut: row r (window position r / G) sees keys <= L - w + r / G
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const int r = rb + h * 32 + j;
+              const bool vis = r < p.rows && key <= p.L - p.w + r / p.G;
+              acc += vis ? fast_exp2(fmaf(v2[h][j], p.scale_log2, -s_off[r])) : 0.f;
+            }
+          }
+        }
+        colsum[((i & 3) * 2 + half) * kN + q4 * 32 + lane] = acc;
       }
       if (p.pass == 2 && ((i & 1) || i == n_tiles - 1)) {
         // one barrier per PAIR of tiles: the partials of tile i live in buffer
         // i&3, which tile i+4 overwrites only after the next pair's barrier
-        // (every thread has read this pair's columns by then); the 256
-        // epilogue threads then sum one (tile, column) each
+        // (every thread has read this pair's keys by then); the 256 epilogue
+        // threads then add the two row halves of one (tile, key) each
         asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
         const int t = threadIdx.x - 64;  // 0..255
         const int ti = (i & 1) ? i - 1 + (t >> 7) : i;
         const int col = t & (kN - 1);
         if ((i & 1) || t < kN) {
-          const float* cs = colsum + (ti & 3) * 4 * kN;
-          const float sum = (cs[col] + cs[kN + col]) + (cs[2 * kN + col] + cs[3 * kN + col]);
+          const float* cs = colsum + (ti & 3) * 2 * kN;
+          const float sum = cs[col] + cs[kN + col];
           const int kt = (tile0 + ti) * kN + col;
           if (kt < p.L) p.out[size_t(unit) * p.row_stride + kt] = sum * inv_rows;
         }
