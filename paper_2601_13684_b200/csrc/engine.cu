@@ -452,6 +452,7 @@ int devdec_create(EngineImpl& e, const hc_engine_desc& c) {
     for (const DevSat& x : sats) per_slot += int64_t(std::max(1, x.k)) * 4;
     d.nq = int32_t(std::max<int64_t>(8, std::min<int64_t>(512, (int64_t(2) << 30) /
                                                                    std::max<int64_t>(1, per_slot))));
+    if (const char* q = getenv("HC_DEVDEC_NQ")) d.nq = std::max(2, atoi(q));  // tests: tiny rings
     for (DevSat& x : sats) {
       x.sel = static_cast<uint32_t*>(dev(size_t(d.nq) * std::max(1, x.k) * 4));
       HC_REQUIRE(x.sel, HC_ENOMEM, "device decisions: transfer rings");

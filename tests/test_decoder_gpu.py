@@ -447,3 +447,19 @@ def test_decode_step_host_matches_device_inputs():
     assert evs[0] == evs[1] and any(evs[0])
     for a, b in zip(*outs):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("nq", ["3", "512"])
+def test_device_decisions_long_run_ring_wraps(nq, monkeypatch):
+    """A long device-decision run (400 steps, a drift every 7 steps, a starved host
+    link so transfers queue) with transfer rings of 3 slots per satellite -- every
+    ring wraps dozens of times -- still gives the oracle's events and rows."""
+    monkeypatch.setenv("HC_DEVDEC_NQ", nq)
+    shifts = tuple(range(6, 396, 7))
+    ctx = _build(B=2, L=300, T=400, window=4, shift=shifts, bandwidth=20000, chunk=128)
+    assert ctx["dec"].devdec
+    rows, _, _, _ = _run(ctx)
+    ctx["dec"].sync()
+    fired = _check_events(ctx, rows)
+    assert fired >= 60
+    ctx["dec"].close()
