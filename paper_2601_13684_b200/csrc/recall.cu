@@ -5,6 +5,8 @@
 // does in Python: IEEE double additions in the same order give the same
 // bits.  Membership follows CacheView.__contains__ (engine.py:98-107).
 
+#include <cub/device/device_segmented_radix_sort.cuh>
+
 #include "hc_common.cuh"
 
 namespace hc {
@@ -35,6 +37,24 @@ __global__ void trace_recall_kernel(const hc_recall_head* __restrict__ heads, in
 }
 
 }  // namespace
+// Measure mode's record order: HCTRACE1 records are sorted by score
+// descending, token index ascending (trace.py invariants; the exporter's
+// selectTopK order), i.e. by the composite key (score_key << 32) | ~index
+// descending -- a segmented radix sort per head from the CUDA toolkit (CUB).
+// temp == nullptr: *temp_bytes receives the scratch size.
+int segmented_sort_desc_u64(void* temp, size_t* temp_bytes, const uint64_t* in, uint64_t* out,
+                            int n_items, int n_segments, const int* offsets, cudaStream_t st) {
+  size_t bytes = temp ? *temp_bytes : 0;
+  cudaError_t r = cub::DeviceSegmentedRadixSort::SortKeysDescending(
+      temp, bytes, in, out, n_items, n_segments, offsets, offsets + 1, 0, 64, st);
+  if (r != cudaSuccess) {
+    set_error("segmented sort: %s", cudaGetErrorString(r));
+    return HC_ECUDA;
+  }
+  if (!temp) *temp_bytes = bytes;
+  return HC_OK;
+}
+
 }  // namespace hc
 
 extern "C" int hc_trace_recall(const hc_recall_head* heads_dev, int n_heads, uint32_t K,
