@@ -132,7 +132,9 @@ __global__ void __launch_bounds__(1024) decide_kernel(DevDec d, int t, int first
         x.buf = -1;
         x.host_off = host_off < 0 ? -1 : int32_t(hoff);
         x.cnt = 0;
-        x.done_ctas = 0;
+        x.done_chunks = 0;
+        x.next_chunk = 0;
+        x.built = 0;
         x.state = kXAlloc;
         FireJob& jb = d.jobs[n_jobs++];
         jb.row = d.rowbuf + size_t(s) * d.row_len;
@@ -176,7 +178,10 @@ __global__ void __launch_bounds__(1024) decide_kernel(DevDec d, int t, int first
 // completion step.  Marks them SCHEDULED (target buffer chosen); the
 // retrieval stream's next build pass picks them up.  One CTA, a thread per
 // satellite.
-__global__ void __launch_bounds__(1024) schedule_kernel(DevDec d) {
+__global__ void __launch_bounds__(1024) schedule_kernel(DevDec d, int t_now) {
+  __shared__ int urgent;
+  if (threadIdx.x == 0) urgent = 0;
+  __syncthreads();
   for (int si = threadIdx.x; si < d.n_sat; si += blockDim.x) {
     DevSat& sat = d.sats[si];
     const int64_t tail = *reinterpret_cast<volatile int64_t*>(&sat.tail);
@@ -202,29 +207,41 @@ __global__ void __launch_bounds__(1024) schedule_kernel(DevDec d) {
         }
       }
       x.buf = target;
-      x.pad0 = 0;  // not yet built by the retrieval stream
+      x.built = 0;  // not yet built by the retrieval stream
       __threadfence();
       sat.staging_owner = int32_t(i);
       atomicExch(&x.state, int(kXScheduled));
+      if (x.completion <= t_now + 1) urgent = 1;
       break;
     }
   }
+  __syncthreads();
+  if (threadIdx.x == 0 && urgent) {  // a running gather pass yields to the next one
+    __threadfence();
+    atomicAdd(d.urgent_epoch, 1u);
+  }
 }
 
-// Retrieval stream, one CTA per satellite: the scheduled transfer not yet
-// taken by a gather pass gets its prefix position list and joins this pass's
-// list (the list belongs to the retrieval stream: passes never overlap).
+// Retrieval stream, one CTA per satellite: its scheduled transfer (the
+// staging buffer's) gets its prefix position list if it has none yet and joins
+// this pass's list -- new ones and the remainder of ones a preempted pass left
+// (the list belongs to the retrieval stream: passes never overlap).
 __global__ void __launch_bounds__(256) build_dev_kernel(DevDec d, int t_max) {
   const int si = blockIdx.x;
   DevSat& sat = d.sats[si];
   __shared__ int64_t s_i;
+  __shared__ int s_new;
   if (threadIdx.x == 0) {
     s_i = -1;
+    s_new = 0;
     const int64_t tail = *reinterpret_cast<volatile int64_t*>(&sat.tail);
     for (int64_t i = sat.head; i < tail; ++i) {
       DevXfer& x = xf(d, si, i);
-      if (vload(&x.state) == kXScheduled && x.pad0 == 0) {
-        if (x.completion <= t_max) s_i = i;  // later passes take the later deadlines
+      if (vload(&x.state) == kXScheduled && x.built != 2) {
+        if (x.completion <= t_max) {  // later passes take the later deadlines
+          s_i = i;
+          s_new = x.built == 0;
+        }
         break;
       }
     }
@@ -233,10 +250,12 @@ __global__ void __launch_bounds__(256) build_dev_kernel(DevDec d, int t_max) {
   if (s_i < 0) return;
   DevXfer& x = xf(d, si, s_i);
   const int slot = int(s_i % d.nq);
-  build_positions_block(sat.sel + size_t(slot) * sat.k, int(x.cnt),
-                        sat.pos + size_t(x.buf) * sat.cap, x.meta, d.L, d.S, d.R, x.completion);
+  if (s_new)
+    build_positions_block(sat.sel + size_t(slot) * sat.k, int(x.cnt),
+                          sat.pos + size_t(x.buf) * sat.cap, x.meta, d.L, d.S, d.R,
+                          x.completion);
   if (threadIdx.x == 0) {
-    x.pad0 = 1;
+    x.built = 1;
     const uint32_t at = atomicAdd(d.n_glist, 1u);
     d.glist[at] = GatherItem{si, slot, x.completion, x.order};
   }
@@ -263,23 +282,57 @@ __global__ void __launch_bounds__(1024) order_kernel(DevDec d) {
   }
 }
 
+// Rows are claimed in chunks of kChunkRows, earliest deadline first, by
+// whichever CTA is free; before each claim a CTA checks the urgent epoch and
+// leaves if a transfer due next step was scheduled after this pass started --
+// the next pass (queued behind this one) re-lists the remainders with the new
+// transfer in deadline order.  A claimed chunk is always finished; the CTA
+// completing a transfer's last chunk flags it GATHERED.
+constexpr int kChunkRows = 256;
+
 __global__ void __launch_bounds__(256) gather_dev_kernel(DevDec d, uint4* __restrict__ K,
                                                          uint4* __restrict__ V) {
   const uint32_t n = *d.n_glist;
-  const int nw = gridDim.x * (blockDim.x >> 5);
-  const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  __shared__ uint32_t s_epoch, s_c;
+  __shared__ int s_stop;
+  if (threadIdx.x == 0) {
+    s_epoch = *reinterpret_cast<volatile uint32_t*>(d.urgent_epoch);
+    s_stop = 0;
+  }
+  __syncthreads();
+  const int wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   for (uint32_t i = 0; i < n; ++i) {
     const GatherItem it = d.glist2[i];
     const DevSat& sat = d.sats[it.sat];
     DevXfer& x = d.xfers[size_t(it.sat) * d.nq + it.slot];
-    gather_rows(sat.pos + size_t(x.buf) * sat.cap, x.meta[0], sat.srcK, sat.srcV, K, V,
-                sat.row0[x.buf], gw, nw);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      if (atomicAdd(&x.done_ctas, 1u) == gridDim.x - 1) {
+    const int rows = x.meta[0];
+    const uint32_t n_chunks = uint32_t((rows + kChunkRows - 1) / kChunkRows);
+    if (n_chunks == 0) {
+      if (threadIdx.x == 0) atomicCAS(&x.state, int(kXScheduled), int(kXGathered));
+      continue;
+    }
+    while (true) {
+      if (threadIdx.x == 0) {
+        if (*reinterpret_cast<volatile uint32_t*>(d.urgent_epoch) != s_epoch) s_stop = 1;
+        s_c = s_stop ? n_chunks : atomicAdd(&x.next_chunk, 1u);
+      }
+      __syncthreads();
+      const uint32_t c = s_c;
+      const int stop = s_stop;
+      __syncthreads();
+      if (stop) return;
+      if (c >= n_chunks) break;
+      const int r0 = int(c) * kChunkRows;
+      const int nr = min(kChunkRows, rows - r0);
+      gather_rows(sat.pos + size_t(x.buf) * sat.cap + r0, nr, sat.srcK, sat.srcV, K, V,
+                  sat.row0[x.buf] + r0, wid, nwarps);
+      __syncthreads();
+      if (threadIdx.x == 0) {
         __threadfence();
-        atomicExch(&x.state, int(kXGathered));
+        if (atomicAdd(&x.done_chunks, 1u) == n_chunks - 1) {
+          __threadfence();
+          atomicExch(&x.state, int(kXGathered));
+        }
       }
     }
   }
@@ -345,7 +398,7 @@ __global__ void __launch_bounds__(256) land_kernel(DevDec d, int t, UnitDesc* un
         // landing of this very pass -- gather it inline below
         if (st == kXSelected) {
           x.buf = 1 - sat.active;
-          x.pad0 = 1;  // gathered here, never by a retrieval pass
+          x.built = 2;  // gathered here, never by a retrieval pass
           __threadfence();
           x.state = kXScheduled;
           sat.staging_owner = int32_t(i);
@@ -393,8 +446,8 @@ int launch_decide(const DevDec& d, int t, int first, int nvals, int bidx, const 
   return HC_OK;
 }
 
-int launch_schedule(const DevDec& d, cudaStream_t st) {
-  schedule_kernel<<<1, 1024, 0, st>>>(d);
+int launch_schedule(const DevDec& d, int t_now, cudaStream_t st) {
+  schedule_kernel<<<1, 1024, 0, st>>>(d, t_now);
   HC_CHECK_LAUNCH();
   return HC_OK;
 }

@@ -48,9 +48,10 @@ enum XState : int32_t {
 
 struct DevXfer {
   int32_t completion, order, trigger, k;
-  int32_t state, buf, host_off, pad0;  // pad0: taken by a gather pass
+  int32_t state, buf, host_off, built;  // built: 0 no, 1 positions built, 2 gathered inline
   int32_t meta[4];  // prefix rows, tail mask, positions >= L (build_positions)
-  uint32_t cnt, done_ctas;
+  uint32_t cnt, done_chunks;
+  uint32_t next_chunk, pad_;  // gather progress: chunks claimed / completed
 };
 
 struct DevSat {
@@ -107,6 +108,8 @@ struct DevDec {
   uint32_t* n_jobs;
   int32_t* restamp_slots;  // [n_piv]
   uint32_t* n_restamp;
+  uint32_t* urgent_epoch;  // bumped when a transfer due next step is scheduled: a
+                           // running gather pass yields (between chunks) to the next
   GatherItem* glist;       // [n_sat] this gather pass (retrieval stream)
   GatherItem* glist2;      // [n_sat] the same, earliest deadline first
   uint32_t* n_glist;
@@ -130,7 +133,7 @@ enum DevDecError : int32_t {
 
 int launch_decide(const DevDec& d, int t, int first, int nvals, int bidx, const uint32_t* ovl_ring,
                   int ring, cudaStream_t st);
-int launch_schedule(const DevDec& d, cudaStream_t st);
+int launch_schedule(const DevDec& d, int t_now, cudaStream_t st);
 int launch_dev_gathers(const DevDec& d, uint4* K, uint4* V, cudaStream_t st, int t_max,
                        cudaEvent_t g0 = nullptr, cudaEvent_t g1 = nullptr);
 int launch_land(const DevDec& d, int t, UnitDesc* units, uint4* K, uint4* V, cudaStream_t st);

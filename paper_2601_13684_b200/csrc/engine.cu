@@ -480,10 +480,11 @@ int devdec_create(EngineImpl& e, const hc_engine_desc& c) {
   d.glist = static_cast<GatherItem*>(dev(ns * sizeof(GatherItem)));
   d.glist2 = static_cast<GatherItem*>(dev(ns * sizeof(GatherItem)));
   d.n_glist = static_cast<uint32_t*>(dev(4));
+  d.urgent_epoch = static_cast<uint32_t*>(dev(4));
   HC_CUDA_TRY(cudaGetLastError());
   HC_REQUIRE(d.seq_piv && d.piv_sat_begin && d.piv_unit && d.sats && d.xfers && d.cum &&
                  d.order && d.svals && d.scnt && d.jobs && d.n_jobs && d.restamp_slots &&
-                 d.n_restamp && d.glist && d.glist2 && d.n_glist,
+                 d.n_restamp && d.glist && d.glist2 && d.n_glist && d.urgent_epoch,
              HC_ENOMEM, "device decisions: state");
   // mapped host memory: the decision log and the fetched sets the host mirrors
   int64_t ksum = 0;
@@ -900,7 +901,7 @@ int devdec_land(EngineImpl& e, int t, cudaStream_t st) {
 
 // A schedule pass on the schedule stream and the gathers it lists.
 int devdec_schedule_and_gather(EngineImpl& e, int t_max) {
-  HC_TRY(launch_schedule(e.dd, e.sched));
+  HC_TRY(launch_schedule(e.dd, t_max - e.dd_horizon, e.sched));
   HC_CUDA_TRY(cudaEventRecord(e.ev_sched, e.sched));
   e.sched_valid = true;
   HC_CUDA_TRY(cudaStreamWaitEvent(e.retr, e.ev_sched, 0));
