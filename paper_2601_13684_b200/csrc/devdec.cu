@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(1024) decide_kernel(DevDec d, int t, int first
         jb.k = uint32_t(ks[i]);
         jb.out_idx = sat.sel + size_t(slot) * sat.k;
         jb.out_count = &x.cnt;
-        jb.host_out = host_off < 0 ? nullptr : d.fetched + hoff;
+        jb.host_out = host_off < 0 || d.no_host_copy ? nullptr : d.fetched + hoff;
         jb.state_out = &x.state;
         hoff += ks[i];
         __threadfence();
@@ -435,7 +435,24 @@ __global__ void __launch_bounds__(256) land_kernel(DevDec d, int t, UnitDesc* un
   }
 }
 
+// The boundary's fetched sets to the host mirror's mapped ring: one CTA per
+// fire-selection job, coalesced stores over the host link, on a low-priority
+// stream after the selection -- never between a decision and its gathers.
+__global__ void __launch_bounds__(256) copy_fetched_kernel(DevDec d) {
+  if (blockIdx.x >= *d.n_jobs) return;
+  const FireJob jb = d.jobs[blockIdx.x];
+  if (!jb.host_out) return;
+  const uint32_t n = *jb.out_count;
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) jb.host_out[i] = jb.out_idx[i];
+}
+
 }  // namespace
+
+int launch_copy_fetched(const DevDec& d, cudaStream_t st) {
+  copy_fetched_kernel<<<std::max(1, d.n_sat), 256, 0, st>>>(d);
+  HC_CHECK_LAUNCH();
+  return HC_OK;
+}
 
 int launch_decide(const DevDec& d, int t, int first, int nvals, int bidx, const uint32_t* ovl_ring,
                   int ring, cudaStream_t st) {

@@ -86,7 +86,7 @@ struct GatherItem {
 struct DevDec {
   // static geometry
   int32_t n_sat, n_piv, B, L, S, R, lbase, window, sliding, delay;
-  int32_t nq, pad_;        // transfer slots per satellite ring
+  int32_t nq, no_host_copy;  // transfer slots per satellite ring; diagnostics switch
   double tau;
   int64_t bw, bpe;
   int32_t* seq_piv;        // [B + 1] pivot slot ranges per sequence
@@ -134,6 +134,7 @@ enum DevDecError : int32_t {
 int launch_decide(const DevDec& d, int t, int first, int nvals, int bidx, const uint32_t* ovl_ring,
                   int ring, cudaStream_t st);
 int launch_schedule(const DevDec& d, int t_now, cudaStream_t st);
+int launch_copy_fetched(const DevDec& d, cudaStream_t st);
 int launch_dev_gathers(const DevDec& d, uint4* K, uint4* V, cudaStream_t st, int t_max,
                        cudaEvent_t g0 = nullptr, cudaEvent_t g1 = nullptr);
 int launch_land(const DevDec& d, int t, UnitDesc* units, uint4* K, uint4* V, cudaStream_t st);

@@ -286,6 +286,9 @@ struct EngineImpl {
   DevDec dd{};
   cudaStream_t sched = nullptr;         // schedule passes (tiny, never behind a gather)
   cudaStream_t lnd = nullptr;           // landing + satellites' K4, beside the main K4
+  cudaStream_t hcp = nullptr;           // low priority: fetched sets to the mapped host ring
+  cudaEvent_t ev_copy = nullptr;
+  bool copy_valid = false;
   cudaEvent_t ev_land = nullptr, ev_sched = nullptr, ev_sel = nullptr, ev_dec = nullptr;
   cudaEvent_t ev_app = nullptr, ev_sats = nullptr;
   bool sched_valid = false, sel_valid = false;
@@ -357,6 +360,8 @@ int engine_destroy(EngineImpl& e) {
   for (cudaEvent_t x : {e.ev_land, e.ev_sched, e.ev_sel, e.ev_dec, e.ev_app, e.ev_sats})
     if (x) cudaEventDestroy(x);
   if (e.lnd) cudaStreamDestroy(e.lnd);
+  if (e.hcp) cudaStreamDestroy(e.hcp);
+  if (e.ev_copy) cudaEventDestroy(e.ev_copy);
   for (cudaEvent_t x : e.ev_log)
     if (x) cudaEventDestroy(x);
   if (e.sched) cudaStreamDestroy(e.sched);
@@ -453,6 +458,7 @@ int devdec_create(EngineImpl& e, const hc_engine_desc& c) {
     d.nq = int32_t(std::max<int64_t>(8, std::min<int64_t>(512, (int64_t(2) << 30) /
                                                                    std::max<int64_t>(1, per_slot))));
     if (const char* q = getenv("HC_DEVDEC_NQ")) d.nq = std::max(2, atoi(q));  // tests: tiny rings
+    d.no_host_copy = getenv("HC_DEVDEC_NO_HOST_COPY") ? 1 : 0;  // timing diagnostics only
     for (DevSat& x : sats) {
       x.sel = static_cast<uint32_t*>(dev(size_t(d.nq) * std::max(1, x.k) * 4));
       HC_REQUIRE(x.sel, HC_ENOMEM, "device decisions: transfer rings");
@@ -527,6 +533,8 @@ int devdec_create(EngineImpl& e, const hc_engine_desc& c) {
   HC_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
   HC_CUDA_TRY(cudaStreamCreateWithPriority(&e.sched, cudaStreamNonBlocking, hi_prio));
   HC_CUDA_TRY(cudaStreamCreateWithPriority(&e.lnd, cudaStreamNonBlocking, hi_prio));
+  HC_CUDA_TRY(cudaStreamCreateWithPriority(&e.hcp, cudaStreamNonBlocking, lo_prio));
+  HC_CUDA_TRY(cudaEventCreateWithFlags(&e.ev_copy, cudaEventDisableTiming));
   for (cudaEvent_t* x : {&e.ev_land, &e.ev_sched, &e.ev_sel, &e.ev_dec, &e.ev_app, &e.ev_sats})
     HC_CUDA_TRY(cudaEventCreateWithFlags(x, cudaEventDisableTiming));
   for (auto& x : e.ev_log) HC_CUDA_TRY(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
@@ -927,6 +935,8 @@ int devdec_decide(EngineImpl& e, int t) {
   const int64_t bidx = e.n_bound++;
   HC_REQUIRE(e.n_bound - e.n_read <= kLogRing, HC_ESTATE,
              "device decisions: %d boundaries unread (poll the decisions)", kLogRing);
+  // the previous boundary's host copy still reads the job list the decision rewrites
+  if (e.copy_valid) HC_CUDA_TRY(cudaStreamWaitEvent(e.mon, e.ev_copy, 0));
   HC_TRY(launch_decide(e.dd, t, first, nvals, int(bidx), e.ovl_ring, kRing, e.mon));
   HC_TRY(launch_restamp_threshold(e.rowbuf, e.row_len, e.dd.restamp_slots, e.n_piv,
                                   uint32_t(e.L + t), e.thr, e.kbase, e.words, e.mon,
@@ -935,8 +945,13 @@ int devdec_decide(EngineImpl& e, int t) {
   HC_CUDA_TRY(cudaStreamWaitEvent(e.side, e.ev_dec, 0));
   HC_TRY(launch_fire_select(e.dd.jobs, std::max(1, e.dd.n_sat), e.side, e.dd.n_jobs));
   HC_CUDA_TRY(cudaEventRecord(e.ev_sel, e.side));
-  HC_CUDA_TRY(cudaEventRecord(e.ev_log[bidx % kLogRing], e.side));
   e.sel_valid = true;
+  // the host mirror's copy of the fetched sets, on a low-priority stream
+  HC_CUDA_TRY(cudaStreamWaitEvent(e.hcp, e.ev_sel, 0));
+  HC_TRY(launch_copy_fetched(e.dd, e.hcp));
+  HC_CUDA_TRY(cudaEventRecord(e.ev_copy, e.hcp));
+  HC_CUDA_TRY(cudaEventRecord(e.ev_log[bidx % kLogRing], e.hcp));
+  e.copy_valid = true;
   HC_CUDA_TRY(cudaStreamWaitEvent(e.sched, e.ev_sel, 0));
   return devdec_schedule_and_gather(e, t + e.dd_horizon);
 }

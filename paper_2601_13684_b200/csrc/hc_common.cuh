@@ -77,7 +77,8 @@ struct FireJob {
   uint32_t n, k;
   uint32_t* out_idx;      // [k] selected positions, ascending
   uint32_t* out_count;
-  uint32_t* host_out;     // optional: the selection also written here (mapped host ring)
+  uint32_t* host_out;     // device decisions: copy_fetched_kernel copies the selection here
+                          // (mapped host ring), off the gathers' critical path
   int32_t* state_out;     // optional: set to 2 (devdec.cuh kXSelected) once written
 };
 

@@ -571,10 +571,7 @@ __global__ void __launch_bounds__(kSelThreads, 2) fire_select_kernel(const FireJ
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (k >= n || k == 0) {  // everything / nothing
     const uint32_t c = k >= n ? n : 0u;
-    for (uint32_t i = tid; i < c; i += kSelThreads) {
-      job.out_idx[i] = i;
-      if (job.host_out) job.host_out[i] = i;
-    }
+    for (uint32_t i = tid; i < c; i += kSelThreads) job.out_idx[i] = i;
     __syncthreads();
     if (tid == 0) {
       *job.out_count = c;
@@ -694,10 +691,7 @@ __global__ void __launch_bounds__(kSelThreads, 2) fire_select_kernel(const FireJ
       uint32_t p = off + incl - c;
 #pragma unroll
       for (int e = 0; e < 4; ++e)
-        if (selm & (1u << e)) {
-          if (job.host_out) job.host_out[p] = 4 * v + e;
-          job.out_idx[p++] = 4 * v + e;
-        }
+        if (selm & (1u << e)) job.out_idx[p++] = 4 * v + e;
       off += __shfl_sync(0xffffffffu, incl, 31);
     }
   }
