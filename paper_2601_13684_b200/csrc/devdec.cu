@@ -78,8 +78,10 @@ __global__ void __launch_bounds__(1024) decide_kernel(DevDec d, int t, int first
   }
   __syncthreads();
   if (threadIdx.x != 0) return;
-  BoundaryHdr* hdr = d.hdr + (bidx % kLogRing);
-  FireLog* log = d.log + size_t(bidx % kLogRing) * d.n_piv;
+  BoundaryHdr* hdr = d.hdr_dev + (bidx % kLogRing);
+  FireLog* log = d.log_dev + size_t(bidx % kLogRing) * d.n_piv;
+  const int64_t host_tail = *d.fetched_tail;  // one read over the host link
+  int64_t head = *d.head_dev;
   const uint32_t* hist = d.ghist + size_t(t & 1) * d.n_piv * 8192;
   int n_fires = 0;
   uint32_t n_jobs = 0, n_rest = 0;
@@ -102,18 +104,18 @@ __global__ void __launch_bounds__(1024) decide_kernel(DevDec d, int t, int first
       cum += nbytes;
       const int32_t completion = max(t + d.delay, int32_t(ceil(double(cum) / double(d.bw))));
       // fetched sets for the host mirror: one contiguous span of the mapped ring
-      int64_t head = *d.fetched_head;
-      int64_t phys = head % d.fetched_cap;
+      int64_t h = head;
+      int64_t phys = h % d.fetched_cap;
       if (phys + n_ent > d.fetched_cap) {  // no wrap inside a span: skip to the ring start
-        head += d.fetched_cap - phys;
+        h += d.fetched_cap - phys;
         phys = 0;
       }
       int32_t host_off = int32_t(phys);
-      if (head + n_ent - *d.fetched_tail > d.fetched_cap || n_ent > d.fetched_cap) {
+      if (h + n_ent - host_tail > d.fetched_cap || n_ent > d.fetched_cap) {
         atomicExch(d.error, int(kDDHostRingFull));
         host_off = -1;
       } else {
-        *d.fetched_head = head + n_ent;
+        head = h + n_ent;
       }
       int64_t hoff = host_off;
       for (int i = 0; i < ns && i < 8; ++i) {
@@ -166,11 +168,11 @@ __global__ void __launch_bounds__(1024) decide_kernel(DevDec d, int t, int first
   }
   *d.n_jobs = n_jobs;
   *d.n_restamp = n_rest;
+  *d.head_dev = head;
   hdr->t = t;
   hdr->n_fires = n_fires;
-  hdr->head_after = *d.fetched_head;
-  __threadfence_system();
-  hdr->pad = 1;  // written: the host reads this boundary once its event completed
+  hdr->head_after = head;
+  hdr->pad = 1;
 }
 
 // Which selected transfers can be gathered now: the satellite's staging
@@ -438,7 +440,22 @@ __global__ void __launch_bounds__(256) land_kernel(DevDec d, int t, UnitDesc* un
 // The boundary's fetched sets to the host mirror's mapped ring: one CTA per
 // fire-selection job, coalesced stores over the host link, on a low-priority
 // stream after the selection -- never between a decision and its gathers.
-__global__ void __launch_bounds__(256) copy_fetched_kernel(DevDec d) {
+__global__ void __launch_bounds__(256) copy_fetched_kernel(DevDec d, int bidx) {
+  if (blockIdx.x == gridDim.x - 1) {  // the decision log of this boundary
+    const int r = bidx % kLogRing;
+    const BoundaryHdr* hs = d.hdr_dev + r;
+    const int n = hs->n_fires;
+    const int32_t* src = reinterpret_cast<const int32_t*>(d.log_dev + size_t(r) * d.n_piv);
+    int32_t* dst = reinterpret_cast<int32_t*>(d.log + size_t(r) * d.n_piv);
+    const int words = n * int(sizeof(FireLog) / 4);
+    for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      d.hdr[r] = *hs;
+    }
+    return;
+  }
   if (blockIdx.x >= *d.n_jobs) return;
   const FireJob jb = d.jobs[blockIdx.x];
   if (!jb.host_out) return;
@@ -448,8 +465,8 @@ __global__ void __launch_bounds__(256) copy_fetched_kernel(DevDec d) {
 
 }  // namespace
 
-int launch_copy_fetched(const DevDec& d, cudaStream_t st) {
-  copy_fetched_kernel<<<std::max(1, d.n_sat), 256, 0, st>>>(d);
+int launch_copy_fetched(const DevDec& d, int bidx, cudaStream_t st) {
+  copy_fetched_kernel<<<std::max(1, d.n_sat) + 1, 256, 0, st>>>(d, bidx);
   HC_CHECK_LAUNCH();
   return HC_OK;
 }

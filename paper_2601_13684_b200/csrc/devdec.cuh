@@ -113,12 +113,16 @@ struct DevDec {
   GatherItem* glist;       // [n_sat] this gather pass (retrieval stream)
   GatherItem* glist2;      // [n_sat] the same, earliest deadline first
   uint32_t* n_glist;
-  // host-mapped log and fetched-set ring
-  BoundaryHdr* hdr;        // [kLogRing]
-  FireLog* log;            // [kLogRing][n_piv]
+  // the decision log: written in device memory by decide_kernel, copied to the
+  // host-mapped copies by copy_fetched_kernel (low priority, off the chain to
+  // the gathers); the fetched-set ring is host-mapped
+  BoundaryHdr* hdr_dev;    // [kLogRing]
+  FireLog* log_dev;        // [kLogRing][n_piv]
+  int64_t* head_dev;       // the fetched ring's virtual head
+  BoundaryHdr* hdr;        // [kLogRing] mapped
+  FireLog* log;            // [kLogRing][n_piv] mapped
   uint32_t* fetched;       // [fetched_cap] host ring (mapped)
   int64_t fetched_cap;
-  int64_t* fetched_head;   // mapped: virtual ring head (device-written)
   volatile int64_t* fetched_tail;  // host-written (mapped): entries consumed
   int32_t* error;          // mapped: 0 ok, else an error code
 };
@@ -134,7 +138,7 @@ enum DevDecError : int32_t {
 int launch_decide(const DevDec& d, int t, int first, int nvals, int bidx, const uint32_t* ovl_ring,
                   int ring, cudaStream_t st);
 int launch_schedule(const DevDec& d, int t_now, cudaStream_t st);
-int launch_copy_fetched(const DevDec& d, cudaStream_t st);
+int launch_copy_fetched(const DevDec& d, int bidx, cudaStream_t st);
 int launch_dev_gathers(const DevDec& d, uint4* K, uint4* V, cudaStream_t st, int t_max,
                        cudaEvent_t g0 = nullptr, cudaEvent_t g1 = nullptr);
 int launch_land(const DevDec& d, int t, UnitDesc* units, uint4* K, uint4* V, cudaStream_t st);

@@ -487,10 +487,14 @@ int devdec_create(EngineImpl& e, const hc_engine_desc& c) {
   d.glist2 = static_cast<GatherItem*>(dev(ns * sizeof(GatherItem)));
   d.n_glist = static_cast<uint32_t*>(dev(4));
   d.urgent_epoch = static_cast<uint32_t*>(dev(4));
+  d.head_dev = static_cast<int64_t*>(dev(8));
+  d.hdr_dev = static_cast<BoundaryHdr*>(dev(sizeof(BoundaryHdr) * kLogRing));
+  d.log_dev = static_cast<FireLog*>(dev(sizeof(FireLog) * kLogRing * std::max(1, e.n_piv)));
   HC_CUDA_TRY(cudaGetLastError());
   HC_REQUIRE(d.seq_piv && d.piv_sat_begin && d.piv_unit && d.sats && d.xfers && d.cum &&
                  d.order && d.svals && d.scnt && d.jobs && d.n_jobs && d.restamp_slots &&
-                 d.n_restamp && d.glist && d.glist2 && d.n_glist && d.urgent_epoch,
+                 d.n_restamp && d.glist && d.glist2 && d.n_glist && d.urgent_epoch &&
+                 d.head_dev && d.hdr_dev && d.log_dev,
              HC_ENOMEM, "device decisions: state");
   // mapped host memory: the decision log and the fetched sets the host mirrors
   int64_t ksum = 0;
@@ -525,7 +529,6 @@ int devdec_create(EngineImpl& e, const hc_engine_desc& c) {
   HC_CUDA_TRY(cudaHostGetDevicePointer(&dp, e.fetched_h, 0));
   d.fetched = static_cast<uint32_t*>(dp);
   HC_CUDA_TRY(cudaHostGetDevicePointer(&dp, ctr, 0));
-  d.fetched_head = static_cast<int64_t*>(dp);
   d.fetched_tail = static_cast<int64_t*>(dp) + 1;
   HC_CUDA_TRY(cudaHostGetDevicePointer(&dp, e.error_h, 0));
   d.error = static_cast<int32_t*>(dp);
@@ -948,7 +951,7 @@ int devdec_decide(EngineImpl& e, int t) {
   e.sel_valid = true;
   // the host mirror's copy of the fetched sets, on a low-priority stream
   HC_CUDA_TRY(cudaStreamWaitEvent(e.hcp, e.ev_sel, 0));
-  HC_TRY(launch_copy_fetched(e.dd, e.hcp));
+  HC_TRY(launch_copy_fetched(e.dd, int(bidx), e.hcp));
   HC_CUDA_TRY(cudaEventRecord(e.ev_copy, e.hcp));
   HC_CUDA_TRY(cudaEventRecord(e.ev_log[bidx % kLogRing], e.hcp));
   e.copy_valid = true;
