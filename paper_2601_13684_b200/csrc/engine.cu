@@ -45,7 +45,7 @@ int launch_score_rows(const AttnParams& p, const int32_t* pivot_units_dev, int n
 int launch_attn_tiles(const CUtensorMap& tmK, const CUtensorMap& tmV, const AttnParams& p,
                       int n_tiles, cudaStream_t st);
 int launch_topk(const hc_topk_job* jobs_dev, int n_jobs, uint32_t n_add, cudaStream_t st);
-size_t obs_scratch_bytes(int n_units, int L);
+size_t obs_scratch_bytes(int n_units, int L, int rows);
 int launch_obs_scores(const void* k, const void* q_obs, int B, int H, int G, int w, int L,
                       float* out, int64_t row_stride, void* scratch, cudaStream_t st, int64_t kstride = 0);
 int launch_monitor(const float* rows, int64_t row_stride, const int32_t* slots, int n_rows,
@@ -1376,7 +1376,7 @@ int engine_prefill_layer(EngineImpl& e, int layer, const __nv_bfloat16* k,
   auto carve = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~size_t(255); return o; };
   const size_t o_rows = carve(size_t(nu) * Lp * 4);
   const size_t o_jobs = carve(size_t(nu) * sizeof(hc_topk_job));
-  const size_t o_obs = carve(obs_scratch_bytes(nu, e.L));
+  const size_t o_obs = carve(obs_scratch_bytes(nu, e.L, e.W * e.G));
   if (off > e.pf_bytes) {
     if (e.pf) {
       HC_CUDA_TRY(cudaStreamSynchronize(st));
@@ -1928,8 +1928,8 @@ int engine_enable_measure(EngineImpl& e, int recall_topk) {
   const int nu = e.B * e.H;
   size_t obs = 0;
   for (int64_t n = e.L; n <= srows; n += std::max<int64_t>(1, (srows - e.L) / 8 + 1))
-    obs = std::max(obs, obs_scratch_bytes(nu, int(n)));
-  obs = std::max(obs, obs_scratch_bytes(nu, int(srows)));
+    obs = std::max(obs, obs_scratch_bytes(nu, int(n), e.G));
+  obs = std::max(obs, obs_scratch_bytes(nu, int(srows), e.G));
   e.mscratch_bytes = ((size_t(nu) * e.G * kHeadDim * 2 + 255) & ~size_t(255)) + obs;
   HC_TRY(dalloc((void**)&e.mscratch, e.mscratch_bytes, &e.dev_bytes));
   return HC_OK;
@@ -1949,7 +1949,7 @@ int engine_measure(EngineImpl& e, int t, const void* q, double* recall_out, cuda
   if (t > 0) {
     __nv_bfloat16* qp = reinterpret_cast<__nv_bfloat16*>(e.mscratch);
     char* obs = e.mscratch + ((size_t(nu) * e.G * kHeadDim * 2 + 255) & ~size_t(255));
-    HC_REQUIRE(obs_scratch_bytes(nu, len) + (obs - e.mscratch) <= e.mscratch_bytes, HC_EINVAL,
+    HC_REQUIRE(obs_scratch_bytes(nu, len, e.G) + (obs - e.mscratch) <= e.mscratch_bytes, HC_EINVAL,
                "measure scratch too small");
     const size_t qrow = size_t(e.H) * e.G * kHeadDim * 2;  // one (b, layer) block of queries
     for (int l = 0; l < e.NL; ++l) {

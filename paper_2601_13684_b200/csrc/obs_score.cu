@@ -26,6 +26,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "hc_common.cuh"
 
@@ -56,6 +57,8 @@ struct ObsParams {
   float* out;        // pass 2 out: [unit][row_stride]
   int64_t row_stride;
   int n_chunks;
+  float* xs;         // small windows (w*G <= 16): pass 1 also keeps the raw scores
+  int64_t xs_stride; // [unit][rows][xs_stride]; pass 2 then reads them instead of K
 };
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -138,6 +141,7 @@ __device__ __forceinline__ float fast_exp2(float x) {
   return y;
 }
 
+template <bool kKeep>  // kKeep: small-window pass 1 also stores the raw scores (p.xs)
 __global__ void __launch_bounds__(kObsThreads, 2)
 obs_score_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmQ,
                  const ObsParams p) {
@@ -209,7 +213,7 @@ obs_score_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant_
         // pass 1: S = Q K^T (TMEM lane = query row, column = key); pass 2: S^T =
         // K Q^T (lane = key, column = query row), so each thread's column sum
         // of probabilities is a plain sum over its registers -- no shuffles
-        const bool tr = p.pass == 2;
+        const bool tr = !kKeep && p.pass == 2;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint32_t off = (kk >> 2) * kBox + (kk & 3) * 32;
@@ -233,7 +237,7 @@ obs_score_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant_
     // pass 2: per query row, exp2(x*scale - M - log2 L) = its probability;
     // rows beyond w*G or with an empty softmax get +inf (probability 0)
     float* s_off = colsum + 4 * 2 * kN;  // [128]
-    if (p.pass == 2) {
+    if (!kKeep && p.pass == 2) {
       const int t = threadIdx.x - 64;  // 0..255
       if (t < kM) {
         float o = INFINITY;
@@ -273,6 +277,18 @@ obs_score_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant_
           // per-element max -- one FFMA + EX2 + FADD; a chunk whose sum would
           // get large falls back to the exact max below
           if (!row_ok) continue;  // padding rows: no statistics
+          if (kKeep && first < p.L) {  // single-read path: keep this row's raw scores
+            float* dst = p.xs + (size_t(unit) * p.rows + r) * p.xs_stride + first;
+            if (first + 31 < p.L) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 4)
+                *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+            } else {  // last chunk (unrolled: v must stay in registers)
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (first + j < p.L) dst[j] = v[j];
+            }
+          }
           if (unmasked && m != -INFINITY) {
             float s = 0.f;
 #pragma unroll
@@ -303,7 +319,7 @@ obs_score_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant_
           m = mn;
         }
       }
-      if (p.pass == 2) {
+      if (!kKeep && p.pass == 2) {
         // transposed accumulator: this thread is key `key`, its 64 columns the
         // query rows [64*half, 64*half + 64); p = exp2(x*scale - off_row)
         const int key = key0 + q4 * 32 + lane;
@@ -334,7 +350,7 @@ obs_score_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant_
         }
         colsum[((i & 3) * 2 + half) * kN + q4 * 32 + lane] = acc;
       }
-      if (p.pass == 2 && ((i & 1) || i == n_tiles - 1)) {
+      if (!kKeep && p.pass == 2 && ((i & 1) || i == n_tiles - 1)) {
         // one barrier per PAIR of tiles: the partials of tile i live in buffer
         // i&3, which tile i+4 overwrites only after the next pair's barrier
         // (every thread has read this pair's keys by then); the 256 epilogue
@@ -362,6 +378,47 @@ obs_score_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant_
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+}
+
+// Single-read pass 2 for small windows (w*G <= 16 rows): the probabilities
+// from the raw scores pass 1 kept, 4 keys per thread, rows in order --
+// score(t) = sum_r exp2(x_rt*scale - M_r - log2 L_r) / rows.  K is read once.
+__global__ void __launch_bounds__(256) obs_rows_from_scores_kernel(const ObsParams p) {
+  __shared__ float off[16];
+  const int unit = blockIdx.y;
+  // each block merges its unit's pass-1 chunk statistics itself (obs_merge's
+  // arithmetic; a few KB from L2) instead of a separate launch
+  const int parts = 2 * p.n_chunks;
+  if (threadIdx.x < p.rows) {
+    const int r = threadIdx.x;
+    const float* src = p.part + (size_t(unit) * parts * kM + r) * 2;
+    float M = -INFINITY;
+    for (int c = 0; c < parts; ++c) M = fmaxf(M, src[size_t(c) * kM * 2]);
+    const float mb = M == -INFINITY ? 0.f : M;
+    float Lt = 0.f;
+    for (int c = 0; c < parts; ++c) {
+      const float l = src[size_t(c) * kM * 2 + 1];
+      if (l > 0.f) Lt += l * exp2f(src[size_t(c) * kM * 2] - mb);
+    }
+    off[r] = Lt > 0.f ? mb + log2f(Lt) : INFINITY;
+  }
+  __syncthreads();
+  const int key = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (key >= p.L) return;
+  const float* xs = p.xs + size_t(unit) * p.rows * p.xs_stride + key;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int r = 0; r < p.rows; ++r) {
+    const float4 x = *reinterpret_cast<const float4*>(xs + size_t(r) * p.xs_stride);
+    const float o = -off[r];
+    const int qpos = p.L - p.w + r / p.G;  // causal limit of row r
+    const float xv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      acc[e] += (key + e <= qpos) ? fast_exp2(fmaf(xv[e], p.scale_log2, o)) : 0.f;
+  }
+  const float inv = 1.f / float(p.rows);
+  float* out = p.out + size_t(unit) * p.row_stride + key;
+  for (int e = 0; e < 4 && key + e < p.L; ++e) out[e] = acc[e] * inv;
 }
 
 // Combine pass-1 chunk statistics: (M, L) per query row, log2 domain.
@@ -410,12 +467,16 @@ int make_kv_tensor_map_rows(CUtensorMap* map, const void* base, int64_t rows, in
 // Score rows for n_units KV heads whose keys are k[unit*L + t][128] and whose
 // observation queries are q_obs [B][w][H*G][128] (n_units = B*H).  `scratch`
 // must hold obs_scratch_bytes(); out rows have stride row_stride floats.
-size_t obs_scratch_bytes(int n_units, int L) {
+constexpr int kSmallRows = 16;  // w*G up to this: K read once, raw scores kept
+
+size_t obs_scratch_bytes(int n_units, int L, int rows) {
   const int n_tiles = (L + kN - 1) / kN;
   const int tiles_per_cta = obs_tiles_per_cta(n_units, n_tiles);
   const int n_chunks = (n_tiles + tiles_per_cta - 1) / tiles_per_cta;
+  const size_t xs = rows <= kSmallRows ? size_t(n_units) * rows * (size_t(L + 3) / 4 * 4) * 4 : 0;
   return size_t(n_units) * kM * 128 * 2 /*packed Q*/ +
-         size_t(n_units) * 2 * n_chunks * kM * 2 * 4 /*partials*/ + size_t(n_units) * kM * 2 * 4;
+         size_t(n_units) * 2 * n_chunks * kM * 2 * 4 /*partials*/ + size_t(n_units) * kM * 2 * 4 +
+         xs + 256;
 }
 
 int launch_obs_scores(const void* k, const void* q_obs, int B, int H, int G, int w, int L,
@@ -428,7 +489,9 @@ int launch_obs_scores(const void* k, const void* q_obs, int B, int H, int G, int
              G);
   static bool configured = false;
   if (!configured) {
-    HC_CUDA_TRY(cudaFuncSetAttribute(obs_score_kernel,
+    HC_CUDA_TRY(cudaFuncSetAttribute(obs_score_kernel<false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemObs));
+    HC_CUDA_TRY(cudaFuncSetAttribute(obs_score_kernel<true>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemObs));
     configured = true;
   }
@@ -440,6 +503,14 @@ int launch_obs_scores(const void* k, const void* q_obs, int B, int H, int G, int
   __nv_bfloat16* qp = reinterpret_cast<__nv_bfloat16*>(sc);
   float* part = reinterpret_cast<float*>(sc + size_t(n_units) * kM * 128 * 2);
   float* stats = part + size_t(n_units) * 2 * n_chunks * kM * 2;
+  static const int small_rows = getenv("HC_K5_SMALL_ROWS") ? atoi(getenv("HC_K5_SMALL_ROWS"))
+                                                           : kSmallRows;  // A/B switch
+  const bool small = w * G <= std::min(small_rows, kSmallRows);
+  float* xs = nullptr;
+  if (small) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(stats + size_t(n_units) * kM * 2);
+    xs = reinterpret_cast<float*>((a + 15) & ~uintptr_t(15));
+  }
   obs_pack_q_kernel<<<dim3(n_units, kM), 128, 0, st>>>(
       static_cast<const __nv_bfloat16*>(q_obs), H, G, w, qp);
   HC_CHECK_LAUNCH();
@@ -459,14 +530,21 @@ int launch_obs_scores(const void* k, const void* q_obs, int B, int H, int G, int
   p.out = out;
   p.row_stride = row_stride;
   p.n_chunks = n_chunks;
+  p.xs = xs;
+  p.xs_stride = (int64_t(L) + 3) / 4 * 4;
   dim3 grid(n_chunks, n_units);
   p.pass = 1;
-  obs_score_kernel<<<grid, kObsThreads, kSmemObs, st>>>(tk, tq, p);
-  HC_CHECK_LAUNCH();
-  obs_merge_kernel<<<n_units, kM, 0, st>>>(part, 2 * n_chunks, stats);
+  if (small) obs_score_kernel<true><<<grid, kObsThreads, kSmemObs, st>>>(tk, tq, p);
+  else obs_score_kernel<false><<<grid, kObsThreads, kSmemObs, st>>>(tk, tq, p);
   HC_CHECK_LAUNCH();
   p.pass = 2;
-  obs_score_kernel<<<grid, kObsThreads, kSmemObs, st>>>(tk, tq, p);
+  if (small) {  // the window's few rows: probabilities from the kept scores, K not re-read
+    obs_rows_from_scores_kernel<<<dim3((L + 1023) / 1024, n_units), 256, 0, st>>>(p);
+  } else {
+    obs_merge_kernel<<<n_units, kM, 0, st>>>(part, 2 * n_chunks, stats);
+    HC_CHECK_LAUNCH();
+    obs_score_kernel<false><<<grid, kObsThreads, kSmemObs, st>>>(tk, tq, p);
+  }
   HC_CHECK_LAUNCH();
   return HC_OK;
 }
@@ -479,7 +557,7 @@ extern "C" int hc_obs_scores(const void* k_dev, const void* q_obs_dev, int32_t b
   HC_REQUIRE(k_dev && q_obs_dev && rows_dev && batch > 0 && kv_heads > 0 && L > 0, HC_EINVAL,
              "hc_obs_scores: bad arguments");
   cudaStream_t st = (cudaStream_t)stream;
-  const size_t bytes = hc::obs_scratch_bytes(batch * kv_heads, L);
+  const size_t bytes = hc::obs_scratch_bytes(batch * kv_heads, L, window * group);
   void* scratch = nullptr;
   HC_CUDA_TRY(cudaMallocAsync(&scratch, bytes, st));
   const int rc = hc::launch_obs_scores(k_dev, q_obs_dev, batch, kv_heads, group, window, L,

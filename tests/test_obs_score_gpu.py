@@ -33,7 +33,9 @@ def _oracle_rows(k, q, B, H, G, w, L):
 
 
 @pytest.mark.parametrize("B,H,G,w,L", [(1, 2, 4, 1, 700), (2, 2, 7, 1, 1300), (1, 2, 4, 32, 1000),
-                                       (1, 1, 8, 16, 9000), (2, 3, 4, 5, 4097)])
+                                       (1, 1, 8, 16, 9000), (2, 3, 4, 5, 4097),
+                                       # w*G <= 16: K read once, probabilities from kept scores
+                                       (2, 2, 4, 4, 3001), (1, 2, 8, 2, 777), (1, 3, 1, 1, 50)])
 def test_obs_scores_match_oracle(B, H, G, w, L):
     import torch
 
