@@ -298,6 +298,8 @@ struct EngineImpl {
   int dd_horizon = 0;
   cudaEvent_t ev_log[kLogRing] = {};    // side stream: boundary decided and selected
   int64_t n_bound = 0, n_read = 0;      // boundaries issued / read by the host
+  int dd_pending_until = 0;             // latest completion step of the read decisions
+  bool dd_quiet = false;                // this step: nothing can land
   std::vector<int32_t> dd_sat_units;
   std::vector<int32_t> dd_sat_of_unit;  // unit -> DevSat index or -1
   std::vector<void*> dd_dev;            // device allocations of the devdec state
@@ -976,9 +978,13 @@ int engine_decode_begin(EngineImpl& e, int t, const void* q, const void* kn, con
                         void* o, bool hold, cudaStream_t st) {
   HC_REQUIRE(t >= 1 && t <= e.T, HC_EINVAL, "step %d outside 1..%d", t, e.T);
   HC_REQUIRE(e.in_step == 0, HC_ESTATE, "decode_begin(%d) while step %d is open", t, e.in_step);
-  if (e.devdec) {  // landings are decided on the device: satellites always run after them
+  e.dd_quiet = false;
+  if (e.devdec) {  // landings are decided on the device: satellites run after them ...
     HC_REQUIRE(e.deferred.empty(), HC_ESTATE, "host landings with device decisions");
-    hold = true;
+    // ... unless nothing can land: every decision is read and every transfer it
+    // made has landed already -- then no landing pass, no split K4
+    e.dd_quiet = e.n_read == e.n_bound && t > e.dd_pending_until;
+    hold = !e.dd_quiet;
   }
   if (!e.deferred.empty() && e.deferred_st != st) {  // landings requested on another stream
     std::vector<int> ids;
@@ -1040,7 +1046,7 @@ int engine_decode_begin(EngineImpl& e, int t, const void* q, const void* kn, con
   if (e.rows_ev[t & 1]) HC_CUDA_TRY(cudaStreamWaitEvent(st, e.rows_ev[t & 1], 0));
   p.skip = hold ? e.d_sat_flags : (land.empty() ? nullptr : e.d_skip);
   HC_TRY(launch_attn_tiles(e.tmK, e.tmV, p, active_tiles(e, t), st));
-  if (e.devdec) {
+  if (e.devdec && !e.dd_quiet) {
     // landing point (device-decided transfers due at t), then the satellites'
     // K4, on their own stream beside the main K4: the landing's wait for a late
     // gather no longer serialises the step
@@ -1079,7 +1085,7 @@ int engine_decode_end(EngineImpl& e, int t, cudaStream_t st) {
   AttnParams pl = e.cur_p;
   pl.skip = nullptr;
   if (e.devdec) {
-    HC_CUDA_TRY(cudaStreamWaitEvent(st, e.ev_sats, 0));  // satellites attended
+    if (!e.dd_quiet) HC_CUDA_TRY(cudaStreamWaitEvent(st, e.ev_sats, 0));  // satellites attended
   } else if (e.cur_hold) {
     std::vector<int> land;
     land.swap(e.deferred);
@@ -2464,6 +2470,7 @@ extern "C" int hc_engine_poll_decisions(hc_engine* eng, int32_t wait, int32_t* s
       cnt += f.ks[j];
     }
     r.fetched_offset = f.host_off < 0 ? -1 : int32_t(off);
+    e.dd_pending_until = std::max(e.dd_pending_until, f.completion);
     if (f.host_off >= 0 && cnt) {
       std::memcpy(fetched_out + off, e.fetched_h + f.host_off, size_t(cnt) * 4);
       if (e.timing)
