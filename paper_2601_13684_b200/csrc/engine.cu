@@ -2470,7 +2470,8 @@ extern "C" int hc_engine_poll_decisions(hc_engine* eng, int32_t wait, int32_t* s
       cnt += f.ks[j];
     }
     r.fetched_offset = f.host_off < 0 ? -1 : int32_t(off);
-    e.dd_pending_until = std::max(e.dd_pending_until, f.completion);
+    // it lands at max(completion, trigger + 1): a step's landing pass precedes its decision
+    e.dd_pending_until = std::max(e.dd_pending_until, std::max(f.completion, f.trigger + 1));
     if (f.host_off >= 0 && cnt) {
       std::memcpy(fetched_out + off, e.fetched_h + f.host_off, size_t(cnt) * 4);
       if (e.timing)
