@@ -406,47 +406,20 @@ def run_b200(args, rank, world):
             import torch.distributed as dist
             dist.barrier()
 
-    # ---- loop A: device-resident inputs ----
-    t_timed = t
-    rows_first = dec.resident_rows(t + 1)
-    clocks = ClockSampler(torch.cuda.current_device())
-    if not os.environ.get("HC_BENCH_NO_CLOCKS"):
-        clocks.start()
-    launches0 = lib.hc_launch_count()
-    dec.retrieval_stats()  # start the retrieval counters with the timed loop
-    dec.kernel_timing(True)
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier()
-    torch.cuda.synchronize()
-    torch.cuda.nvtx.range_push("timed")  # ncu --nvtx-include "timed/" selects loop A
-    ev0.record(stream)
-    for _ in range(K):
-        t += 1
-        dec.decode_step(t, *inputs(t), par_out if t == t_par else out, rows=False)
-    dec.join()  # the last step's monitor runs on the engine's side stream
-    ev1.record(stream)
-    torch.cuda.nvtx.range_pop()
-    torch.cuda.synchronize()
-    barrier()
-    ms = ev0.elapsed_time(ev1)
-    launches = lib.hc_launch_count() - launches0
-    phases = dec.kernel_timing(True)  # same instrumentation stays on for loop B
-    retr = dec.retrieval_stats()
-    attn_ms, attn_n = phases["attention"], phases["steps"]
-    clk = clocks.stop()
-    rows_last = dec.resident_rows(t)
-
-    # ---- loop B: end to end through the API with pinned host buffers ----
-    # Every step's Q / K_new / V_new cross H2D from pinned memory and its O
-    # comes back D2H inside the timed region; copies run on a side stream,
-    # double-buffered, so step t+1's upload and step t's download (and, sharded,
-    # the all-gather of O) overlap the decode of step t.
-    hq_all = qs[t + 1:t + K + 1].cpu().pin_memory()
+    # ---- timed region ----
+    # loop A: inputs resident on the device (`value`); loop B: end to end through
+    # the API, every step's Q / K_new / V_new H2D from pinned host memory and its
+    # O D2H (`e2e`).  They run interleaved, B1 A1 B2 A2 (halves of K each), so
+    # both measure the same stretch of the run -- the same drift events and
+    # landings -- with the same instrumentation.
+    halves = [K // 2, K - K // 2]
+    t_start = t
+    hq_all = qs[t + 1:t + 2 * K + 1].cpu().pin_memory()  # step s: hq_all[s - t_start - 1]
     hkv = [[x.cpu().pin_memory() for x in kv] for kv in kv_pool]
     hout = [torch.empty((w.batch,) + tuple(out.shape[1:]), dtype=out.dtype, pin_memory=True)
             for _ in range(2)]
+    hout_par = torch.empty_like(hout[0], pin_memory=True)
     dbuf = [tuple(torch.empty_like(x) for x in inputs(1)) for _ in range(2)]
-    t_e2e0 = t
     # the job's result: O of the whole batch (batch mode: this rank's sequences
     # are one contiguous slab of it, gathered in place)
     obuf = [torch.empty((w.batch,) + tuple(out.shape[1:]), dtype=out.dtype, device=out.device)
@@ -478,60 +451,116 @@ def run_b200(args, rank, world):
     h2d = hq_all[0].numel() * hq_all[0].element_size() + sum(
         x.numel() * x.element_size() for x in hkv[0])
     d2h = hout[0].numel() * hout[0].element_size()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
     def upload(tt, slot):
-        src = (hq_all[tt - t_e2e0 - 1],) + tuple(hkv[tt % 4])
+        src = (hq_all[tt - t_start - 1],) + tuple(hkv[tt % 4])
         with torch.cuda.stream(copy):
             copy.wait_event(ev_used[slot])  # the decode that last read this slot is done
             for dst, x in zip(dbuf[slot], src):
                 dst.copy_(x, non_blocking=True)
             ev_in[slot].record(copy)
 
-    for e in ev_used + ev_out:
-        e.record(stream)
-    barrier()
-    torch.cuda.synchronize()
-    ev0.record(stream)
-    if world == 1 and dec.devdec:
-        # the C-ABI per-step call with HOST buffers (hc_engine_decode_step_host):
-        # inputs H2D and O D2H on the engine's copy stream, one call per step
-        for i in range(K):
+    def loop_a(n):
+        nonlocal t
+        dec.kernel_timing(True)  # (discards the previous block's phases)
+        dec.retrieval_stats()
+        l0 = lib.hc_launch_count()
+        barrier()
+        torch.cuda.synchronize()
+        torch.cuda.nvtx.range_push("timed")  # ncu --nvtx-include "timed/" selects loop A
+        ev0.record(stream)
+        lo = t
+        for _ in range(n):
             t += 1
-            dec.decode_step_host(t, hq_all[i], *hkv[t % 4], hout[i % 2], rows=False)
-        K_left = 0
-    else:
-        K_left = K
-        upload(t + 1, 0)
-    for i in range(K_left):
-        t += 1
-        slot = i % 2
-        if i + 1 < K_left:
-            upload(t + 1, 1 - slot)
-        stream.wait_event(ev_in[slot])
-        stream.wait_event(ev_out[slot])  # previous download of this output slot finished
-        dec.decode_step(t, *dbuf[slot], oview[slot], rows=False)
-        ev_used[slot].record(stream)
-        with torch.cuda.stream(copy):
-            copy.wait_event(ev_used[slot])
-            if gather_o is not None:
-                gather_o(obuf[slot])
-            hout[slot].copy_(obuf[slot], non_blocking=True)
-            ev_out[slot].record(copy)
-    stream.wait_stream(copy)
-    dec.join()
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    barrier()
-    ms_e2e = ev0.elapsed_time(ev1)
+            dec.decode_step(t, *inputs(t), par_out if t == t_par else out, rows=False)
+        dec.join()  # the last step's monitor runs on the engine's side stream
+        ev1.record(stream)
+        torch.cuda.nvtx.range_pop()
+        torch.cuda.synchronize()
+        barrier()
+        return (ev0.elapsed_time(ev1), lib.hc_launch_count() - l0, dec.kernel_timing(True),
+                dec.retrieval_stats(), (lo, t))
+
+    def loop_b(n):
+        nonlocal t
+        for e in ev_used + ev_out:
+            e.record(stream)
+        barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        if world == 1 and dec.devdec:
+            # the C-ABI per-step call with HOST buffers (hc_engine_decode_step_host):
+            # inputs H2D and O D2H on the engine's copy streams, one call per step
+            for i in range(n):
+                t += 1
+                dec.decode_step_host(t, hq_all[t - t_start - 1], *hkv[t % 4],
+                                     hout_par if t == t_par else hout[i % 2], rows=False)
+            n_py = 0
+        else:
+            n_py = n
+            upload(t + 1, 0)
+        for i in range(n_py):
+            t += 1
+            slot = i % 2
+            if i + 1 < n_py:
+                upload(t + 1, 1 - slot)
+            stream.wait_event(ev_in[slot])
+            stream.wait_event(ev_out[slot])  # previous download of this output slot finished
+            dec.decode_step(t, *dbuf[slot], oview[slot], rows=False)
+            ev_used[slot].record(stream)
+            with torch.cuda.stream(copy):
+                copy.wait_event(ev_used[slot])
+                if gather_o is not None:
+                    gather_o(obuf[slot])
+                hout[slot].copy_(obuf[slot], non_blocking=True)
+                ev_out[slot].record(copy)
+        stream.wait_stream(copy)
+        dec.join()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        return ev0.elapsed_time(ev1)
+
+    clocks = ClockSampler(torch.cuda.current_device())
+    if not os.environ.get("HC_BENCH_NO_CLOCKS"):
+        clocks.start()
+    ms = ms_e2e = 0.0
+    launches = 0
+    phases, retr_parts, a_ranges = {}, [], []
+    rows_first = rows_last = None
+    for h in halves:
+        ms_e2e += loop_b(h)
+        if rows_first is None:
+            rows_first = dec.resident_rows(t + 1)
+        m_a, l_a, ph, rs, rng = loop_a(h)
+        ms += m_a
+        launches += l_a
+        for key, val in ph.items():
+            phases[key] = phases.get(key, 0) + val
+        retr_parts.append(rs)
+        a_ranges.append(rng)
+    rows_last = dec.resident_rows(t)
+    clk = clocks.stop()
     dec.kernel_timing(False)
     dec.finish()
     dec.sync()
+    attn_ms, attn_n = phases["attention"], phases["steps"]
+    rb = sum(r["bytes"] for r in retr_parts)
+    rg = sum(r["gather_ms"] for r in retr_parts)
+    retr = {"bytes": rb, "gather_ms": rg,
+            "landing_stall_ms": sum(r["landing_stall_ms"] for r in retr_parts),
+            "batches": sum(r["batches"] for r in retr_parts),
+            "host_link_gbs": (rb / (rg * 1e-3) / 1e9) if rg > 0 else None}
+    if t_par > 0 and t_par not in range(*(x + 1 for x in a_ranges[0])) and \
+            t_par not in range(*(x + 1 for x in a_ranges[1])) and t_par > t_start:
+        par_out.copy_(hout_par)  # the parity step ran through the host-buffer path
 
     # fires of loop A (its last boundary is decided during loop B) and the
     # reference's exposed-transfer measure (reporting.py:127-132): steps a
     # satellite served its stale set beyond trigger + update_delay_steps
     timed_ev = [e for s in dec.states for e in s.raw_events
-                if t_timed < e.trigger_step <= t_timed + K]
+                if any(lo < e.trigger_step <= hi for lo, hi in a_ranges)]
     events = len(timed_ev)
     exposed = sum(max(0, e.completion_step - (e.trigger_step + cfg.update_delay_steps))
                   for e in timed_ev)
