@@ -738,6 +738,64 @@ def cpu_sample(w, args):
     return list(range(n))
 
 
+def reference_engine_timing(seconds_cap: float = 60.0):
+    """The reference package's OWN engine (heterocache.engine.CacheEngine, the
+    unmodified install in baseline/_ref, pure Python, one core) replaying the
+    committed HCTRACE1 export of a 128K GPU run (tests/golden/scale_128k: a
+    cfg3-shaped slice, 2 layers x 4 KV heads x 1 sequence, every head's records
+    so its _measure runs too) -- SURVEY.md 8d CPU baseline (i).  Decision
+    bookkeeping only: the reference has no attention."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "heterocache").exists():
+        return {"unavailable": "reference not installed into baseline/_ref"}
+    import numpy as np
+
+    sys.path[:0] = [str(ref), str(ROOT / "tests")]
+    from golden_io import key
+    from heterocache.budget import BudgetPlan
+    from heterocache.engine import CacheEngine, EngineConfig
+    from heterocache.profiling import Cluster, HeadProfile, TaxonomyResult
+    from heterocache.trace import TraceManifest, make_trace
+
+    d = ROOT / "tests" / "golden" / "scale_128k"
+    run = json.loads((d / "scale_run.json").read_text())
+    z = np.load(d / "scale_trace.npz")
+    tr = make_trace(TraceManifest(**run["manifest"]), z["indices"], z["scores"])
+    cid, clusters = {}, []
+    for i, (p, sats) in enumerate(run["clusters"]):
+        clusters.append(Cluster(i, tuple(p), tuple(tuple(x) for x in sats)))
+        for mm in [tuple(p)] + [tuple(x) for x in sats]:
+            cid[mm] = i
+    heads = {key(h): HeadProfile(layer=key(h)[0], head=key(h)[1], s_stable=run["s_stable"][h],
+                                 s_sim=0.0, role=r, cluster_id=cid.get(key(h)))
+             for h, r in run["roles"].items()}
+    m = run["manifest"]
+    tax = TaxonomyResult(num_layers=m["num_layers"], heads_per_layer=m["heads_per_layer"],
+                         tau_stable=0.5, tau_sim=0.5, profiling_topk=None, heads=heads,
+                         clusters=tuple(clusters))
+    p = run["plan"]
+    plan = BudgetPlan(rho=p["rho"], prefill_len=p["prefill_len"], num_heads=p["num_heads"],
+                      num_full=p["num_full"], num_comp=p["num_comp"], l_base=p["l_base"],
+                      l_base_int=p["l_base_int"],
+                      lengths={key(h): n for h, n in p["lengths"].items()})
+    eng = CacheEngine(tr, tax, plan, EngineConfig(**run["config"]))
+    st = eng.prefill_init()
+    t0 = time.perf_counter()
+    n = 0
+    for t in range(1, m["decode_steps"] + 1):
+        eng.decode_step(st, t)
+        n += 1
+        if time.perf_counter() - t0 > seconds_cap:
+            break
+    dt = (time.perf_counter() - t0) / n
+    scale = 28 * 4 / m["num_layers"]  # cfg3: 28 layers x 4 sequences
+    return {"engine": "heterocache.engine.CacheEngine (baseline/_ref, unmodified)",
+            "cores": 1, "sample": f"HCTRACE1 export of a 128K GPU run: {m['num_layers']} layers x "
+                                  f"{m['heads_per_layer']} KV heads x 1 sequence, {n} decode steps",
+            "ms_per_step_sample": dt * 1e3,
+            "cfg3_steps_per_s": 1.0 / (dt * scale), "cfg3_extrapolation_factor": scale}
+
+
 def run_reference(args, world):
     """--impl reference: the CPU path (oracle port) on the host cores."""
     import torch
@@ -789,6 +847,8 @@ def run_reference(args, world):
                                 "hc_oracle.plan_budget)" if args.roles == "profiled" else
                       "fixed survey mix", "profiling_s": profiling_s},
         "prefill_seconds": prefill_s,
+        # SURVEY 8d baseline (i): the reference's own engine, decision bookkeeping only
+        "reference_engine": reference_engine_timing(),
     }
     return res
 
