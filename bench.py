@@ -559,7 +559,8 @@ def run_b200(args, rank, world):
             "landing_stall_ms": sum(r["landing_stall_ms"] for r in retr_parts),
             "batches": sum(r["batches"] for r in retr_parts),
             "host_link_gbs": (rb / (rg * 1e-3) / 1e9) if rg > 0 else None}
-    if t_par > 0 and t_par not in range(*(x + 1 for x in a_ranges[0])) and \
+    if world == 1 and dec.devdec and t_par > 0 and \
+            t_par not in range(*(x + 1 for x in a_ranges[0])) and \
             t_par not in range(*(x + 1 for x in a_ranges[1])) and t_par > t_start:
         par_out.copy_(hout_par)  # the parity step ran through the host-buffer path
 
