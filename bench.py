@@ -123,6 +123,44 @@ def peaks():
     return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)", {}
 
 
+def read_probe(gib: int = 4) -> dict:
+    """Live read-only HBM bandwidth (hc_read_probe over a buffer larger than L2).
+
+    The copy peak in MEASURED_PEAKS.json moves read+write traffic; K4 reads
+    K/V and writes almost nothing, so it can exceed that figure.  This is the
+    read-only ceiling measured on the same box, best over grid sizes and
+    repetitions, timed with CUDA events on the launching stream."""
+    import torch
+
+    from paper_2601_13684_b200 import _lib
+
+    lib = _lib.load()
+    nbytes = gib << 30
+    buf = torch.ones(nbytes // 4, dtype=torch.int32, device="cuda")
+    sm = torch.cuda.get_device_properties(0).multi_processor_count
+    sink = torch.empty(sm * 16, dtype=torch.int32, device="cuda")
+    st = torch.cuda.current_stream()
+    best = {}
+    for per_sm in (4, 8, 16):
+        ms = []
+        for _ in range(6):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            rc = lib.hc_read_probe(buf.data_ptr(), nbytes, sink.data_ptr(), sm * per_sm,
+                                   st.cuda_stream)
+            b.record(st)
+            if rc != 0:
+                raise RuntimeError(lib.hc_last_error().decode())
+            b.synchronize()
+            ms.append(a.elapsed_time(b))
+        best[per_sm] = nbytes / (min(ms[1:]) * 1e-3) / 1e9
+    del buf, sink
+    torch.cuda.empty_cache()
+    per_sm = max(best, key=best.get)
+    return {"gbs": best[per_sm], "bytes": nbytes, "ctas_per_sm": per_sm,
+            "by_ctas_per_sm": {str(k): round(v, 1) for k, v in best.items()}}
+
+
 def cpu_model() -> str:
     try:
         for line in Path("/proc/cpuinfo").read_text().splitlines():
@@ -594,6 +632,12 @@ def run_b200(args, rank, world):
     attn_avg_ms = attn_ms / max(1, attn_n)
     stall_avg_ms = max(0.0, attn_ms - retr["landing_stall_ms"]) / max(1, attn_n)
     peak, peak_src, pk = peaks()
+    rprobe = None
+    if world == 1 and os.environ.get("HC_NO_READ_PROBE") != "1":
+        try:
+            rprobe = read_probe()
+        except (RuntimeError, torch.OutOfMemoryError):  # a diagnostic: never fails the run
+            rprobe = None
     achieved = attn_bytes / (attn_avg_ms * 1e-3) / 1e9 if attn_avg_ms > 0 else 0.0
     traffic = None
     tf = ROOT / "profiles" / f"traffic_{args.workload}.json"
@@ -630,7 +674,10 @@ def run_b200(args, rank, world):
                      "launches_timed": attn_n,
                      "frac_excluding_landing_waits":
                          attn_bytes / (stall_avg_ms * 1e-3) / 1e9 / peak if stall_avg_ms else None,
-                     "vs_nominal_8tbs": achieved / 8000.0},
+                     "vs_nominal_8tbs": achieved / 8000.0,
+                     "read_only_peak_gbs": rprobe["gbs"] if rprobe else None,
+                     "frac_vs_read_only_peak": achieved / rprobe["gbs"] if rprobe else None,
+                     "read_only_probe": rprobe},
         "clocks": clk,
         "phase_ms_per_step": {k: v / max(1, attn_n) for k, v in phases.items() if k != "steps"},
         "timed_blocks_ms": blocks,  # run order A1 B1 B2 A2 (device-input / e2e halves)

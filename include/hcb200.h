@@ -417,6 +417,12 @@ int hc_engine_active_tiles(const hc_engine* eng, int32_t step, int32_t* n_tiles)
  * ------------------------------------------------------------------------- */
 int hc_synth_normal(float* out_dev, int64_t n, uint64_t key, int64_t offset, void* stream);
 
+/* Read-only HBM probe (bench roofline denominator; no reference counterpart):
+ * streams `bytes` (a multiple of 16) of buf_dev once with `ctas` CTAs of 256
+ * threads and writes one XOR per CTA into sink_dev[ctas]. */
+int hc_read_probe(const void* buf_dev, int64_t bytes, uint32_t* sink_dev, int32_t ctas,
+                  void* stream);
+
 #ifdef __cplusplus
 }
 #endif

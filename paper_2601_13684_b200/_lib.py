@@ -103,6 +103,7 @@ def _declare(lib):
         "hc_engine_gaps": (i32, [vp, vp, i32, vp]),
         "hc_engine_prefill_stats": (i32, [vp, vp]),
         "hc_synth_normal": (i32, [vp, C.c_int64, C.c_uint64, C.c_int64, vp]),
+        "hc_read_probe": (i32, [vp, C.c_int64, vp, i32, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
