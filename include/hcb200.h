@@ -389,7 +389,9 @@ int hc_engine_set_prefill_dump(hc_engine* eng, float* dst_dev);
  * call of phase_ms[8] = {append, K4 attention, combine, pivot score rows,
  * K1/K2 monitor, overlap copy, whole step, gaps between steps} and the
  * number of steps, then
- * resets and enables (enable != 0) or disables recording. */
+ * resets and enables (enable 1: every phase; 2: the K4 attention phase only,
+ * two timed events per step, for launch-bound timed regions) or disables
+ * (0) recording. */
 int hc_engine_timing(hc_engine* eng, int32_t enable, double* phase_ms, int32_t* steps);
 
 /* Retrieval statistics since the last call (timing must be enabled):

@@ -23,10 +23,13 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <new>
+#include <optional>
 #include <tuple>
 #include <unordered_map>
 #include <vector>
@@ -123,6 +126,38 @@ int dalloc(void** p, size_t bytes, int64_t* counter) {
 }
 
 }  // namespace
+
+// Host submission profile (diagnostics: HC_HOST_PROF=1 prints, at engine
+// destroy, the host time spent per decode-step section).
+struct HostProf {
+  static constexpr int kN = 12;
+  bool on = getenv("HC_HOST_PROF") != nullptr;
+  double ns[kN] = {};
+  long n[kN] = {};
+};
+HostProf g_hprof;
+const char* const kHostProfNames[HostProf::kN] = {
+    "decode_begin", "append", "k4_main", "devdec_land", "schedule_gather", "k4_sats",
+    "decode_end", "combine", "rows_monitor", "decide", "gc_events", "step_host"};
+struct HostProfScope {
+  int k;
+  std::chrono::steady_clock::time_point t0;
+  explicit HostProfScope(int k_) : k(g_hprof.on ? k_ : -1) {
+    if (k >= 0) t0 = std::chrono::steady_clock::now();
+  }
+  ~HostProfScope() {
+    if (k < 0) return;
+    g_hprof.ns[k] += std::chrono::duration<double, std::nano>(std::chrono::steady_clock::now() - t0).count();
+    ++g_hprof.n[k];
+  }
+};
+void host_prof_report() {
+  if (!g_hprof.on) return;
+  for (int k = 0; k < HostProf::kN; ++k)
+    if (g_hprof.n[k])
+      fprintf(stderr, "hc_host_prof %-16s %8ld calls %9.2f us/call\n", kHostProfNames[k],
+              g_hprof.n[k], g_hprof.ns[k] / g_hprof.n[k] * 1e-3);
+}
 
 struct EngineImpl {
   hc_engine_desc cfg{};
@@ -242,6 +277,8 @@ struct EngineImpl {
   // stream) | end (step stream)
   static constexpr int kPhaseEvents = 7;
   bool timing = false;
+  bool timing_light = false;  // only the attention phase (ev[1] -> ev[2]) is recorded
+  std::vector<cudaEvent_t> tpool;  // timed events for gather / landing pairs, reused
   std::vector<cudaEvent_t> tev;
   size_t tev_used = 0;  // steps recorded
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> gather_ev;  // retrieval-stream gathers
@@ -327,6 +364,7 @@ namespace {
 
 int engine_destroy(EngineImpl& e) {
   cudaDeviceSynchronize();
+  host_prof_report();
   for (auto& pr : e.stage_busy) cudaEventDestroy(std::get<2>(pr));
   if (e.stage) cudaFreeHost(e.stage);
   if (e.ovl_host) cudaFreeHost(e.ovl_host);
@@ -381,6 +419,9 @@ int engine_destroy(EngineImpl& e) {
   if (e.pf_ev0) cudaEventDestroy(e.pf_ev0);
   if (e.pf_ev1) cudaEventDestroy(e.pf_ev1);
   for (auto x : e.tev) cudaEventDestroy(x);
+  for (auto x : e.tpool) cudaEventDestroy(x);
+  for (auto& pr : e.gather_ev) cudaEventDestroy(pr.first), cudaEventDestroy(pr.second);
+  for (auto& pr : e.land_ev) cudaEventDestroy(pr.first), cudaEventDestroy(pr.second);
   return HC_OK;
 }
 
@@ -857,6 +898,18 @@ int new_event(EngineImpl& e, cudaEvent_t* out, bool timed = false) {
   return HC_OK;
 }
 
+// A timed event for a gather / landing timing pair, from the engine's pool
+// (returned by hc_engine_retrieval_stats once read): no event creation inside a step.
+int timed_event(EngineImpl& e, cudaEvent_t* out) {
+  if (e.tpool.empty()) {
+    HC_CUDA_TRY(cudaEventCreate(out));
+  } else {
+    *out = e.tpool.back();
+    e.tpool.pop_back();
+  }
+  return HC_OK;
+}
+
 // Retire ordering events older than kRing steps that have completed and that
 // no pending transfer or timing record still refers to (a long decode would
 // otherwise accumulate one per fire / gather / landing).
@@ -920,8 +973,8 @@ int devdec_schedule_and_gather(EngineImpl& e, int t_max) {
   HC_CUDA_TRY(cudaStreamWaitEvent(e.retr, e.ev_sched, 0));
   cudaEvent_t g0 = nullptr, g1 = nullptr;
   if (e.timing) {
-    HC_TRY(new_event(e, &g0, true));
-    HC_TRY(new_event(e, &g1, true));
+    HC_TRY(timed_event(e, &g0));
+    HC_TRY(timed_event(e, &g1));
   }
   HC_TRY(launch_dev_gathers(e.dd, reinterpret_cast<uint4*>(e.K), reinterpret_cast<uint4*>(e.V),
                             e.retr, t_max, g0, g1));
@@ -978,6 +1031,7 @@ int engine_decode_begin(EngineImpl& e, int t, const void* q, const void* kn, con
                         void* o, bool hold, cudaStream_t st) {
   HC_REQUIRE(t >= 1 && t <= e.T, HC_EINVAL, "step %d outside 1..%d", t, e.T);
   HC_REQUIRE(e.in_step == 0, HC_ESTATE, "decode_begin(%d) while step %d is open", t, e.in_step);
+  HostProfScope prof_all(0);
   e.dd_quiet = false;
   if (e.devdec) {  // landings are decided on the device: satellites run after them ...
     HC_REQUIRE(e.deferred.empty(), HC_ESTATE, "host landings with device decisions");
@@ -1031,28 +1085,35 @@ int engine_decode_begin(EngineImpl& e, int t, const void* q, const void* kn, con
     }
     ev = e.tev.data() + e.tev_used * EngineImpl::kPhaseEvents;
     ++e.tev_used;
-    HC_CUDA_TRY(cudaEventRecord(ev[0], st));
+    if (!e.timing_light) HC_CUDA_TRY(cudaEventRecord(ev[0], st));
   }
+  std::optional<HostProfScope> prof_sec;
+  prof_sec.emplace(1);
   append_kernel<<<(e.n_units + 7) / 8, 256, 0, st>>>(
       e.d_units, e.n_units, e.L, t, reinterpret_cast<const uint4*>(kn),
       reinterpret_cast<const uint4*>(vn), reinterpret_cast<uint4*>(e.K),
       reinterpret_cast<uint4*>(e.V), reinterpret_cast<uint4*>(e.shadowK), e.NL, e.H,
       int64_t(e.L) + e.T);
   HC_CHECK_LAUNCH();
-  if (ev) HC_CUDA_TRY(cudaEventRecord(ev[1], st));
+  if (ev) HC_CUDA_TRY(cudaEventRecord(ev[1], st));  // light timing: this ...
   if (e.devdec) HC_CUDA_TRY(cudaEventRecord(e.ev_app, st));  // the token is appended
   AttnParams p = decode_params(e, t, q, o);
   // K4 overwrites the score material of parity t&1: step t-2's rows must be done
   if (e.rows_ev[t & 1]) HC_CUDA_TRY(cudaStreamWaitEvent(st, e.rows_ev[t & 1], 0));
   p.skip = hold ? e.d_sat_flags : (land.empty() ? nullptr : e.d_skip);
+  prof_sec.emplace(2);
   HC_TRY(launch_attn_tiles(e.tmK, e.tmV, p, active_tiles(e, t), st));
+  prof_sec.reset();
   if (e.devdec && !e.dd_quiet) {
     // landing point (device-decided transfers due at t), then the satellites'
     // K4, on their own stream beside the main K4: the landing's wait for a late
     // gather no longer serialises the step
+    prof_sec.emplace(3);
     HC_CUDA_TRY(cudaStreamWaitEvent(e.lnd, e.ev_app, 0));
     HC_TRY(devdec_land(e, t, e.lnd));
+    prof_sec.emplace(4);
     HC_TRY(devdec_schedule_and_gather(e, t + e.dd_horizon));
+    prof_sec.emplace(5);
     AttnParams ps = p;
     ps.skip = nullptr;
     ps.tiles = e.d_sat_tiles;
@@ -1062,8 +1123,8 @@ int engine_decode_begin(EngineImpl& e, int t, const void* q, const void* kn, con
     HC_CUDA_TRY(cudaEventRecord(e.ev_sats, e.lnd));
     if (e.timing) {  // landing stall = how far the satellites' path ends after the main K4
       cudaEvent_t w0 = nullptr, w1 = nullptr;
-      HC_TRY(new_event(e, &w0, true));
-      HC_TRY(new_event(e, &w1, true));
+      HC_TRY(timed_event(e, &w0));
+      HC_TRY(timed_event(e, &w1));
       HC_CUDA_TRY(cudaEventRecord(w0, st));
       HC_CUDA_TRY(cudaEventRecord(w1, e.lnd));
       e.land_ev.emplace_back(w0, w1);
@@ -1081,6 +1142,8 @@ int engine_decode_begin(EngineImpl& e, int t, const void* q, const void* kn, con
 int engine_decode_end(EngineImpl& e, int t, cudaStream_t st) {
   HC_REQUIRE(e.in_step == t, HC_ESTATE, "decode_end(%d) without decode_begin(%d)", t, t);
   HC_REQUIRE(st == e.cur_st, HC_EINVAL, "decode_end on another stream than decode_begin");
+  HostProfScope prof_all(6);
+  std::optional<HostProfScope> prof_sec;
   e.in_step = 0;  // landings below are applied for real
   AttnParams pl = e.cur_p;
   pl.skip = nullptr;
@@ -1106,7 +1169,9 @@ int engine_decode_end(EngineImpl& e, int t, cudaStream_t st) {
   }
   e.cur_land.clear();
   cudaEvent_t* ev = e.cur_ev;
-  if (ev) HC_CUDA_TRY(cudaEventRecord(ev[2], st));
+  prof_sec.emplace(7);
+  if (ev) HC_CUDA_TRY(cudaEventRecord(ev[2], st));  // ... and this one only
+  if (ev && e.timing_light) ev = nullptr;
   HC_TRY(launch_combine(e.cur_p, st));  // O: the step's output
   if (ev) HC_CUDA_TRY(cudaEventRecord(ev[3], st));
   e.last_t = t;
@@ -1119,6 +1184,7 @@ int engine_decode_end(EngineImpl& e, int t, cudaStream_t st) {
     // beside the next step's attention.  Readers (overlaps, fire, measure,
     // pivot_row) wait for step_end; the attention two steps later waits for
     // this step's rows before it overwrites the score material of its parity.
+    prof_sec.emplace(8);
     if (!e.rows_done)
       HC_CUDA_TRY(cudaEventCreateWithFlags(&e.rows_done, cudaEventDisableTiming));
     HC_CUDA_TRY(cudaEventRecord(e.rows_done, st));
@@ -1134,7 +1200,9 @@ int engine_decode_end(EngineImpl& e, int t, cudaStream_t st) {
                           uint32_t(e.lbase), e.kbase, e.words, e.thr,
                           e.ovl_ring + size_t(t % kRing) * e.n_piv, e.mon,
                           e.ghist + size_t(t & 1) * e.n_piv * 8192));
+    prof_sec.emplace(9);
     if (e.devdec) HC_TRY(devdec_decide(e, t));
+    prof_sec.reset();
   } else if (ev) {
     HC_CUDA_TRY(cudaEventRecord(ev[4], st));
   }
@@ -1144,6 +1212,7 @@ int engine_decode_end(EngineImpl& e, int t, cudaStream_t st) {
     HC_CUDA_TRY(cudaEventRecord(ev[6], st));
   }
   HC_CUDA_TRY(cudaEventRecord(e.step_end, ms));
+  prof_sec.emplace(10);
   return gc_events(e, t);
 }
 
@@ -1178,6 +1247,7 @@ int engine_decode_step_host(EngineImpl& e, int t, const void* q_h, const void* k
   const size_t qb = size_t(e.B) * e.NL * e.Hq * kHeadDim * 2;
   const size_t kb = size_t(e.B) * e.NL * e.H * kHeadDim * 2;
   if (!e.hcopy) HC_TRY(host_io_init(e));
+  HostProfScope prof_all(11);
   const int s = t & 1;
   char* d = static_cast<char*>(e.hbuf[s]);
   void *dq = d, *dkn = d + qb, *dvn = d + qb + kb, *dout = d + qb + 2 * kb;
@@ -1345,8 +1415,8 @@ int issue_gathers(EngineImpl& e, const std::vector<int>& ids_in, cudaEvent_t aft
     HC_CHECK_LAUNCH();
     cudaEvent_t t0 = nullptr, t1 = nullptr;
     if (e.timing) {
-      HC_TRY(new_event(e, &t0, true));
-      HC_TRY(new_event(e, &t1, true));
+      HC_TRY(timed_event(e, &t0));
+      HC_TRY(timed_event(e, &t1));
       HC_CUDA_TRY(cudaEventRecord(t0, e.retr));
     }
     (void)max_cap;
@@ -1748,8 +1818,8 @@ int apply_landings(EngineImpl& e, const std::vector<int>& idv, cudaStream_t st) 
     if (x.done != last_wait) {
       cudaEvent_t w0 = nullptr, w1 = nullptr;
       if (e.timing) {
-        HC_TRY(new_event(e, &w0, true));
-        HC_TRY(new_event(e, &w1, true));
+        HC_TRY(timed_event(e, &w0));
+        HC_TRY(timed_event(e, &w1));
         HC_CUDA_TRY(cudaEventRecord(w0, st));
       }
       HC_CUDA_TRY(cudaStreamWaitEvent(st, x.done, 0));
@@ -2333,6 +2403,13 @@ extern "C" int hc_engine_timing(hc_engine* eng, int32_t enable, double* phase_ms
     for (int k = 0; k <= P; ++k) phase_ms[k] = 0;
     for (size_t i = 0; i < e.tev_used; ++i) {
       const cudaEvent_t* ev = e.tev.data() + i * P;
+      if (e.timing_light) {  // the attention phase only
+        HC_CUDA_TRY(cudaEventSynchronize(ev[2]));
+        float ms = 0;
+        HC_CUDA_TRY(cudaEventElapsedTime(&ms, ev[1], ev[2]));
+        phase_ms[1] += ms;
+        continue;
+      }
       HC_CUDA_TRY(cudaEventSynchronize(ev[P - 1]));
       HC_CUDA_TRY(cudaEventSynchronize(ev[5]));
       // append | attention | combine on the step's stream; score rows (ev3 ->
@@ -2356,6 +2433,7 @@ extern "C" int hc_engine_timing(hc_engine* eng, int32_t enable, double* phase_ms
   }
   e.tev_used = 0;
   e.timing = enable != 0;
+  e.timing_light = enable == 2;
   return HC_OK;
 }
 
@@ -2380,6 +2458,8 @@ extern "C" int hc_engine_retrieval_stats(hc_engine* eng, double* out4) {
   out4[1] = g;                                                     // gather kernel ms
   out4[2] = w;                                                     // landing stall ms
   out4[3] = double(e.gather_ev.size());
+  for (auto& pr : e.gather_ev) e.tpool.push_back(pr.first), e.tpool.push_back(pr.second);
+  for (auto& pr : e.land_ev) e.tpool.push_back(pr.first), e.tpool.push_back(pr.second);
   e.gather_ev.clear();
   e.land_ev.clear();
   e.gather_rows_issued = 0;
@@ -2391,7 +2471,7 @@ extern "C" int hc_engine_gaps(hc_engine* eng, float* out, int32_t cap, int32_t* 
   auto& e = eng->e;
   constexpr int P = hc::EngineImpl::kPhaseEvents;
   int m = 0;
-  for (size_t i = 1; i < e.tev_used && m < cap; ++i) {
+  for (size_t i = 1; !e.timing_light && i < e.tev_used && m < cap; ++i) {
     const cudaEvent_t* ev = e.tev.data() + i * P;
     HC_CUDA_TRY(cudaEventSynchronize(ev[P - 1]));
     float gap = 0;

@@ -741,11 +741,14 @@ class HeteroCacheDecoder:
     PHASES = ("append", "attention", "combine", "score_rows", "monitor", "tail", "step",
               "inter_step_gap")
 
-    def kernel_timing(self, enable: bool = True) -> dict:
-        """Summed device milliseconds per decode-step phase since the last call."""
+    def kernel_timing(self, enable: bool = True, light: bool = False) -> dict:
+        """Summed device milliseconds per decode-step phase since the last call;
+        then record every phase (enable), only the K4 attention phase (enable,
+        light: two events per step) or nothing."""
         ms = (C.c_double * 8)()
         n = C.c_int32()
-        _lib.check(self.lib.hc_engine_timing(self.handle, int(enable), ms, C.byref(n)))
+        level = (2 if light else 1) if enable else 0
+        _lib.check(self.lib.hc_engine_timing(self.handle, level, ms, C.byref(n)))
         out = dict(zip(self.PHASES, list(ms)))
         out["steps"] = n.value
         return out
