@@ -271,6 +271,8 @@ struct EngineImpl {
   void* hbuf[2] = {nullptr, nullptr};
   cudaEvent_t h_in[2] = {}, h_used[2] = {}, h_out[2] = {};
   int h_last = -1;
+  bool small_io = false;  // decode_step_host moves its inputs / output by zero-copy kernels
+  std::vector<std::pair<const void*, void*>> hmap;  // pinned host -> device-mapped pointer
   cudaEvent_t last_selected = nullptr;  // side stream: the last fire batch's copies are done
   // per-step phase timeline (bench roofline): 7 events per step: start |
   // append | K4 | combine (step stream) | score rows | monitor (monitor
@@ -1227,9 +1229,50 @@ int engine_decode_step(EngineImpl& e, int t, const void* q, const void* kn, cons
 // download and step t+1's upload overlap the decode (the e2e path of a
 // serving runtime: one call per step, no framework on the host).
 // Staging of decode_step_host, set up with the engine (not inside a timed step).
+//
+// Small steps (inputs + output <= 512 KB, e.g. one layer at batch 1) are
+// launch-bound: their inputs are read from the caller's pinned buffers by one
+// zero-copy kernel on the step's stream and the combine writes O straight into
+// the caller's pinned output -- two fewer copies, events and streams per step.
+// Larger steps copy on the engine's copy streams, overlapped with the decode.
+constexpr size_t kSmallHostIo = size_t(512) << 10;
+
+__global__ void stage_in_kernel(const uint4* q, const uint4* kn, const uint4* vn, uint4* dq,
+                                uint4* dkn, uint4* dvn, int nq, int nk) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint4* src;
+  uint4* dst;
+  if (i < nq) src = q + i, dst = dq + i;
+  else if (i < nq + nk) src = kn + (i - nq), dst = dkn + (i - nq);
+  else if (i < nq + 2 * nk) src = vn + (i - nq - nk), dst = dvn + (i - nq - nk);
+  else return;
+  uint4 v;  // .cv: system-memory lines are fetched again, never served stale from L2
+  asm volatile("ld.global.cv.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(src));
+  *dst = v;
+}
+
+// Device address of a pinned (page-locked, mapped) host buffer; cached per pointer.
+int mapped_ptr(EngineImpl& e, const void* h, void** d) {
+  for (const auto& pr : e.hmap)
+    if (pr.first == h) {
+      *d = pr.second;
+      return HC_OK;
+    }
+  const cudaError_t rc = cudaHostGetDevicePointer(d, const_cast<void*>(h), 0);
+  if (rc != cudaSuccess) {
+    cudaGetLastError();
+    HC_REQUIRE(false, HC_EINVAL, "decode_step_host: %p is not pinned host memory", h);
+  }
+  if (e.hmap.size() >= 64) e.hmap.erase(e.hmap.begin());
+  e.hmap.emplace_back(h, *d);
+  return HC_OK;
+}
+
 int host_io_init(EngineImpl& e) {
   const size_t qb = size_t(e.B) * e.NL * e.Hq * kHeadDim * 2;
   const size_t kb = size_t(e.B) * e.NL * e.H * kHeadDim * 2;
+  e.small_io = 2 * qb + 2 * kb <= kSmallHostIo && !getenv("HC_HOST_IO_COPY");
   HC_CUDA_TRY(cudaStreamCreateWithFlags(&e.hcopy, cudaStreamNonBlocking));
   HC_CUDA_TRY(cudaStreamCreateWithFlags(&e.hdown, cudaStreamNonBlocking));
   for (int i = 0; i < 2; ++i) {
@@ -1251,6 +1294,23 @@ int engine_decode_step_host(EngineImpl& e, int t, const void* q_h, const void* k
   const int s = t & 1;
   char* d = static_cast<char*>(e.hbuf[s]);
   void *dq = d, *dkn = d + qb, *dvn = d + qb + kb, *dout = d + qb + 2 * kb;
+  if (e.small_io) {
+    void *mq, *mk, *mv, *mo;
+    HC_TRY(mapped_ptr(e, q_h, &mq));
+    HC_TRY(mapped_ptr(e, kn_h, &mk));
+    HC_TRY(mapped_ptr(e, vn_h, &mv));
+    HC_TRY(mapped_ptr(e, o_h, &mo));
+    const int nq = int(qb / 16), nk = int(kb / 16);
+    stage_in_kernel<<<(nq + 2 * nk + 255) / 256, 256, 0, st>>>(
+        static_cast<const uint4*>(mq), static_cast<const uint4*>(mk),
+        static_cast<const uint4*>(mv), static_cast<uint4*>(dq), static_cast<uint4*>(dkn),
+        static_cast<uint4*>(dvn), nq, nk);
+    HC_CHECK_LAUNCH();
+    HC_TRY(engine_decode_step(e, t, dq, dkn, dvn, mo, st));  // the combine writes O to the host
+    HC_CUDA_TRY(cudaEventRecord(e.h_out[s], st));
+    e.h_last = s;
+    return HC_OK;
+  }
   HC_CUDA_TRY(cudaStreamWaitEvent(e.hcopy, e.h_used[s], 0));  // the decode that read this slot
   HC_CUDA_TRY(cudaMemcpyAsync(dq, q_h, qb, cudaMemcpyHostToDevice, e.hcopy));
   HC_CUDA_TRY(cudaMemcpyAsync(dkn, kn_h, kb, cudaMemcpyHostToDevice, e.hcopy));

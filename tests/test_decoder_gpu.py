@@ -416,21 +416,33 @@ def test_fetched_ring_wraps_without_track_sets():
     assert logs[0] == logs[1] and sum(len(x) for x in logs[0]) >= 10
 
 
-def test_decode_step_host_matches_device_inputs():
-    """hc_engine_decode_step_host (pinned host in / out, the engine's copy stream)
-    gives bit-identical outputs and events to decode_step on device tensors."""
+@pytest.mark.parametrize("io", ["zero_copy", "copy"])
+def test_decode_step_host_matches_device_inputs(io, monkeypatch):
+    """hc_engine_decode_step_host (pinned host in / out) gives bit-identical outputs
+    and events to decode_step on device tensors -- through the zero-copy path of
+    small steps (inputs read by a kernel, O written by the combine) and through the
+    copy streams.  The pinned buffers are reused and rewritten every step, so a
+    stale system-memory line would show up as a wrong output."""
     import torch
 
+    if io == "copy":
+        monkeypatch.setenv("HC_HOST_IO_COPY", "1")
     outs, evs = [], []
     for host in (False, True):
         ctx = _build(B=2, T=24, window=4, shift=(5, 13))
         dec, gen = ctx["dec"], ctx["gen"]
         seq = []
+        bufs = None
         for t in range(1, 25):
             q, kn, vn = gen.step_inputs(t, ctx["shift"])
             if host:
-                hq, hk, hv = (x.cpu().pin_memory() for x in (q, kn, vn))
-                ho = torch.empty(q.shape, dtype=q.dtype, pin_memory=True)
+                if bufs is None or t % 3 == 0:  # fresh buffers now and then, else rewrite
+                    bufs = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
+                            for x in (q, kn, vn, q)]
+                hq, hk, hv, ho = bufs
+                for dst, x in zip((hq, hk, hv), (q, kn, vn)):
+                    dst.copy_(x.cpu())
+                ho.fill_(float("nan"))
                 dec.decode_step_host(t, hq, hk, hv, ho)
                 dec.join()
                 torch.cuda.synchronize()
