@@ -330,7 +330,8 @@ struct EngineImpl {
   bool copy_valid = false;
   cudaEvent_t ev_land = nullptr, ev_sched = nullptr, ev_sel = nullptr, ev_dec = nullptr;
   cudaEvent_t ev_app = nullptr, ev_sats = nullptr;
-  bool sched_valid = false, sel_valid = false;
+  bool sched_valid = false;
+  bool sel_valid = false;  // a fire selection the monitor stream is not yet ordered after
   // a gather pass takes only transfers due within this many steps (0: all of
   // them, the default -- keeping the host link busy as early as possible beat
   // every horizon of 1-8 steps at cfg4; HC_DEVDEC_HORIZON overrides)
@@ -1098,7 +1099,8 @@ int engine_decode_begin(EngineImpl& e, int t, const void* q, const void* kn, con
       int64_t(e.L) + e.T);
   HC_CHECK_LAUNCH();
   if (ev) HC_CUDA_TRY(cudaEventRecord(ev[1], st));  // light timing: this ...
-  if (e.devdec) HC_CUDA_TRY(cudaEventRecord(e.ev_app, st));  // the token is appended
+  if (e.devdec && !e.dd_quiet)  // the token is appended (the landing stream waits for it)
+    HC_CUDA_TRY(cudaEventRecord(e.ev_app, st));
   AttnParams p = decode_params(e, t, q, o);
   // K4 overwrites the score material of parity t&1: step t-2's rows must be done
   if (e.rows_ev[t & 1]) HC_CUDA_TRY(cudaStreamWaitEvent(st, e.rows_ev[t & 1], 0));
@@ -1192,7 +1194,10 @@ int engine_decode_end(EngineImpl& e, int t, cudaStream_t st) {
     HC_CUDA_TRY(cudaEventRecord(e.rows_done, st));
     HC_CUDA_TRY(cudaStreamWaitEvent(e.mon, e.rows_done, 0));
     // the previous boundary's fetch selection still reads the rows and histograms
-    if (e.sel_valid) HC_CUDA_TRY(cudaStreamWaitEvent(e.mon, e.ev_sel, 0));
+    if (e.sel_valid) {  // (once per selection: the monitor stream stays ordered after it)
+      HC_CUDA_TRY(cudaStreamWaitEvent(e.mon, e.ev_sel, 0));
+      e.sel_valid = false;
+    }
     HC_TRY(launch_score_rows(e.cur_p, e.d_piv_units, e.n_piv, e.mon));
     cudaEvent_t& re = e.rows_ev[t & 1];
     if (!re) HC_CUDA_TRY(cudaEventCreateWithFlags(&re, cudaEventDisableTiming));
