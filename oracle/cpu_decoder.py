@@ -19,7 +19,10 @@ exporter (model.ts:232-291) in fp32 on the host cores:
                                 accounting, K_base <- current top (engine.py:
                                 313-357)
 
-Selection is hc_oracle.top_k_dense (metrics.py:26-45 order).  The decision
+Selection is hc_oracle.top_k_dense's order (metrics.py:26-45), through its
+O(n) twin top_k_dense_select (identical output, tested).  K / V are kept as fp32
+copies of the bf16 inputs (exact), so a step reads each resident row once
+instead of converting whole caches.  The decision
 logic is the same sequence of operations as hc_oracle.replay (pinned to the
 reference's own runs); only the rows come from this module's fp32 attention
 instead of a trace.
@@ -66,6 +69,8 @@ class CpuDecoder:
         self.pending, self.events = [], []
         self.cum, self.order = 0, 0
         self.rows0 = {}
+        self._base = {}  # hd -> (dynamic array, recency start, sorted positions < L)
+        self._gath = {}  # hd -> (dynamic, recency start, K rows, V rows, rows < L, steps)
 
     def eff_len(self, hd) -> int:  # engine.py:218-221
         return self.l_base if self.variant == "no_allocation" else self.lengths[hd]
@@ -79,11 +84,11 @@ class CpuDecoder:
         w = q.shape[0]
         for h in range(self.H):
             hd = (layer, h)
-            kb = torch.empty(L + self.T, D, dtype=torch.bfloat16)
-            vb = torch.empty(L + self.T, D, dtype=torch.bfloat16)
+            kb = torch.empty(L + self.T, D, dtype=torch.float32)  # bf16 values, exact
+            vb = torch.empty(L + self.T, D, dtype=torch.float32)
             kb[:L], vb[:L] = k[h], v[h]
             self.K[hd], self.V[hd] = kb, vb
-            kf = k[h].float()
+            kf = kb[:L]
             acc = torch.zeros(L, dtype=torch.float32)
             for i in range(w):  # query i sits at prompt position L - w + i (causal)
                 lim = L - w + i + 1
@@ -93,9 +98,9 @@ class CpuDecoder:
             row = (acc / (w * G)).numpy()
             self.rows0[hd] = row
             if hd in self.comp:
-                self.dynamic[hd] = O.top_k_dense(row, self.eff_len(hd))
+                self.dynamic[hd] = O.top_k_dense_select(row, self.eff_len(hd))
             elif hd in self.pivots and self.monitor:
-                self.k_base[hd] = O.top_k_dense(row, self.l_base)
+                self.k_base[hd] = O.top_k_dense_select(row, self.l_base)
                 self.buffers[hd] = []
 
     # ---- decode (engine.py:290-370) ---------------------------------------------
@@ -105,9 +110,49 @@ class CpuDecoder:
         if hd in self.full:
             return None
         L = self.L
-        extra = np.concatenate([np.arange(min(self.S, L)), np.arange(max(0, L + t - self.R), L),
-                                np.arange(L, L + t)]).astype(np.int64)
-        return np.union1d(self.dynamic[hd].astype(np.int64), extra)
+        dyn, r0 = self.dynamic[hd], min(L, max(0, L + t - self.R))
+        base = self._base.get(hd)
+        if base is None or base[0] is not dyn or base[1] != r0:
+            # dynamic | sinks | recency tail below L (union1d sorts); a fetched set
+            # may hold decode positions >= L, which the appends [L, L + t) cover
+            extra = np.concatenate([np.arange(min(self.S, L)), np.arange(r0, L)]).astype(np.int64)
+            d64 = dyn.astype(np.int64)
+            base = (dyn, r0, np.union1d(d64[d64 < L], extra))
+            self._base[hd] = base
+        return np.concatenate([base[2], np.arange(L, L + t, dtype=np.int64)])  # decode appends
+
+    def resident_kv(self, hd, t):
+        """K, V rows of head hd's resident set at step t, in position order (views).
+
+        Full heads: the cache prefix.  Compressed heads: the rows below L (dynamic |
+        sinks | recency tail) gathered once per change of that set into a per-head
+        buffer, then the decode appends [L, L + t) -- the same rows in the same
+        order as indexing the cache with resident(hd, t)."""
+        L = self.L
+        if hd in self.full:
+            return self.K[hd][:L + t], self.V[hd][:L + t]
+        dyn, r0 = self.dynamic[hd], min(L, max(0, L + t - self.R))
+        g = self._gath.get(hd)
+        if g is None or g[0] is not dyn or g[1] != r0:
+            self.resident(hd, t)  # (re)computes the sorted positions below L
+            base = self._base[hd][2]
+            n0 = base.size
+            kb = torch.empty(n0 + self.T, self.D, dtype=torch.float32)
+            vb = torch.empty(n0 + self.T, self.D, dtype=torch.float32)
+            ix = torch.from_numpy(base)
+            torch.index_select(self.K[hd], 0, ix, out=kb[:n0])
+            torch.index_select(self.V[hd], 0, ix, out=vb[:n0])
+            kb[n0:n0 + t] = self.K[hd][L:L + t]
+            vb[n0:n0 + t] = self.V[hd][L:L + t]
+            g = (dyn, r0, kb, vb, n0, t)
+        else:
+            n0, kb, vb = g[4], g[2], g[3]
+            if g[5] < t:  # the appends since the buffer was last used
+                kb[n0 + g[5]:n0 + t] = self.K[hd][L + g[5]:L + t]
+                vb[n0 + g[5]:n0 + t] = self.V[hd][L + g[5]:L + t]
+            g = (dyn, r0, kb, vb, n0, t)
+        self._gath[hd] = g
+        return kb[:n0 + t], vb[:n0 + t]
 
     def step(self, t: int, q, k_new, v_new):
         """q [NL, H*G, D], k_new / v_new [NL, H, D] (bf16).  Returns (O [NL, H*G, D]
@@ -125,13 +170,7 @@ class CpuDecoder:
                 self.K[hd][L + t - 1] = k_new[l, h]
                 self.V[hd][L + t - 1] = v_new[l, h]
                 qh = q[l, h * G:(h + 1) * G].float()
-                pos = self.resident(hd, t)
-                if pos is None:
-                    kk, vv = self.K[hd][:L + t].float(), self.V[hd][:L + t].float()
-                else:
-                    ix = torch.from_numpy(pos)
-                    kk = self.K[hd].index_select(0, ix).float()
-                    vv = self.V[hd].index_select(0, ix).float()
+                kk, vv = self.resident_kv(hd, t)
                 s = (qh @ kk.T) * (1.0 / math.sqrt(self.D))
                 s = s - s.max(dim=-1, keepdim=True).values
                 e = torch.exp(s)
@@ -148,7 +187,7 @@ class CpuDecoder:
         if self.monitor:
             cur = {}
             for pv in self.pivots:
-                cur[pv] = O.top_k_dense(rows[pv], self.l_base)
+                cur[pv] = O.top_k_dense_select(rows[pv], self.l_base)
                 self.buffers[pv].append(
                     np.intersect1d(cur[pv], self.k_base[pv], assume_unique=True).size / self.l_base)
             if t % self.W == 0:
@@ -158,7 +197,7 @@ class CpuDecoder:
                         flag = 1
                         fetches, n_ent = [], 0
                         for s in self.sats_of[pv]:  # engine.py:326-329
-                            got = O.top_k_dense(rows[pv], min(self.eff_len(s), L + t))
+                            got = O.top_k_dense_select(rows[pv], min(self.eff_len(s), L + t))
                             fetches.append((s, tuple(int(x) for x in got)))
                             n_ent += len(got)
                         nbytes = n_ent * self.bpe

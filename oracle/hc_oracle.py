@@ -75,6 +75,27 @@ def top_k_dense(weights, k: int, pool_kernel: int = 0) -> np.ndarray:
     return np.sort(order[:k]).astype(np.uint32)
 
 
+def top_k_dense_select(weights, k: int) -> np.ndarray:
+    """top_k_dense(weights, k) (no pooling) in O(n): the k-th largest value by
+    partition, every value above it, then the tied values in position order --
+    the same set as the lexsort order (value desc, position asc), sorted.
+    Rows holding NaN take the lexsort path."""
+    w = np.asarray(weights, dtype=np.float64)
+    n = w.size
+    if k <= 0:
+        return np.zeros(0, dtype=np.uint32)
+    if k >= n:
+        return np.arange(n, dtype=np.uint32)
+    if np.isnan(w).any():
+        return top_k_dense(w, k)
+    thr = np.partition(w, n - k)[n - k]
+    above = np.flatnonzero(w > thr)
+    ties = np.flatnonzero(w == thr)
+    sel = np.concatenate([above, ties[:k - above.size]])
+    sel.sort()
+    return sel.astype(np.uint32)
+
+
 def overlap_coefficient(a, b) -> float:
     """metrics.py:74-79 -- |A&B| / min(|A|,|B|)."""
     sa, sb = set(int(x) for x in a), set(int(x) for x in b)

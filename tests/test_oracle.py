@@ -146,3 +146,25 @@ def test_oracle_static_policies_match_reference_run_policy():
         assert got["events"] == list(exp["events"]) and got["policy"] == exp["policy"]
         n += 1
     assert n >= 50
+
+
+def test_top_k_dense_select_matches_lexsort_order():
+    """The O(n) selection the CPU decoder uses gives top_k_dense's exact output:
+    random rows, rows with heavy ties at the k-th value, signed zeros, k at the
+    edges, NaN rows (lexsort path)."""
+    rng = np.random.default_rng(7)
+    cases = []
+    for n in (1, 2, 17, 1000, 4099):
+        cases.append(rng.random(n, dtype=np.float32))
+        cases.append(rng.integers(0, 5, n).astype(np.float32))  # few distinct values
+        z = np.zeros(n, dtype=np.float32)
+        z[::3] = -0.0
+        z[::5] = 1.0
+        cases.append(z)
+        x = rng.random(n).astype(np.float32)
+        x[rng.integers(0, n, max(1, n // 7))] = np.nan
+        cases.append(x)
+    for w in cases:
+        n = w.size
+        for k in sorted({0, 1, 2, n // 3, n // 2, n - 1, n, n + 3}):
+            assert np.array_equal(O.top_k_dense_select(w, k), O.top_k_dense(w, k)), (n, k)
