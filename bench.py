@@ -83,6 +83,9 @@ def parse(argv=None):
     ap.add_argument("--cpu-seqs", type=int, default=1,
                     help="sequences the CPU decoder samples (cpu_baseline, parity, reference)")
     ap.add_argument("--chunk", type=int, default=1024)
+    ap.add_argument("--l2", choices=("auto", "flush", "none"), default="auto",
+                    help="flush L2 between timed steps (auto: when a step's resident K/V "
+                         "would fit in 4x L2), timing each step on its own")
     ap.add_argument("--start-step", type=int, default=0,
                     help="decode this many steps untimed before warm-up (e.g. cfg4 at t = 8K)")
     ap.add_argument("--policy", choices=("heterocache", "full", "static_topk", "sink_window"),
@@ -303,6 +306,19 @@ def layer_mixes(roles: dict, NL: int, H: int) -> dict:
     return mixes
 
 
+L2_BYTES = 126 << 20  # B200 L2
+
+
+def l2_flush(args, w, rho: float, world: int) -> bool:
+    """Whether the timed steps run with an L2 flush between them: a step whose
+    resident K/V (about rho of the full context at 512 B per token and KV head)
+    fits in 4x L2 would otherwise be served from L2 on every step."""
+    if args.l2 == "none" or world > 1:
+        return False
+    est = w.batch * w.num_layers * w.model.kv_heads * w.prefill_len * 512 * rho
+    return args.l2 == "flush" or est < 4 * L2_BYTES
+
+
 def make_config(args, w, cfg, rho, l_base_int, roles: dict, world: int, mode: str) -> dict:
     """The `config` object of both arms' lines (identical for the same run)."""
     from paper_2601_13684_b200.workload import DRIFT_PERIOD
@@ -332,7 +348,10 @@ def make_config(args, w, cfg, rho, l_base_int, roles: dict, world: int, mode: st
         "transfer_bandwidth_bytes_per_step": cfg.transfer_bandwidth,
         "score_material": args.score_material,
         "decisions": args.decisions,
-        "l2": "inputs larger than L2 (resident K/V per step >> 126 MB)",
+        "l2": (f"flushed between timed steps ({2 * L2_BYTES >> 20} MB written; each step "
+               f"timed on its own, start to end of its monitor, flush excluded)"
+               if l2_flush(args, w, rho, world) else
+               "inputs larger than L2 (resident K/V per step >> 126 MB)"),
         "parallelism": par,
     }
 
@@ -517,15 +536,20 @@ def run_b200(args, rank, world):
         torch.cuda.nvtx.range_push("timed")  # ncu --nvtx-include "timed/" selects loop A
         ev0.record(stream)
         lo = t
-        for _ in range(n):
+        for i in range(n):
             t += 1
+            if flush:
+                flush_l2(i)
             dec.decode_step(t, *inputs(t), par_out if t == t_par else out, rows=False)
+            if flush:
+                dec.join()
+                fe[i].record(stream)
         dec.join()  # the last step's monitor runs on the engine's side stream
         ev1.record(stream)
         torch.cuda.nvtx.range_pop()
         torch.cuda.synchronize()
         barrier()
-        return (ev0.elapsed_time(ev1), lib.hc_launch_count() - l0,
+        return (flushed_ms(n) if flush else ev0.elapsed_time(ev1), lib.hc_launch_count() - l0,
                 dec.kernel_timing(True, light=True), dec.retrieval_stats(), (lo, t))
 
     def loop_b(n):
@@ -540,8 +564,13 @@ def run_b200(args, rank, world):
             # inputs H2D and O D2H on the engine's copy streams, one call per step
             for i in range(n):
                 t += 1
+                if flush:
+                    flush_l2(i)
                 dec.decode_step_host(t, hq_all[t - t_start - 1], *hkv[t % 4],
                                      hout_par if t == t_par else hout[i % 2], rows=False)
+                if flush:
+                    dec.join()
+                    fe[i].record(stream)
             n_py = 0
         else:
             n_py = n
@@ -566,7 +595,23 @@ def run_b200(args, rank, world):
         ev1.record(stream)
         torch.cuda.synchronize()
         barrier()
-        return ev0.elapsed_time(ev1)
+        return flushed_ms(n) if flush and n_py == 0 else ev0.elapsed_time(ev1)
+
+    # L2 flush between timed steps (small configurations): a 252 MB write, then the
+    # step between two events -- its time excludes the flush
+    flush = l2_flush(args, w, plan.rho, world) and (world == 1 and dec.devdec)
+    if l2_flush(args, w, plan.rho, world) and not flush:
+        raise SystemExit("--l2 flush needs one GPU and device decisions")
+    l2buf = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device="cuda") if flush else None
+    fs = [torch.cuda.Event(enable_timing=True) for _ in range(K)] if flush else []
+    fe = [torch.cuda.Event(enable_timing=True) for _ in range(K)] if flush else []
+
+    def flush_l2(i):
+        l2buf.fill_(i & 0xff)
+        fs[i].record(stream)
+
+    def flushed_ms(n):
+        return sum(a.elapsed_time(b) for a, b in zip(fs[:n], fe[:n]))
 
     clocks = ClockSampler(torch.cuda.current_device())
     if not os.environ.get("HC_BENCH_NO_CLOCKS"):

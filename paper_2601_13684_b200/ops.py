@@ -63,7 +63,7 @@ def topk_rows(idx, scores, k, base_bitmaps=None):
     R, K = sc.shape
     ix = None
     if idx is not None:
-        ix = torch.as_tensor(np.ascontiguousarray(idx, dtype=np.uint32).view(np.int32)).cuda()
+        ix = torch.from_numpy(np.array(idx, dtype=np.uint32, order="C").view(np.int32)).cuda()
     ks = np.broadcast_to(np.asarray(k, dtype=np.int64), (R,))
     kmax = int(max(1, ks.max())) if R else 1
     out = torch.zeros((R, kmax), dtype=torch.int32, device="cuda")
@@ -71,7 +71,8 @@ def topk_rows(idx, scores, k, base_bitmaps=None):
     ovl = torch.zeros(R, dtype=torch.int32, device="cuda")
     bm = None
     if base_bitmaps is not None:
-        bm = torch.as_tensor(np.ascontiguousarray(base_bitmaps, dtype=np.uint32).view(np.int32)).cuda()
+        bm = torch.from_numpy(np.array(base_bitmaps, dtype=np.uint32, order="C")
+                              .view(np.int32)).cuda()
     jobs = np.zeros(R, dtype=TOPK_JOB_DTYPE)
     row_bytes = K * 4
     jobs["scores"] = _lib.ptr(sc) + np.arange(R, dtype=np.uint64) * row_bytes
