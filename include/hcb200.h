@@ -251,10 +251,13 @@ int hc_engine_decode_step(hc_engine* eng, int32_t step, const void* q_dev, const
 
 /* decode_step from pinned HOST buffers (a serving runtime's per-step call):
  * q_host / o_host [B, NL, H*G, 128] and k_new_host / v_new_host [B, NL, H, 128]
- * bf16.  The inputs cross H2D and the output D2H on an engine-owned copy
- * stream, double-buffered by step parity so they overlap the neighbouring
- * steps' decode; o_host holds the step's output once `stream` has passed
- * hc_engine_join. */
+ * bf16, page-locked (cudaHostAlloc / cudaHostRegister).  Steps moving more
+ * than 512 KB cross H2D and D2H on engine-owned copy streams, double-buffered
+ * by step parity so they overlap the neighbouring steps' decode; smaller
+ * steps (launch-bound) read their inputs with one zero-copy kernel on
+ * `stream` and the combine writes O straight into o_host.  Either way o_host
+ * holds the step's output once `stream` has passed hc_engine_join.  The
+ * caller must not rewrite the input buffers before then. */
 int hc_engine_decode_step_host(hc_engine* eng, int32_t step, const void* q_host,
                                const void* k_new_host, const void* v_new_host, void* o_host,
                                void* stream);
