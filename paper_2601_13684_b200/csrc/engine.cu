@@ -859,8 +859,7 @@ int engine_create(EngineImpl& e, const hc_engine_desc& c, const int32_t* roles,
   HC_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
   HC_CUDA_TRY(cudaStreamCreateWithPriority(&e.retr, cudaStreamNonBlocking, hi_prio));
   HC_CUDA_TRY(cudaStreamCreateWithPriority(&e.side, cudaStreamNonBlocking, hi_prio));
-  HC_CUDA_TRY(cudaStreamCreateWithPriority(&e.mon, cudaStreamNonBlocking,
-                                           getenv("HC_MON_PRIO_LO") ? lo_prio : hi_prio));
+  HC_CUDA_TRY(cudaStreamCreateWithPriority(&e.mon, cudaStreamNonBlocking, hi_prio));
   if (c.device_decisions) HC_TRY(devdec_create(e, c));
   return host_io_init(e);  // decode_step_host staging, outside any timed step
 }
