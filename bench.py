@@ -257,11 +257,20 @@ def schedule(args, w):
     from paper_2601_13684_b200.workload import staggered_shifts
 
     K, W, S0 = args.steps, args.warmup, args.start_step
-    shifts = staggered_shifts(w.batch, w.num_layers, S0 + W + 1, 2 * K + 8, w.shift_every)
+    Z = settle_steps(w)
+    shifts = staggered_shifts(w.batch, w.num_layers, S0 + W + 1, Z + 2 * K + 8, w.shift_every)
     if S0:  # the fast-forward drifts too
         pre = staggered_shifts(w.batch, w.num_layers, 1, S0 + W, w.shift_every)
         shifts = {key: pre[key] + shifts[key] for key in shifts}
-    return shifts, S0 + W + 2 * K + 8 + phase_steps(args)
+    return shifts, S0 + W + Z + 2 * K + 8 + phase_steps(args)
+
+
+def settle_steps(w) -> int:
+    """Untimed steps after the warm-up with the drift schedule already running, for
+    workloads that drift every few steps (cfg4): eight drift periods, so the timed
+    region starts in the steady state of fires, gathers and landings rather than
+    at the schedule's first burst.  0 for the one-shift-per-run workloads."""
+    return 8 * w.shift_every if 0 < w.shift_every <= 32 else 0
 
 
 def phase_steps(args) -> int:
@@ -345,6 +354,7 @@ def make_config(args, w, cfg, rho, l_base_int, roles: dict, world: int, mode: st
         "topic_shifts": (f"every cluster (sequence, layer) once per "
                          f"{w.shift_every or DRIFT_PERIOD} steps, staggered phases"),
         "split_k_chunk": args.chunk, "start_step": args.start_step,
+        "settle_steps": settle_steps(w),
         "transfer_bandwidth_bytes_per_step": cfg.transfer_bandwidth,
         "score_material": args.score_material,
         "decisions": args.decisions,
@@ -458,7 +468,7 @@ def run_b200(args, rank, world):
     t_par = min(S0 + W + K, PARITY_STEP) if S0 == 0 else -1
     stream = torch.cuda.current_stream()
     t = 0
-    for _ in range(S0 + W):
+    for _ in range(S0 + W + settle_steps(w)):  # warm-up (+ the drift schedule's first periods)
         t += 1
         dec.decode_step(t, *inputs(t), par_out if t == t_par else out, rows=False)
     torch.cuda.synchronize()
