@@ -300,6 +300,14 @@ def shard_mode(args, w, world: int) -> str:
     return mode
 
 
+def scaling_of(args, mode: str) -> str:
+    """strong: one batch whatever N (N=1 included, unless --shard sequences asks
+    for a batch per rank); weak: every rank decodes its own batch."""
+    if mode == "sequences" or (mode == "replicas" and args.shard == "sequences"):
+        return "weak"
+    return "strong"
+
+
 def calib_spec(args):
     from paper_2601_13684_b200.calibration import CalibSpec
 
@@ -333,7 +341,8 @@ def make_config(args, w, cfg, rho, l_base_int, roles: dict, world: int, mode: st
     from paper_2601_13684_b200.workload import DRIFT_PERIOD
 
     m = w.model
-    par = {"replicas": f"replicas x{world} (weak: each GPU decodes its own batch)",
+    par = {"replicas": "one GPU: the whole batch (the N=1 point of the batch-sharded series: "
+                       "--gpus N splits this batch's sequences over N ranks)",
            "sequences": f"sequences x{world} (weak: each GPU decodes its own batch)",
            "batch": f"batch x{world} (strong: rank r decodes sequences [r*B/N, (r+1)*B/N) of "
                     f"one batch, decisions on its device, no exchange; O all-gathered in place)",
@@ -725,7 +734,7 @@ def run_b200(args, rank, world):
         "warmup": W,
         "ms_per_step": ms / K,
         "higher_is_better": True,
-        "scaling": "weak" if mode in ("replicas", "sequences") else "strong",
+        "scaling": scaling_of(args, mode),
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic: counter-generated bf16 K/V/Q with planted per-cluster hot sets "
@@ -965,7 +974,7 @@ def run_reference(args, world):
         "impl": "reference", "metric": METRIC, "value": v, "unit": "steps/s",
         "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": per_step * 1e3, "higher_is_better": True,
-        "scaling": "weak" if world == 1 else "strong",
+        "scaling": scaling_of(args, shard_mode(args, w, world)),
         "vs_baseline": None, "dtype": "fp32",
         "data": "synthetic: counter-generated bf16 K/V/Q with planted per-cluster hot sets "
                 "and topic shifts (random-init shapes; no checkpoint)",
