@@ -492,6 +492,8 @@ int devdec_create(EngineImpl& e, const hc_engine_desc& c) {
       sats.push_back(x);
       e.dd_sat_units.push_back(u);
     }
+    HC_REQUIRE(int(sats.size()) - psb.back() <= 8, HC_EINVAL,
+               "device decisions: a pivot with more than 8 satellites (use host decisions)");
     psb.push_back(int32_t(sats.size()));
   }
   for (int b = 0; b < e.B; ++b) seq_piv[b + 1] += seq_piv[b];

@@ -158,11 +158,12 @@ class HeteroCacheDecoder:
         for p, sats in self.satellites_of.items():
             for s in sats:
                 cpiv[s[0] * self.H + s[1]] = p[1]
+        most_sats = max((len(s) for s in self.satellites_of.values()), default=0)
         ok_dev = (self.monitor and owned is None and not recall_topk and config.window <= 64
-                  and len(plan.lengths) > 0)
+                  and len(plan.lengths) > 0 and most_sats <= 8)
         if device_decisions and not ok_dev:
             raise EngineError("device decisions need monitored pivots, an unsharded engine, "
-                              "no measure mode and window <= 64")
+                              "no measure mode, window <= 64 and at most 8 satellites per pivot")
         self.devdec = ok_dev if device_decisions is None else bool(device_decisions)
         desc = _lib.EngineDesc(batch=batch, num_layers=self.NL, kv_heads=self.H, group=group,
                                head_dim=head_dim, prefill_len=self.L, max_decode=max_decode,

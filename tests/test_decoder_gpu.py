@@ -475,3 +475,42 @@ def test_device_decisions_long_run_ring_wraps(nq, monkeypatch):
     fired = _check_events(ctx, rows)
     assert fired >= 60
     ctx["dec"].close()
+
+
+def test_more_than_eight_satellites_take_host_decisions():
+    """The device decision log holds up to 8 satellites per pivot: a cluster of 10
+    makes the decoder take its decisions on the host (auto), asking for device
+    decisions explicitly is an error, and the host path still decodes."""
+    import torch
+
+    from paper_2601_13684_b200.budget import BudgetConfig, plan_budget
+    from paper_2601_13684_b200.decoder import EngineError, HeteroCacheDecoder
+    from paper_2601_13684_b200.engine import EngineConfig
+    from paper_2601_13684_b200.profiling import taxonomy_from_roles
+
+    H, L, T = 12, 600, 12
+    roles = {(0, 0): "pivot", (0, 11): "anchor"}
+    roles.update({(0, h): "satellite" for h in range(1, 11)})
+    tax = taxonomy_from_roles(roles, [((0, 0), [(0, h) for h in range(1, 11)])], num_layers=1,
+                              heads_per_layer=H, s_stable={hd: 0.5 for hd in roles})
+    plan = plan_budget(tax, BudgetConfig(rho=0.3, min_length=4), L)
+    cfg = EngineConfig(window=4)
+    with pytest.raises(EngineError):
+        HeteroCacheDecoder(tax, plan, cfg, batch=1, group=2, max_decode=T, chunk=128,
+                           device_decisions=True)
+    dec = HeteroCacheDecoder(tax, plan, cfg, batch=1, group=2, max_decode=T, chunk=128)
+    assert not dec.devdec
+    g = torch.Generator(device="cuda").manual_seed(5)
+
+    def rnd(*shape):
+        return torch.randn(*shape, generator=g, device="cuda").bfloat16()
+
+    dec.prefill_layer(0, rnd(1, H, L, 128), rnd(1, H, L, 128), rnd(1, 2 * H, 128))
+    dec.finish_prefill()
+    for t in range(1, T + 1):
+        q, kn, vn = rnd(1, 1, 2 * H, 128), rnd(1, 1, H, 128), rnd(1, 1, H, 128)
+        o = torch.empty_like(q)
+        dec.decode_step(t, q, kn, vn, o)
+    dec.sync()
+    assert torch.isfinite(o.float()).all()
+    dec.close()
