@@ -141,10 +141,10 @@ def read_probe(gib: int = 4) -> dict:
     nbytes = gib << 30
     buf = torch.ones(nbytes // 4, dtype=torch.int32, device="cuda")
     sm = torch.cuda.get_device_properties(0).multi_processor_count
-    sink = torch.empty(sm * 16, dtype=torch.int32, device="cuda")
+    sink = torch.empty(sm * 32, dtype=torch.int32, device="cuda")
     st = torch.cuda.current_stream()
     best = {}
-    for per_sm in (4, 8, 16):
+    for per_sm in (4, 8, 16, 32):
         ms = []
         for _ in range(6):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
