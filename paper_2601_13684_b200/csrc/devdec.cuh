@@ -105,6 +105,7 @@ struct DevDec {
   int32_t* scnt;           // [n_piv]
   // per-boundary work lists (written by decide)
   FireJob* jobs;           // [n_sat]
+  int32_t* bump;           // [n_sat] the satellite of each job (its ring tail advances)
   uint32_t* n_jobs;
   int32_t* restamp_slots;  // [n_piv]
   uint32_t* n_restamp;

@@ -528,6 +528,7 @@ int devdec_create(EngineImpl& e, const hc_engine_desc& c) {
   d.svals = static_cast<double*>(dev(size_t(e.n_piv) * 64 * 8));
   d.scnt = static_cast<int32_t*>(dev(size_t(e.n_piv) * 4));
   d.jobs = static_cast<FireJob*>(dev(ns * sizeof(FireJob)));
+  d.bump = static_cast<int32_t*>(dev(ns * 4));
   d.n_jobs = static_cast<uint32_t*>(dev(4));
   d.restamp_slots = static_cast<int32_t*>(dev(size_t(e.n_piv) * 4));
   d.n_restamp = static_cast<uint32_t*>(dev(4));
@@ -540,7 +541,7 @@ int devdec_create(EngineImpl& e, const hc_engine_desc& c) {
   d.log_dev = static_cast<FireLog*>(dev(sizeof(FireLog) * kLogRing * std::max(1, e.n_piv)));
   HC_CUDA_TRY(cudaGetLastError());
   HC_REQUIRE(d.seq_piv && d.piv_sat_begin && d.piv_unit && d.sats && d.xfers && d.cum &&
-                 d.order && d.svals && d.scnt && d.jobs && d.n_jobs && d.restamp_slots &&
+                 d.order && d.svals && d.scnt && d.jobs && d.bump && d.n_jobs && d.restamp_slots &&
                  d.n_restamp && d.glist && d.glist2 && d.n_glist && d.urgent_epoch &&
                  d.head_dev && d.hdr_dev && d.log_dev,
              HC_ENOMEM, "device decisions: state");
