@@ -35,6 +35,24 @@ def _run(args, timeout=900, ranks=1, **env_kw):
     return json.loads(lines[0])
 
 
+def test_timing_protocol_per_workload():
+    """L2 flush only where a step's K/V fits in L2 (cfg1); settle steps only for the
+    frequently drifting workload (cfg4); both enter the config both arms print."""
+    sys.path.insert(0, str(ROOT))
+    import bench
+
+    args = bench.parse(["--workload", "cfg1"])
+    flush = {}
+    for name in ("cfg1", "cfg2", "cfg3", "cfg4", "cfg5"):
+        w = bench.workload_of(bench.parse(["--workload", name]))
+        from paper_2601_13684_b200.workload import rho_for
+
+        flush[name] = bench.l2_flush(args, w, rho_for(w.model, w.compression), 1)
+        assert bench.settle_steps(w) == (96 if name == "cfg4" else 0)
+        assert not bench.l2_flush(args, w, rho_for(w.model, w.compression), 2)
+    assert flush == {"cfg1": True, "cfg2": False, "cfg3": False, "cfg4": False, "cfg5": False}
+
+
 def test_reference_arm_runs_on_the_host():
     d = _run(["--impl", "reference", "--workload", "cfg1", "--steps", "2", "--warmup", "3"])
     assert d["impl"] == "reference" and d["value"] > 0
@@ -51,6 +69,8 @@ def test_b200_arm_full_line_with_cpu_baseline_and_parity():
     assert d["cpu_baseline"]["value"] > 0 and d["roofline"]["bound"] == "hbm"
     p = d["parity"]
     assert p["within_tolerance"] and p["events_identical"] and p["step"] == 15
+    assert d["config"]["l2"].startswith("flushed")  # cfg1's K/V fits in L2
+    assert d["roofline"]["read_only_peak_gbs"] > 1000 and d["phase_block"]["steps"] == 12
     ref = _run(["--impl", "reference"] + args)
     assert ref["config"] == d["config"]  # both arms run the same workload
 
