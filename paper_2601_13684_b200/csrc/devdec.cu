@@ -47,12 +47,19 @@ __device__ double median_of(double* v, int n) {
 
 constexpr int kMaxPiv = 8192;
 
+// The decision chain's kernels are small and latency-bound and run while K4
+// holds two CTAs (2 x 160 threads x 168 registers, 2 x 97 KB of shared memory)
+// on every SM.  Sized to fit beside them (256 threads, <= 42 registers, <= 24 KB
+// of shared memory), they start at once instead of waiting for a K4 CTA to retire.
+constexpr int kChainThreads = 256;
+constexpr int kChainMinBlocks = 6;  // 65536 / (256 * 6) -> at most 42 registers
+
 // One CTA.  Boundary mode: the window's values are overlap ring rows first ..
 // first + nvals - 1.  Sliding mode (eval_every_step): this step's value joins
 // the pivot's buffer; the test runs once it holds >= window values and clears
 // it on a fire (engine.py:313-321, 358-360).  Then, per sequence in order and
 // per pivot in sorted order (engine.py:313), the fires' accounting.
-__global__ void __launch_bounds__(1024) decide_kernel(DevDec d, int t, int first, int nvals,
+__global__ void __launch_bounds__(kChainThreads, kChainMinBlocks) decide_kernel(DevDec d, int t, int first, int nvals,
                                                       int bidx, const uint32_t* __restrict__ ovl,
                                                       int ring) {
   __shared__ uint8_t fired[kMaxPiv];
@@ -192,7 +199,7 @@ __global__ void __launch_bounds__(1024) decide_kernel(DevDec d, int t, int first
 // completion step.  Marks them SCHEDULED (target buffer chosen); the
 // retrieval stream's next build pass picks them up.  One CTA, a thread per
 // satellite.
-__global__ void __launch_bounds__(1024) schedule_kernel(DevDec d, int t_now) {
+__global__ void __launch_bounds__(kChainThreads, kChainMinBlocks) schedule_kernel(DevDec d, int t_now) {
   __shared__ int urgent;
   if (threadIdx.x == 0) urgent = 0;
   __syncthreads();
@@ -240,7 +247,7 @@ __global__ void __launch_bounds__(1024) schedule_kernel(DevDec d, int t_now) {
 // staging buffer's) gets its prefix position list if it has none yet and joins
 // this pass's list -- new ones and the remainder of ones a preempted pass left
 // (the list belongs to the retrieval stream: passes never overlap).
-__global__ void __launch_bounds__(256) build_dev_kernel(DevDec d, int t_max) {
+__global__ void __launch_bounds__(kChainThreads, kChainMinBlocks) build_dev_kernel(DevDec d, int t_max) {
   const int si = blockIdx.x;
   DevSat& sat = d.sats[si];
   __shared__ int64_t s_i;
@@ -277,7 +284,7 @@ __global__ void __launch_bounds__(256) build_dev_kernel(DevDec d, int t_max) {
 
 // Earliest deadline first: rank sort of the pass's list by (completion,
 // sequence, order) into glist2.
-__global__ void __launch_bounds__(1024) order_kernel(DevDec d) {
+__global__ void __launch_bounds__(kChainThreads, kChainMinBlocks) order_kernel(DevDec d) {
   const uint32_t n = *d.n_glist;
   for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
     const GatherItem a = d.glist[i];
@@ -304,7 +311,7 @@ __global__ void __launch_bounds__(1024) order_kernel(DevDec d) {
 // completing a transfer's last chunk flags it GATHERED.
 constexpr int kChunkRows = 256;
 
-__global__ void __launch_bounds__(256) gather_dev_kernel(DevDec d, uint4* __restrict__ K,
+__global__ void __launch_bounds__(kChainThreads, kChainMinBlocks) gather_dev_kernel(DevDec d, uint4* __restrict__ K,
                                                          uint4* __restrict__ V) {
   const uint32_t n = *d.n_glist;
   __shared__ uint32_t s_epoch, s_c;
@@ -366,7 +373,7 @@ __device__ void land_one(const DevDec& d, DevSat& sat, DevXfer& x, int64_t idx, 
 
 // Landing point of step t (engine.py:293-299).  One small CTA (it runs beside
 // the step's main attention), a thread per satellite.
-__global__ void __launch_bounds__(256) land_kernel(DevDec d, int t, UnitDesc* units,
+__global__ void __launch_bounds__(kChainThreads, kChainMinBlocks) land_kernel(DevDec d, int t, UnitDesc* units,
                                                     uint4* __restrict__ K,
                                                     uint4* __restrict__ V) {
   __shared__ int32_t inl_sat[2048];
@@ -487,13 +494,13 @@ int launch_decide(const DevDec& d, int t, int first, int nvals, int bidx, const 
                   int ring, cudaStream_t st) {
   HC_REQUIRE(nvals <= 64 && d.window <= 64, HC_EINVAL, "decision window > 64");
   HC_REQUIRE(d.n_piv <= kMaxPiv, HC_EINVAL, "more than %d monitored pivots", kMaxPiv);
-  decide_kernel<<<1, 1024, 0, st>>>(d, t, first, nvals, bidx, ovl_ring, ring);
+  decide_kernel<<<1, kChainThreads, 0, st>>>(d, t, first, nvals, bidx, ovl_ring, ring);
   HC_CHECK_LAUNCH();
   return HC_OK;
 }
 
 int launch_schedule(const DevDec& d, int t_now, cudaStream_t st) {
-  schedule_kernel<<<1, 1024, 0, st>>>(d, t_now);
+  schedule_kernel<<<1, kChainThreads, 0, st>>>(d, t_now);
   HC_CHECK_LAUNCH();
   return HC_OK;
 }
@@ -501,19 +508,19 @@ int launch_schedule(const DevDec& d, int t_now, cudaStream_t st) {
 int launch_dev_gathers(const DevDec& d, uint4* K, uint4* V, cudaStream_t st, int t_max,
                        cudaEvent_t g0, cudaEvent_t g1) {
   HC_CUDA_TRY(cudaMemsetAsync(d.n_glist, 0, 4, st));
-  build_dev_kernel<<<std::max(1, d.n_sat), 256, 0, st>>>(d, t_max);
+  build_dev_kernel<<<std::max(1, d.n_sat), kChainThreads, 0, st>>>(d, t_max);
   HC_CHECK_LAUNCH();
-  order_kernel<<<1, 1024, 0, st>>>(d);
+  order_kernel<<<1, kChainThreads, 0, st>>>(d);
   HC_CHECK_LAUNCH();
   if (g0) HC_CUDA_TRY(cudaEventRecord(g0, st));
-  gather_dev_kernel<<<40, 256, 0, st>>>(d, K, V);
+  gather_dev_kernel<<<40, kChainThreads, 0, st>>>(d, K, V);
   if (g1) HC_CUDA_TRY(cudaEventRecord(g1, st));
   HC_CHECK_LAUNCH();
   return HC_OK;
 }
 
 int launch_land(const DevDec& d, int t, UnitDesc* units, uint4* K, uint4* V, cudaStream_t st) {
-  land_kernel<<<1, 256, 0, st>>>(d, t, units, K, V);
+  land_kernel<<<1, kChainThreads, 0, st>>>(d, t, units, K, V);
   HC_CHECK_LAUNCH();
   return HC_OK;
 }

@@ -1,0 +1,13 @@
+timeout 900 python -m pytest tests/test_decoder_gpu.py -x -q 2>&1 | tail -1
+run() { # tag lib workload
+  HCB200_LIB=$2 HC_NO_READ_PROBE=1 timeout 900 python bench.py --workload $3 --steps 300 --warmup 5 --secondary none --no-cpu-baseline > gpurun_out/ab_$1.json 2> gpurun_out/ab_$1.err
+  python -c "import json;d=json.loads(open('gpurun_out/ab_$1.json').read().strip().splitlines()[-1]);print('$1', round(d['value'],1), round(d['e2e']['value'],1), round(d['retrieval']['landing_stall_ms_total'],2))"
+}
+NEW=paper_2601_13684_b200/libhcb200.so; OLD=paper_2601_13684_b200/libhcb200_old.so
+for rep in 1 2; do
+  for w in cfg2 cfg4; do
+    run ${w}_old_$rep $OLD $w
+    run ${w}_new_$rep $NEW $w
+  done
+done
+run cfg5_new $NEW cfg5
