@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "devdec.cuh"
 #include "retrieval.cuh"
@@ -45,7 +46,56 @@ __device__ double median_of(double* v, int n) {
   return (n & 1) ? v[n / 2] : (v[n / 2 - 1] + v[n / 2]) / 2.0;
 }
 
+// The same median for n <= 16 values v_j = c_j / lb (c_j: overlap counts, lb
+// > 0): the division is monotone, so the two middle values are those of the
+// middle counts -- found by rank counting on integers held in registers --
+// and are then formed exactly as median_of forms them.
+__device__ __forceinline__ double median_counts16(const uint32_t (&c)[16], int n, double lb) {
+  uint32_t lo = 0, hi = 0;
+  const int k0 = (n - 1) / 2, k1 = n / 2;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    int r = 0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) r += (j < n && (c[j] < c[i] || (c[j] == c[i] && j < i))) ? 1 : 0;
+    if (i < n && r == k0) lo = c[i];
+    if (i < n && r == k1) hi = c[i];
+  }
+  const double vlo = double(lo) / lb, vhi = double(hi) / lb;
+  return (n & 1) ? vhi : (vlo + vhi) / 2.0;
+}
+
 constexpr int kMaxPiv = 8192;
+
+// The window test of pivot slot s at boundary t (engine.py:247-250, 313-321,
+// 358-360): median of the window's overlap / l_base_int values < tau.
+__device__ bool window_test(const DevDec& d, int s, int t, int first, int nvals,
+                            const uint32_t* __restrict__ ovl, int ring) {
+  const double lb = double(d.lbase);
+  if (!d.sliding) {
+    if (nvals <= 16) {
+      uint32_t c[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) c[j] = j < nvals ? ovl[size_t((first + j) % ring) * d.n_piv + s] : 0u;
+      return nvals > 0 && median_counts16(c, nvals, lb) < d.tau;
+    }
+    double v[64];
+    for (int j = 0; j < nvals; ++j) v[j] = double(ovl[size_t((first + j) % ring) * d.n_piv + s]) / lb;
+    return nvals > 0 && median_of(v, nvals) < d.tau;
+  }
+  int c = d.scnt[s];
+  d.svals[size_t(s) * 64 + (c % 64)] = double(ovl[size_t(t % ring) * d.n_piv + s]) / lb;
+  ++c;
+  bool f = false;
+  if (c >= d.window) {
+    double v[64];
+    for (int j = 0; j < d.window; ++j) v[j] = d.svals[size_t(s) * 64 + ((c - d.window + j) % 64)];
+    f = median_of(v, d.window) < d.tau;
+    if (f) c = 0;  // the buffer is cleared on a fire
+  }
+  d.scnt[s] = c;
+  return f;
+}
 
 // The decision chain's kernels are small and latency-bound and run while K4
 // holds two CTAs (2 x 160 threads x 168 registers, 2 x 97 KB of shared memory)
@@ -53,34 +103,44 @@ constexpr int kMaxPiv = 8192;
 // of shared memory), they start at once instead of waiting for a K4 CTA to retire.
 constexpr int kChainThreads = 256;
 constexpr int kChainMinBlocks = 6;  // 65536 / (256 * 6) -> at most 42 registers
+constexpr int kDecideThreads = 128, kDecideMinBlocks = 8;  // <= 64 registers, 8K in all
 
 // One CTA.  Boundary mode: the window's values are overlap ring rows first ..
 // first + nvals - 1.  Sliding mode (eval_every_step): this step's value joins
 // the pivot's buffer; the test runs once it holds >= window values and clears
 // it on a fire (engine.py:313-321, 358-360).  Then, per sequence in order and
 // per pivot in sorted order (engine.py:313), the fires' accounting.
-__global__ void __launch_bounds__(kChainThreads, kChainMinBlocks) decide_kernel(DevDec d, int t, int first, int nvals,
+__global__ void __launch_bounds__(kDecideThreads, kDecideMinBlocks) decide_kernel(DevDec d, int t, int first, int nvals,
                                                       int bidx, const uint32_t* __restrict__ ovl,
                                                       int ring) {
+  // The serial accounting below runs while K4 saturates HBM, where every
+  // dependent global access costs microseconds: its inputs are fetched up front
+  // (in parallel, or by loads whose latency the window tests hide) and the ring
+  // tails it advances are kept in shared memory, not re-read.
+  constexpr int kSeqSm = 256, kBumpSm = 512;
   __shared__ uint8_t fired[kMaxPiv];
-  const double lb = double(d.lbase);
-  for (int s = threadIdx.x; s < d.n_piv; s += blockDim.x) {
-    double v[64];
-    bool f = false;
-    if (!d.sliding) {
-      for (int j = 0; j < nvals; ++j) v[j] = double(ovl[size_t((first + j) % ring) * d.n_piv + s]) / lb;
-      f = nvals > 0 && median_of(v, nvals) < d.tau;
-    } else {
-      int c = d.scnt[s];
-      d.svals[size_t(s) * 64 + (c % 64)] = double(ovl[size_t(t % ring) * d.n_piv + s]) / lb;
-      ++c;
-      if (c >= d.window) {
-        for (int j = 0; j < d.window; ++j) v[j] = d.svals[size_t(s) * 64 + ((c - d.window + j) % 64)];
-        f = median_of(v, d.window) < d.tau;
-        if (f) c = 0;  // the buffer is cleared on a fire
+  __shared__ int32_t s_seq[kSeqSm + 1], s_ord[kSeqSm];
+  __shared__ int64_t s_cum[kSeqSm];
+  __shared__ int32_t s_bsat[kBumpSm];
+  __shared__ int64_t s_btail[kBumpSm];
+  int64_t host_tail = 0, head = 0;
+  unsigned long long g0 = 0, g1 = 0;
+  if (d.dbg && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
+  if (threadIdx.x == 0) {
+    host_tail = *d.fetched_tail;  // one read over the host link
+    head = *d.head_dev;
+  }
+  const bool seq_sm = d.B <= kSeqSm;
+  if (seq_sm)
+    for (int b = threadIdx.x; b <= d.B; b += blockDim.x) {
+      s_seq[b] = d.seq_piv[b];
+      if (b < d.B) {
+        s_cum[b] = d.cum[b];
+        s_ord[b] = d.order[b];
       }
-      d.scnt[s] = c;
     }
+  for (int s = threadIdx.x; s < d.n_piv; s += blockDim.x) {
+    const bool f = window_test(d, s, t, first, nvals, ovl, ring);
     fired[s] = f ? 1 : 0;
     if (f) {  // warm this CTA's L1 with the satellites thread 0 is about to walk
       uint32_t touch = 0;
@@ -94,17 +154,17 @@ __global__ void __launch_bounds__(kChainThreads, kChainMinBlocks) decide_kernel(
   }
   __syncthreads();
   if (threadIdx.x != 0) return;
+  if (d.dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
   BoundaryHdr* hdr = d.hdr_dev + (bidx % kLogRing);
   FireLog* log = d.log_dev + size_t(bidx % kLogRing) * d.n_piv;
-  const int64_t host_tail = *d.fetched_tail;  // one read over the host link
-  int64_t head = *d.head_dev;
   const uint32_t* hist = d.ghist + size_t(t & 1) * d.n_piv * 8192;
   int n_fires = 0;
   uint32_t n_jobs = 0, n_rest = 0;
   for (int b = 0; b < d.B; ++b) {
-    int64_t cum = d.cum[b];
-    int32_t ord = d.order[b];
-    for (int s = d.seq_piv[b]; s < d.seq_piv[b + 1]; ++s) {
+    int64_t cum = seq_sm ? s_cum[b] : d.cum[b];
+    int32_t ord = seq_sm ? s_ord[b] : d.order[b];
+    const int s_end = seq_sm ? s_seq[b + 1] : d.seq_piv[b + 1];
+    for (int s = seq_sm ? s_seq[b] : d.seq_piv[b]; s < s_end; ++s) {
       if (!fired[s]) continue;
       const int a0 = d.piv_sat_begin[s], a1 = d.piv_sat_begin[s + 1];
       const int ns = a1 - a0;
@@ -141,7 +201,13 @@ __global__ void __launch_bounds__(kChainThreads, kChainMinBlocks) decide_kernel(
           atomicExch(d.error, int(kDDRingFull));
           continue;
         }
-        d.bump[n_jobs] = a0 + i;  // its tail advances once every slot is written
+        // its tail advances once every slot is written
+        if (n_jobs < uint32_t(kBumpSm)) {
+          s_bsat[n_jobs] = a0 + i;
+          s_btail[n_jobs] = idx + 1;
+        } else {
+          d.bump[n_jobs] = a0 + i;
+        }
         DevXfer& x = xf(d, a0 + i, idx);
         const int slot = int(idx % d.nq);
         x.completion = completion;
@@ -178,13 +244,16 @@ __global__ void __launch_bounds__(kChainThreads, kChainMinBlocks) decide_kernel(
       lg.host_off = host_off;
       for (int i = 0; i < 8; ++i) lg.ks[i] = i < ns ? ks[i] : 0;
     }
-    d.cum[b] = cum;
-    d.order[b] = ord;
+    if (!seq_sm || cum != s_cum[b]) d.cum[b] = cum;
+    if (!seq_sm || ord != s_ord[b]) d.order[b] = ord;
   }
   // one fence for every slot written above, then the new tails: a schedule pass
   // running concurrently on another stream sees a slot only once it is complete
   __threadfence();
-  for (uint32_t j = 0; j < n_jobs; ++j) ++d.sats[d.bump[j]].tail;
+  for (uint32_t j = 0; j < n_jobs; ++j) {
+    if (j < uint32_t(kBumpSm)) d.sats[s_bsat[j]].tail = s_btail[j];
+    else ++d.sats[d.bump[j]].tail;
+  }
   *d.n_jobs = n_jobs;
   *d.n_restamp = n_rest;
   *d.head_dev = head;
@@ -192,6 +261,207 @@ __global__ void __launch_bounds__(kChainThreads, kChainMinBlocks) decide_kernel(
   hdr->n_fires = n_fires;
   hdr->head_after = head;
   hdr->pad = 1;
+  if (d.dbg) {
+    unsigned long long g2;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g2));
+    d.dbg[0] += g1 - g0;  // window tests (parallel part)
+    d.dbg[1] += g2 - g1;  // accounting (serial part)
+    d.dbg[2] += 1;
+  }
+}
+
+
+// The same decision for up to kFastPiv pivots and kFastSeq sequences, in four
+// phases so that no thread walks a chain of dependent global accesses while K4
+// saturates HBM: (1) per pivot, in parallel: the window test, and for a fire
+// its satellites' entry counts and ring room; (2) one thread: the per-sequence
+// accounting in sorted pivot order (engine.py:313, 330-337) over shared memory
+// only; (3) per fired pivot, in parallel: its transfer slots, fire-selection
+// jobs and log entry; (4) after one fence per thread and a barrier, the ring
+// tails.  Results equal decide_kernel's.
+constexpr int kFastPiv = 256, kFastSeq = 256;
+
+__global__ void __launch_bounds__(kDecideThreads, kDecideMinBlocks)
+decide_fast_kernel(DevDec d, int t, int first, int nvals, int bidx,
+                   const uint32_t* __restrict__ ovl, int ring) {
+  __shared__ int32_t f_a0[kFastPiv], f_nent[kFastPiv], f_comp[kFastPiv], f_ord0[kFastPiv];
+  __shared__ int32_t f_job0[kFastPiv], f_hoff[kFastPiv], f_fidx[kFastPiv];
+  __shared__ int64_t f_cum[kFastPiv];
+  __shared__ uint8_t f_fired[kFastPiv], f_ns[kFastPiv], f_full[kFastPiv];
+  __shared__ int32_t s_seq[kFastSeq + 1], s_ord[kFastSeq];
+  __shared__ int64_t s_cum[kFastSeq];
+  __shared__ uint32_t s_jobs, s_fires;
+  __shared__ int64_t s_head;
+  const int tid = threadIdx.x;
+  unsigned long long g0 = 0, g1 = 0;
+  if (d.dbg && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
+  int64_t host_tail = 0, head = 0;
+  if (tid == 0) {  // used after the window tests: their latency hides these loads
+    host_tail = *d.fetched_tail;  // one read over the host link
+    head = *d.head_dev;
+  }
+  for (int b = tid; b <= d.B; b += blockDim.x) {
+    s_seq[b] = d.seq_piv[b];
+    if (b < d.B) {
+      s_cum[b] = d.cum[b];
+      s_ord[b] = d.order[b];
+    }
+  }
+  const int Lt = d.L + t;
+  // (1) window tests; a fire's satellites: entries and ring room
+  for (int s = tid; s < d.n_piv; s += blockDim.x) {
+    const bool f = window_test(d, s, t, first, nvals, ovl, ring);
+    f_fired[s] = f ? 1 : 0;
+    if (!f) continue;
+    const int a0 = d.piv_sat_begin[s], a1 = d.piv_sat_begin[s + 1];
+    const int ns = min(a1 - a0, 8);
+    int32_t nent = 0;
+    uint32_t full = 0;
+    for (int i = 0; i < ns; ++i) {
+      const DevSat& x = d.sats[a0 + i];
+      nent += min(x.k, Lt);
+      if (x.tail - x.head >= d.nq) full |= 1u << i;
+    }
+    if (a1 - a0 > 8) atomicExch(d.error, int(kDDTooManySats));
+    f_a0[s] = a0;
+    f_ns[s] = uint8_t(a1 - a0 > 255 ? 255 : a1 - a0);
+    f_nent[s] = nent;
+    f_full[s] = uint8_t(full);
+  }
+  __syncthreads();
+  if (d.dbg && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
+  // (2) accounting, per sequence in sorted pivot order
+  if (tid == 0) {
+    uint32_t n_jobs = 0, n_fires = 0;
+    for (int b = 0; b < d.B; ++b) {
+      int64_t cum = s_cum[b];
+      int32_t ord = s_ord[b];
+      for (int s = s_seq[b]; s < s_seq[b + 1]; ++s) {
+        if (!f_fired[s]) continue;
+        const int64_t n_ent = f_nent[s];
+        cum += n_ent * d.bpe;
+        const int32_t completion = max(t + d.delay, int32_t(ceil(double(cum) / double(d.bw))));
+        int64_t h = head;
+        int64_t phys = h % d.fetched_cap;
+        if (phys + n_ent > d.fetched_cap) {  // no wrap inside a span: skip to the ring start
+          h += d.fetched_cap - phys;
+          phys = 0;
+        }
+        int32_t host_off = int32_t(phys);
+        if (h + n_ent - host_tail > d.fetched_cap || n_ent > d.fetched_cap) {
+          atomicExch(d.error, int(kDDHostRingFull));
+          host_off = -1;
+        } else {
+          head = h + n_ent;
+        }
+        const uint32_t full = f_full[s];
+        if (full) atomicExch(d.error, int(kDDRingFull));
+        const int nfree = min(int(f_ns[s]), 8) - __popc(full);
+        f_comp[s] = completion;
+        f_ord0[s] = ord;
+        f_job0[s] = int32_t(n_jobs);
+        f_hoff[s] = host_off;
+        f_fidx[s] = int32_t(n_fires);
+        f_cum[s] = cum;
+        ord += nfree;
+        n_jobs += uint32_t(nfree);
+        ++n_fires;
+      }
+      s_cum[b] = cum;
+      s_ord[b] = ord;
+    }
+    s_jobs = n_jobs;
+    s_fires = n_fires;
+    s_head = head;
+  }
+  __syncthreads();
+  // (3) slots, jobs and log entries of every fire
+  FireLog* log = d.log_dev + size_t(bidx % kLogRing) * d.n_piv;
+  const uint32_t* hist = d.ghist + size_t(t & 1) * d.n_piv * 8192;
+  for (int b = tid; b < d.B; b += blockDim.x) {
+    d.cum[b] = s_cum[b];
+    d.order[b] = s_ord[b];
+  }
+  for (int s = tid; s < d.n_piv; s += blockDim.x) {
+    if (!f_fired[s]) continue;
+    const int a0 = f_a0[s], ns = min(int(f_ns[s]), 8);
+    const uint32_t full = f_full[s];
+    const int32_t host_off = f_hoff[s];
+    int32_t ord = f_ord0[s];
+    uint32_t job = uint32_t(f_job0[s]);
+    int64_t hoff = host_off;
+    int32_t ks[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ks[i] = i < ns ? min(d.sats[a0 + i].k, Lt) : 0;
+    for (int i = 0; i < ns; ++i) {
+      if ((full >> i) & 1u) continue;
+      DevSat& sat = d.sats[a0 + i];
+      const int64_t idx = sat.tail;
+      DevXfer& x = xf(d, a0 + i, idx);
+      const int slot = int(idx % d.nq);
+      x.completion = f_comp[s];
+      x.order = ord++;
+      x.trigger = t;
+      x.k = ks[i];
+      x.buf = -1;
+      x.host_off = host_off < 0 ? -1 : int32_t(hoff);
+      x.cnt = 0;
+      x.done_chunks = 0;
+      x.next_chunk = 0;
+      x.built = 0;
+      x.state = kXAlloc;
+      FireJob& jb = d.jobs[job++];
+      jb.row = d.rowbuf + size_t(s) * d.row_len;
+      jb.hist = hist + size_t(s) * 8192;
+      jb.n = uint32_t(Lt);
+      jb.k = uint32_t(ks[i]);
+      jb.out_idx = sat.sel + size_t(slot) * sat.k;
+      jb.out_count = &x.cnt;
+      jb.host_out = host_off < 0 || d.no_host_copy ? nullptr : d.fetched + hoff;
+      jb.state_out = &x.state;
+      hoff += ks[i];
+    }
+    const int fi = f_fidx[s];
+    d.restamp_slots[fi] = s;
+    FireLog& lg = log[fi];
+    lg.trigger = t;
+    lg.pivot_unit = d.piv_unit[s];
+    lg.completion = f_comp[s];
+    lg.n_sats = f_ns[s];
+    lg.bytes = int64_t(f_nent[s]) * d.bpe;
+    lg.cum_after = f_cum[s];
+    lg.first_sat = a0;
+    lg.host_off = host_off;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) lg.ks[i] = ks[i];
+  }
+  // (4) every slot is written (fence, barrier): now the ring tails
+  __threadfence();
+  __syncthreads();
+  for (int s = tid; s < d.n_piv; s += blockDim.x) {
+    if (!f_fired[s]) continue;
+    const int a0 = f_a0[s], ns = min(int(f_ns[s]), 8);
+    const uint32_t full = f_full[s];
+    for (int i = 0; i < ns; ++i)
+      if (!((full >> i) & 1u)) d.sats[a0 + i].tail += 1;
+  }
+  if (tid == 0) {
+    *d.n_jobs = s_jobs;
+    *d.n_restamp = s_fires;
+    *d.head_dev = s_head;
+    BoundaryHdr* hdr = d.hdr_dev + (bidx % kLogRing);
+    hdr->t = t;
+    hdr->n_fires = int32_t(s_fires);
+    hdr->head_after = s_head;
+    hdr->pad = 1;
+    if (d.dbg) {
+      unsigned long long g2;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g2));
+      d.dbg[0] += g1 - g0;
+      d.dbg[1] += g2 - g1;
+      d.dbg[2] += 1;
+    }
+  }
 }
 
 // Which selected transfers can be gathered now: the satellite's staging
@@ -490,11 +760,18 @@ int launch_copy_fetched(const DevDec& d, int bidx, cudaStream_t st) {
   return HC_OK;
 }
 
+bool getenv_serial_decide() {  // tests: force the general kernel (read per boundary)
+  return getenv("HC_DECIDE_SERIAL") != nullptr;
+}
+
 int launch_decide(const DevDec& d, int t, int first, int nvals, int bidx, const uint32_t* ovl_ring,
                   int ring, cudaStream_t st) {
   HC_REQUIRE(nvals <= 64 && d.window <= 64, HC_EINVAL, "decision window > 64");
   HC_REQUIRE(d.n_piv <= kMaxPiv, HC_EINVAL, "more than %d monitored pivots", kMaxPiv);
-  decide_kernel<<<1, kChainThreads, 0, st>>>(d, t, first, nvals, bidx, ovl_ring, ring);
+  if (d.n_piv <= kFastPiv && d.B <= kFastSeq && !getenv_serial_decide())
+    decide_fast_kernel<<<1, kDecideThreads, 0, st>>>(d, t, first, nvals, bidx, ovl_ring, ring);
+  else
+    decide_kernel<<<1, kDecideThreads, 0, st>>>(d, t, first, nvals, bidx, ovl_ring, ring);
   HC_CHECK_LAUNCH();
   return HC_OK;
 }

@@ -126,6 +126,7 @@ struct DevDec {
   int64_t fetched_cap;
   volatile int64_t* fetched_tail;  // host-written (mapped): entries consumed
   int32_t* error;          // mapped: 0 ok, else an error code
+  unsigned long long* dbg; // diagnostics (HC_CHAIN_TRACE): decide-kernel phase times, or null
 };
 
 enum DevDecError : int32_t {

@@ -23,6 +23,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -280,6 +281,14 @@ struct EngineImpl {
   static constexpr int kPhaseEvents = 7;
   bool timing = false;
   bool timing_light = false;  // only the attention phase (ev[1] -> ev[2]) is recorded
+  // decision-chain trace (diagnostics, HC_CHAIN_TRACE=1): per boundary t, timed
+  // events from step t's combine to step t+1's satellites
+  static constexpr int kChainMarks = 11;
+  bool chain_trace = getenv("HC_CHAIN_TRACE") != nullptr;
+  std::vector<std::array<cudaEvent_t, kChainMarks>> ctr;
+  int ctr_open = -1;    // trace of the boundary whose landing step has not run yet
+  int ctr_step = -1;    // that step
+  bool ctr_in_decide = false;
   std::vector<cudaEvent_t> tpool;  // timed events for gather / landing pairs, reused
   std::vector<cudaEvent_t> tev;
   size_t tev_used = 0;  // steps recorded
@@ -365,9 +374,15 @@ struct hc_engine {
 namespace hc {
 namespace {
 
+void chain_report(EngineImpl& e);
+
 int engine_destroy(EngineImpl& e) {
   cudaDeviceSynchronize();
   host_prof_report();
+  chain_report(e);
+  for (auto& tr : e.ctr)
+    for (auto ev : tr)
+      if (ev) cudaEventDestroy(ev);
   for (auto& pr : e.stage_busy) cudaEventDestroy(std::get<2>(pr));
   if (e.stage) cudaFreeHost(e.stage);
   if (e.ovl_host) cudaFreeHost(e.ovl_host);
@@ -529,6 +544,10 @@ int devdec_create(EngineImpl& e, const hc_engine_desc& c) {
   d.scnt = static_cast<int32_t*>(dev(size_t(e.n_piv) * 4));
   d.jobs = static_cast<FireJob*>(dev(ns * sizeof(FireJob)));
   d.bump = static_cast<int32_t*>(dev(ns * 4));
+  if (e.chain_trace) {
+    d.dbg = static_cast<unsigned long long*>(dev(64));
+    HC_CUDA_TRY(cudaMemset(d.dbg, 0, 64));
+  }
   d.n_jobs = static_cast<uint32_t*>(dev(4));
   d.restamp_slots = static_cast<int32_t*>(dev(size_t(e.n_piv) * 4));
   d.n_restamp = static_cast<uint32_t*>(dev(4));
@@ -904,6 +923,47 @@ int new_event(EngineImpl& e, cudaEvent_t* out, bool timed = false) {
   return HC_OK;
 }
 
+// Chain trace mark k of the open boundary trace on stream st (diagnostics).
+int chain_mark(EngineImpl& e, int k, cudaStream_t st) {
+  if (!e.chain_trace || e.ctr_open < 0) return HC_OK;
+  cudaEvent_t& ev = e.ctr[e.ctr_open][k];
+  if (!ev) HC_CUDA_TRY(cudaEventCreate(&ev));
+  HC_CUDA_TRY(cudaEventRecord(ev, st));
+  return HC_OK;
+}
+
+void chain_report(EngineImpl& e) {
+  if (!e.chain_trace || e.ctr.empty()) return;
+  static const char* names[EngineImpl::kChainMarks] = {
+      "combine(t) done", "monitor(t)", "decide+restamp", "fire_select", "schedule",
+      "gathers done", "main K4(t+1)", "landing(t+1)", "sats K4(t+1)", "step t+1 joins",
+      "decide only"};
+  double sum[EngineImpl::kChainMarks] = {};
+  int n = 0;
+  for (auto& tr : e.ctr) {
+    bool ok = true;
+    for (auto ev : tr) ok = ok && ev && cudaEventSynchronize(ev) == cudaSuccess;
+    if (!ok) continue;
+    for (int k = 1; k < EngineImpl::kChainMarks; ++k) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, tr[0], tr[k]);
+      sum[k] += ms;
+    }
+    ++n;
+  }
+  cudaGetLastError();
+  if (e.dd.dbg) {
+    unsigned long long h[3] = {};
+    cudaMemcpy(h, e.dd.dbg, sizeof(h), cudaMemcpyDeviceToHost);
+    if (h[2])
+      fprintf(stderr, "hc_chain_trace decide kernel: window tests %.1f us, accounting %.1f us (%llu)\n",
+              h[0] / 1e3 / h[2], h[1] / 1e3 / h[2], h[2]);
+  }
+  fprintf(stderr, "hc_chain_trace %d boundaries (us after step t's combine):\n", n);
+  for (int k = 1; k < EngineImpl::kChainMarks; ++k)
+    fprintf(stderr, "hc_chain_trace %-18s %8.1f\n", names[k], n ? sum[k] / n * 1e3 : 0.0);
+}
+
 // A timed event for a gather / landing timing pair, from the engine's pool
 // (returned by hc_engine_retrieval_stats once read): no event creation inside a step.
 int timed_event(EngineImpl& e, cudaEvent_t* out) {
@@ -975,6 +1035,7 @@ int devdec_land(EngineImpl& e, int t, cudaStream_t st) {
 int devdec_schedule_and_gather(EngineImpl& e, int t_max) {
   HC_TRY(launch_schedule(e.dd, t_max - e.dd_horizon, e.sched));
   HC_CUDA_TRY(cudaEventRecord(e.ev_sched, e.sched));
+  if (e.ctr_in_decide) HC_TRY(chain_mark(e, 4, e.sched));
   e.sched_valid = true;
   HC_CUDA_TRY(cudaStreamWaitEvent(e.retr, e.ev_sched, 0));
   cudaEvent_t g0 = nullptr, g1 = nullptr;
@@ -1002,13 +1063,16 @@ int devdec_decide(EngineImpl& e, int t) {
   // the previous boundary's host copy still reads the job list the decision rewrites
   if (e.copy_valid) HC_CUDA_TRY(cudaStreamWaitEvent(e.mon, e.ev_copy, 0));
   HC_TRY(launch_decide(e.dd, t, first, nvals, int(bidx), e.ovl_ring, kRing, e.mon));
+  HC_TRY(chain_mark(e, 10, e.mon));
   HC_TRY(launch_restamp_threshold(e.rowbuf, e.row_len, e.dd.restamp_slots, e.n_piv,
                                   uint32_t(e.L + t), e.thr, e.kbase, e.words, e.mon,
                                   e.dd.n_restamp));
   HC_CUDA_TRY(cudaEventRecord(e.ev_dec, e.mon));
+  HC_TRY(chain_mark(e, 2, e.mon));
   HC_CUDA_TRY(cudaStreamWaitEvent(e.side, e.ev_dec, 0));
   HC_TRY(launch_fire_select(e.dd.jobs, std::max(1, e.dd.n_sat), e.side, e.dd.n_jobs));
   HC_CUDA_TRY(cudaEventRecord(e.ev_sel, e.side));
+  HC_TRY(chain_mark(e, 3, e.side));
   e.sel_valid = true;
   // the host mirror's copy of the fetched sets, on a low-priority stream
   HC_CUDA_TRY(cudaStreamWaitEvent(e.hcp, e.ev_sel, 0));
@@ -1017,7 +1081,12 @@ int devdec_decide(EngineImpl& e, int t) {
   HC_CUDA_TRY(cudaEventRecord(e.ev_log[bidx % kLogRing], e.hcp));
   e.copy_valid = true;
   HC_CUDA_TRY(cudaStreamWaitEvent(e.sched, e.ev_sel, 0));
-  return devdec_schedule_and_gather(e, t + e.dd_horizon);
+  e.ctr_in_decide = true;
+  const int rc = devdec_schedule_and_gather(e, t + e.dd_horizon);
+  e.ctr_in_decide = false;
+  HC_TRY(rc);
+  HC_TRY(chain_mark(e, 5, e.retr));
+  return HC_OK;
 }
 
 // Decode step t, in two halves so a host decision can overlap the attention:
@@ -1118,6 +1187,8 @@ int engine_decode_begin(EngineImpl& e, int t, const void* q, const void* kn, con
     prof_sec.emplace(3);
     HC_CUDA_TRY(cudaStreamWaitEvent(e.lnd, e.ev_app, 0));
     HC_TRY(devdec_land(e, t, e.lnd));
+    const bool traced = e.ctr_open >= 0 && e.ctr_step == t;
+    if (traced) HC_TRY(chain_mark(e, 7, e.lnd));
     prof_sec.emplace(4);
     HC_TRY(devdec_schedule_and_gather(e, t + e.dd_horizon));
     prof_sec.emplace(5);
@@ -1127,6 +1198,10 @@ int engine_decode_begin(EngineImpl& e, int t, const void* q, const void* kn, con
     const int n = int(std::upper_bound(e.sat_t_act.begin(), e.sat_t_act.end(), uint32_t(t)) -
                       e.sat_t_act.begin());
     HC_TRY(launch_attn_tiles(e.tmK, e.tmV, ps, n, e.lnd));
+    if (traced) {
+      HC_TRY(chain_mark(e, 8, e.lnd));
+      HC_TRY(chain_mark(e, 6, st));  // the main K4 was queued on st before the landing
+    }
     HC_CUDA_TRY(cudaEventRecord(e.ev_sats, e.lnd));
     if (e.timing) {  // landing stall = how far the satellites' path ends after the main K4
       cudaEvent_t w0 = nullptr, w1 = nullptr;
@@ -1156,6 +1231,10 @@ int engine_decode_end(EngineImpl& e, int t, cudaStream_t st) {
   pl.skip = nullptr;
   if (e.devdec) {
     if (!e.dd_quiet) HC_CUDA_TRY(cudaStreamWaitEvent(st, e.ev_sats, 0));  // satellites attended
+    if (e.ctr_open >= 0 && e.ctr_step == t) {
+      HC_TRY(chain_mark(e, 9, st));
+      e.ctr_open = -1;
+    }
   } else if (e.cur_hold) {
     std::vector<int> land;
     land.swap(e.deferred);
@@ -1211,6 +1290,13 @@ int engine_decode_end(EngineImpl& e, int t, cudaStream_t st) {
                           e.ovl_ring + size_t(t % kRing) * e.n_piv, e.mon,
                           e.ghist + size_t(t & 1) * e.n_piv * 8192));
     prof_sec.emplace(9);
+    if (e.chain_trace && e.devdec && (e.dd.sliding || t % e.dd.window == 0)) {
+      e.ctr.push_back({});
+      e.ctr_open = int(e.ctr.size()) - 1;
+      e.ctr_step = t + 1;
+      HC_TRY(chain_mark(e, 0, st));     // combine(t) done (the caller's stream)
+      HC_TRY(chain_mark(e, 1, e.mon));  // score rows + monitor done
+    }
     if (e.devdec) HC_TRY(devdec_decide(e, t));
     prof_sec.reset();
   } else if (ev) {

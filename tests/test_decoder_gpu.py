@@ -375,12 +375,19 @@ def test_single_call_fire_and_land_abi():
     assert want <= pre
 
 
-@pytest.mark.parametrize("dd", [None, False], ids=["auto", "host"])
+@pytest.mark.parametrize("dd", [None, False, "serial"], ids=["auto", "host", "serial-decide"])
 @pytest.mark.parametrize("seed", range(N_RANDOM_CONFIGS))
-def test_randomized_configs_match_oracle(seed, dd):
+def test_randomized_configs_match_oracle(seed, dd, monkeypatch):
     """Seeded random engine configurations (window, delay, host-link model, sinks /
     recency, chunk, batch, prompt length, shift schedule, decision order): events,
-    StepRows and dynamic sets must equal the oracle's replay of the GPU rows."""
+    StepRows and dynamic sets must equal the oracle's replay of the GPU rows --
+    with device decisions (the parallel decide kernel, or the general serial one),
+    and with host decisions."""
+    if dd == "serial":
+        if seed % 4:
+            pytest.skip("the general decide kernel on a quarter of the configurations")
+        monkeypatch.setenv("HC_DECIDE_SERIAL", "1")
+        dd = None
     rng = np.random.default_rng(1000 + seed)
     T = int(rng.integers(16, 41))
     n_shift = int(rng.integers(1, 4))
