@@ -330,10 +330,14 @@ def l2_flush(args, w, rho: float, world: int) -> bool:
     """Whether the timed steps run with an L2 flush between them: a step whose
     resident K/V (about rho of the full context at 512 B per token and KV head)
     fits in 4x L2 would otherwise be served from L2 on every step."""
-    if args.l2 == "none" or world > 1:
+    if args.l2 == "none" or world > 1 or args.policy != "heterocache":
         return False
-    est = w.batch * w.num_layers * w.model.kv_heads * w.prefill_len * 512 * rho
-    return args.l2 == "flush" or est < 4 * L2_BYTES
+    return args.l2 == "flush" or l2_resident_bytes(w, rho) < 4 * L2_BYTES
+
+
+def l2_resident_bytes(w, rho: float) -> float:
+    """About a step's resident K/V: rho of the full context, 512 B per token and KV head."""
+    return w.batch * w.num_layers * w.model.kv_heads * w.prefill_len * 512 * rho
 
 
 def make_config(args, w, cfg, rho, l_base_int, roles: dict, world: int, mode: str) -> dict:
@@ -370,7 +374,10 @@ def make_config(args, w, cfg, rho, l_base_int, roles: dict, world: int, mode: st
         "l2": (f"flushed between timed steps ({2 * L2_BYTES >> 20} MB written; each step "
                f"timed on its own, start to end of its monitor, flush excluded)"
                if l2_flush(args, w, rho, world) else
-               "inputs larger than L2 (resident K/V per step >> 126 MB)"),
+               "inputs larger than L2 (resident K/V per step >> 126 MB)"
+               if l2_resident_bytes(w, rho) >= 4 * L2_BYTES else
+               "resident K/V per step fits in L2 and is not flushed (--l2 none, N > 1 or a "
+               "baseline policy)"),
         "parallelism": par,
     }
 
