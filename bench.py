@@ -82,7 +82,9 @@ def parse(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seqs", type=int, default=1,
                     help="sequences the CPU decoder samples (cpu_baseline, parity, reference)")
-    ap.add_argument("--chunk", type=int, default=1024)
+    ap.add_argument("--chunk", type=int, default=0,
+                    help="split-K chunk (rows per K4 tile); 0: 1024, smaller for a step too "
+                         "small to fill the GPU with 1024-row tiles")
     ap.add_argument("--l2", choices=("auto", "flush", "none"), default="auto",
                     help="flush L2 between timed steps (auto: when a step's resident K/V "
                          "would fit in 4x L2), timing each step on its own")
@@ -265,6 +267,18 @@ def schedule(args, w):
     return shifts, S0 + W + Z + 2 * K + 8 + phase_steps(args)
 
 
+def chunk_of(args, w) -> int:
+    """The split-K chunk: 1024 rows, halved (down to 128) while the full-context
+    tiles of one step would not give every SM four (cfg1: 32 tiles at 1024)."""
+    if args.chunk:
+        return args.chunk
+    chunk = 1024
+    units = w.batch * w.num_layers * w.model.kv_heads
+    while chunk > 128 and units * -(-w.prefill_len // chunk) < 4 * 148:
+        chunk //= 2
+    return chunk
+
+
 def settle_steps(w) -> int:
     """Untimed steps after the warm-up with the drift schedule already running, for
     workloads that drift every few steps (cfg4): eight drift periods, so the timed
@@ -366,7 +380,7 @@ def make_config(args, w, cfg, rho, l_base_int, roles: dict, world: int, mode: st
         "policy": args.policy, "decode_window": cfg.window, "tau_drift": cfg.tau_drift,
         "topic_shifts": (f"every cluster (sequence, layer) once per "
                          f"{w.shift_every or DRIFT_PERIOD} steps, staggered phases"),
-        "split_k_chunk": args.chunk, "start_step": args.start_step,
+        "split_k_chunk": chunk_of(args, w), "start_step": args.start_step,
         "settle_steps": settle_steps(w),
         "transfer_bandwidth_bytes_per_step": cfg.transfer_bandwidth,
         "score_material": args.score_material,
@@ -425,7 +439,7 @@ def run_b200(args, rank, world):
     cfg = engine_config(args, w)
     lib = _lib.load()
     obs = obs_of(args, w)
-    dkw = dict(batch=w.batch, group=m.group, max_decode=T, chunk=args.chunk, host_pool=True,
+    dkw = dict(batch=w.batch, group=m.group, max_decode=T, chunk=chunk_of(args, w), host_pool=True,
                track_sets=False, obs_window=obs, score_material=args.score_material,
                device_decisions=None if args.decisions == "device" else False)
     mode = shard_mode(args, w, world)
