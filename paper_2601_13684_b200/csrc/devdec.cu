@@ -579,7 +579,7 @@ __global__ void __launch_bounds__(kChainThreads, kChainMinBlocks) order_kernel(D
 // the next pass (queued behind this one) re-lists the remainders with the new
 // transfer in deadline order.  A claimed chunk is always finished; the CTA
 // completing a transfer's last chunk flags it GATHERED.
-constexpr int kChunkRows = 256;
+constexpr int kChunkRows = 256;  // default of DevDec::gather_chunk
 
 __global__ void __launch_bounds__(kChainThreads, kChainMinBlocks) gather_dev_kernel(DevDec d, uint4* __restrict__ K,
                                                          uint4* __restrict__ V) {
@@ -597,7 +597,8 @@ __global__ void __launch_bounds__(kChainThreads, kChainMinBlocks) gather_dev_ker
     const DevSat& sat = d.sats[it.sat];
     DevXfer& x = d.xfers[size_t(it.sat) * d.nq + it.slot];
     const int rows = x.meta[0];
-    const uint32_t n_chunks = uint32_t((rows + kChunkRows - 1) / kChunkRows);
+    const int chunk_rows = d.gather_chunk;
+    const uint32_t n_chunks = uint32_t((rows + chunk_rows - 1) / chunk_rows);
     if (n_chunks == 0) {
       if (threadIdx.x == 0) atomicCAS(&x.state, int(kXScheduled), int(kXGathered));
       continue;
@@ -613,8 +614,8 @@ __global__ void __launch_bounds__(kChainThreads, kChainMinBlocks) gather_dev_ker
       __syncthreads();
       if (stop) return;
       if (c >= n_chunks) break;
-      const int r0 = int(c) * kChunkRows;
-      const int nr = min(kChunkRows, rows - r0);
+      const int r0 = int(c) * chunk_rows;
+      const int nr = min(chunk_rows, rows - r0);
       gather_rows(sat.pos + size_t(x.buf) * sat.cap + r0, nr, sat.srcK, sat.srcV, K, V,
                   sat.row0[x.buf] + r0, wid, nwarps);
       __syncthreads();
@@ -790,7 +791,7 @@ int launch_dev_gathers(const DevDec& d, uint4* K, uint4* V, cudaStream_t st, int
   order_kernel<<<1, kChainThreads, 0, st>>>(d);
   HC_CHECK_LAUNCH();
   if (g0) HC_CUDA_TRY(cudaEventRecord(g0, st));
-  gather_dev_kernel<<<40, kChainThreads, 0, st>>>(d, K, V);
+  gather_dev_kernel<<<d.gather_ctas, kChainThreads, 0, st>>>(d, K, V);
   if (g1) HC_CUDA_TRY(cudaEventRecord(g1, st));
   HC_CHECK_LAUNCH();
   return HC_OK;

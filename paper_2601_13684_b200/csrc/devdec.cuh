@@ -87,6 +87,7 @@ struct DevDec {
   // static geometry
   int32_t n_sat, n_piv, B, L, S, R, lbase, window, sliding, delay;
   int32_t nq, no_host_copy;  // transfer slots per satellite ring; diagnostics switch
+  int32_t gather_ctas, gather_chunk;  // retrieval gather grid and rows per claimed chunk
   double tau;
   int64_t bw, bpe;
   int32_t* seq_piv;        // [B + 1] pivot slot ranges per sequence

@@ -522,6 +522,10 @@ int devdec_create(EngineImpl& e, const hc_engine_desc& c) {
                                                                    std::max<int64_t>(1, per_slot))));
     if (const char* q = getenv("HC_DEVDEC_NQ")) d.nq = std::max(2, atoi(q));  // tests: tiny rings
     d.no_host_copy = getenv("HC_DEVDEC_NO_HOST_COPY") ? 1 : 0;  // timing diagnostics only
+    d.gather_ctas = 40;
+    d.gather_chunk = 256;
+    if (const char* g = getenv("HC_GATHER_CTAS")) d.gather_ctas = std::max(1, atoi(g));
+    if (const char* g = getenv("HC_GATHER_CHUNK")) d.gather_chunk = std::max(32, atoi(g));
     for (DevSat& x : sats) {
       x.sel = static_cast<uint32_t*>(dev(size_t(d.nq) * std::max(1, x.k) * 4));
       HC_REQUIRE(x.sel, HC_ENOMEM, "device decisions: transfer rings");
