@@ -44,11 +44,14 @@ SHAPES = {
     "cfg3": dict(heads=(28, 4), L=131072, compression=0.05),
     # cfg5: Llama-3.1-8B-shaped, 224K context, 10% budget
     "cfg5": dict(heads=(32, 8), L=229376, compression=0.10),
+    # cfg4: R1-Distill-Llama-8B-shaped, 64K prompt, 10% budget (frequent drift)
+    "cfg4": dict(heads=(32, 8), L=65536, compression=0.10),
 }
 
 
 def build(shape: str, *, B: int, NL: int, T: int = 24, shift=9, window: int = 8,
-          chunk: int = 1024, seed: int = 5, score_material: str = "fp32"):
+          chunk: int = 1024, seed: int = 5, score_material: str = "fp32",
+          bandwidth: int = 1 << 30, delay: int = 1):
     import torch
 
     from paper_2601_13684_b200.decoder import HeteroCacheDecoder
@@ -60,8 +63,8 @@ def build(shape: str, *, B: int, NL: int, T: int = 24, shift=9, window: int = 8,
     L = sp["L"]
     w = Workload(shape, model, L, B, sp["compression"], T, 0, layers=NL)
     tax, plan = plan_for(w)
-    cfg = EngineConfig(tau_drift=0.5, window=window, update_delay_steps=1,
-                       transfer_bandwidth=1 << 30)
+    cfg = EngineConfig(tau_drift=0.5, window=window, update_delay_steps=delay,
+                       transfer_bandwidth=bandwidth)
     dec = HeteroCacheDecoder(tax, plan, cfg, batch=B, group=model.group, max_decode=T,
                              chunk=chunk, host_pool=True, obs_window=1,
                              score_material=score_material)

@@ -54,6 +54,31 @@ def test_outputs_rows_events_and_selection_at_scale(shape, layout):
         torch.cuda.empty_cache()
 
 
+def test_frequent_drift_with_a_constrained_link_at_64k():
+    """cfg4-shaped (64K, the Llama role mix): topic shifts every 8 steps and a
+    modelled link of 1 MB per step, so fires queue behind one another, complete
+    steps after their trigger and land while later fires are pending.  Outputs
+    of every role at every landing step, the event log and the dynamic sets
+    must match the oracle."""
+    import torch
+
+    ctx = SP.build("cfg4", B=1, NL=2, T=40, shift=tuple(range(6, 38, 8)),
+                   bandwidth=1 << 20, delay=1)
+    try:
+        SP.run(ctx)
+        events = SP.check_events(ctx)
+        assert len(events) >= 3, "the shifts must fire repeatedly"
+        late = [e for _, e in events if e["completion_step"] > e["trigger_step"] + 1]
+        assert late, "the constrained link must delay some completions"
+        lands = sorted({e["completion_step"] for _, e in events if e["completion_step"] <= 40})
+        st = SP.check_outputs(ctx, sorted({1, 40} | set(lands)))
+        assert not st["violations"], st["violations"][:5]
+        print(f"cfg4: {len(events)} fires, {len(late)} delayed, max|O-O_ref| {st['max_abs']:.2e}")
+    finally:
+        ctx["dec"].close()
+        torch.cuda.empty_cache()
+
+
 def test_fp16_material_keeps_outputs_and_event_replay():
     """The compact fp16 score material still gives in-tolerance outputs and
     events equal to the replay of its own rows (decisions bit-exact given the
