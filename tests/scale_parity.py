@@ -51,7 +51,7 @@ SHAPES = {
 
 def build(shape: str, *, B: int, NL: int, T: int = 24, shift=9, window: int = 8,
           chunk: int = 1024, seed: int = 5, score_material: str = "fp32",
-          bandwidth: int = 1 << 30, delay: int = 1):
+          bandwidth: int = 1 << 30, delay: int = 1, eval_every_step: bool = False):
     import torch
 
     from paper_2601_13684_b200.decoder import HeteroCacheDecoder
@@ -64,7 +64,7 @@ def build(shape: str, *, B: int, NL: int, T: int = 24, shift=9, window: int = 8,
     w = Workload(shape, model, L, B, sp["compression"], T, 0, layers=NL)
     tax, plan = plan_for(w)
     cfg = EngineConfig(tau_drift=0.5, window=window, update_delay_steps=delay,
-                       transfer_bandwidth=bandwidth)
+                       transfer_bandwidth=bandwidth, eval_every_step=eval_every_step)
     dec = HeteroCacheDecoder(tax, plan, cfg, batch=B, group=model.group, max_decode=T,
                              chunk=chunk, host_pool=True, obs_window=1,
                              score_material=score_material)

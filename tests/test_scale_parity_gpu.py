@@ -79,6 +79,28 @@ def test_frequent_drift_with_a_constrained_link_at_64k():
         torch.cuda.empty_cache()
 
 
+def test_sliding_window_decisions_two_sequences_at_224k():
+    """cfg5-shaped (224K), two sequences, eval_every_step (a decision at every step
+    once the window holds W values, cleared on a fire, engine.py:358-360), window
+    4 and update delay 2: events and dynamic sets per sequence and outputs at the
+    landing steps must match the oracle."""
+    import torch
+
+    ctx = SP.build("cfg5", B=2, NL=1, T=24, shift=(5, 14), window=4, delay=2,
+                   eval_every_step=True)
+    try:
+        SP.run(ctx)
+        events = SP.check_events(ctx)
+        assert {b for b, _ in events} == {0, 1}, "both sequences must fire"
+        lands = sorted({e["completion_step"] for _, e in events if e["completion_step"] <= 24})
+        st = SP.check_outputs(ctx, sorted({1, 24} | set(lands)))
+        assert not st["violations"], st["violations"][:5]
+        print(f"cfg5 sliding: {len(events)} fires, max|O-O_ref| {st['max_abs']:.2e}")
+    finally:
+        ctx["dec"].close()
+        torch.cuda.empty_cache()
+
+
 def test_fp16_material_keeps_outputs_and_event_replay():
     """The compact fp16 score material still gives in-tolerance outputs and
     events equal to the replay of its own rows (decisions bit-exact given the
