@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(kDecideThreads, kDecideMinBlocks) decide_kerne
 // only; (3) per fired pivot, in parallel: its transfer slots, fire-selection
 // jobs and log entry; (4) after one fence per thread and a barrier, the ring
 // tails.  Results equal decide_kernel's.
-constexpr int kFastPiv = 256, kFastSeq = 256;
+constexpr int kFastPiv = 512, kFastSeq = 256;
 
 __global__ void __launch_bounds__(kDecideThreads, kDecideMinBlocks)
 decide_fast_kernel(DevDec d, int t, int first, int nvals, int bidx,
