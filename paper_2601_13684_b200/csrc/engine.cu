@@ -1067,11 +1067,13 @@ int devdec_decide(EngineImpl& e, int t) {
   // the previous boundary's host copy still reads the job list the decision rewrites
   if (e.copy_valid) HC_CUDA_TRY(cudaStreamWaitEvent(e.mon, e.ev_copy, 0));
   HC_TRY(launch_decide(e.dd, t, first, nvals, int(bidx), e.ovl_ring, kRing, e.mon));
+  // the fire selection needs the decision's job list, not the K_base restamp
+  // (which only the next monitor reads): it starts beside the restamp
+  HC_CUDA_TRY(cudaEventRecord(e.ev_dec, e.mon));
   HC_TRY(chain_mark(e, 10, e.mon));
   HC_TRY(launch_restamp_threshold(e.rowbuf, e.row_len, e.dd.restamp_slots, e.n_piv,
                                   uint32_t(e.L + t), e.thr, e.kbase, e.words, e.mon,
                                   e.dd.n_restamp));
-  HC_CUDA_TRY(cudaEventRecord(e.ev_dec, e.mon));
   HC_TRY(chain_mark(e, 2, e.mon));
   HC_CUDA_TRY(cudaStreamWaitEvent(e.side, e.ev_dec, 0));
   HC_TRY(launch_fire_select(e.dd.jobs, std::max(1, e.dd.n_sat), e.side, e.dd.n_jobs));
