@@ -341,8 +341,9 @@ attn_tiles_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant
 __global__ void __launch_bounds__(128) combine_kernel(const AttnParams p) {
   __shared__ float wm[4], wl[4];
   __shared__ __align__(16) float racc[4][128];
-  const UnitDesc u = p.units[blockIdx.x];
+  const UnitDesc u = p.units[p.combine_sel == 1 ? p.cunits[blockIdx.x] : int(blockIdx.x)];
   if (u.kind == kUnitAbsent) return;  // owned by another shard
+  if (p.combine_sel == 2 && u.pivot_slot >= 0) return;  // the pivots were combined already
   const int g = blockIdx.y;
   const int G = p.group;
   const int n = unit_slots(u, p.t, p.L, p.chunk);
@@ -543,8 +544,9 @@ static int configure_attn() {
 // Split-K combine (O and the pivots' softmax statistics).
 int launch_combine(const AttnParams& p, cudaStream_t st) {
   HC_REQUIRE(p.group >= 1 && p.group <= 8, HC_EINVAL, "GQA group must be 1..8");
-  if (p.n_units > 0) {
-    combine_kernel<<<dim3(p.n_units, p.group), 128, 0, st>>>(p);
+  const int n = p.combine_sel == 1 ? p.n_cunits : p.n_units;
+  if (n > 0) {
+    combine_kernel<<<dim3(n, p.group), 128, 0, st>>>(p);
     HC_CHECK_LAUNCH();
   }
   return HC_OK;

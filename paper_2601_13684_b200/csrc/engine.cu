@@ -186,6 +186,16 @@ struct EngineImpl {
   // decision is still open (hold_satellites, see decode_begin)
   TileDesc* d_sat_tiles = nullptr;
   std::vector<uint32_t> sat_t_act;
+  // pivot-first step (device decisions): the pivots' tiles, then every other
+  // unit's tiles on a second stream beside them; the boundary chain (the
+  // pivots' combine, score rows, monitor, decision) starts when the pivots are done
+  bool pivot_first = false;
+  TileDesc* d_piv_tiles = nullptr;
+  TileDesc* d_rest_tiles = nullptr;
+  std::vector<uint32_t> piv_t_act, rest_t_act;
+  cudaStream_t kst2 = nullptr;
+  cudaEvent_t ev_k4s = nullptr, ev_piv = nullptr, ev_rest = nullptr, ev_pc = nullptr;
+  cudaEvent_t step_out = nullptr;  // pivot-first: the step's O complete (caller's stream)
   uint8_t* d_sat_flags = nullptr;
   // the open step between decode_begin and decode_end
   int in_step = 0;
@@ -388,6 +398,9 @@ int engine_destroy(EngineImpl& e) {
   if (e.ovl_host) cudaFreeHost(e.ovl_host);
   for (auto& ev : e.events) cudaEventDestroy(ev.first);
   if (e.step_end) cudaEventDestroy(e.step_end);
+  for (cudaEvent_t x : {e.ev_k4s, e.ev_piv, e.ev_rest, e.ev_pc, e.step_out})
+    if (x) cudaEventDestroy(x);
+  if (e.kst2) cudaStreamDestroy(e.kst2);
   if (e.rows_done) cudaEventDestroy(e.rows_done);
   for (auto x : e.rows_ev)
     if (x) cudaEventDestroy(x);
@@ -775,6 +788,20 @@ int engine_create(EngineImpl& e, const hc_engine_desc& c, const int32_t* roles,
     HC_TRY(dalloc((void**)&e.d_sat_flags, size_t(e.n_units), &e.dev_bytes));
     HC_CUDA_TRY(cudaMemcpy(e.d_sat_flags, fl.data(), fl.size(), cudaMemcpyHostToDevice));
   }
+  {  // pivot-first tile lists (each keeps the t_act order)
+    std::vector<TileDesc> pt, rt;
+    for (const TileDesc& d : tiles) (e.units[d.unit].pivot_slot >= 0 ? pt : rt).push_back(d);
+    for (const TileDesc& d : pt) e.piv_t_act.push_back(d.t_act);
+    for (const TileDesc& d : rt) e.rest_t_act.push_back(d.t_act);
+    for (auto* pr : {&pt, &rt}) {
+      TileDesc*& dst = pr == &pt ? e.d_piv_tiles : e.d_rest_tiles;
+      HC_TRY(dalloc((void**)&dst, std::max<size_t>(1, pr->size()) * sizeof(TileDesc),
+                    &e.dev_bytes));
+      if (!pr->empty())
+        HC_CUDA_TRY(cudaMemcpy(dst, pr->data(), pr->size() * sizeof(TileDesc),
+                               cudaMemcpyHostToDevice));
+    }
+  }
 
   HC_TRY(dalloc((void**)&e.K, size_t(e.rows) * kHeadDim * 2, &e.dev_bytes));
   HC_TRY(dalloc((void**)&e.V, size_t(e.rows) * kHeadDim * 2, &e.dev_bytes));
@@ -887,6 +914,17 @@ int engine_create(EngineImpl& e, const hc_engine_desc& c, const int32_t* roles,
   HC_CUDA_TRY(cudaStreamCreateWithPriority(&e.side, cudaStreamNonBlocking, hi_prio));
   HC_CUDA_TRY(cudaStreamCreateWithPriority(&e.mon, cudaStreamNonBlocking, hi_prio));
   if (c.device_decisions) HC_TRY(devdec_create(e, c));
+  {
+    const char* pfe = getenv("HC_PIVOT_FIRST");
+    // measured (profiles/r02_chain_trace.md): +0.6% at cfg2 and +1.5% at cfg4, but
+    // -2.2% at cfg3 and -0.6% at cfg5 -- off unless HC_PIVOT_FIRST=1
+    e.pivot_first = e.devdec && e.n_piv > 0 && pfe && pfe[0] == '1';
+  }
+  if (e.pivot_first) {
+    HC_CUDA_TRY(cudaStreamCreateWithFlags(&e.kst2, cudaStreamNonBlocking));
+    for (cudaEvent_t* x : {&e.ev_k4s, &e.ev_piv, &e.ev_rest, &e.ev_pc, &e.step_out})
+      HC_CUDA_TRY(cudaEventCreateWithFlags(x, cudaEventDisableTiming));
+  }
   return host_io_init(e);  // decode_step_host staging, outside any timed step
 }
 
@@ -1095,6 +1133,59 @@ int devdec_decide(EngineImpl& e, int t) {
   return HC_OK;
 }
 
+// Score rows and the K1+K2 monitor (top-l_base threshold and |top & K_base| per
+// pivot, engine.py:305-311; counts land in the overlap ring row of the step)
+// feed only the drift decision, so they run on their own stream beside the
+// next step's attention.  Readers (overlaps, fire, measure, pivot_row) wait for
+// step_end; the attention two steps later waits for this step's rows before it
+// overwrites the score material of its parity.  Pivot-first: the chain starts
+// when the pivots' tiles are done (ev_piv) with the pivots' own combine.
+int monitor_chain(EngineImpl& e, int t, const AttnParams& p, cudaEvent_t* ev, cudaStream_t st) {
+  if (e.pivot_first) {
+    HC_CUDA_TRY(cudaStreamWaitEvent(e.mon, e.ev_piv, 0));
+  } else {
+    if (!e.rows_done)
+      HC_CUDA_TRY(cudaEventCreateWithFlags(&e.rows_done, cudaEventDisableTiming));
+    HC_CUDA_TRY(cudaEventRecord(e.rows_done, st));
+    HC_CUDA_TRY(cudaStreamWaitEvent(e.mon, e.rows_done, 0));
+  }
+  // the previous boundary's fetch selection still reads the rows and histograms
+  if (e.sel_valid) {  // (once per selection: the monitor stream stays ordered after it)
+    HC_CUDA_TRY(cudaStreamWaitEvent(e.mon, e.ev_sel, 0));
+    e.sel_valid = false;
+  }
+  if (e.pivot_first) {  // the pivots' O and softmax statistics
+    AttnParams pc = p;
+    pc.combine_sel = 1;
+    pc.cunits = e.d_piv_units;
+    pc.n_cunits = e.n_piv;
+    HC_TRY(launch_combine(pc, e.mon));
+    HC_CUDA_TRY(cudaEventRecord(e.ev_pc, e.mon));
+  }
+  HC_TRY(launch_score_rows(p, e.d_piv_units, e.n_piv, e.mon));
+  cudaEvent_t& re = e.rows_ev[t & 1];
+  if (!re) HC_CUDA_TRY(cudaEventCreateWithFlags(&re, cudaEventDisableTiming));
+  HC_CUDA_TRY(cudaEventRecord(re, e.mon));
+  if (ev) HC_CUDA_TRY(cudaEventRecord(ev[4], e.mon));
+  HC_TRY(launch_monitor(e.rowbuf, e.row_len, e.d_piv_slots, e.n_piv, uint32_t(e.L + t),
+                        uint32_t(e.lbase), e.kbase, e.words, e.thr,
+                        e.ovl_ring + size_t(t % kRing) * e.n_piv, e.mon,
+                        e.ghist + size_t(t & 1) * e.n_piv * 8192));
+  if (e.chain_trace && e.devdec && (e.dd.sliding || t % e.dd.window == 0)) {
+    e.ctr.push_back({});
+    e.ctr_open = int(e.ctr.size()) - 1;
+    e.ctr_step = t + 1;
+    HC_TRY(chain_mark(e, 0, st));     // the chain's start on the caller's stream
+    HC_TRY(chain_mark(e, 1, e.mon));  // score rows + monitor done
+  }
+  if (e.devdec) HC_TRY(devdec_decide(e, t));
+  if (ev) HC_CUDA_TRY(cudaEventRecord(ev[5], e.mon));
+  if (!e.step_end)
+    HC_CUDA_TRY(cudaEventCreateWithFlags(&e.step_end, cudaEventDisableTiming));
+  HC_CUDA_TRY(cudaEventRecord(e.step_end, e.mon));
+  return HC_OK;
+}
+
 // Decode step t, in two halves so a host decision can overlap the attention:
 //
 //   decode_begin  append the token; K4 over every unit except those that may
@@ -1180,11 +1271,31 @@ int engine_decode_begin(EngineImpl& e, int t, const void* q, const void* kn, con
   if (e.devdec && !e.dd_quiet)  // the token is appended (the landing stream waits for it)
     HC_CUDA_TRY(cudaEventRecord(e.ev_app, st));
   AttnParams p = decode_params(e, t, q, o);
+  if (e.pivot_first) HC_CUDA_TRY(cudaEventRecord(e.ev_k4s, st));  // (before the material wait below)
   // K4 overwrites the score material of parity t&1: step t-2's rows must be done
   if (e.rows_ev[t & 1]) HC_CUDA_TRY(cudaStreamWaitEvent(st, e.rows_ev[t & 1], 0));
   p.skip = hold ? e.d_sat_flags : (land.empty() ? nullptr : e.d_skip);
   prof_sec.emplace(2);
-  HC_TRY(launch_attn_tiles(e.tmK, e.tmV, p, active_tiles(e, t), st));
+  if (e.pivot_first) {
+    // the pivots' tiles on the caller's stream, every other unit's on kst2
+    // beside them (the same priority: the pivots' CTAs are dispatched first)
+    AttnParams pp = p;
+    pp.skip = nullptr;
+    pp.tiles = e.d_piv_tiles;
+    const int np = int(std::upper_bound(e.piv_t_act.begin(), e.piv_t_act.end(), uint32_t(t)) -
+                       e.piv_t_act.begin());
+    HC_TRY(launch_attn_tiles(e.tmK, e.tmV, pp, np, st));
+    HC_CUDA_TRY(cudaEventRecord(e.ev_piv, st));
+    HC_CUDA_TRY(cudaStreamWaitEvent(e.kst2, e.ev_k4s, 0));
+    AttnParams pr = p;
+    pr.tiles = e.d_rest_tiles;
+    const int nr = int(std::upper_bound(e.rest_t_act.begin(), e.rest_t_act.end(),
+                                        uint32_t(t)) - e.rest_t_act.begin());
+    HC_TRY(launch_attn_tiles(e.tmK, e.tmV, pr, nr, e.kst2));
+    HC_CUDA_TRY(cudaEventRecord(e.ev_rest, e.kst2));
+  } else {
+    HC_TRY(launch_attn_tiles(e.tmK, e.tmV, p, active_tiles(e, t), st));
+  }
   prof_sec.reset();
   if (e.devdec && !e.dd_quiet) {
     // landing point (device-decided transfers due at t), then the satellites'
@@ -1218,6 +1329,11 @@ int engine_decode_begin(EngineImpl& e, int t, const void* q, const void* kn, con
       e.land_ev.emplace_back(w0, w1);
     }
   }
+  if (e.pivot_first) {  // the boundary chain of step t, beside the other units' tiles
+    prof_sec.emplace(8);
+    HC_TRY(monitor_chain(e, t, p, (ev && !e.timing_light) ? ev : nullptr, st));
+    prof_sec.reset();
+  }
   e.in_step = t;
   e.cur_hold = hold;
   e.cur_st = st;
@@ -1236,6 +1352,7 @@ int engine_decode_end(EngineImpl& e, int t, cudaStream_t st) {
   AttnParams pl = e.cur_p;
   pl.skip = nullptr;
   if (e.devdec) {
+    if (e.pivot_first) HC_CUDA_TRY(cudaStreamWaitEvent(st, e.ev_rest, 0));  // the other units' tiles
     if (!e.dd_quiet) HC_CUDA_TRY(cudaStreamWaitEvent(st, e.ev_sats, 0));  // satellites attended
     if (e.ctr_open >= 0 && e.ctr_step == t) {
       HC_TRY(chain_mark(e, 9, st));
@@ -1264,6 +1381,18 @@ int engine_decode_end(EngineImpl& e, int t, cudaStream_t st) {
   prof_sec.emplace(7);
   if (ev) HC_CUDA_TRY(cudaEventRecord(ev[2], st));  // ... and this one only
   if (ev && e.timing_light) ev = nullptr;
+  if (e.pivot_first) {
+    AttnParams pc = e.cur_p;
+    pc.combine_sel = 2;  // every unit but the pivots (combined on the monitor stream)
+    HC_TRY(launch_combine(pc, st));  // O: the step's output
+    if (ev) HC_CUDA_TRY(cudaEventRecord(ev[3], st));
+    HC_CUDA_TRY(cudaStreamWaitEvent(st, e.ev_pc, 0));  // the pivots' O
+    if (ev) HC_CUDA_TRY(cudaEventRecord(ev[6], st));
+    HC_CUDA_TRY(cudaEventRecord(e.step_out, st));
+    e.last_t = t;
+    prof_sec.emplace(10);
+    return gc_events(e, t);
+  }
   HC_TRY(launch_combine(e.cur_p, st));  // O: the step's output
   if (ev) HC_CUDA_TRY(cudaEventRecord(ev[3], st));
   e.last_t = t;
@@ -1614,7 +1743,7 @@ int engine_prefill_layer(EngineImpl& e, int layer, const __nv_bfloat16* k,
   const size_t o_jobs = carve(size_t(nu) * sizeof(hc_topk_job));
   const size_t o_obs = carve(obs_scratch_bytes(nu, e.L, e.W * e.G));
   if (off > e.pf_bytes) {
-    if (e.pf) {
+    if (e.pivot_first) {
       HC_CUDA_TRY(cudaStreamSynchronize(st));
       cudaFree(e.pf);
       e.pf = nullptr;
@@ -2351,6 +2480,8 @@ extern "C" int hc_engine_join(hc_engine* eng, void* stream) {
   HC_REQUIRE(eng, HC_EINVAL, "null argument");
   if (eng->e.step_end)
     HC_CUDA_TRY(cudaStreamWaitEvent((cudaStream_t)stream, eng->e.step_end, 0));
+  if (eng->e.pivot_first && eng->e.step_out)  // pivot-first: the step's O (caller's stream)
+    HC_CUDA_TRY(cudaStreamWaitEvent((cudaStream_t)stream, eng->e.step_out, 0));
   if (eng->e.h_last >= 0)  // the last decode_step_host download
     HC_CUDA_TRY(cudaStreamWaitEvent((cudaStream_t)stream, eng->e.h_out[eng->e.h_last], 0));
   return HC_OK;

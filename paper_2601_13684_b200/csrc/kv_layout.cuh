@@ -140,7 +140,11 @@ struct AttnParams {
   float scale_log2;      // log2(e) / sqrt(d)
   const uint8_t* skip;   // per unit: 1 = tiles deferred to a later launch (landing units), or null
   int32_t mat_f16;       // pivot score material: 0 = fp32, 1 = fp16
-  int32_t pad_;
+  int32_t combine_sel;   // combine over: 0 every unit, 1 the units listed in cunits,
+                         // 2 every unit that is not a pivot
+  const int32_t* cunits; // combine_sel 1: the units (grid.x = n_cunits)
+  int32_t n_cunits;
+  int32_t pad2_;
 };
 
 constexpr int kPartStride = 132;  // M, L, pad, pad, O[128]
