@@ -375,7 +375,8 @@ def test_single_call_fire_and_land_abi():
     assert want <= pre
 
 
-@pytest.mark.parametrize("dd", [None, False, "serial"], ids=["auto", "host", "serial-decide"])
+@pytest.mark.parametrize("dd", [None, False, "serial", "pivot-first"],
+                         ids=["auto", "host", "serial-decide", "pivot-first"])
 @pytest.mark.parametrize("seed", range(N_RANDOM_CONFIGS))
 def test_randomized_configs_match_oracle(seed, dd, monkeypatch):
     """Seeded random engine configurations (window, delay, host-link model, sinks /
@@ -387,6 +388,11 @@ def test_randomized_configs_match_oracle(seed, dd, monkeypatch):
         if seed % 4:
             pytest.skip("the general decide kernel on a quarter of the configurations")
         monkeypatch.setenv("HC_DECIDE_SERIAL", "1")
+        dd = None
+    elif dd == "pivot-first":
+        if seed % 4 != 1:
+            pytest.skip("the pivot-first step on a quarter of the configurations")
+        monkeypatch.setenv("HC_PIVOT_FIRST", "1")
         dd = None
     rng = np.random.default_rng(1000 + seed)
     T = int(rng.integers(16, 41))
